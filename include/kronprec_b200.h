@@ -1,0 +1,202 @@
+/*
+ * kronprec_b200.h — C ABI of the B200-native PCG / FPCG / CGLS hot path.
+ *
+ * Drop-in boundary for the reference `kronprec` solver path (namespace
+ * kronprec, /root/reference/proj/include/kronprec/*.hpp). Every entry point
+ * names the reference interface it replaces. Plain pointers and sizes only:
+ * matrices are dense column-major float64 (n-by-n, leading dimension n),
+ * vectors are vec() = column stacking (kron.cpp:52-60), exactly like the
+ * reference's Eigen::MatrixXd / VectorXd arguments.
+ *
+ * Error model (mirrors the reference's exception types):
+ *   KP_OK                    0  success
+ *   KP_ERR_INVALID_ARGUMENT  1  std::invalid_argument (shape / argument errors)
+ *   KP_ERR_RUNTIME           2  std::runtime_error (SVD failure, NaN objective)
+ *   KP_ERR_NO_ROOT           3  kronprec::NoRootError (discrepancy principle)
+ *   KP_ERR_CUDA              4  CUDA runtime / launch failure (no CPU fallback)
+ *   KP_ERR_UNSUPPORTED       5  option combination not implemented on device
+ * The message of the last failure on the calling thread is kp_last_error().
+ * Solver numerical breakdowns are NOT errors: as in the reference
+ * (krylov.cpp:75-139) they are reported in kp_history.abort_reason with
+ * converged = 0 and status KP_OK.
+ *
+ * Threading: one library context per process, one CUDA stream per context;
+ * handles are not thread-safe. Host buffers are owned by the caller; handles
+ * own device memory.
+ */
+#ifndef KRONPREC_B200_H
+#define KRONPREC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KP_OK 0
+#define KP_ERR_INVALID_ARGUMENT 1
+#define KP_ERR_RUNTIME 2
+#define KP_ERR_NO_ROOT 3
+#define KP_ERR_CUDA 4
+#define KP_ERR_UNSUPPORTED 5
+
+/* PrecisionFormat (precision.hpp:14-37). significand_bits counts the implicit
+ * bit (fp16: t=11, emax=15). A format with t>=53, emax>=1023 and subnormals
+ * "covers double" and makes every rounding the identity. */
+typedef struct kp_format {
+  int significand_bits;
+  int max_exponent;
+  int subnormals_enabled;
+} kp_format;
+
+/* Accumulation semantics of the low-precision preconditioner solve.
+ * KP_ACCUM_REFERENCE: every product rounded to fmt, sums over the fixed
+ *   pairwise tree with one rounding per stage — bit-identical to
+ *   lp_matmul (lpblas.cpp:13-70). Default.
+ * KP_ACCUM_TENSOR: fp16 operands on the tcgen05 tensor pipe, fp32
+ *   accumulation, one rounding of each GEMM result to fp16 (north-star mode;
+ *   iteration counts may differ from the reference by a few). fp16 only. */
+#define KP_ACCUM_REFERENCE 0
+#define KP_ACCUM_TENSOR 1
+
+/* SolverOptions (krylov.hpp:14-22). When device_pointers != 0, b, x and
+ * x_true passed to the solvers are device pointers (kp_device_alloc). */
+typedef struct kp_solver_options {
+  double lambda;
+  int max_iterations;
+  double rel_residual_tol;
+  const double* x_true; /* NULL = no relative-error track */
+  int track_search_direction_orthogonality;
+  int record_iterates; /* requires kp_history.iterates != NULL */
+  int device_pointers;
+} kp_solver_options;
+
+/* ConvergenceHistory (krylov.hpp:29-42). The caller provides arrays with
+ * `capacity` rows (max_iterations + 1 is always enough); row k is the state
+ * after k iterations. iterates (optional) holds capacity * n^2 doubles. */
+typedef struct kp_history {
+  int capacity;
+  double* relative_error;   /* may be NULL; filled only when x_true given */
+  double* residual_norm;
+  double* work_units;
+  double* residual_cosines; /* may be NULL; capacity entries */
+  double* iterates;         /* may be NULL */
+  int rows;                 /* rows written (= iterations_used + 1) */
+  int n_cosines;
+  int iterations_used;
+  int converged;
+  int msolve_count;
+  char abort_reason[192];   /* empty on a clean run */
+} kp_history;
+
+/* ParamChoice (regparam.hpp:36-46). method: 0 opt, 1 gcv, 2 wgcv,
+ * 3 discrepancy, 4 gcv on an explicit grid. */
+typedef struct kp_param_choice {
+  double lambda;
+  int method;
+  double omega;
+  double eta;
+  double noise_norm;
+  double objective_value;
+  double bracket_lo;
+  double bracket_hi;
+  int flat_objective;
+  int grid_index; /* grid selectors only; -1 otherwise */
+} kp_param_choice;
+
+typedef struct kp_operator kp_operator; /* KroneckerSum (kron.hpp:19-22)   */
+typedef struct kp_precond kp_precond;   /* KronSvdPreconditioner (factor.hpp:42-54) */
+typedef struct kp_spectral kp_spectral; /* SpectralData (regparam.hpp:19-24) */
+
+/* ---- context ---------------------------------------------------------- */
+const char* kp_last_error(void);
+int kp_init(int device);            /* selects the device, creates the stream */
+int kp_synchronize(void);
+int kp_device_alloc(size_t bytes, void** dptr);
+int kp_device_free(void* dptr);
+int kp_memcpy_h2d(void* dst, const void* src, size_t bytes);
+int kp_memcpy_d2h(void* dst, const void* src, size_t bytes);
+/* Per-kernel-class device timing (CUDA events on the library stream).
+ * class ids: 0 fp64 operator GEMM, 1 preconditioner GEMM, 2 vector kernels,
+ * 3 spectral / lambda kernels. */
+int kp_profile_enable(int on);
+int kp_profile_read(int kernel_class, double* total_ms, long long* launches);
+int kp_profile_reset(void);
+long long kp_launch_count(void);   /* kernels launched by this library */
+
+/* ---- operator: kron.hpp / kron.cpp ------------------------------------ */
+/* row_factors / col_factors: r consecutive n-by-n column-major matrices,
+ * term k = (row_factor_k, col_factor_k) as in KronTerm (kron.hpp:12-15). */
+int kp_operator_create(int n, int r, const double* row_factors,
+                       const double* col_factors, kp_operator** out);
+int kp_operator_destroy(kp_operator* op);
+int kp_operator_info(const kp_operator* op, int* n, int* r);
+/* kronsum_apply (kron.cpp:73-79) / kronsum_apply_transpose (kron.cpp:81-88) */
+int kp_kronsum_apply(const kp_operator* op, const double* y, double* out);
+int kp_kronsum_apply_transpose(const kp_operator* op, const double* y,
+                               double* out);
+/* normal_matvec (krylov.cpp:146-152): A^T(A p) + lambda^2 p */
+int kp_normal_matvec(const kp_operator* op, double lambda, const double* p,
+                     double* out);
+
+/* ---- preconditioner: factor.hpp / factor.cpp -------------------------- */
+/* build_preconditioner (factor.cpp:80-104): host LAPACK SVDs of a_r, a_c,
+ * weights S(i,j)=1/((s_r(j) s_c(i))^2+lambda^2), rounded V_r, V_c, S. */
+int kp_precond_build(const double* a_r, const double* a_c, int n,
+                     double lambda, kp_format fmt, int accum,
+                     kp_precond** out);
+/* Same, from a caller-supplied SVD (u, s, v per factor; s nonincreasing). */
+int kp_precond_build_from_svd(int n, const double* u_r, const double* s_r,
+                              const double* v_r, const double* u_c,
+                              const double* s_c, const double* v_c,
+                              double lambda, kp_format fmt, int accum,
+                              kp_precond** out);
+/* with_lambda (factor.cpp:106-115) */
+int kp_precond_with_lambda(const kp_precond* p, double lambda,
+                           kp_precond** out);
+int kp_precond_destroy(kp_precond* p);
+/* precond_solve (factor.cpp:117-132) */
+int kp_precond_solve(const kp_precond* p, const double* r, double* z);
+/* Export a field (n*n doubles, or n for singular values):
+ * 0 s_weights, 1 s_lp, 2 vr_lp, 3 vc_lp, 4 svd_r.s, 5 svd_c.s,
+ * 6 svd_r.u, 7 svd_r.v, 8 svd_c.u, 9 svd_c.v */
+int kp_precond_export(const kp_precond* p, int field, double* out);
+int kp_precond_info(const kp_precond* p, int* n, double* lambda,
+                    kp_format* fmt, int* accum);
+
+/* ---- solvers: krylov.hpp / krylov.cpp --------------------------------- */
+int kp_cgls(const kp_operator* op, const double* b,
+            const kp_solver_options* opts, double* x, kp_history* hist);
+int kp_pcg(const kp_operator* op, const double* b, const kp_precond* m,
+           const kp_solver_options* opts, double* x, kp_history* hist);
+int kp_fpcg(const kp_operator* op, const double* b, const kp_precond* m,
+            const kp_solver_options* opts, double* x, kp_history* hist);
+
+/* ---- lambda selection: regparam.hpp / regparam.cpp -------------------- */
+/* make_spectral_data (regparam.cpp:119-126): device-resident sigma_hat =
+ * s_r(j) s_c(i) and b_hat = vec(U_c^T B U_r) from the FP64 SVD factors. */
+int kp_spectral_create(const kp_precond* p, const double* b,
+                       kp_spectral** out);
+int kp_spectral_destroy(kp_spectral* sd);
+/* Sorted nonincreasing like approx_spectrum/project_b (factor.cpp:134-177). */
+int kp_spectral_export(const kp_spectral* sd, double* sigma_hat,
+                       double* b_hat);
+int kp_gcv_objective(const kp_spectral* sd, double lambda, double* value);
+int kp_discrepancy_gap(const kp_spectral* sd, double epsilon, double lambda,
+                       double* value);
+/* GCV over an explicit lambda grid (one batched reduction); argmin is the
+ * first minimum, as a left-to-right scan would pick it. */
+int kp_gcv_grid(const kp_spectral* sd, const double* lambdas, int m,
+                double* values, kp_param_choice* choice);
+/* gcv (regparam.cpp:254-258): 1024-point log grid + golden refinement. */
+int kp_gcv(const kp_spectral* sd, kp_param_choice* choice);
+/* discrepancy (regparam.cpp:288-327); KP_ERR_NO_ROOT when no root. */
+int kp_discrepancy(const kp_spectral* sd, double noise_norm, double eta,
+                   kp_param_choice* choice);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KRONPREC_B200_H */

@@ -1,0 +1,1156 @@
+// C ABI of the B200 hot path (include/kronprec_b200.h): handles, setup, the
+// device-driven PCG / FPCG / CGLS loops and lambda selection.
+//
+// Reference behaviour mirrored here (file:line in /root/reference/proj):
+//   KroneckerSum / kronsum_apply(_transpose)   kron.hpp:19-35, kron.cpp:73-88
+//   normal_matvec                              krylov.cpp:146-152
+//   build_preconditioner / with_lambda          factor.cpp:80-115
+//   precond_solve                              factor.cpp:117-132
+//   pcg / fpcg (pcg_core), cgls                krylov.cpp:58-142, 154-208
+//   make_spectral_data, gcv, discrepancy        regparam.cpp:119-134, 254-327
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/kronprec_b200.h"
+#include "common.cuh"
+#include "gemm_f16ref.cuh"
+#include "gemm_f64.cuh"
+#include "host_la.h"
+#include "vec.cuh"
+
+// ============================================================================
+// context
+// ============================================================================
+namespace kp {
+
+static thread_local std::string g_last_error;
+
+Ctx& ctx() {
+  static Ctx c;
+  return c;
+}
+
+void ensure_init() {
+  Ctx& c = ctx();
+  if (c.device >= 0) return;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    throw CudaError(std::string("no CUDA device available: ") + cudaGetErrorString(e) +
+                    " (the B200 path has no CPU fallback)");
+  KP_CUDA(cudaSetDevice(0));
+  KP_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  KP_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, 0));
+  c.device = 0;
+}
+
+void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+LaunchScope::LaunchScope(int c) : cls(c) {
+  Ctx& x = ctx();
+  x.launches++;
+  if (x.profile) {
+    if (!x.pool.empty()) {
+      ev = x.pool.back();
+      x.pool.pop_back();
+    } else {
+      KP_CUDA(cudaEventCreate(&ev.first));
+      KP_CUDA(cudaEventCreate(&ev.second));
+    }
+    KP_CUDA(cudaEventRecord(ev.first, x.stream));
+  }
+}
+LaunchScope::~LaunchScope() noexcept(false) {
+  if (ev.first) {
+    Ctx& x = ctx();
+    KP_CUDA(cudaEventRecord(ev.second, x.stream));
+    x.pending[cls].push_back(ev);
+  }
+}
+
+static void profile_collect() {
+  Ctx& x = ctx();
+  KP_CUDA(cudaStreamSynchronize(x.stream));
+  for (int c = 0; c < KC_COUNT; ++c) {
+    for (auto& ev : x.pending[c]) {
+      float ms = 0.f;
+      KP_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
+      x.total_ms[c] += ms;
+      x.count[c]++;
+      x.pool.push_back(ev);
+    }
+    x.pending[c].clear();
+  }
+}
+
+static void sync() { KP_CUDA(cudaStreamSynchronize(ctx().stream)); }
+
+// ============================================================================
+// small device helpers
+// ============================================================================
+__global__ void transpose_blocks_kernel(const double* src, double* dst, int n, int r) {
+  __shared__ double tile[32][33];
+  const int b = blockIdx.z;
+  const size_t off = size_t(b) * n * n;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int c = y0 + j, rr = x0 + threadIdx.x;
+    if (c < n && rr < n) tile[j][threadIdx.x] = src[off + size_t(c) * n + rr];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int c = x0 + j, rr = y0 + threadIdx.x;
+    if (c < n && rr < n) dst[off + size_t(c) * n + rr] = tile[threadIdx.x][j];
+  }
+}
+// dst = transpose of each of the r n-by-n column-major blocks of src
+static void transpose_blocks(const double* src, double* dst, int n, int r) {
+  LaunchScope s(KC_VECTOR);
+  dim3 grid(cdiv(n, 32), cdiv(n, 32), r), block(32, 8);
+  transpose_blocks_kernel<<<grid, block, 0, ctx().stream>>>(src, dst, n, r);
+  check_launch("transpose_blocks");
+}
+
+// Host-pinned scratch for small readbacks.
+template <typename T>
+struct Pinned {
+  T* p = nullptr;
+  size_t n = 0;
+  explicit Pinned(size_t count) : n(count) { KP_CUDA(cudaMallocHost(&p, count * sizeof(T))); }
+  ~Pinned() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+// Buffer that is either caller-owned device memory or a staged copy of host
+// memory (kp_solver_options.device_pointers).
+struct VecArg {
+  const double* d = nullptr;
+  DBuf<double> own;
+  VecArg(const double* src, size_t nn, bool device) {
+    if (!src) return;
+    if (device) {
+      d = src;
+    } else {
+      own.alloc(nn);
+      own.upload(src, nn);
+      d = own.p;
+    }
+  }
+};
+
+}  // namespace kp
+
+using namespace kp;
+
+// ============================================================================
+// handle types
+// ============================================================================
+struct kp_operator {
+  int n = 0, r = 0;
+  DBuf<double> Cs_rm, Cs_cm, Rr_rm, Rr_cm;  // r stacked n*n blocks
+  DBuf<double> W;                           // r*n*n workspace
+  DBuf<double> part;                        // GEMM epilogue partials
+};
+
+struct PrecondShared {
+  int n = 0;
+  std::vector<double> u_r, s_r, v_r, u_c, s_c, v_c;  // FP64 SVDs (host)
+  DBuf<double> d_u_r, d_u_c, d_s_r, d_s_c;            // for spectral data
+  // binary16 operands (padded, K-major), exact / tensor modes
+  long ldh = 0;
+  DBuf<__half> vc_a, vr_b, vct_a, vrt_b;
+  // FP64 operands (fmt covers double)
+  DBuf<double> vc, vr, vct, vrt;
+};
+
+struct kp_precond {
+  std::shared_ptr<PrecondShared> sh;
+  int n = 0;
+  double lambda = 0.0;
+  kp_format fmt{};
+  int accum = KP_ACCUM_REFERENCE;
+  std::vector<double> s_weights;  // host FP64 (factor.cpp:62-76)
+  DBuf<double> s64;               // fp64 format
+  DBuf<__half> s16;               // fp16 format (col-major n*n)
+  // workspace
+  DBuf<__half> r16, t1h, wh, t3h;
+  DBuf<double> t1d, wd, t3d;
+  DBuf<double> part;
+};
+
+struct kp_spectral {
+  int n = 0;
+  std::shared_ptr<PrecondShared> sh;
+  DBuf<double> bhat;
+  double smax = 0.0, smin = 0.0;
+};
+
+namespace {
+
+bool covers_double(const kp_format& f) {
+  return f.significand_bits >= 53 && f.max_exponent >= 1023 && f.subnormals_enabled;
+}
+bool is_fp16(const kp_format& f) {
+  return f.significand_bits == 11 && f.max_exponent == 15 && f.subnormals_enabled;
+}
+long round_up(long v, long m) { return (v + m - 1) / m * m; }
+
+// ---------------------------------------------------------------------------
+// operator application (kron.cpp:73-88) as two DMMA GEMMs with the Kronecker
+// sum folded into the M (first) and K (second) dimensions.
+void op_apply(kp_operator* op, const double* in, double* out, bool transpose,
+              const F64Epilogue* extra, const int* status) {
+  const int n = op->n, r = op->r;
+  const long nn = long(n) * n;
+  F64GemmArgs g1;
+  g1.M = r * n, g1.N = n, g1.nb = 1, g1.Kb = n;
+  g1.A = {transpose ? op->Cs_cm.p : op->Cs_rm.p, n, 0};
+  g1.B = {in, n, 0};
+  g1.epi.C = op->W.p, g1.epi.cm = n, g1.epi.cn = 1;
+  g1.status = status;
+  gemm_f64(g1, KC_OPERATOR);
+  F64GemmArgs g2;
+  g2.M = n, g2.N = n, g2.nb = r, g2.Kb = n;
+  g2.A = {op->W.p, n, nn};
+  g2.B = {transpose ? op->Rr_cm.p : op->Rr_rm.p, n, nn};
+  if (extra) g2.epi = *extra;
+  g2.epi.C = out, g2.epi.cm = 1, g2.epi.cn = n, g2.epi.vm = 1, g2.epi.vn = n;
+  g2.status = status;
+  gemm_f64(g2, KC_OPERATOR);
+}
+
+int op_partials_ctas(const kp_operator* op) { return gemm_f64_num_ctas(op->n, op->n); }
+
+void ensure_ws(kp_precond* p) {
+  const int n = p->n;
+  const size_t nn = size_t(n) * n;
+  if (covers_double(p->fmt)) {
+    if (!p->t1d.p) p->t1d.alloc(nn), p->wd.alloc(nn), p->t3d.alloc(nn);
+    if (!p->part.p) p->part.alloc(size_t(gemm_f64_num_ctas(n, n)) * 4);
+  } else {
+    const long ldh = p->sh->ldh;
+    if (!p->r16.p) {
+      p->r16.alloc(size_t(n) * ldh), p->t1h.alloc(size_t(n) * ldh);
+      p->wh.alloc(size_t(n) * ldh), p->t3h.alloc(size_t(n) * ldh);
+      fill_u16(p->r16.p, p->r16.n, 0x0000);  // B operands: +0 padding
+      fill_u16(p->wh.p, p->wh.n, 0x0000);
+      fill_u16(p->t1h.p, p->t1h.n, 0x8000);  // A operands: -0 padding
+      fill_u16(p->t3h.p, p->t3h.n, 0x8000);
+    }
+    if (!p->part.p) p->part.alloc(size_t(gemm_f16ref_num_ctas(n, n)) * 4);
+  }
+}
+
+int msolve_partials_ctas(const kp_precond* p) {
+  return covers_double(p->fmt) ? gemm_f64_num_ctas(p->n, p->n) : gemm_f16ref_num_ctas(p->n, p->n);
+}
+
+// precond_solve (factor.cpp:117-132). In fp16 mode r16 must already hold
+// round16(unvec(r)) (written by the caller's fused update kernel); r is the
+// FP64 residual used by the fused dot products.
+void msolve(kp_precond* p, const double* r, double* z, const double* d0, const double* d1a,
+            const double* d1b, const int* status) {
+  const int n = p->n;
+  auto* sh = p->sh.get();
+  ensure_ws(p);
+  if (covers_double(p->fmt)) {
+    F64GemmArgs g;
+    g.M = n, g.N = n, g.nb = 1, g.Kb = n, g.status = status;
+    g.A = {sh->vc.p, n, 0}, g.B = {r, n, 0};  // t1 = V_c^T R
+    g.epi = F64Epilogue{}, g.epi.C = p->t1d.p, g.epi.cm = n, g.epi.cn = 1;
+    gemm_f64(g, KC_PRECOND);
+    g.A = {p->t1d.p, n, 0}, g.B = {sh->vr.p, n, 0};  // w = S .* (t1 V_r)
+    g.epi = F64Epilogue{}, g.epi.C = p->wd.p, g.epi.cm = 1, g.epi.cn = n;
+    g.epi.vm = 1, g.epi.vn = n, g.epi.mul = p->s64.p;
+    gemm_f64(g, KC_PRECOND);
+    g.A = {sh->vct.p, n, 0}, g.B = {p->wd.p, n, 0};  // t3 = V_c w
+    g.epi = F64Epilogue{}, g.epi.C = p->t3d.p, g.epi.cm = n, g.epi.cn = 1;
+    gemm_f64(g, KC_PRECOND);
+    g.A = {p->t3d.p, n, 0}, g.B = {sh->vrt.p, n, 0};  // z = t3 V_r^T
+    g.epi = F64Epilogue{}, g.epi.C = z, g.epi.cm = 1, g.epi.cn = n, g.epi.vm = 1, g.epi.vn = n;
+    g.epi.d0 = d0, g.epi.d1a = d1a, g.epi.d1b = d1b, g.epi.count_nonfinite = 1;
+    g.epi.partials = p->part.p;
+    gemm_f64(g, KC_PRECOND);
+    return;
+  }
+  if (!is_fp16(p->fmt)) throw Unsupported("precond_solve: only fp16 and double-covering formats run on the B200 path");
+  if (p->accum != KP_ACCUM_REFERENCE) throw Unsupported("precond_solve: tensor accumulation not built");
+  const long ldh = sh->ldh;
+  F16GemmArgs g;
+  g.M = n, g.N = n, g.K = n, g.status = status;
+  g.A = {sh->vc_a.p, ldh}, g.B = {p->r16.p, ldh};  // t1 = lp(V_c^T R)
+  g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = ldh, g.epi.cn = 1;
+  gemm_f16ref(g, KC_PRECOND);
+  g.A = {p->t1h.p, ldh}, g.B = {sh->vr_b.p, ldh};  // w = round(S .* lp(t1 V_r))
+  g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF_SCALED, g.epi.Ch = p->wh.p, g.epi.cm = 1,
+  g.epi.cn = ldh, g.epi.scale = p->s16.p, g.epi.sm = 1, g.epi.sn = n;
+  gemm_f16ref(g, KC_PRECOND);
+  g.A = {sh->vct_a.p, ldh}, g.B = {p->wh.p, ldh};  // t3 = lp(V_c w)
+  g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t3h.p, g.epi.cm = ldh, g.epi.cn = 1;
+  gemm_f16ref(g, KC_PRECOND);
+  g.A = {p->t3h.p, ldh}, g.B = {sh->vrt_b.p, ldh};  // z = lp(t3 V_r^T)
+  g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z, g.epi.cm = 1, g.epi.cn = n;
+  g.epi.vm = 1, g.epi.vn = n, g.epi.d0 = d0, g.epi.d1a = d1a, g.epi.d1b = d1b;
+  g.epi.partials = p->part.p;
+  gemm_f16ref(g, KC_PRECOND);
+}
+
+void cast_r16(kp_precond* p, const double* r, const int* status) {
+  ensure_ws(p);
+  cast_f64_to_f16_padded(r, p->r16.p, p->n, p->n, p->n, p->sh->ldh, status);
+}
+
+// weight_matrix (factor.cpp:62-76)
+std::vector<double> weight_matrix(const PrecondShared& sh, double lambda) {
+  const int n = sh.n;
+  std::vector<double> s(size_t(n) * n);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      const double prod = sh.s_r[j] * sh.s_c[i];
+      const double denom = prod * prod + lambda * lambda;
+      if (denom == 0.0)
+        throw InvalidArgument("build_preconditioner: singular factors need lambda > 0");
+      s[size_t(j) * n + i] = 1.0 / denom;
+    }
+  return s;
+}
+
+void set_weights(kp_precond* p) {
+  const int n = p->n;
+  const size_t nn = size_t(n) * n;
+  p->s_weights = weight_matrix(*p->sh, p->lambda);
+  if (covers_double(p->fmt)) {
+    p->s64.alloc(nn);
+    p->s64.upload(p->s_weights.data(), nn);
+  } else {
+    DBuf<double> tmp(nn);
+    tmp.upload(p->s_weights.data(), nn);
+    p->s16.alloc(nn);
+    cast_f64_to_f16_padded(tmp.p, p->s16.p, n, n, n, n, nullptr);  // round_array(s_weights)
+    sync();
+  }
+}
+
+std::vector<double> host_transpose(const std::vector<double>& a, int n) {
+  std::vector<double> t(a.size());
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) t[size_t(i) * n + j] = a[size_t(j) * n + i];
+  return t;
+}
+
+kp_precond* precond_from_svd(int n, std::vector<double> ur, std::vector<double> sr,
+                             std::vector<double> vr, std::vector<double> uc,
+                             std::vector<double> sc, std::vector<double> vc, double lambda,
+                             kp_format fmt, int accum) {
+  if (n < 1) throw InvalidArgument("build_preconditioner: empty factors");
+  if (lambda < 0.0) throw InvalidArgument("build_preconditioner: negative lambda");
+  if (!covers_double(fmt) && !is_fp16(fmt))
+    throw Unsupported("build_preconditioner: the B200 path stores fp16 or FP64 factors only");
+  if (accum == KP_ACCUM_TENSOR && !is_fp16(fmt))
+    throw InvalidArgument("build_preconditioner: tensor accumulation requires fp16");
+  if (accum == KP_ACCUM_TENSOR) throw Unsupported("build_preconditioner: tensor accumulation not built");
+  auto sh = std::make_shared<PrecondShared>();
+  sh->n = n;
+  sh->u_r = std::move(ur), sh->s_r = std::move(sr), sh->v_r = std::move(vr);
+  sh->u_c = std::move(uc), sh->s_c = std::move(sc), sh->v_c = std::move(vc);
+  const size_t nn = size_t(n) * n;
+  sh->d_u_r.alloc(nn), sh->d_u_r.upload(sh->u_r.data(), nn);
+  sh->d_u_c.alloc(nn), sh->d_u_c.upload(sh->u_c.data(), nn);
+  sh->d_s_r.alloc(n), sh->d_s_r.upload(sh->s_r.data(), n);
+  sh->d_s_c.alloc(n), sh->d_s_c.upload(sh->s_c.data(), n);
+  const std::vector<double> vct = host_transpose(sh->v_c, n), vrt = host_transpose(sh->v_r, n);
+  if (covers_double(fmt)) {
+    sh->vc.alloc(nn), sh->vc.upload(sh->v_c.data(), nn);
+    sh->vr.alloc(nn), sh->vr.upload(sh->v_r.data(), nn);
+    sh->vct.alloc(nn), sh->vct.upload(vct.data(), nn);
+    sh->vrt.alloc(nn), sh->vrt.upload(vrt.data(), nn);
+  } else {
+    sh->ldh = round_up(n, 64);
+    const size_t hn = size_t(n) * sh->ldh;
+    DBuf<double> tmp(nn);
+    auto put = [&](DBuf<__half>& dst, const std::vector<double>& src, uint16_t pad) {
+      dst.alloc(hn);
+      fill_u16(dst.p, hn, pad);
+      tmp.upload(src.data(), nn);
+      cast_f64_to_f16_padded(tmp.p, dst.p, n, n, n, sh->ldh, nullptr);  // round_array(v, fmt)
+      sync();
+    };
+    put(sh->vc_a, sh->v_c, 0x8000);  // A of t1 = V_c^T R   (row a = V_c(:,a))
+    put(sh->vr_b, sh->v_r, 0x0000);  // B of t1 V_r          (row j = V_r(:,j))
+    put(sh->vct_a, vct, 0x8000);     // A of V_c w           (row b = V_c(b,:))
+    put(sh->vrt_b, vrt, 0x0000);     // B of t3 V_r^T        (row c = V_r(c,:))
+  }
+  auto* p = new kp_precond;
+  p->sh = sh;
+  p->n = n;
+  p->lambda = lambda;
+  p->fmt = fmt;
+  p->accum = accum;
+  try {
+    set_weights(p);
+  } catch (...) {
+    delete p;
+    throw;
+  }
+  sync();
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// solver driver
+struct Solve {
+  kp_operator* op;
+  size_t nn;
+  DBuf<DevState> st;
+  DBuf<double> resid, relerr, cosines, iterates;
+  DevHistory dh{};
+  int capacity = 0;
+};
+
+void check_common(const kp_operator* op, const kp_solver_options* o, kp_history* h) {
+  if (!op) throw InvalidArgument("solver: null operator");
+  if (!o || !h) throw InvalidArgument("solver: null options or history");
+  if (o->max_iterations < 1) throw InvalidArgument("solver: max_iterations must be at least 1");
+  if (!(o->rel_residual_tol > 0.0)) throw InvalidArgument("solver: tolerance must be positive");
+  if (h->capacity < 1 || !h->residual_norm || !h->work_units)
+    throw InvalidArgument("solver: history arrays missing");
+}
+
+std::string abort_message(int code, int k) {
+  const std::string ks = std::to_string(k);
+  switch (code) {
+    case AB_M_NONFINITE_INIT: return "non-finite preconditioner output before iteration 1";
+    case AB_POSITIVITY_INIT: return "preconditioner lost positivity before iteration 1";
+    case AB_CURV_NONFINITE: return "non-finite curvature at iteration " + ks;
+    case AB_CURV_BREAKDOWN: return "curvature breakdown at iteration " + ks;
+    case AB_RESID_NONFINITE: return "non-finite residual at iteration " + ks;
+    case AB_M_NONFINITE:
+      return "non-finite preconditioner output at iteration " + ks +
+             " (overflow in the storage format)";
+    case AB_INNER_NONFINITE: return "non-finite inner product at iteration " + ks;
+    case AB_POSITIVITY: return "preconditioner lost positivity at iteration " + ks;
+    default: return "";
+  }
+}
+
+void setup_state(Solve& s, const kp_solver_options* o, bool has_xt, bool flexible,
+                 double work) {
+  DevState h{};
+  h.status = ST_RUNNING;
+  h.k = 1;
+  h.maxit = o->max_iterations;
+  h.flexible = flexible;
+  h.track_cos = o->track_search_direction_orthogonality != 0;
+  h.has_xt = has_xt;
+  h.record = o->record_iterates != 0;
+  h.tol = o->rel_residual_tol;
+  h.l2 = o->lambda * o->lambda;
+  h.work_per_iter = work;
+  s.st.alloc(1);
+  s.st.upload(&h, 1);
+  s.capacity = o->max_iterations + 1;
+  s.resid.alloc(s.capacity);
+  s.relerr.alloc(s.capacity);
+  s.cosines.alloc(s.capacity);
+  if (o->record_iterates) s.iterates.alloc(size_t(s.capacity) * s.nn);
+  s.dh.resid = s.resid.p;
+  s.dh.relerr = s.relerr.p;
+  s.dh.cosines = s.cosines.p;
+  s.dh.iterates = s.iterates.p;
+  s.dh.capacity = s.capacity;
+}
+
+// Runs `iteration` repeatedly until the device status leaves RUNNING. Without
+// profiling the iteration is captured once into a CUDA graph and replayed;
+// the host polls the status word in growing chunks (overshoot iterations are
+// device no-ops).
+void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
+  Ctx& c = ctx();
+  Pinned<DevState> hst(1);
+  cudaGraphExec_t exec = nullptr;
+  long long per_iter_launches = 0;
+  if (!c.profile) {
+    const long long before = c.launches;
+    KP_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      iteration();
+    } catch (...) {
+      cudaGraph_t g;
+      cudaStreamEndCapture(c.stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cudaGraph_t graph;
+    KP_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    KP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    KP_CUDA(cudaGraphDestroy(graph));
+    per_iter_launches = c.launches - before;
+    c.launches = before;
+  }
+  int done = 0, chunk = 1;
+  while (done < maxit) {
+    const int todo = std::min(chunk, maxit - done);
+    for (int i = 0; i < todo; ++i) {
+      if (exec) {
+        KP_CUDA(cudaGraphLaunch(exec, c.stream));
+        c.launches += per_iter_launches;
+      } else {
+        iteration();
+      }
+    }
+    done += todo;
+    KP_CUDA(cudaMemcpyAsync(&hst.p->status, &s.st.p->status, sizeof(int), cudaMemcpyDeviceToHost,
+                            c.stream));
+    sync();
+    if (hst.p->status != ST_RUNNING) break;
+    chunk = std::min(chunk * 2, 16);
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+}
+
+void finish(Solve& s, const kp_solver_options* o, kp_history* h, double work) {
+  DevState st;
+  s.st.download(&st, 1);
+  sync();
+  const int rows = std::min(st.rows, h->capacity);
+  std::vector<double> buf(std::max(rows, 1));
+  s.resid.download(buf.data(), rows);
+  sync();
+  std::memcpy(h->residual_norm, buf.data(), rows * sizeof(double));
+  if (o->x_true && h->relative_error) {
+    s.relerr.download(buf.data(), rows);
+    sync();
+    std::memcpy(h->relative_error, buf.data(), rows * sizeof(double));
+  }
+  for (int k = 0; k < rows; ++k) h->work_units[k] = work * k;
+  const int ncos = std::min(st.ncos, h->capacity);
+  if (o->track_search_direction_orthogonality && h->residual_cosines && ncos > 0) {
+    s.cosines.download(h->residual_cosines, ncos);
+    sync();
+  }
+  if (o->record_iterates && h->iterates) {
+    KP_CUDA(cudaMemcpyAsync(h->iterates, s.iterates.p, size_t(rows) * s.nn * sizeof(double),
+                            cudaMemcpyDeviceToHost, ctx().stream));
+    sync();
+  }
+  h->rows = rows;
+  h->n_cosines = ncos;
+  h->iterations_used = st.iterations_used;
+  h->converged = st.status == ST_CONVERGED;
+  h->msolve_count = st.msolve_count;
+  const std::string msg = st.status == ST_ABORTED ? abort_message(st.abort_code, st.abort_iter) : "";
+  std::snprintf(h->abort_reason, sizeof(h->abort_reason), "%s", msg.c_str());
+}
+
+// pcg_core (krylov.cpp:58-142)
+void run_pcg(kp_operator* op, const double* b_in, kp_precond* m, const kp_solver_options* o,
+             double* x_out, kp_history* hist, bool flexible) {
+  check_common(op, o, hist);
+  if (!m) throw InvalidArgument("solver: null preconditioner");
+  if (m->n != op->n) throw InvalidArgument("solver: preconditioner size mismatch");
+  const int n = op->n;
+  const size_t nn = size_t(n) * n;
+  const bool dev = o->device_pointers != 0;
+  VecArg b(b_in, nn, dev), xt(o->x_true, nn, dev);
+  Solve s;
+  s.op = op;
+  s.nn = nn;
+  setup_state(s, o, xt.d != nullptr, flexible, 2.25);
+  int* status = &s.st.p->status;
+  DBuf<double> xown;
+  double* x;
+  if (dev) {
+    x = x_out;
+  } else {
+    xown.alloc(nn);
+    x = xown.p;
+  }
+  DBuf<double> r(nn), p(nn), q(nn), z(nn), rprev(flexible ? nn : 0);
+  const int nop = op_partials_ctas(op);
+  const int nms = msolve_partials_ctas(m);
+  DBuf<double> part_op(size_t(nop) * 4), part_vec(size_t(VEC_CTAS) * 4), part_xt(size_t(VEC_CTAS) * 4);
+  const bool fp16 = !covers_double(m->fmt);
+
+  vec_zero(x, nn);
+  F64Epilogue e;
+  e.d0_self = 1;
+  e.d0 = r.p;  // any non-null: self product
+  e.partials = part_op.p;
+  op_apply(op, b.d, r.p, true, &e, status);  // r = A^T b, ||r||^2 partials
+  if (xt.d) vec_dot_partials(xt.d, xt.d, nn, part_xt.p);
+  pcg_init_scalar(s.st.p, s.dh, part_op.p, nop, part_xt.p, VEC_CTAS);
+  if (fp16) cast_r16(m, r.p, status);
+  msolve(m, r.p, z.p, r.p, nullptr, nullptr, status);
+  pcg_init_msolve_scalar(s.st.p, m->part.p, nms);
+  vec_copy(p.p, z.p, nn, status);
+
+  DBuf<double> ap(nn);
+  auto iteration = [&]() {
+    // q = A^T (A p) + lambda^2 p, with p.q partials (normal_matvec)
+    op_apply(op, p.p, ap.p, false, nullptr, status);
+    F64Epilogue ne;
+    ne.addv = p.p, ne.addc = o->lambda * o->lambda;
+    ne.d0 = p.p, ne.partials = part_op.p;
+    op_apply(op, ap.p, q.p, true, &ne, status);
+    pcg_alpha_scalar(s.st.p, part_op.p, nop);
+    pcg_update(s.st.p, s.dh, x, r.p, flexible ? rprev.p : nullptr, p.p, q.p, z.p, xt.d,
+               fp16 ? m->r16.p : nullptr, n, fp16 ? m->sh->ldh : 0, part_vec.p);
+    pcg_resid_scalar(s.st.p, s.dh, part_vec.p, VEC_CTAS);
+    msolve(m, r.p, z.p, r.p, flexible ? r.p : nullptr, flexible ? rprev.p : nullptr, status);
+    pcg_beta_scalar(s.st.p, m->part.p, nms);
+    pcg_p_update(s.st.p, p.p, z.p, nn);
+  };
+  drive(s, o->max_iterations, iteration);
+  finish(s, o, hist, 2.25);
+  if (!dev) {
+    xown.download(x_out, nn);
+    sync();
+  }
+}
+
+// cgls (krylov.cpp:154-208)
+void run_cgls(kp_operator* op, const double* b_in, const kp_solver_options* o, double* x_out,
+              kp_history* hist) {
+  check_common(op, o, hist);
+  const int n = op->n;
+  const size_t nn = size_t(n) * n;
+  const bool dev = o->device_pointers != 0;
+  VecArg b(b_in, nn, dev), xt(o->x_true, nn, dev);
+  Solve s;
+  s.op = op;
+  s.nn = nn;
+  setup_state(s, o, xt.d != nullptr, false, 2.0);
+  int* status = &s.st.p->status;
+  DBuf<double> xown;
+  double* x;
+  if (dev) {
+    x = x_out;
+  } else {
+    xown.alloc(nn);
+    x = xown.p;
+  }
+  const bool track = o->track_search_direction_orthogonality != 0;
+  DBuf<double> rt(nn), sv(nn), p(nn), q(nn), sprev(track ? nn : 0);
+  const int nop = op_partials_ctas(op);
+  DBuf<double> part_q(size_t(nop) * 4), part_s(size_t(nop) * 4), part_vec(size_t(VEC_CTAS) * 4),
+      part_p(size_t(VEC_CTAS) * 4), part_xt(size_t(VEC_CTAS) * 4);
+
+  vec_zero(x, nn);
+  vec_copy(rt.p, b.d, nn, nullptr);
+  F64Epilogue e;
+  e.d0_self = 1, e.d0 = sv.p, e.partials = part_s.p;
+  op_apply(op, rt.p, sv.p, true, &e, status);  // s = A^T rt
+  if (xt.d) vec_dot_partials(xt.d, xt.d, nn, part_xt.p);
+  cgls_init_scalar(s.st.p, s.dh, part_s.p, nop, part_xt.p, VEC_CTAS);
+  vec_copy(p.p, sv.p, nn, status);
+  if (track) vec_copy(sprev.p, sv.p, nn, status);
+
+  auto iteration = [&]() {
+    F64Epilogue qe;
+    qe.d0_self = 1, qe.d0 = q.p, qe.partials = part_q.p;
+    op_apply(op, p.p, q.p, false, &qe, status);  // q = A p, ||q||^2
+    cgls_alpha_scalar(s.st.p, part_q.p, nop, part_p.p, VEC_CTAS);
+    cgls_update(s.st.p, s.dh, x, rt.p, p.p, q.p, xt.d, nn, part_vec.p);
+    F64Epilogue se;  // s = A^T rt - lambda^2 x, ||s||^2 and s.s_prev
+    se.addv = x, se.addc = -(o->lambda * o->lambda);
+    se.d0_self = 1, se.d0 = sv.p;
+    se.d1a = track ? sprev.p : nullptr;
+    se.partials = part_s.p;
+    op_apply(op, rt.p, sv.p, true, &se, status);
+    cgls_resid_scalar(s.st.p, s.dh, part_s.p, nop, part_vec.p, VEC_CTAS);
+    cgls_p_update(s.st.p, p.p, sv.p, track ? sprev.p : nullptr, nn, part_p.p);
+  };
+  drive(s, o->max_iterations, iteration);
+  finish(s, o, hist, 2.0);
+  if (!dev) {
+    xown.download(x_out, nn);
+    sync();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// lambda selection helpers (regparam.cpp)
+double probe(const std::function<double(double)>& f, double x, const char* who) {
+  const double v = f(x);
+  if (std::isnan(v)) throw std::runtime_error(std::string(who) + ": objective is NaN");
+  return v;
+}
+
+void gcv_values(const kp_spectral* sd, const double* lambdas, int m, double* values) {
+  DBuf<double> dl(m), out(size_t(m) * 2);
+  dl.upload(lambdas, m);
+  spectral_gcv_sums(sd->sh->d_s_r.p, sd->sh->d_s_c.p, sd->bhat.p, sd->n, dl.p, m, out.p);
+  std::vector<double> h(size_t(m) * 2);
+  out.download(h.data(), h.size());
+  sync();
+  const double N = double(sd->n) * sd->n;
+  for (int q = 0; q < m; ++q) values[q] = N * h[2 * q] / (h[2 * q + 1] * h[2 * q + 1]);
+}
+double gcv_value(const kp_spectral* sd, double lambda) {
+  double v;
+  gcv_values(sd, &lambda, 1, &v);
+  return v;
+}
+double gap_value(const kp_spectral* sd, double eps, double lambda) {
+  DBuf<double> dl(1), out(1);
+  dl.upload(&lambda, 1);
+  spectral_resid_sums(sd->sh->d_s_r.p, sd->sh->d_s_c.p, sd->bhat.p, sd->n, dl.p, 1, out.p);
+  double h;
+  out.download(&h, 1);
+  sync();
+  return h - eps * eps;
+}
+
+// minimize_1d (regparam.cpp:149-181)
+std::pair<double, double> minimize_1d(const std::function<double(double)>& f, double lo, double hi,
+                                      double tol) {
+  constexpr double invphi = 0.6180339887498949;
+  double a = lo, b = hi;
+  double c = b - invphi * (b - a), d = a + invphi * (b - a);
+  double fc = probe(f, c, "minimize_1d"), fd = probe(f, d, "minimize_1d");
+  for (int it = 0; it < 300 && b - a > tol * (1.0 + std::min(std::abs(a), std::abs(b))); ++it) {
+    if (fc < fd) {
+      b = d, d = c, fd = fc;
+      c = b - invphi * (b - a);
+      if (c <= a || c >= d) break;
+      fc = probe(f, c, "minimize_1d");
+    } else {
+      a = c, c = d, fc = fd;
+      d = a + invphi * (b - a);
+      if (d <= c || d >= b) break;
+      fd = probe(f, d, "minimize_1d");
+    }
+  }
+  return fc < fd ? std::make_pair(c, fc) : std::make_pair(d, fd);
+}
+
+// find_root (regparam.cpp:184-214)
+double find_root(const std::function<double(double)>& f, double lo, double hi, double tol) {
+  double flo = probe(f, lo, "find_root"), fhi = probe(f, hi, "find_root");
+  if (!std::isfinite(flo) || !std::isfinite(fhi))
+    throw std::runtime_error("find_root: endpoint value not finite");
+  if (flo == 0.0) return lo;
+  if (fhi == 0.0) return hi;
+  if ((flo > 0.0) == (fhi > 0.0)) throw InvalidArgument("find_root: no sign change over [lo, hi]");
+  double a = lo, b = hi;
+  while (b - a > tol * (1.0 + 0.5 * (std::abs(a) + std::abs(b)))) {
+    const double m = a + 0.5 * (b - a);
+    if (m <= a || m >= b) break;
+    const double fm = probe(f, m, "find_root");
+    if (!std::isfinite(fm)) throw std::runtime_error("find_root: function value not finite");
+    if (fm == 0.0) return m;
+    if ((fm > 0.0) == (flo > 0.0)) {
+      a = m, flo = fm;
+    } else {
+      b = m;
+    }
+  }
+  return a + 0.5 * (b - a);
+}
+
+}  // namespace
+
+// ============================================================================
+// extern "C"
+// ============================================================================
+#define KP_API(...)                                     \
+  try {                                                 \
+    ensure_init();                                      \
+    __VA_ARGS__;                                        \
+    return KP_OK;                                       \
+  } catch (const kp::NoRoot& e) {                       \
+    kp::g_last_error = e.what();                        \
+    return KP_ERR_NO_ROOT;                              \
+  } catch (const kp::CudaError& e) {                    \
+    kp::g_last_error = e.what();                        \
+    return KP_ERR_CUDA;                                 \
+  } catch (const kp::Unsupported& e) {                  \
+    kp::g_last_error = e.what();                        \
+    return KP_ERR_UNSUPPORTED;                          \
+  } catch (const std::invalid_argument& e) {            \
+    kp::g_last_error = e.what();                        \
+    return KP_ERR_INVALID_ARGUMENT;                     \
+  } catch (const std::exception& e) {                   \
+    kp::g_last_error = e.what();                        \
+    return KP_ERR_RUNTIME;                              \
+  }
+
+extern "C" {
+
+const char* kp_last_error(void) { return kp::g_last_error.c_str(); }
+
+int kp_init(int device) {
+  KP_API({
+    Ctx& c = ctx();
+    if (device != c.device) {
+      KP_CUDA(cudaSetDevice(device));
+      if (c.stream) cudaStreamDestroy(c.stream);
+      KP_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      KP_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
+      c.device = device;
+    }
+  })
+}
+int kp_synchronize(void) { KP_API(sync()) }
+int kp_device_alloc(size_t bytes, void** dptr) { KP_API(KP_CUDA(cudaMalloc(dptr, bytes))) }
+int kp_device_free(void* dptr) { KP_API(KP_CUDA(cudaFree(dptr))) }
+int kp_memcpy_h2d(void* dst, const void* src, size_t bytes) {
+  KP_API(KP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx().stream)); sync())
+}
+int kp_memcpy_d2h(void* dst, const void* src, size_t bytes) {
+  KP_API(KP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx().stream)); sync())
+}
+int kp_profile_enable(int on) { KP_API(ctx().profile = on != 0) }
+int kp_profile_reset(void) {
+  KP_API({
+    profile_collect();
+    for (int c = 0; c < KC_COUNT; ++c) ctx().total_ms[c] = 0.0, ctx().count[c] = 0;
+  })
+}
+int kp_profile_read(int cls, double* total_ms, long long* launches) {
+  KP_API({
+    if (cls < 0 || cls >= KC_COUNT) throw InvalidArgument("profile_read: bad class");
+    profile_collect();
+    *total_ms = ctx().total_ms[cls];
+    *launches = ctx().count[cls];
+  })
+}
+long long kp_launch_count(void) { return ctx().launches; }
+
+// ---- operator ------------------------------------------------------------
+int kp_operator_create(int n, int r, const double* row_factors, const double* col_factors,
+                       kp_operator** out) {
+  KP_API({
+    if (r < 1) throw InvalidArgument("KroneckerSum: no terms");
+    if (n < 1 || !row_factors || !col_factors || !out)
+      throw InvalidArgument("KroneckerSum: factor shape mismatch");
+    auto op = std::make_unique<kp_operator>();
+    op->n = n, op->r = r;
+    const size_t tot = size_t(r) * n * n;
+    op->Cs_cm.alloc(tot), op->Cs_cm.upload(col_factors, tot);
+    op->Rr_cm.alloc(tot), op->Rr_cm.upload(row_factors, tot);
+    op->Cs_rm.alloc(tot), op->Rr_rm.alloc(tot);
+    transpose_blocks(op->Cs_cm.p, op->Cs_rm.p, n, r);
+    transpose_blocks(op->Rr_cm.p, op->Rr_rm.p, n, r);
+    op->W.alloc(tot);
+    op->part.alloc(size_t(op_partials_ctas(op.get())) * 4);
+    sync();
+    *out = op.release();
+  })
+}
+int kp_operator_destroy(kp_operator* op) { KP_API(delete op) }
+int kp_operator_info(const kp_operator* op, int* n, int* r) {
+  KP_API({
+    if (!op) throw InvalidArgument("null operator");
+    *n = op->n, *r = op->r;
+  })
+}
+int kp_kronsum_apply(const kp_operator* opc, const double* y, double* out) {
+  KP_API({
+    auto* op = const_cast<kp_operator*>(opc);
+    const size_t nn = size_t(op->n) * op->n;
+    DBuf<double> dy(nn), dz(nn);
+    dy.upload(y, nn);
+    op_apply(op, dy.p, dz.p, false, nullptr, nullptr);
+    dz.download(out, nn);
+    sync();
+  })
+}
+int kp_kronsum_apply_transpose(const kp_operator* opc, const double* y, double* out) {
+  KP_API({
+    auto* op = const_cast<kp_operator*>(opc);
+    const size_t nn = size_t(op->n) * op->n;
+    DBuf<double> dy(nn), dz(nn);
+    dy.upload(y, nn);
+    op_apply(op, dy.p, dz.p, true, nullptr, nullptr);
+    dz.download(out, nn);
+    sync();
+  })
+}
+int kp_normal_matvec(const kp_operator* opc, double lambda, const double* p, double* out) {
+  KP_API({
+    auto* op = const_cast<kp_operator*>(opc);
+    const size_t nn = size_t(op->n) * op->n;
+    DBuf<double> dp(nn), da(nn), dz(nn);
+    dp.upload(p, nn);
+    op_apply(op, dp.p, da.p, false, nullptr, nullptr);
+    F64Epilogue e;
+    e.addv = dp.p, e.addc = lambda * lambda;
+    op_apply(op, da.p, dz.p, true, &e, nullptr);
+    dz.download(out, nn);
+    sync();
+  })
+}
+
+// ---- preconditioner ---------------------------------------------------------
+int kp_precond_build(const double* a_r, const double* a_c, int n, double lambda, kp_format fmt,
+                     int accum, kp_precond** out) {
+  KP_API({
+    if (n < 1 || !a_r || !a_c) throw InvalidArgument("build_preconditioner: factors must be square and equally sized");
+    if (lambda < 0.0) throw InvalidArgument("build_preconditioner: negative lambda");
+    kpla::Svd r = kpla::svd(a_r, n, n);
+    kpla::Svd c = kpla::svd(a_c, n, n);
+    *out = precond_from_svd(n, std::move(r.u), std::move(r.s), std::move(r.v), std::move(c.u),
+                            std::move(c.s), std::move(c.v), lambda, fmt, accum);
+  })
+}
+int kp_precond_build_from_svd(int n, const double* u_r, const double* s_r, const double* v_r,
+                              const double* u_c, const double* s_c, const double* v_c,
+                              double lambda, kp_format fmt, int accum, kp_precond** out) {
+  KP_API({
+    const size_t nn = size_t(n) * n;
+    auto vec = [&](const double* p, size_t k) { return std::vector<double>(p, p + k); };
+    *out = precond_from_svd(n, vec(u_r, nn), vec(s_r, n), vec(v_r, nn), vec(u_c, nn), vec(s_c, n),
+                            vec(v_c, nn), lambda, fmt, accum);
+  })
+}
+int kp_precond_with_lambda(const kp_precond* p, double lambda, kp_precond** out) {
+  KP_API({
+    if (!p) throw InvalidArgument("with_lambda: null preconditioner");
+    if (lambda < 0.0) throw InvalidArgument("with_lambda: negative lambda");
+    auto q = std::make_unique<kp_precond>();
+    q->sh = p->sh, q->n = p->n, q->lambda = lambda, q->fmt = p->fmt, q->accum = p->accum;
+    set_weights(q.get());
+    *out = q.release();
+  })
+}
+int kp_precond_destroy(kp_precond* p) { KP_API(delete p) }
+int kp_precond_solve(const kp_precond* pc, const double* r, double* z) {
+  KP_API({
+    auto* p = const_cast<kp_precond*>(pc);
+    const size_t nn = size_t(p->n) * p->n;
+    DBuf<double> dr(nn), dz(nn);
+    dr.upload(r, nn);
+    if (!covers_double(p->fmt)) cast_r16(p, dr.p, nullptr);
+    msolve(p, dr.p, dz.p, nullptr, nullptr, nullptr, nullptr);
+    dz.download(z, nn);
+    sync();
+  })
+}
+int kp_precond_export(const kp_precond* p, int field, double* out) {
+  KP_API({
+    if (!p) throw InvalidArgument("precond_export: null");
+    const int n = p->n;
+    const size_t nn = size_t(n) * n;
+    auto* sh = p->sh.get();
+    auto put = [&](const std::vector<double>& v) { std::memcpy(out, v.data(), v.size() * sizeof(double)); };
+    auto put_half = [&](const __half* d, long ld, bool transpose_back) {
+      std::vector<__half> h(size_t(n) * ld);
+      KP_CUDA(cudaMemcpyAsync(h.data(), d, h.size() * sizeof(__half), cudaMemcpyDeviceToHost, ctx().stream));
+      sync();
+      for (int a = 0; a < n; ++a)
+        for (int i = 0; i < n; ++i) {
+          const double v = double(__half2float(h[size_t(a) * ld + i]));
+          if (transpose_back) out[size_t(i) * n + a] = v;  // row a holds column a
+          else out[size_t(a) * n + i] = v;
+        }
+    };
+    switch (field) {
+      case 0: put(p->s_weights); break;
+      case 1:
+        if (covers_double(p->fmt)) put(p->s_weights);
+        else put_half(p->s16.p, n, false);
+        break;
+      case 2:
+        if (covers_double(p->fmt)) put(sh->v_r);
+        else put_half(sh->vr_b.p, sh->ldh, false);
+        break;
+      case 3:
+        if (covers_double(p->fmt)) put(sh->v_c);
+        else put_half(sh->vc_a.p, sh->ldh, false);
+        break;
+      case 4: put(sh->s_r); break;
+      case 5: put(sh->s_c); break;
+      case 6: put(sh->u_r); break;
+      case 7: put(sh->v_r); break;
+      case 8: put(sh->u_c); break;
+      case 9: put(sh->v_c); break;
+      default: throw InvalidArgument("precond_export: bad field");
+    }
+    (void)nn;
+  })
+}
+int kp_precond_info(const kp_precond* p, int* n, double* lambda, kp_format* fmt, int* accum) {
+  KP_API({
+    if (!p) throw InvalidArgument("null preconditioner");
+    *n = p->n, *lambda = p->lambda, *fmt = p->fmt, *accum = p->accum;
+  })
+}
+
+// ---- solvers --------------------------------------------------------------------
+int kp_cgls(const kp_operator* op, const double* b, const kp_solver_options* o, double* x,
+            kp_history* h) {
+  KP_API(run_cgls(const_cast<kp_operator*>(op), b, o, x, h))
+}
+int kp_pcg(const kp_operator* op, const double* b, const kp_precond* m, const kp_solver_options* o,
+           double* x, kp_history* h) {
+  KP_API(run_pcg(const_cast<kp_operator*>(op), b, const_cast<kp_precond*>(m), o, x, h, false))
+}
+int kp_fpcg(const kp_operator* op, const double* b, const kp_precond* m,
+            const kp_solver_options* o, double* x, kp_history* h) {
+  KP_API(run_pcg(const_cast<kp_operator*>(op), b, const_cast<kp_precond*>(m), o, x, h, true))
+}
+
+// ---- lambda selection ------------------------------------------------------------
+int kp_spectral_create(const kp_precond* p, const double* b, kp_spectral** out) {
+  KP_API({
+    if (!p || !b) throw InvalidArgument("make_spectral_data: null argument");
+    const int n = p->n;
+    const size_t nn = size_t(n) * n;
+    auto sd = std::make_unique<kp_spectral>();
+    sd->n = n;
+    sd->sh = p->sh;
+    sd->bhat.alloc(nn);
+    DBuf<double> db(nn), t(nn);
+    db.upload(b, nn);
+    F64GemmArgs g;  // b_hat = vec(U_c^T B U_r)  (factor.cpp:157-177)
+    g.M = n, g.N = n, g.nb = 1, g.Kb = n;
+    g.A = {sd->sh->d_u_c.p, n, 0}, g.B = {db.p, n, 0};
+    g.epi.C = t.p, g.epi.cm = n, g.epi.cn = 1;
+    gemm_f64(g, KC_SPECTRAL);
+    g.A = {t.p, n, 0}, g.B = {sd->sh->d_u_r.p, n, 0};
+    g.epi = F64Epilogue{}, g.epi.C = sd->bhat.p, g.epi.cm = 1, g.epi.cn = n;
+    gemm_f64(g, KC_SPECTRAL);
+    sync();
+    const auto& sr = sd->sh->s_r;
+    const auto& sc = sd->sh->s_c;
+    sd->smax = sr[0] * sc[0];
+    sd->smin = std::numeric_limits<double>::infinity();
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) sd->smin = std::min(sd->smin, sr[j] * sc[i]);
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) sd->smax = std::max(sd->smax, sr[j] * sc[i]);
+    *out = sd.release();
+  })
+}
+int kp_spectral_destroy(kp_spectral* sd) { KP_API(delete sd) }
+int kp_spectral_export(const kp_spectral* sd, double* sigma_hat, double* b_hat) {
+  KP_API({
+    const int n = sd->n;
+    const size_t nn = size_t(n) * n;
+    std::vector<double> prod(nn), bh(nn);
+    for (long j = 0; j < n; ++j)
+      for (long i = 0; i < n; ++i) prod[j * n + i] = sd->sh->s_r[j] * sd->sh->s_c[i];
+    sd->bhat.download(bh.data(), nn);
+    sync();
+    std::vector<long> perm(nn);
+    std::iota(perm.begin(), perm.end(), 0L);
+    std::stable_sort(perm.begin(), perm.end(), [&](long a, long b) { return prod[a] > prod[b]; });
+    for (size_t k = 0; k < nn; ++k) {
+      if (sigma_hat) sigma_hat[k] = prod[perm[k]];
+      if (b_hat) b_hat[k] = bh[perm[k]];
+    }
+  })
+}
+int kp_gcv_objective(const kp_spectral* sd, double lambda, double* value) {
+  KP_API(*value = gcv_value(sd, lambda))
+}
+int kp_discrepancy_gap(const kp_spectral* sd, double epsilon, double lambda, double* value) {
+  KP_API(*value = gap_value(sd, epsilon, lambda))
+}
+int kp_gcv_grid(const kp_spectral* sd, const double* lambdas, int m, double* values,
+                kp_param_choice* choice) {
+  KP_API({
+    if (!sd || !lambdas || m < 1) throw InvalidArgument("gcv_grid: bad arguments");
+    std::vector<double> v(m);
+    gcv_values(sd, lambdas, m, v.data());
+    int best = -1;
+    double bv = std::numeric_limits<double>::infinity();
+    for (int q = 0; q < m; ++q) {
+      if (std::isnan(v[q])) throw std::runtime_error("gcv_grid: objective is NaN");
+      if (v[q] < bv) bv = v[q], best = q;
+    }
+    if (best < 0) throw std::runtime_error("gcv_grid: objective infinite everywhere");
+    if (values) std::memcpy(values, v.data(), m * sizeof(double));
+    if (choice) {
+      *choice = kp_param_choice{};
+      choice->lambda = lambdas[best];
+      choice->method = 4;
+      choice->objective_value = bv;
+      choice->bracket_lo = lambdas[0];
+      choice->bracket_hi = lambdas[m - 1];
+      choice->grid_index = best;
+    }
+  })
+}
+// gcv (regparam.cpp:254-258) = run_selector(minimize_log)
+int kp_gcv(const kp_spectral* sd, kp_param_choice* choice) {
+  KP_API({
+    const double lo = std::max(sd->smin, 1e-10 * sd->smax), hi = sd->smax;
+    auto g = [&](double l) { return gcv_value(sd, l); };
+    kp_param_choice c{};
+    c.method = 1, c.bracket_lo = lo, c.bracket_hi = hi, c.grid_index = -1;
+    if (hi <= lo * (1.0 + 1e-12)) {
+      c.lambda = lo, c.objective_value = probe(g, lo, "minimize_log"), c.flat_objective = 1;
+    } else {  // minimize_log (regparam.cpp:54-88), grid evaluated in one batched launch
+      const double ulo = std::log(lo), uhi = std::log(hi);
+      const int grid = 1024;
+      std::vector<double> ls(grid), vs(grid);
+      for (int k = 0; k < grid; ++k) ls[k] = std::exp(ulo + (uhi - ulo) * k / (grid - 1));
+      gcv_values(sd, ls.data(), grid, vs.data());
+      int best_k = -1;
+      double best_v = std::numeric_limits<double>::infinity();
+      double vmin = best_v, vmax = -best_v;
+      for (int k = 0; k < grid; ++k) {
+        const double v = vs[k];
+        if (std::isnan(v)) throw std::runtime_error("minimize_log: objective is NaN");
+        if (!std::isfinite(v)) continue;
+        vmin = std::min(vmin, v), vmax = std::max(vmax, v);
+        if (v < best_v) best_v = v, best_k = k;
+      }
+      if (best_k < 0) throw std::runtime_error("minimize_log: objective infinite everywhere");
+      const double scale = std::max({std::abs(vmin), std::abs(vmax), 1e-300});
+      if (vmax - vmin <= 1e-14 * scale) {
+        const double mid = std::exp(0.5 * (ulo + uhi));
+        c.lambda = mid, c.objective_value = probe(g, mid, "minimize_log"), c.flat_objective = 1;
+      } else {
+        const double step = (uhi - ulo) / (grid - 1);
+        const double a = std::max(ulo, ulo + (best_k - 1) * step);
+        const double b = std::min(uhi, ulo + (best_k + 1) * step);
+        const auto r = minimize_1d([&](double u) { return g(std::exp(u)); }, a, b, 1e-12);
+        c.lambda = std::exp(r.first), c.objective_value = r.second;
+      }
+    }
+    *choice = c;
+  })
+}
+// discrepancy (regparam.cpp:288-327)
+int kp_discrepancy(const kp_spectral* sd, double noise_norm, double eta, kp_param_choice* choice) {
+  KP_API({
+    if (!(noise_norm > 0.0)) throw InvalidArgument("discrepancy: noise_norm must be positive");
+    if (!(eta > 0.0)) throw InvalidArgument("discrepancy: eta must be positive");
+    const double eps = eta * noise_norm;
+    const double lo = 1e-10 * sd->smax, hi = sd->smax;
+    const double glo = gap_value(sd, eps, lo), ghi = gap_value(sd, eps, hi);
+    if (ghi < 0.0)
+      throw NoRoot("no root; eta * noise_norm too large: the residual cannot reach it inside the bracket");
+    if (glo > 0.0)
+      throw NoRoot("no root; eta * noise_norm too small: the residual exceeds it everywhere in the bracket");
+    double lambda;
+    if (glo == 0.0) lambda = lo;
+    else if (ghi == 0.0) lambda = hi;
+    else
+      lambda = std::exp(find_root([&](double u) { return gap_value(sd, eps, std::exp(u)); },
+                                  std::log(lo), std::log(hi), 1e-12));
+    kp_param_choice c{};
+    c.lambda = lambda, c.method = 3, c.eta = eta, c.noise_norm = noise_norm;
+    c.objective_value = gap_value(sd, eps, lambda);
+    c.bracket_lo = lo, c.bracket_hi = hi, c.grid_index = -1;
+    *choice = c;
+  })
+}
+
+}  // extern "C"

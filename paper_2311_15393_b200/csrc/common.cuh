@@ -1,0 +1,100 @@
+// Shared infrastructure for the sm_100a kernels and the C-ABI host layer:
+// library context (device, stream), error capture, per-class launch timing.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace kp {
+
+// Exceptions mapped to the C-ABI status codes (include/kronprec_b200.h).
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct NoRoot : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct Unsupported : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define KP_CUDA(expr)                                                        \
+  do {                                                                       \
+    cudaError_t e_ = (expr);                                                 \
+    if (e_ != cudaSuccess)                                                   \
+      throw ::kp::CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+enum KernelClass { KC_OPERATOR = 0, KC_PRECOND = 1, KC_VECTOR = 2, KC_SPECTRAL = 3, KC_COUNT = 4 };
+
+struct Ctx {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  bool profile = false;
+  long long launches = 0;
+  // timing: event pairs recorded around launches, per kernel class
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[KC_COUNT];
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+  double total_ms[KC_COUNT] = {0, 0, 0, 0};
+  long long count[KC_COUNT] = {0, 0, 0, 0};
+};
+
+Ctx& ctx();            // lazily initialised on first use (device 0)
+void ensure_init();
+void check_launch(const char* what);
+
+// RAII launch bracket: counts the launch and, when profiling, records events.
+struct LaunchScope {
+  int cls;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  explicit LaunchScope(int c);
+  ~LaunchScope() noexcept(false);
+};
+
+// Device buffer with RAII.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    free();
+    if (count) KP_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { free(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    free();
+    p = o.p, n = o.n;
+    o.p = nullptr, o.n = 0;
+    return *this;
+  }
+  void upload(const T* h, size_t count) {
+    KP_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, ctx().stream));
+  }
+  void download(T* h, size_t count) const {
+    KP_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, ctx().stream));
+  }
+};
+
+inline unsigned cdiv(long a, long b) { return unsigned((a + b - 1) / b); }
+
+}  // namespace kp

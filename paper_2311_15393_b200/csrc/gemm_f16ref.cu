@@ -1,0 +1,292 @@
+// Reference-exact binary16 GEMM: C(m,n) = pairwise-tree over k of
+// round16(A(m,k) * B(n,k)), each freshly formed sum rounded once — the value
+// lp_matmul (lpblas.cpp:59-70 + pairwise_block_reduce :13-30) produces,
+// computed per output element instead of materialising the m x (K n) matrix.
+//
+// Arithmetic: explicit mul.rn.f16x2 / add.rn.f16x2 (IEEE binary16, RNE,
+// subnormals kept, no FMA contraction) on the CUDA-core f16x2 pipe — measured
+// 36.9 T half-ops/s on B200 (profiles/r01_microbench_peaks.txt). The tensor
+// pipe cannot be used: it accumulates in fp32 without per-add rounding.
+//
+// Tree bookkeeping: the stage tree of pairwise_block_reduce (adjacent pairs,
+// odd tail carried) equals a binary counter over the leaves whose leftover
+// levels are merged bottom-up at the end. Leaves are consumed in aligned
+// 8-leaf register subtrees, two of which form a 16-leaf value pushed into a
+// per-thread counter stack kept in shared memory (levels >= 4). Padded leaves
+// (k in [K, ld)) are exact -0 products and leave every sum unchanged.
+//
+// Packing: one f16x2 register holds outputs (m, n) and (m, n+16) of the same
+// k, so A is broadcast (PRMT) and all tree adds are vertical.
+#include "gemm_f16ref.cuh"
+
+namespace kp {
+namespace {
+
+constexpr int BM = 32, BN = 64, BKH = 64, THREADS = 128, STAGES = 3;
+constexpr int ROW_BYTES = BKH * 2;  // 128
+constexpr int STAGE_BYTES = (BM + BN) * ROW_BYTES;
+constexpr int NACC = 8;  // 4 m-rows x 2 n-pairs per thread
+constexpr int GROUP_M = 8;
+
+__device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t hadd2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t lows(uint32_t a, uint32_t b) { return __byte_perm(a, b, 0x5410); }
+__device__ __forceinline__ uint32_t highs(uint32_t a, uint32_t b) { return __byte_perm(a, b, 0x7632); }
+__device__ __forceinline__ uint32_t bcast_lo(uint32_t a) { return __byte_perm(a, 0, 0x1010); }
+__device__ __forceinline__ uint32_t bcast_hi(uint32_t a) { return __byte_perm(a, 0, 0x3232); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t part(const uint4& v, int q) {
+  return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
+}
+
+__global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs args, int levels) {
+  if (args.status && *args.status != 0) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t* stack = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES);
+
+  const int M = args.M, N = args.N;
+  const int grid_m = (M + BM - 1) / BM, grid_n = (N + BN - 1) / BN;
+  const int pid = blockIdx.x;
+  const int group = pid / (GROUP_M * grid_n);
+  const int first_m = group * GROUP_M;
+  const int gsize = min(grid_m - first_m, GROUP_M);
+  const int tile_m = first_m + (pid % (GROUP_M * grid_n)) % gsize;
+  const int tile_n = (pid % (GROUP_M * grid_n)) / gsize;
+  const int m_base = tile_m * BM, n_base = tile_n * BN;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tn = lane & 15, tm = warp * 2 + (lane >> 4);
+
+  // K extent actually streamed: whole 64-wide tiles (padding is neutral).
+  const int KT = (args.K + BKH - 1) / BKH;
+  const uint32_t sbase = smem_u32(smem);
+
+  auto load_tile = [&](int kt, int stage) {
+    const uint32_t sa = sbase + uint32_t(stage * STAGE_BYTES);
+    const uint32_t sb = sa + uint32_t(BM * ROW_BYTES);
+    constexpr int CA = BM * 8, CB = BN * 8;
+#pragma unroll
+    for (int id = tid; id < CA + CB; id += THREADS) {
+      const bool isA = id < CA;
+      const int cid = isA ? id : id - CA;
+      const int row = cid >> 3, ch = cid & 7;
+      const int grow = (isA ? m_base : n_base) + row;
+      const bool v = grow < (isA ? M : N);
+      const F16Operand& op = isA ? args.A : args.B;
+      const __half* src = op.p + long(grow) * op.ld + kt * BKH + ch * 8;
+      const uint32_t dst = (isA ? sa : sb) + uint32_t(row * ROW_BYTES + ((ch ^ (row & 7)) << 4));
+      cp_async16(dst, v ? src : op.p, v);
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_tile(s, s);
+    cp_async_commit();
+  }
+
+  uint32_t l3[NACC];
+  int c16 = 0;  // 16-leaf values pushed so far
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < KT) load_tile(nk, nk % STAGES);
+      cp_async_commit();
+    }
+    const uint32_t sa = sbase + uint32_t((kt % STAGES) * STAGE_BYTES);
+    const uint32_t sb = sa + uint32_t(BM * ROW_BYTES);
+#pragma unroll 1
+    for (int sub = 0; sub < 8; ++sub) {  // 8-leaf sub-chunk = one 16-byte smem chunk
+      uint4 af[4], bfr[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = tm + 8 * i;
+        af[i] = lds128(sa + uint32_t(row * ROW_BYTES + ((sub ^ (row & 7)) << 4)));
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int row = tn + 16 * j;
+        bfr[j] = lds128(sb + uint32_t(row * ROW_BYTES + ((sub ^ (row & 7)) << 4)));
+      }
+      uint32_t v8[NACC];
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        uint32_t blo[4], bhi[4];
+#pragma unroll
+        for (int kp = 0; kp < 4; ++kp) {
+          blo[kp] = lows(part(bfr[2 * p], kp), part(bfr[2 * p + 1], kp));
+          bhi[kp] = highs(part(bfr[2 * p], kp), part(bfr[2 * p + 1], kp));
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t s[4];
+#pragma unroll
+          for (int kp = 0; kp < 4; ++kp) {
+            const uint32_t a = part(af[i], kp);
+            const uint32_t p0 = hmul2(bcast_lo(a), blo[kp]);  // leaf k = 2kp
+            const uint32_t p1 = hmul2(bcast_hi(a), bhi[kp]);  // leaf k = 2kp+1
+            s[kp] = hadd2(p0, p1);
+          }
+          v8[i * 2 + p] = hadd2(hadd2(s[0], s[1]), hadd2(s[2], s[3]));
+        }
+      }
+      if ((sub & 1) == 0) {
+#pragma unroll
+        for (int q = 0; q < NACC; ++q) l3[q] = v8[q];
+      } else {
+        uint32_t v[NACC];
+#pragma unroll
+        for (int q = 0; q < NACC; ++q) v[q] = hadd2(l3[q], v8[q]);
+        int L = 0, cnt = c16;
+        while (cnt & 1) {  // uniform across the CTA
+#pragma unroll
+          for (int q = 0; q < NACC; ++q) v[q] = hadd2(stack[(L * NACC + q) * THREADS + tid], v[q]);
+          cnt >>= 1;
+          ++L;
+        }
+#pragma unroll
+        for (int q = 0; q < NACC; ++q) stack[(L * NACC + q) * THREADS + tid] = v[q];
+        ++c16;
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // Bottom-up merge of the leftover counter levels (bits of c16).
+  uint32_t acc[NACC];
+  bool have = false;
+  for (int L = 0; L < levels; ++L) {
+    if (!((c16 >> L) & 1)) continue;
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) {
+      const uint32_t s = stack[(L * NACC + q) * THREADS + tid];
+      acc[q] = have ? hadd2(s, acc[q]) : s;
+    }
+    have = true;
+  }
+  if (!have) {
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) acc[q] = 0x80008000u;  // K == 0 cannot occur (checked)
+  }
+
+  // ---- epilogue ----
+  const F16Epilogue& e = args.epi;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = m_base + tm + 8 * i;
+        const int n = n_base + tn + 32 * p + 16 * h;
+        if (m >= M || n >= N) continue;
+        const uint32_t word = acc[i * 2 + p];
+        const unsigned short bits = h ? (unsigned short)(word >> 16) : (unsigned short)(word & 0xffffu);
+        if (e.mode == F16OUT_HALF) {
+          e.Ch[long(m) * e.cm + long(n) * e.cn] = __ushort_as_half(bits);
+        } else if (e.mode == F16OUT_HALF_SCALED) {
+          const __half sc = e.scale[long(m) * e.sm + long(n) * e.sn];
+          unsigned short r;
+          asm("mul.rn.f16 %0, %1, %2;" : "=h"(r) : "h"(__half_as_ushort(sc)), "h"(bits));
+          e.Ch[long(m) * e.cm + long(n) * e.cn] = __ushort_as_half(r);
+        } else {
+          const double v = double(__half2float(__ushort_as_half(bits)));
+          e.Cd[long(m) * e.cm + long(n) * e.cn] = v;
+          if (e.partials) {
+            const long vi = long(m) * e.vm + long(n) * e.vn;
+            if (e.d0) s0 += v * e.d0[vi];
+            if (e.d1a) s1 += v * (e.d1b ? (e.d1a[vi] - e.d1b[vi]) : e.d1a[vi]);
+            if (!isfinite(v)) s2 += 1.0;
+          }
+        }
+      }
+  if (e.mode == F16OUT_F64 && e.partials) {
+    __shared__ double red[THREADS / 32][3];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, off);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+    }
+    if (lane == 0) red[warp][0] = s0, red[warp][1] = s1, red[warp][2] = s2;
+    __syncthreads();
+    if (tid == 0) {
+      double a0 = 0, a1 = 0, a2 = 0;
+      for (int w = 0; w < THREADS / 32; ++w) a0 += red[w][0], a1 += red[w][1], a2 += red[w][2];
+      double* o = e.partials + long(pid) * 4;
+      o[0] = a0, o[1] = a1, o[2] = a2, o[3] = 0.0;
+    }
+  }
+}
+
+__global__ void fill_u16_kernel(unsigned short* p, size_t n, unsigned short bits) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    p[i] = bits;
+}
+
+}  // namespace
+
+int gemm_f16ref_num_ctas(int M, int N) { return int(cdiv(M, BM) * cdiv(N, BN)); }
+
+void gemm_f16ref(const F16GemmArgs& a, int kernel_class) {
+  if (a.M <= 0 || a.N <= 0) return;
+  if (a.K <= 0) throw InvalidArgument("lp_matmul: empty input");
+  if (a.A.ld % BKH || a.B.ld % BKH || a.A.ld < a.K || a.B.ld < a.K)
+    throw InvalidArgument("gemm_f16ref: operand leading dimension must be a multiple of 64 >= K");
+  const int kt = (a.K + BKH - 1) / BKH;
+  const int c16 = kt * (BKH / 16);
+  int levels = 1;
+  while ((1 << levels) <= c16) ++levels;
+  const size_t smem = size_t(STAGES) * STAGE_BYTES + size_t(levels) * NACC * THREADS * 4;
+  static size_t attr_smem = 0;
+  if (smem > attr_smem) {
+    KP_CUDA(cudaFuncSetAttribute(gemm_f16ref_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem)));
+    attr_smem = smem;
+  }
+  LaunchScope scope(kernel_class);
+  const unsigned grid = cdiv(a.M, BM) * cdiv(a.N, BN);
+  gemm_f16ref_kernel<<<grid, THREADS, smem, ctx().stream>>>(a, levels);
+  check_launch("gemm_f16ref");
+}
+
+void fill_u16(__half* p, size_t count, uint16_t bits) {
+  if (!count) return;
+  LaunchScope scope(KC_VECTOR);
+  const unsigned grid = std::min<unsigned>(cdiv(long(count), 256), 4096u);
+  fill_u16_kernel<<<grid, 256, 0, ctx().stream>>>(reinterpret_cast<unsigned short*>(p), count, bits);
+  check_launch("fill_u16");
+}
+
+}  // namespace kp

@@ -1,0 +1,48 @@
+// Reference-exact binary16 matrix product: the device form of lp_matmul
+// (lpblas.cpp:13-70) for fmt = fp16.
+#pragma once
+
+#include "common.cuh"
+
+namespace kp {
+
+// K-major binary16 operand: element (row, k) at p[row*ld + k]. Requirements
+// (all internal buffers satisfy them): ld % 64 == 0, ld >= K, 16-byte aligned,
+// and the padding columns k in [K, ld) hold -0 for A and +0 for B, so every
+// padded product is exactly -0 — a neutral element of the pairwise tree.
+struct F16Operand {
+  const __half* p = nullptr;
+  long ld = 0;
+};
+
+enum F16OutMode { F16OUT_HALF = 0, F16OUT_HALF_SCALED = 1, F16OUT_F64 = 2 };
+
+struct F16Epilogue {
+  int mode = F16OUT_HALF;
+  __half* Ch = nullptr;  // F16OUT_HALF[_SCALED]: Ch[m*cm + n*cn]
+  double* Cd = nullptr;  // F16OUT_F64:           Cd[m*cm + n*cn]
+  long cm = 1, cn = 0;
+  const __half* scale = nullptr;  // HALF_SCALED: out = round16(scale(m,n) * acc)
+  long sm = 1, sn = 0;
+  // F64 partials (vectors indexed m*vm + n*vn), per CTA at partials[cta*4+q]:
+  // 0: sum out*d0, 1: sum out*(d1a - d1b) (d1b optional), 2: #non-finite.
+  long vm = 1, vn = 0;
+  const double* d0 = nullptr;
+  const double* d1a = nullptr;
+  const double* d1b = nullptr;
+  double* partials = nullptr;
+};
+
+struct F16GemmArgs {
+  int M = 0, N = 0, K = 0;
+  F16Operand A, B;  // C(m,n) = tree_k round16(A(m,k) * B(n,k))
+  F16Epilogue epi;
+  const int* status = nullptr;
+};
+
+int gemm_f16ref_num_ctas(int M, int N);
+void gemm_f16ref(const F16GemmArgs& a, int kernel_class);
+// Fill helper for padded binary16 buffers (bits = 0x8000 for -0, 0 for +0).
+void fill_u16(__half* p, size_t count, uint16_t bits);
+
+}  // namespace kp

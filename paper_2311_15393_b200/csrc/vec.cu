@@ -1,0 +1,557 @@
+// Fused FP64 CG vector kernels (krylov.cpp:58-208), the device-resident
+// solver state machine, and the lambda-selection reductions
+// (regparam.cpp:224-246).
+//
+// Every kernel first reads DevState::status and returns when the solve has
+// stopped, so the host can enqueue iterations without synchronising; the
+// scalar kernels reproduce the reference's check order and abort messages.
+// All reductions use a fixed grid (VEC_CTAS) and fixed-order combination, so
+// results are run-to-run deterministic.
+#include "vec.cuh"
+
+namespace kp {
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// Block-wide sum of NV values per thread; result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double (*red)[NV]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) red[warp][q] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += red[w][q];
+      v[q] = s;
+    }
+  }
+}
+
+// Sum of component q of a [n][4] partials array, fixed order, one block.
+__device__ double sum_partials(const double* part, int n, int q) {
+  __shared__ double red[VEC_THREADS / 32][1];
+  double v[1] = {0.0};
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v[0] += part[size_t(i) * 4 + q];
+  block_sum<1>(v, red);
+  __syncthreads();
+  __shared__ double out;
+  if (threadIdx.x == 0) out = v[0];
+  __syncthreads();
+  return out;
+}
+
+__device__ __forceinline__ bool stopped(const DevState* st) { return st->status != ST_RUNNING; }
+
+// ---------------------------------------------------------------------------
+__global__ void copy_kernel(double* dst, const double* src, size_t n, const int* status) {
+  if (status && *status) return;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void zero_kernel(double* dst, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    dst[i] = 0.0;
+}
+__global__ void dot_partials_kernel(const double* x, const double* y, size_t n, double* part) {
+  __shared__ double red[VEC_THREADS / 32][1];
+  double v[1] = {0.0};
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    v[0] += x[i] * y[i];
+  block_sum<1>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = part + size_t(blockIdx.x) * 4;
+    o[0] = v[0], o[1] = 0.0, o[2] = 0.0, o[3] = 0.0;
+  }
+}
+
+__global__ void cast_f16_kernel(const double* src, __half* dst, int rows, int cols, long ld_src,
+                                long ld_dst, const int* status) {
+  if (status && *status) return;
+  const size_t total = size_t(rows) * cols;
+  for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += size_t(gridDim.x) * blockDim.x) {
+    const size_t l = idx / cols, i = idx % cols;
+    dst[l * ld_dst + i] = __double2half(src[l * ld_src + i]);  // cvt.rn.f16.f64
+  }
+}
+
+// ---------------------------------------------------------------------------
+// PCG (pcg_core, krylov.cpp:58-142)
+__global__ void pcg_init_scalar_kernel(DevState* st, DevHistory h, const double* part_r, int nr,
+                                       const double* part_xt, int nxt) {
+  if (stopped(st)) return;
+  const double rr = sum_partials(part_r, nr, 0);
+  const double xx = st->has_xt ? sum_partials(part_xt, nxt, 0) : 0.0;
+  if (threadIdx.x) return;
+  st->r0 = sqrt(rr);
+  st->xnorm = sqrt(xx);
+  h.resid[0] = st->r0;  // rec.row(0, x = 0, r0)
+  if (st->has_xt) h.relerr[0] = st->xnorm / st->xnorm;
+  st->rows = 1;
+  st->iterations_used = 0;
+  st->k = 1;
+  if (st->r0 == 0.0) st->status = ST_CONVERGED;
+}
+
+__global__ void pcg_init_msolve_scalar_kernel(DevState* st, const double* part_z, int nz) {
+  if (stopped(st)) return;
+  const double rz = sum_partials(part_z, nz, 0);
+  const double bad = sum_partials(part_z, nz, 2);
+  if (threadIdx.x) return;
+  st->msolve_count = 1;
+  if (bad > 0.0) {
+    st->status = ST_ABORTED, st->abort_code = AB_M_NONFINITE_INIT, st->abort_iter = 0;
+    return;
+  }
+  st->rho = rz;
+  if (!isfinite(rz) || rz <= 0.0)
+    st->status = ST_ABORTED, st->abort_code = AB_POSITIVITY_INIT, st->abort_iter = 0;
+}
+
+__global__ void pcg_alpha_scalar_kernel(DevState* st, const double* part, int n) {
+  if (stopped(st)) return;
+  const double pq = sum_partials(part, n, 0);
+  if (threadIdx.x) return;
+  if (!isfinite(pq)) {
+    st->status = ST_ABORTED, st->abort_code = AB_CURV_NONFINITE, st->abort_iter = st->k;
+    return;
+  }
+  if (pq <= 0.0) {
+    st->status = ST_ABORTED, st->abort_code = AB_CURV_BREAKDOWN, st->abort_iter = st->k;
+    return;
+  }
+  st->alpha = st->rho / pq;
+}
+
+__global__ void pcg_update_kernel(const DevState* st, DevHistory h, double* x, double* r,
+                                  double* r_prev, const double* p, const double* q,
+                                  const double* z, const double* xt, __half* r16, int n,
+                                  long ldh, double* part) {
+  if (stopped(st)) return;
+  __shared__ double red[VEC_THREADS / 32][4];
+  const double alpha = st->alpha;
+  const bool has_xt = st->has_xt, cos = st->track_cos;
+  double* it = (st->record && h.iterates) ? h.iterates + size_t(st->rows) * n * n : nullptr;
+  const size_t nn = size_t(n) * n;
+  double v[4] = {0.0, 0.0, 0.0, 0.0};
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const double ri = r[i];
+    if (r_prev) r_prev[i] = ri;
+    const double xi = x[i] + alpha * p[i];
+    const double rn = ri - alpha * q[i];
+    x[i] = xi;
+    r[i] = rn;
+    if (it) it[i] = xi;
+    if (r16) r16[(i / n) * ldh + (i % n)] = __double2half(rn);
+    v[0] += rn * rn;
+    if (has_xt) {
+      const double d = xi - xt[i];
+      v[1] += d * d;
+    }
+    if (cos) {
+      const double zi = z[i];
+      v[2] += rn * zi;
+      v[3] += zi * zi;
+    }
+  }
+  block_sum<4>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = part + size_t(blockIdx.x) * 4;
+    o[0] = v[0], o[1] = v[1], o[2] = v[2], o[3] = v[3];
+  }
+}
+
+__global__ void pcg_resid_scalar_kernel(DevState* st, DevHistory h, const double* part, int n) {
+  if (stopped(st)) return;
+  const double rr = sum_partials(part, n, 0);
+  const double ee = st->has_xt ? sum_partials(part, n, 1) : 0.0;
+  const double rz = st->track_cos ? sum_partials(part, n, 2) : 0.0;
+  const double zz = st->track_cos ? sum_partials(part, n, 3) : 0.0;
+  if (threadIdx.x) return;
+  const int k = st->k;
+  const double rnorm = sqrt(rr);
+  if (!isfinite(rnorm)) {
+    st->status = ST_ABORTED, st->abort_code = AB_RESID_NONFINITE, st->abort_iter = k;
+    return;
+  }
+  if (st->track_cos) {  // rec.cosine(r, z) (krylov.cpp:40-46)
+    const double denom = rnorm * sqrt(zz);
+    if (h.cosines) h.cosines[st->ncos] = denom > 0.0 ? fabs(rz) / denom : 0.0;
+    st->ncos++;
+  }
+  const int row = st->rows;
+  h.resid[row] = rnorm;
+  if (st->has_xt) h.relerr[row] = sqrt(ee) / st->xnorm;
+  st->rows = row + 1;
+  st->iterations_used = k;
+  if (rnorm <= st->tol * st->r0) {
+    st->status = ST_CONVERGED;
+    return;
+  }
+  if (k == st->maxit) st->status = ST_MAXIT;
+}
+
+__global__ void pcg_beta_scalar_kernel(DevState* st, const double* part, int n) {
+  if (stopped(st)) return;
+  const double rz = sum_partials(part, n, 0);
+  const double zdr = sum_partials(part, n, 1);
+  const double bad = sum_partials(part, n, 2);
+  if (threadIdx.x) return;
+  const int k = st->k;
+  st->msolve_count++;
+  if (bad > 0.0) {
+    st->status = ST_ABORTED, st->abort_code = AB_M_NONFINITE, st->abort_iter = k;
+    return;
+  }
+  const double beta = st->flexible ? zdr / st->rho : rz / st->rho;
+  if (!isfinite(beta) || !isfinite(rz)) {
+    st->status = ST_ABORTED, st->abort_code = AB_INNER_NONFINITE, st->abort_iter = k;
+    return;
+  }
+  st->beta = beta;
+  st->rz = rz;
+}
+
+// p = z + beta p, then rho = rz with the positivity check (krylov.cpp:133-138)
+__global__ void pcg_p_update_kernel(DevState* st, double* p, const double* z, size_t nn) {
+  if (stopped(st)) return;
+  const double beta = st->beta;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
+       i += size_t(gridDim.x) * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+}
+__global__ void pcg_rho_scalar_kernel(DevState* st) {
+  if (stopped(st) || threadIdx.x) return;
+  st->rho = st->rz;
+  if (st->rho <= 0.0) {
+    st->status = ST_ABORTED, st->abort_code = AB_POSITIVITY, st->abort_iter = st->k;
+    return;
+  }
+  st->k++;
+}
+
+// ---------------------------------------------------------------------------
+// CGLS (krylov.cpp:154-208)
+__global__ void cgls_init_scalar_kernel(DevState* st, DevHistory h, const double* part_s, int ns,
+                                        const double* part_xt, int nxt) {
+  if (stopped(st)) return;
+  const double ss = sum_partials(part_s, ns, 0);
+  const double xx = st->has_xt ? sum_partials(part_xt, nxt, 0) : 0.0;
+  if (threadIdx.x) return;
+  st->r0 = sqrt(ss);
+  st->xnorm = sqrt(xx);
+  h.resid[0] = st->r0;
+  if (st->has_xt) h.relerr[0] = st->xnorm / st->xnorm;
+  st->rows = 1;
+  st->iterations_used = 0;
+  st->k = 1;
+  st->gamma = ss;   // gamma = s.squaredNorm()
+  st->pnorm2 = ss;  // p = s
+  st->snorm_prev = st->r0;
+  if (st->r0 == 0.0) st->status = ST_CONVERGED;
+}
+
+__global__ void cgls_alpha_scalar_kernel(DevState* st, const double* part_q, int nq,
+                                         const double* part_p, int np) {
+  if (stopped(st)) return;
+  const double qq = sum_partials(part_q, nq, 0);
+  const double pp = (st->k > 1) ? sum_partials(part_p, np, 0) : 0.0;
+  if (threadIdx.x) return;
+  if (st->k > 1) st->pnorm2 = pp;
+  const double delta = qq + st->l2 * st->pnorm2;
+  if (!isfinite(delta)) {
+    st->status = ST_ABORTED, st->abort_code = AB_CURV_NONFINITE, st->abort_iter = st->k;
+    return;
+  }
+  if (delta == 0.0) {
+    st->status = ST_ABORTED, st->abort_code = AB_CURV_BREAKDOWN, st->abort_iter = st->k;
+    return;
+  }
+  st->alpha = st->gamma / delta;
+}
+
+__global__ void cgls_update_kernel(const DevState* st, DevHistory h, double* x, double* rt,
+                                   const double* p, const double* q, const double* xt, size_t nn,
+                                   double* part) {
+  if (stopped(st)) return;
+  __shared__ double red[VEC_THREADS / 32][1];
+  const double alpha = st->alpha;
+  const bool has_xt = st->has_xt;
+  double* it = (st->record && h.iterates) ? h.iterates + size_t(st->rows) * nn : nullptr;
+  double v[1] = {0.0};
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const double xi = x[i] + alpha * p[i];
+    x[i] = xi;
+    rt[i] = rt[i] - alpha * q[i];
+    if (it) it[i] = xi;
+    if (has_xt) {
+      const double d = xi - xt[i];
+      v[0] += d * d;
+    }
+  }
+  block_sum<1>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = part + size_t(blockIdx.x) * 4;
+    o[0] = 0.0, o[1] = v[0], o[2] = 0.0, o[3] = 0.0;
+  }
+}
+
+// part_s from the s = A^T rt - l2 x GEMM epilogue: [0] ||s||^2, [1] s.s_prev
+__global__ void cgls_resid_scalar_kernel(DevState* st, DevHistory h, const double* part_s, int ns,
+                                         const double* part_x, int nx) {
+  if (stopped(st)) return;
+  const double ss = sum_partials(part_s, ns, 0);
+  const double sp = st->track_cos ? sum_partials(part_s, ns, 1) : 0.0;
+  const double ee = st->has_xt ? sum_partials(part_x, nx, 1) : 0.0;
+  if (threadIdx.x) return;
+  const int k = st->k;
+  const double snorm = sqrt(ss);
+  if (!isfinite(snorm)) {
+    st->status = ST_ABORTED, st->abort_code = AB_RESID_NONFINITE, st->abort_iter = k;
+    return;
+  }
+  if (st->track_cos) {  // rec.cosine(snew, s_prev)
+    const double denom = snorm * st->snorm_prev;
+    if (h.cosines) h.cosines[st->ncos] = denom > 0.0 ? fabs(sp) / denom : 0.0;
+    st->ncos++;
+  }
+  const int row = st->rows;
+  h.resid[row] = snorm;
+  if (st->has_xt) h.relerr[row] = sqrt(ee) / st->xnorm;
+  st->rows = row + 1;
+  st->iterations_used = k;
+  if (snorm <= st->tol * st->r0) {
+    st->status = ST_CONVERGED;
+    return;
+  }
+  const double beta = ss / st->gamma;
+  st->beta = beta;
+  st->gamma = ss;
+  st->snorm_prev = snorm;
+  if (k == st->maxit) {
+    st->status = ST_MAXIT;
+    return;
+  }
+}
+
+__global__ void cgls_p_update_kernel(DevState* st, double* p, const double* s, double* s_prev,
+                                     size_t nn, double* part) {
+  if (stopped(st)) return;
+  __shared__ double red[VEC_THREADS / 32][1];
+  const double beta = st->beta;
+  double v[1] = {0.0};
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const double si = s[i];
+    const double pi = si + beta * p[i];
+    p[i] = pi;
+    if (s_prev) s_prev[i] = si;
+    v[0] += pi * pi;
+  }
+  block_sum<1>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = part + size_t(blockIdx.x) * 4;
+    o[0] = v[0], o[1] = 0.0, o[2] = 0.0, o[3] = 0.0;
+  }
+}
+__global__ void cgls_next_kernel(DevState* st) {
+  if (stopped(st) || threadIdx.x) return;
+  st->k++;
+}
+
+// ---------------------------------------------------------------------------
+// Spectral sums. sigma(i,j) = s_r[j] * s_c[i] at linear index j*n + i.
+constexpr int LCHUNK = 16;
+
+__global__ void gcv_sums_kernel(const double* s_r, const double* s_c, const double* bhat, int n,
+                                const double* lambdas, int m, double* part) {
+  __shared__ double red[VEC_THREADS / 32][2 * LCHUNK];
+  const size_t nn = size_t(n) * n;
+  for (int q0 = 0; q0 < m; q0 += LCHUNK) {
+    double l2[LCHUNK];
+    double v[2 * LCHUNK];
+#pragma unroll
+    for (int c = 0; c < LCHUNK; ++c) {
+      const double l = (q0 + c < m) ? lambdas[q0 + c] : 1.0;
+      l2[c] = l * l;
+      v[2 * c] = 0.0, v[2 * c + 1] = 0.0;
+    }
+    for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < nn;
+         idx += size_t(gridDim.x) * blockDim.x) {
+      const double s = s_r[idx / n] * s_c[idx % n];
+      const double s2 = s * s, b = bhat[idx];
+#pragma unroll
+      for (int c = 0; c < LCHUNK; ++c) {
+        const double d = s2 + l2[c];
+        const double t = b / d;
+        v[2 * c] += t * t;
+        v[2 * c + 1] += 1.0 / d;
+      }
+    }
+    block_sum<2 * LCHUNK>(v, red);
+    if (threadIdx.x == 0)
+      for (int c = 0; c < LCHUNK && q0 + c < m; ++c) {
+        part[(size_t(q0 + c) * gridDim.x + blockIdx.x) * 2 + 0] = v[2 * c];
+        part[(size_t(q0 + c) * gridDim.x + blockIdx.x) * 2 + 1] = v[2 * c + 1];
+      }
+    __syncthreads();
+  }
+}
+
+__global__ void resid_sums_kernel(const double* s_r, const double* s_c, const double* bhat, int n,
+                                  const double* lambdas, int m, double* part) {
+  __shared__ double red[VEC_THREADS / 32][LCHUNK];
+  const size_t nn = size_t(n) * n;
+  for (int q0 = 0; q0 < m; q0 += LCHUNK) {
+    double l2[LCHUNK];
+    double v[LCHUNK];
+#pragma unroll
+    for (int c = 0; c < LCHUNK; ++c) {
+      const double l = (q0 + c < m) ? lambdas[q0 + c] : 1.0;
+      l2[c] = l * l;
+      v[c] = 0.0;
+    }
+    for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < nn;
+         idx += size_t(gridDim.x) * blockDim.x) {
+      const double s = s_r[idx / n] * s_c[idx % n];
+      const double s2 = s * s, b = bhat[idx];
+#pragma unroll
+      for (int c = 0; c < LCHUNK; ++c) {
+        const double t = l2[c] * b / (s2 + l2[c]);
+        v[c] += t * t;
+      }
+    }
+    block_sum<LCHUNK>(v, red);
+    if (threadIdx.x == 0)
+      for (int c = 0; c < LCHUNK && q0 + c < m; ++c)
+        part[size_t(q0 + c) * gridDim.x + blockIdx.x] = v[c];
+    __syncthreads();
+  }
+}
+
+// out[q*stride_out + j] = sum over ctas of part[(q*ctas + cta)*width + j]
+__global__ void finish_sums_kernel(const double* part, int ctas, int width, int m, double* out) {
+  const int q = blockIdx.x;
+  if (q >= m) return;
+  for (int j = threadIdx.x; j < width; j += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < ctas; ++c) s += part[(size_t(q) * ctas + c) * width + j];
+    out[size_t(q) * width + j] = s;
+  }
+}
+
+unsigned vec_grid(size_t nn) {
+  return unsigned(std::min<size_t>(VEC_CTAS, std::max<size_t>(1, (nn + VEC_THREADS - 1) / VEC_THREADS)));
+}
+
+}  // namespace
+
+// Host wrappers. The vector kernels always use VEC_CTAS CTAs (fixed
+// reduction order); the CTAs beyond the data simply contribute zero.
+#define KP_LAUNCH(cls, kernel, grid, block, ...)                   \
+  do {                                                             \
+    LaunchScope scope_(cls);                                       \
+    kernel<<<(grid), (block), 0, ctx().stream>>>(__VA_ARGS__);     \
+    check_launch(#kernel);                                         \
+  } while (0)
+
+void vec_copy(double* dst, const double* src, size_t n, const int* status) {
+  KP_LAUNCH(KC_VECTOR, copy_kernel, vec_grid(n), VEC_THREADS, dst, src, n, status);
+}
+void vec_zero(double* dst, size_t n) {
+  KP_LAUNCH(KC_VECTOR, zero_kernel, vec_grid(n), VEC_THREADS, dst, n);
+}
+void vec_dot_partials(const double* x, const double* y, size_t n, double* partials) {
+  KP_LAUNCH(KC_VECTOR, dot_partials_kernel, VEC_CTAS, VEC_THREADS, x, y, n, partials);
+}
+void cast_f64_to_f16_padded(const double* src, __half* dst, int rows, int cols, long ld_src,
+                            long ld_dst, const int* status) {
+  KP_LAUNCH(KC_VECTOR, cast_f16_kernel, vec_grid(size_t(rows) * cols), VEC_THREADS, src, dst,
+            rows, cols, ld_src, ld_dst, status);
+}
+
+void pcg_init_scalar(DevState* st, DevHistory h, const double* part_r, int nr,
+                     const double* part_xt, int nxt) {
+  KP_LAUNCH(KC_VECTOR, pcg_init_scalar_kernel, 1, VEC_THREADS, st, h, part_r, nr, part_xt, nxt);
+}
+void pcg_init_msolve_scalar(DevState* st, const double* part_z, int nz) {
+  KP_LAUNCH(KC_VECTOR, pcg_init_msolve_scalar_kernel, 1, VEC_THREADS, st, part_z, nz);
+}
+void pcg_alpha_scalar(DevState* st, const double* part_pq, int n) {
+  KP_LAUNCH(KC_VECTOR, pcg_alpha_scalar_kernel, 1, VEC_THREADS, st, part_pq, n);
+}
+void pcg_update(DevState* st, DevHistory h, double* x, double* r, double* r_prev, const double* p,
+                const double* q, const double* z, const double* xt, __half* r16, int n, long ldh,
+                double* partials) {
+  KP_LAUNCH(KC_VECTOR, pcg_update_kernel, VEC_CTAS, VEC_THREADS, st, h, x, r, r_prev, p, q, z, xt,
+            r16, n, ldh, partials);
+}
+void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n) {
+  KP_LAUNCH(KC_VECTOR, pcg_resid_scalar_kernel, 1, VEC_THREADS, st, h, part, n);
+}
+void pcg_beta_scalar(DevState* st, const double* part_z, int n) {
+  KP_LAUNCH(KC_VECTOR, pcg_beta_scalar_kernel, 1, VEC_THREADS, st, part_z, n);
+}
+void pcg_p_update(DevState* st, double* p, const double* z, size_t nn) {
+  KP_LAUNCH(KC_VECTOR, pcg_p_update_kernel, vec_grid(nn), VEC_THREADS, st, p, z, nn);
+  KP_LAUNCH(KC_VECTOR, pcg_rho_scalar_kernel, 1, 32, st);
+}
+
+void cgls_init_scalar(DevState* st, DevHistory h, const double* part_s, int ns,
+                      const double* part_xt, int nxt) {
+  KP_LAUNCH(KC_VECTOR, cgls_init_scalar_kernel, 1, VEC_THREADS, st, h, part_s, ns, part_xt, nxt);
+}
+void cgls_alpha_scalar(DevState* st, const double* part_q, int nq, const double* part_p, int np) {
+  KP_LAUNCH(KC_VECTOR, cgls_alpha_scalar_kernel, 1, VEC_THREADS, st, part_q, nq, part_p, np);
+}
+void cgls_update(DevState* st, DevHistory h, double* x, double* rt, const double* p,
+                 const double* q, const double* xt, size_t nn, double* partials) {
+  KP_LAUNCH(KC_VECTOR, cgls_update_kernel, VEC_CTAS, VEC_THREADS, st, h, x, rt, p, q, xt, nn,
+            partials);
+}
+void cgls_resid_scalar(DevState* st, DevHistory h, const double* part_s, int ns,
+                       const double* part_x, int nx) {
+  KP_LAUNCH(KC_VECTOR, cgls_resid_scalar_kernel, 1, VEC_THREADS, st, h, part_s, ns, part_x, nx);
+}
+void cgls_p_update(DevState* st, double* p, const double* s, double* s_prev, size_t nn,
+                   double* partials) {
+  KP_LAUNCH(KC_VECTOR, cgls_p_update_kernel, VEC_CTAS, VEC_THREADS, st, p, s, s_prev, nn,
+            partials);
+  KP_LAUNCH(KC_VECTOR, cgls_next_kernel, 1, 32, st);
+}
+
+void spectral_gcv_sums(const double* s_r, const double* s_c, const double* bhat, int n,
+                       const double* lambdas, int m, double* out) {
+  DBuf<double> part(size_t(m) * VEC_CTAS * 2);
+  KP_LAUNCH(KC_SPECTRAL, gcv_sums_kernel, VEC_CTAS, VEC_THREADS, s_r, s_c, bhat, n, lambdas, m,
+            part.p);
+  KP_LAUNCH(KC_SPECTRAL, finish_sums_kernel, m, 32, part.p, VEC_CTAS, 2, m, out);
+  KP_CUDA(cudaStreamSynchronize(ctx().stream));
+}
+void spectral_resid_sums(const double* s_r, const double* s_c, const double* bhat, int n,
+                         const double* lambdas, int m, double* out) {
+  DBuf<double> part(size_t(m) * VEC_CTAS);
+  KP_LAUNCH(KC_SPECTRAL, resid_sums_kernel, VEC_CTAS, VEC_THREADS, s_r, s_c, bhat, n, lambdas, m,
+            part.p);
+  KP_LAUNCH(KC_SPECTRAL, finish_sums_kernel, m, 32, part.p, VEC_CTAS, 1, m, out);
+  KP_CUDA(cudaStreamSynchronize(ctx().stream));
+}
+
+}  // namespace kp

@@ -1,0 +1,104 @@
+// Fused FP64 CG vector kernels, the device-resident solver state machine and
+// the spectral (lambda-selection) reductions.
+#pragma once
+
+#include "common.cuh"
+
+namespace kp {
+
+// Solver status values (DevState::status).
+enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_ABORTED = 2, ST_MAXIT = 3 };
+// Abort codes -> reference messages (krylov.cpp:75-139, 175-194).
+enum {
+  AB_NONE = 0,
+  AB_M_NONFINITE_INIT = 1,   // "non-finite preconditioner output before iteration 1"
+  AB_POSITIVITY_INIT = 2,    // "preconditioner lost positivity before iteration 1"
+  AB_CURV_NONFINITE = 3,     // "non-finite curvature at iteration k"
+  AB_CURV_BREAKDOWN = 4,     // "curvature breakdown at iteration k"
+  AB_RESID_NONFINITE = 5,    // "non-finite residual at iteration k"
+  AB_M_NONFINITE = 6,        // "non-finite preconditioner output at iteration k (overflow ...)"
+  AB_INNER_NONFINITE = 7,    // "non-finite inner product at iteration k"
+  AB_POSITIVITY = 8,         // "preconditioner lost positivity at iteration k"
+};
+
+struct DevState {
+  int status;
+  int k;  // iteration being executed (1-based)
+  int abort_code;
+  int abort_iter;
+  int msolve_count;
+  int iterations_used;
+  int rows;
+  int ncos;
+  int maxit;
+  int flexible;
+  int track_cos;
+  int has_xt;
+  int record;
+  int pad0;
+  double tol, l2, work_per_iter;
+  double r0, xnorm, rho, alpha, beta, gamma, pnorm2, rz, snorm_prev;
+};
+
+// History arrays on device (capacity rows).
+struct DevHistory {
+  double* resid;
+  double* relerr;
+  double* cosines;
+  double* iterates;  // capacity * nn, optional
+  int capacity;
+};
+
+// Partial-sum buffers are [ctas][4] doubles.
+constexpr int VEC_CTAS = 296;   // fixed grid of the vector kernels (2 x 148 SMs)
+constexpr int VEC_THREADS = 256;
+
+// ---- generic helpers -------------------------------------------------------
+void vec_copy(double* dst, const double* src, size_t n, const int* status);
+void vec_zero(double* dst, size_t n);
+// partials[cta*4+0] = sum x*y over a fixed 296-CTA grid
+void vec_dot_partials(const double* x, const double* y, size_t n, double* partials);
+// dst16[l*ldh + i] = round16(src[l*n + i]) (RNE binary16, overflow -> inf)
+void cast_f64_to_f16_padded(const double* src, __half* dst, int rows, int cols, long ld_src,
+                            long ld_dst, const int* status);
+
+// ---- PCG -------------------------------------------------------------------
+// init after r = A^T b (partials_r: [ctas] of ||r||^2) and xnorm partials.
+void pcg_init_scalar(DevState* st, DevHistory h, const double* part_r, int nr,
+                     const double* part_xt, int nxt);
+// after first M-solve (partials: [0]=r.z, [2]=#nonfinite)
+void pcg_init_msolve_scalar(DevState* st, const double* part_z, int nz);
+void pcg_alpha_scalar(DevState* st, const double* part_pq, int n);
+// x += a p; r -= a q; [r_prev = r]; R16 = round16(r); partials:
+// [0] ||r||^2, [1] ||x - xt||^2, [2] r.z, [3] ||z||^2
+void pcg_update(DevState* st, DevHistory h, double* x, double* r, double* r_prev,
+                const double* p, const double* q, const double* z, const double* xt, __half* r16,
+                int n, long ldh, double* partials);
+void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n);
+void pcg_beta_scalar(DevState* st, const double* part_z, int n);
+// p = z + beta p
+void pcg_p_update(DevState* st, double* p, const double* z, size_t nn);
+
+// ---- CGLS ------------------------------------------------------------------
+void cgls_init_scalar(DevState* st, DevHistory h, const double* part_s, int ns,
+                      const double* part_xt, int nxt);
+void cgls_alpha_scalar(DevState* st, const double* part_q, int nq, const double* part_p, int np);
+// x += a p; rt -= a q; partials [1] ||x - xt||^2
+void cgls_update(DevState* st, DevHistory h, double* x, double* rt, const double* p,
+                 const double* q, const double* xt, size_t nn, double* partials);
+void cgls_resid_scalar(DevState* st, DevHistory h, const double* part_s, int ns,
+                       const double* part_x, int nx);
+// p = s + beta p; [s_prev = s]; partials [0] ||p||^2
+void cgls_p_update(DevState* st, double* p, const double* s, double* s_prev, size_t nn,
+                   double* partials);
+
+// ---- spectral ----------------------------------------------------------------
+// For each lambda_q: num_q = sum (bhat/d)^2, den_q = sum 1/d, d = sigma^2 +
+// lambda^2, sigma(i,j) = s_r[j] s_c[i]. out[q*2+{0,1}] (device).
+void spectral_gcv_sums(const double* s_r, const double* s_c, const double* bhat, int n,
+                       const double* lambdas, int m, double* out);
+// out[q] = sum (lambda^2 bhat / d)^2 for each lambda_q (device).
+void spectral_resid_sums(const double* s_r, const double* s_c, const double* bhat, int n,
+                         const double* lambdas, int m, double* out);
+
+}  // namespace kp

@@ -1,0 +1,515 @@
+"""Host-side mirror of the reference ``kronprec`` solver API for the hot path.
+
+Same names, argument meaning and error behaviour as the reference C++
+headers (/root/reference/proj/include/kronprec/*.hpp), with numpy
+column-major arrays in place of Eigen matrices. Every compute call goes
+through the C ABI (include/kronprec_b200.h) into the sm_100a kernels.
+
+Exceptions: std::invalid_argument -> ValueError, std::runtime_error ->
+RuntimeError, kronprec::NoRootError -> NoRootError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import re
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import (KP_ACCUM_REFERENCE, KP_ACCUM_TENSOR, NoRootError, check, f64, kp_format,
+                   kp_history, kp_param_choice, kp_solver_options, lib, ptr)
+
+__all__ = [
+    "PrecisionFormat", "KronTerm", "KroneckerSum", "vec", "unvec", "kronsum_apply",
+    "kronsum_apply_transpose", "normal_matvec", "KronSvdPreconditioner",
+    "build_preconditioner", "build_preconditioner_from_svd", "with_lambda", "precond_solve",
+    "SolverOptions", "ConvergenceHistory", "SolveResult", "cgls", "pcg", "fpcg",
+    "plateau_iteration", "WorkReport", "work_report", "SpectralData", "make_spectral_data",
+    "ParamChoice", "gcv_objective", "discrepancy_gap", "gcv", "gcv_grid", "discrepancy",
+    "NoRootError",
+]
+
+
+# ---------------------------------------------------------------------------
+# precision.hpp:14-37
+@dataclass(frozen=True)
+class PrecisionFormat:
+    significand_bits: int = 53
+    max_exponent: int = 1023
+    subnormals_enabled: bool = True
+    name: str = "fp64"
+
+    @staticmethod
+    def fp16() -> "PrecisionFormat":
+        return PrecisionFormat(11, 15, True, "fp16")
+
+    @staticmethod
+    def bfloat16() -> "PrecisionFormat":
+        return PrecisionFormat(8, 127, True, "bfloat16")
+
+    @staticmethod
+    def fp32() -> "PrecisionFormat":
+        return PrecisionFormat(24, 127, True, "fp32")
+
+    @staticmethod
+    def fp64() -> "PrecisionFormat":
+        return PrecisionFormat(53, 1023, True, "fp64")
+
+    @staticmethod
+    def parse(text: str) -> "PrecisionFormat":  # precision.cpp:50-63
+        presets = {"fp16": PrecisionFormat.fp16, "bfloat16": PrecisionFormat.bfloat16,
+                   "fp32": PrecisionFormat.fp32, "fp64": PrecisionFormat.fp64}
+        if text in presets:
+            return presets[text]()
+        m = re.fullmatch(r"custom:t=(-?\d+),emax=(-?\d+),subnormals=(-?\d+)", text)
+        if m:
+            t, e, s = (int(g) for g in m.groups())
+            if t >= 2 and e >= 1 and s in (0, 1):
+                return PrecisionFormat(t, e, s == 1, text)
+        raise ValueError(f"unknown precision format: {text}")
+
+    def unit_roundoff(self) -> float:
+        return math.ldexp(1.0, -self.significand_bits)
+
+    def max_finite(self) -> float:
+        return math.ldexp(2.0 - math.ldexp(1.0, 1 - self.significand_bits), self.max_exponent)
+
+    def overflow_threshold(self) -> float:
+        return math.ldexp(2.0 - math.ldexp(1.0, -self.significand_bits), self.max_exponent)
+
+    def min_exponent(self) -> int:
+        return 1 - self.max_exponent
+
+    def covers_double(self) -> bool:
+        return self.significand_bits >= 53 and self.max_exponent >= 1023 and self.subnormals_enabled
+
+    def c(self) -> kp_format:
+        return kp_format(self.significand_bits, self.max_exponent, int(self.subnormals_enabled))
+
+
+# ---------------------------------------------------------------------------
+# kron.hpp:9-35
+def vec(y: np.ndarray) -> np.ndarray:
+    """Column stacking (kron.cpp:52-55)."""
+    return np.asarray(y, dtype=np.float64).reshape(-1, order="F").copy()
+
+
+def unvec(y: np.ndarray, n: int) -> np.ndarray:
+    y = np.asarray(y, dtype=np.float64)
+    if y.size != n * n:
+        raise ValueError("unvec: length is not n^2")
+    return y.reshape(n, n, order="F").copy()
+
+
+@dataclass
+class KronTerm:
+    row_factor: np.ndarray
+    col_factor: np.ndarray
+
+
+class KroneckerSum:
+    """A = sum_k row_factor_k (x) col_factor_k; device copy created lazily."""
+
+    def __init__(self, terms: list[KronTerm], n: int):
+        self.terms = list(terms)
+        self.n = int(n)
+        self._h = None
+
+    def _check(self) -> None:  # kron.cpp:12-20
+        if not self.terms:
+            raise ValueError("KroneckerSum: no terms")
+        for t in self.terms:
+            if np.shape(t.row_factor) != (self.n, self.n) or np.shape(t.col_factor) != (self.n, self.n):
+                raise ValueError("KroneckerSum: factor shape mismatch")
+
+    def handle(self) -> int:
+        if self._h is None:
+            self._check()
+            r = len(self.terms)
+            rows = np.empty((self.n, self.n * r), order="F")
+            cols = np.empty((self.n, self.n * r), order="F")
+            for k, t in enumerate(self.terms):
+                rows[:, k * self.n:(k + 1) * self.n] = t.row_factor
+                cols[:, k * self.n:(k + 1) * self.n] = t.col_factor
+            h = C.c_void_p()
+            check(lib().kp_operator_create(self.n, r, ptr(rows), ptr(cols), C.byref(h)))
+            self._h = h
+        return self._h
+
+    def release(self) -> None:
+        if self._h is not None:
+            lib().kp_operator_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+def _vec_arg(a, n: int, who: str) -> np.ndarray:
+    v = np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1, order="F"))
+    if v.size != n * n:
+        raise ValueError(f"{who}: vector length is not n^2")
+    return v
+
+
+def kronsum_apply(k: KroneckerSum, y) -> np.ndarray:  # kron.cpp:73-79
+    k._check()
+    y = _vec_arg(y, k.n, "kronsum_apply")
+    out = np.empty_like(y)
+    check(lib().kp_kronsum_apply(k.handle(), ptr(y), ptr(out)))
+    return out
+
+
+def kronsum_apply_transpose(k: KroneckerSum, y) -> np.ndarray:  # kron.cpp:81-88
+    k._check()
+    y = _vec_arg(y, k.n, "kronsum_apply_transpose")
+    out = np.empty_like(y)
+    check(lib().kp_kronsum_apply_transpose(k.handle(), ptr(y), ptr(out)))
+    return out
+
+
+def normal_matvec(a: KroneckerSum, lambda_: float, p) -> np.ndarray:  # krylov.cpp:146-152
+    p = np.ascontiguousarray(np.asarray(p, dtype=np.float64).reshape(-1))
+    if p.size != a.n * a.n:
+        raise ValueError("normal_matvec: length mismatch")
+    out = np.empty_like(p)
+    check(lib().kp_normal_matvec(a.handle(), float(lambda_), ptr(p), ptr(out)))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# factor.hpp:42-71
+@dataclass
+class SvdTriple:
+    u: np.ndarray
+    s: np.ndarray
+    v: np.ndarray
+
+
+class KronSvdPreconditioner:
+    """Device-resident one-term Kronecker-SVD preconditioner (factor.hpp:42-54).
+
+    ``accum``: "reference" (bit-identical to lp_matmul's per-op rounding) or
+    "tensor" (tcgen05 fp16 GEMMs with fp32 accumulation)."""
+
+    _FIELDS = {"s_weights": 0, "s_lp": 1, "vr_lp": 2, "vc_lp": 3}
+
+    def __init__(self, handle, n: int, lambda_: float, fmt: PrecisionFormat, accum: str,
+                 a_r=None, a_c=None):
+        self._h = handle
+        self.n = n
+        self.lambda_ = lambda_
+        self.fmt = fmt
+        self.accum = accum
+        self.a_r = a_r
+        self.a_c = a_c
+
+    def _export(self, field: int, shape) -> np.ndarray:
+        out = np.empty(shape, order="F")
+        check(lib().kp_precond_export(self._h, field, ptr(out)))
+        return out
+
+    def __getattr__(self, name):
+        if name in KronSvdPreconditioner._FIELDS:
+            return self._export(KronSvdPreconditioner._FIELDS[name], (self.n, self.n))
+        if name in ("svd_r", "svd_c"):
+            base = 6 if name == "svd_r" else 8
+            s = self._export(4 if name == "svd_r" else 5, (self.n,))
+            return SvdTriple(self._export(base, (self.n, self.n)), s,
+                             self._export(base + 1, (self.n, self.n)))
+        raise AttributeError(name)
+
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h is not None:
+                lib().kp_precond_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def _accum_code(accum: str) -> int:
+    if accum == "reference":
+        return KP_ACCUM_REFERENCE
+    if accum == "tensor":
+        return KP_ACCUM_TENSOR
+    raise ValueError(f"unknown accumulation mode: {accum}")
+
+
+def build_preconditioner(a_r, a_c, lambda_: float, fmt: PrecisionFormat,
+                         accum: str = "reference") -> KronSvdPreconditioner:
+    """factor.cpp:80-104 (host LAPACK SVDs, device-resident rounded factors)."""
+    a_r = f64(a_r)
+    a_c = f64(a_c)
+    n = a_r.shape[0]
+    if a_r.shape != (n, n) or a_c.shape != (n, n):
+        raise ValueError("build_preconditioner: factors must be square and equally sized")
+    h = C.c_void_p()
+    check(lib().kp_precond_build(ptr(a_r), ptr(a_c), n, float(lambda_), fmt.c(),
+                                 _accum_code(accum), C.byref(h)))
+    return KronSvdPreconditioner(h, n, float(lambda_), fmt, accum, a_r, a_c)
+
+
+def build_preconditioner_from_svd(svd_r: SvdTriple, svd_c: SvdTriple, lambda_: float,
+                                  fmt: PrecisionFormat, accum: str = "reference"
+                                  ) -> KronSvdPreconditioner:
+    n = np.shape(svd_r.s)[0]
+    arrs = [f64(x) for x in (svd_r.u, svd_r.s, svd_r.v, svd_c.u, svd_c.s, svd_c.v)]
+    h = C.c_void_p()
+    check(lib().kp_precond_build_from_svd(n, *[ptr(x) for x in arrs], float(lambda_), fmt.c(),
+                                          _accum_code(accum), C.byref(h)))
+    return KronSvdPreconditioner(h, n, float(lambda_), fmt, accum)
+
+
+def with_lambda(p: KronSvdPreconditioner, lambda_: float) -> KronSvdPreconditioner:
+    """factor.cpp:106-115: same SVDs, new weights."""
+    h = C.c_void_p()
+    check(lib().kp_precond_with_lambda(p.handle(), float(lambda_), C.byref(h)))
+    return KronSvdPreconditioner(h, p.n, float(lambda_), p.fmt, p.accum, p.a_r, p.a_c)
+
+
+def precond_solve(p: KronSvdPreconditioner, r) -> np.ndarray:  # factor.cpp:117-132
+    r = np.ascontiguousarray(np.asarray(r, dtype=np.float64).reshape(-1))
+    if r.size != p.n * p.n:
+        raise ValueError("precond_solve: vector length is not n^2")
+    z = np.empty_like(r)
+    check(lib().kp_precond_solve(p.handle(), ptr(r), ptr(z)))
+    return z
+
+
+# ---------------------------------------------------------------------------
+# krylov.hpp:14-47
+@dataclass
+class SolverOptions:
+    lambda_: float = 0.0
+    max_iterations: int = 100
+    rel_residual_tol: float = 1e-8
+    x_true: np.ndarray | None = None
+    track_search_direction_orthogonality: bool = False
+    record_iterates: bool = False
+
+
+@dataclass
+class ConvergenceHistory:
+    relative_error: list = field(default_factory=list)
+    residual_norm: list = field(default_factory=list)
+    work_units: list = field(default_factory=list)
+    residual_cosines: list = field(default_factory=list)
+    iterates: list = field(default_factory=list)
+    iterations_used: int = 0
+    converged: bool = False
+    abort_reason: str = ""
+    msolve_count: int = 0
+
+
+@dataclass
+class SolveResult:
+    x: np.ndarray
+    history: ConvergenceHistory
+
+
+def _solve(kind: str, a: KroneckerSum, b, m: KronSvdPreconditioner | None,
+           opts: SolverOptions) -> SolveResult:
+    nn = a.n * a.n
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64).reshape(-1))
+    if b.size != nn:
+        raise ValueError("solver: right-hand side length mismatch")
+    if opts.max_iterations < 1:
+        raise ValueError("solver: max_iterations must be at least 1")
+    if not opts.rel_residual_tol > 0.0:
+        raise ValueError("solver: tolerance must be positive")
+    xt = None
+    if opts.x_true is not None:
+        xt = np.ascontiguousarray(np.asarray(opts.x_true, dtype=np.float64).reshape(-1))
+        if xt.size != nn:
+            raise ValueError("solver: x_true length mismatch")
+        if np.linalg.norm(xt) == 0.0:
+            raise ValueError("solver: x_true must be nonzero")
+    cap = opts.max_iterations + 1
+    rel = np.zeros(cap)
+    res = np.zeros(cap)
+    work = np.zeros(cap)
+    cos = np.zeros(cap)
+    its = np.zeros((cap, nn)) if opts.record_iterates else None
+    h = kp_history(capacity=cap, relative_error=ptr(rel), residual_norm=ptr(res),
+                   work_units=ptr(work), residual_cosines=ptr(cos), iterates=ptr(its))
+    o = kp_solver_options(lambda_=float(opts.lambda_), max_iterations=int(opts.max_iterations),
+                          rel_residual_tol=float(opts.rel_residual_tol), x_true=ptr(xt),
+                          track_search_direction_orthogonality=int(
+                              opts.track_search_direction_orthogonality),
+                          record_iterates=int(opts.record_iterates), device_pointers=0)
+    x = np.empty(nn)
+    L = lib()
+    if kind == "cgls":
+        st = L.kp_cgls(a.handle(), ptr(b), C.byref(o), ptr(x), C.byref(h))
+    else:
+        f = L.kp_pcg if kind == "pcg" else L.kp_fpcg
+        st = f(a.handle(), ptr(b), m.handle(), C.byref(o), ptr(x), C.byref(h))
+    check(st)
+    rows = h.rows
+    hist = ConvergenceHistory(
+        relative_error=list(rel[:rows]) if xt is not None else [],
+        residual_norm=list(res[:rows]), work_units=list(work[:rows]),
+        residual_cosines=list(cos[:h.n_cosines]),
+        iterates=[its[k].copy() for k in range(rows)] if its is not None else [],
+        iterations_used=h.iterations_used, converged=bool(h.converged),
+        abort_reason=h.abort_reason.decode(), msolve_count=h.msolve_count)
+    return SolveResult(x, hist)
+
+
+def cgls(a: KroneckerSum, b, opts: SolverOptions) -> SolveResult:  # krylov.cpp:154-208
+    return _solve("cgls", a, b, None, opts)
+
+
+def pcg(a: KroneckerSum, b, m: KronSvdPreconditioner, opts: SolverOptions) -> SolveResult:
+    """Fletcher-Reeves PCG (krylov.cpp:58-142, 210-213)."""
+    if m.n != a.n:
+        raise ValueError("solver: preconditioner size mismatch")
+    return _solve("pcg", a, b, m, opts)
+
+
+def fpcg(a: KroneckerSum, b, m: KronSvdPreconditioner, opts: SolverOptions) -> SolveResult:
+    """Polak-Ribiere flexible PCG (krylov.cpp:58-142, 215-218)."""
+    if m.n != a.n:
+        raise ValueError("solver: preconditioner size mismatch")
+    return _solve("fpcg", a, b, m, opts)
+
+
+def plateau_iteration(h: ConvergenceHistory, tol: float = 0.01) -> int:  # krylov.cpp:220-231
+    if not h.relative_error:
+        raise ValueError("plateau_iteration: run has no relative-error track")
+    if not tol >= 0.0:
+        raise ValueError("plateau_iteration: negative tolerance")
+    best = min(h.relative_error)
+    for k, e in enumerate(h.relative_error):
+        if e <= (1.0 + tol) * best:
+            return k
+    return len(h.relative_error) - 1
+
+
+@dataclass
+class WorkReport:
+    m_precond: int = 0
+    m_baseline: int = 0
+    threshold: float = 0.0
+    preconditioning_pays: bool = False
+    plateau_tolerance: float = 0.01
+
+
+def work_report(h_precond, h_baseline, plateau_tol: float = 0.01) -> WorkReport:
+    w = WorkReport(plateau_tolerance=plateau_tol)  # krylov.cpp:233-243
+    w.m_precond = plateau_iteration(h_precond, plateau_tol)
+    w.m_baseline = plateau_iteration(h_baseline, plateau_tol)
+    w.threshold = (8.0 * w.m_baseline) / 9.0
+    w.preconditioning_pays = float(w.m_precond) < w.threshold
+    return w
+
+
+# ---------------------------------------------------------------------------
+# regparam.hpp:19-90
+@dataclass
+class ParamChoice:
+    lambda_: float = 0.0
+    method: str = "gcv"
+    omega: float = 0.0
+    eta: float = 0.0
+    noise_norm: float = 0.0
+    objective_value: float = 0.0
+    bracket_lo: float = 0.0
+    bracket_hi: float = 0.0
+    flat_objective: bool = False
+    grid_index: int = -1
+
+
+_METHODS = {0: "opt", 1: "gcv", 2: "wgcv", 3: "discrepancy", 4: "gcv_grid"}
+
+
+def _choice(c: kp_param_choice) -> ParamChoice:
+    return ParamChoice(c.lambda_, _METHODS.get(c.method, "?"), c.omega, c.eta, c.noise_norm,
+                       c.objective_value, c.bracket_lo, c.bracket_hi, bool(c.flat_objective),
+                       c.grid_index)
+
+
+class SpectralData:
+    """Device-resident sigma_hat = s_r(j) s_c(i) and b_hat = vec(U_c^T B U_r)."""
+
+    def __init__(self, handle, n: int):
+        self._h = handle
+        self.n = n * n
+        self._side = n
+
+    def handle(self):
+        return self._h
+
+    def exported(self) -> tuple[np.ndarray, np.ndarray]:
+        """(sigma_hat, b_hat) sorted like approx_spectrum / project_b."""
+        s = np.empty(self.n)
+        b = np.empty(self.n)
+        check(lib().kp_spectral_export(self._h, ptr(s), ptr(b)))
+        return s, b
+
+    @property
+    def sigma_hat(self) -> np.ndarray:
+        return self.exported()[0]
+
+    @property
+    def b_hat(self) -> np.ndarray:
+        return self.exported()[1]
+
+    def __del__(self):
+        try:
+            if self._h is not None:
+                lib().kp_spectral_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def make_spectral_data(p: KronSvdPreconditioner, b) -> SpectralData:  # regparam.cpp:119-126
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64).reshape(-1))
+    if b.size != p.n * p.n:
+        raise ValueError("project: vector length is not n^2")
+    h = C.c_void_p()
+    check(lib().kp_spectral_create(p.handle(), ptr(b), C.byref(h)))
+    return SpectralData(h, p.n)
+
+
+def gcv_objective(sd: SpectralData, lambda_: float) -> float:  # regparam.cpp:224-229
+    v = C.c_double()
+    check(lib().kp_gcv_objective(sd.handle(), float(lambda_), C.byref(v)))
+    return v.value
+
+
+def discrepancy_gap(sd: SpectralData, epsilon: float, lambda_: float) -> float:  # :242-246
+    v = C.c_double()
+    check(lib().kp_discrepancy_gap(sd.handle(), float(epsilon), float(lambda_), C.byref(v)))
+    return v.value
+
+
+def gcv(sd: SpectralData) -> ParamChoice:  # regparam.cpp:254-258
+    c = kp_param_choice()
+    check(lib().kp_gcv(sd.handle(), C.byref(c)))
+    return _choice(c)
+
+
+def gcv_grid(sd: SpectralData, lambdas) -> tuple[ParamChoice, np.ndarray]:
+    """North-star GCV: one batched reduction over an explicit lambda grid;
+    returns the first argmin (grid_index) and the objective values."""
+    lam = np.ascontiguousarray(np.asarray(lambdas, dtype=np.float64))
+    vals = np.empty_like(lam)
+    c = kp_param_choice()
+    check(lib().kp_gcv_grid(sd.handle(), ptr(lam), lam.size, ptr(vals), C.byref(c)))
+    return _choice(c), vals
+
+
+def discrepancy(sd: SpectralData, noise_norm: float, eta: float) -> ParamChoice:  # :288-327
+    c = kp_param_choice()
+    check(lib().kp_discrepancy(sd.handle(), float(noise_norm), float(eta), C.byref(c)))
+    return _choice(c)

@@ -1,0 +1,133 @@
+// Microbenchmarks fixing the roofline denominators that MEASURED_PEAKS.json lacks:
+// FP64 DFMA vs DMMA (mma.sync f64) peak, and f16x2 CUDA-core add/mul rate.
+#include <cstdio>
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#define CK(x) do{cudaError_t e=(x); if(e!=cudaSuccess){printf("CUDA %s @%d\n",cudaGetErrorString(e),__LINE__);return 1;}}while(0)
+
+template<int ILP>
+__global__ void dfma_k(double* out, int iters, double a, double b) {
+  double acc[ILP];
+  #pragma unroll
+  for (int i=0;i<ILP;i++) acc[i] = threadIdx.x*1e-3 + i;
+  for (int it=0; it<iters; ++it) {
+    #pragma unroll
+    for (int i=0;i<ILP;i++) acc[i] = fma(acc[i], a, b);
+  }
+  double s=0; for(int i=0;i<ILP;i++) s+=acc[i];
+  if (s == 12345.678) out[0]=s;
+}
+
+__global__ void dmma_k4(double* out, int iters) {
+  double a0 = threadIdx.x*1e-3, a1 = a0+1, b0 = 0.5;
+  double c[8][4];
+  #pragma unroll
+  for (int t=0;t<8;t++) for(int i=0;i<4;i++) c[t][i]=0;
+  for (int it=0; it<iters; ++it) {
+    #pragma unroll
+    for (int t=0;t<8;t++)
+      asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+        : "+d"(c[t][0]),"+d"(c[t][1]),"+d"(c[t][2]),"+d"(c[t][3]) : "d"(a0),"d"(a1),"d"(b0));
+  }
+  double s=0; for(int t=0;t<8;t++) for(int i=0;i<4;i++) s+=c[t][i];
+  if (s == 12345.678) out[0]=s;
+}
+
+__global__ void dmma_k16(double* out, int iters) {
+  double a[8], b[4];
+  for (int i=0;i<8;i++) a[i]=threadIdx.x*1e-3+i;
+  for (int i=0;i<4;i++) b[i]=0.25*i;
+  double c[4][4];
+  #pragma unroll
+  for (int t=0;t<4;t++) for(int i=0;i<4;i++) c[t][i]=0;
+  for (int it=0; it<iters; ++it) {
+    #pragma unroll
+    for (int t=0;t<4;t++)
+      asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
+        : "+d"(c[t][0]),"+d"(c[t][1]),"+d"(c[t][2]),"+d"(c[t][3])
+        : "d"(a[0]),"d"(a[1]),"d"(a[2]),"d"(a[3]),"d"(a[4]),"d"(a[5]),"d"(a[6]),"d"(a[7]),
+          "d"(b[0]),"d"(b[1]),"d"(b[2]),"d"(b[3]));
+  }
+  double s=0; for(int t=0;t<4;t++) for(int i=0;i<4;i++) s+=c[t][i];
+  if (s == 12345.678) out[0]=s;
+}
+
+template<int ILP>
+__global__ void h2_k(double* out, int iters) {
+  unsigned acc[ILP]; unsigned m = 0x3c003c01u; // {1.0, ~1.0}
+  #pragma unroll
+  for (int i=0;i<ILP;i++) acc[i] = 0x3c003c00u + threadIdx.x + i;
+  for (int it=0; it<iters; ++it) {
+    #pragma unroll
+    for (int i=0;i<ILP;i++) {
+      unsigned p;
+      asm volatile("mul.rn.f16x2 %0, %1, %2;" : "=r"(p) : "r"(acc[i]), "r"(m));
+      asm volatile("add.rn.f16x2 %0, %1, %2;" : "=r"(acc[i]) : "r"(p), "r"(acc[i]));
+    }
+  }
+  unsigned s=0; for(int i=0;i<ILP;i++) s^=acc[i];
+  if (s == 0x12345678u) out[0]=s;
+}
+
+template<int ILP>
+__global__ void ffma_k(double* out, int iters, float a, float b) {
+  float acc[ILP];
+  #pragma unroll
+  for (int i=0;i<ILP;i++) acc[i] = threadIdx.x*1e-3f + i;
+  for (int it=0; it<iters; ++it) {
+    #pragma unroll
+    for (int i=0;i<ILP;i++) acc[i] = fmaf(acc[i], a, b);
+  }
+  float s=0; for(int i=0;i<ILP;i++) s+=acc[i];
+  if (s == 12345.678f) out[0]=s;
+}
+
+// f16 semantic probes: subnormal add/mul, overflow, cvt from f64
+__global__ void probe_k(unsigned short* o) {
+  __half tiny = __ushort_as_half(0x0001);          // 2^-24
+  __half h1   = __ushort_as_half(0x0400);          // 2^-14 (min normal)
+  unsigned short r;
+  asm("add.rn.f16 %0, %1, %2;" : "=h"(r) : "h"(__half_as_ushort(tiny)), "h"(__half_as_ushort(tiny))); o[0]=r; // 2^-23 = 0x0002
+  asm("mul.rn.f16 %0, %1, %2;" : "=h"(r) : "h"(__half_as_ushort(h1)), "h"((unsigned short)0x3800)); o[1]=r;   // 2^-15 = 0x0200
+  asm("add.rn.f16 %0, %1, %2;" : "=h"(r) : "h"((unsigned short)0x7bff), "h"((unsigned short)0x5000)); o[2]=r;  // 65504+32 -> inf 0x7c00
+  double d = 65519.999; __half hd = __double2half(d); o[3]=__half_as_ushort(hd); // 0x7bff
+  d = 65520.0; hd = __double2half(d); o[4]=__half_as_ushort(hd);                // 0x7c00
+  d = 0x1.8p-25; hd = __double2half(d); o[5]=__half_as_ushort(hd);             // 0x0001
+  d = 0x1.0p-25; hd = __double2half(d); o[6]=__half_as_ushort(hd);             // 0x0000 (tie -> even 0)
+  d = -0x1.0p-25; hd = __double2half(d); o[7]=__half_as_ushort(hd);            // 0x8000
+  asm("mul.rn.f16 %0, %1, %2;" : "=h"(r) : "h"((unsigned short)0x0001), "h"((unsigned short)0x3800)); o[8]=r;  // 2^-25 tie -> 0
+  asm("mul.rn.f16 %0, %1, %2;" : "=h"(r) : "h"((unsigned short)0x0003), "h"((unsigned short)0x3800)); o[9]=r;  // 1.5*2^-24 -> 2^-23 (even) 0x0002
+}
+
+int main() {
+  double* d; CK(cudaMalloc(&d, 64));
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t e0,e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float ms;
+  auto run = [&](const char* name, auto launch, double flops) {
+    launch(); cudaDeviceSynchronize();
+    cudaEventRecord(e0); for(int i=0;i<3;i++) launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("%-28s %9.2f T/s  (%.3f ms)\n", name, 3*flops/(ms*1e-3)/1e12, ms/3);
+  };
+  int iters = 4096;
+  for (int bpsm : {1,2,4}) for (int thr : {256, 512}) {
+    long blocks = (long)sms*bpsm;
+    char nm[64];
+    snprintf(nm, 64, "DFMA ilp8 b%d t%d", bpsm, thr);
+    run(nm, [&]{ dfma_k<8><<<blocks,thr>>>(d, iters, 1.0000001, 1e-9); }, 2.0*blocks*thr*8*iters);
+    snprintf(nm, 64, "DMMA k4 b%d t%d", bpsm, thr);
+    run(nm, [&]{ dmma_k4<<<blocks,thr>>>(d, iters/4); }, 2.0*blocks*(thr/32)*8*(iters/4)*16*8*4);
+    snprintf(nm, 64, "DMMA k16 b%d t%d", bpsm, thr);
+    run(nm, [&]{ dmma_k16<<<blocks,thr>>>(d, iters/8); }, 2.0*blocks*(thr/32)*4*(iters/8)*16*8*16);
+    snprintf(nm, 64, "HMUL2+HADD2 b%d t%d", bpsm, thr);
+    run(nm, [&]{ h2_k<8><<<blocks,thr>>>(d, iters); }, 4.0*blocks*thr*8*iters);
+    snprintf(nm, 64, "FFMA b%d t%d", bpsm, thr);
+    run(nm, [&]{ ffma_k<8><<<blocks,thr>>>(d, iters, 1.0000001f, 1e-9f); }, 2.0*blocks*thr*8*iters);
+  }
+  unsigned short* hp; CK(cudaMallocManaged(&hp, 64));
+  probe_k<<<1,1>>>(hp); CK(cudaDeviceSynchronize());
+  printf("f16 probes:"); for (int i=0;i<10;i++) printf(" %04x", hp[i]); printf("\n");
+  printf("expected:   0002 0200 7c00 7bff 7c00 0001 0000 8000 0000 0002\n");
+  return 0;
+}
