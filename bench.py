@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 PCG / FPCG hot path (BASELINE.json metric).
+
+Workload (N=1): config C5 — n=4096 (16.7M unknowns), rank-5 Kronecker-sum
+blur, FPCG with the fp16 Kronecker-SVD preconditioner (reference-exact
+per-op rounding), lambda=0.01, tol 1e-6, max 100 iterations. One "step" is
+one full FPCG solve; the metric is solver iterations per second over the K
+timed steps. N>1: one independent C5 image per GPU (weak scaling, replicas;
+no data-path collective — results are gathered with NCCL).
+
+  value       device-resident b / x (kp_fpcg with device pointers)
+  e2e         the C-ABI call with pinned HOST buffers (b, x_true in; x out)
+  roofline    dominant kernel = FP64 DMMA operator GEMM, FLOP-bound against
+              the measured DMMA peak (profiles/r01_microbench_peaks.txt)
+  cpu_baseline  the CPU oracle (C++ restatement of the reference, OpenBLAS +
+              streamed fp16 emulation) timed on the host cores for one
+              iteration's operator + preconditioner work
+
+`--impl reference` times that CPU implementation as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DMMA_PEAK_TFLOPS = 37.0   # measured, profiles/r01_microbench_peaks.txt (m16n8k16 f64)
+F16X2_PEAK_TOPS = 36.9    # measured f16x2 mul+add half-ops/s, same file
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def build_problem(name: str, image: int, n: int | None, device_apply: bool):
+    """Config problem; b_true computed on the device for large n (setup only)."""
+    from paper_2311_15393_b200 import configs, problems as P
+    import paper_2311_15393_b200 as K
+    if not device_apply:
+        return configs.build(name, image=image, n=n)
+    orig = P.kronsum_apply_host
+    P.kronsum_apply_host = lambda k, x: K.kronsum_apply(k, x)
+    try:
+        return configs.build(name, image=image, n=n)
+    finally:
+        P.kronsum_apply_host = orig
+
+
+def svd_pair(term, how: str):
+    from paper_2311_15393_b200 import problems as P
+    from paper_2311_15393_b200.kronprec import SvdTriple
+    if how == "host":
+        return SvdTriple(*P.host_svd(term.row_factor)), SvdTriple(*P.host_svd(term.col_factor))
+    import torch
+    out = []
+    for a in (term.row_factor, term.col_factor):
+        t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        u, s, vh = torch.linalg.svd(t)
+        out.append(SvdTriple(np.asfortranarray(u.cpu().numpy()), s.cpu().numpy().copy(),
+                             np.asfortranarray(vh.T.cpu().numpy())))
+    return out[0], out[1]
+
+
+def cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads: int) -> float:
+    """Seconds for one FPCG iteration's operator + preconditioner work on the
+    CPU oracle (normal_matvec + precond_solve)."""
+    from oracle import pyoracle as O
+    O.set_threads(threads)
+    po = O.build_preconditioner_from_svd((svd_r.u, svd_r.s, svd_r.v),
+                                         (svd_c.u, svd_c.s, svd_c.v), cfg.lambda_, fmt)
+    p = np.random.default_rng(0).standard_normal(cfg.n * cfg.n)
+    t0 = time.perf_counter()
+    O.normal_matvec(cfg.problem.a, cfg.lambda_, p)
+    O.precond_solve(po, p)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import paper_2311_15393_b200 as K
+    threads = os.cpu_count() or 1
+    t0 = time.time()
+    cfg = build_problem(args.config, 0, args.n, device_apply=False)
+    svd_r, svd_c = svd_pair(cfg.term, "host")
+    setup_s = time.time() - t0
+    fmt = K.PrecisionFormat.fp16()
+    for _ in range(args.warmup):
+        cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads)
+    times = [cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads) for _ in range(args.steps)]
+    total = sum(times)
+    value = args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "iterations/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64+f16(emulated)", "data": "synthetic",
+        "config": workload_config(cfg),
+        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": threads, "kind": "port",
+                         "sample": "one FPCG iteration's normal_matvec + precond_solve (fp16 "
+                                   "reference-exact emulation) per step"},
+        "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "setup_s": setup_s,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "PCG iterations/s at 4096^2 image"
+
+
+def workload_config(cfg) -> dict:
+    return {"workload": f"{cfg.name}: n={cfg.n} r={len(cfg.problem.a.terms)} FPCG, fp16 "
+                        f"Kronecker-SVD preconditioner (reference-exact rounding), "
+                        f"lambda={cfg.lambda_}, tol={cfg.tol}, maxit 100",
+            "unknowns": cfg.n * cfg.n,
+            "l2": "working set (~4 GB) far larger than the 126 MB L2; no flush needed"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--n", type=int, default=None, help="override image side (quick runs)")
+    ap.add_argument("--svd", default="gpu", choices=["gpu", "host"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    ws, rank, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2311_15393_b200 as K
+    from paper_2311_15393_b200._lib import check, lib, ptr
+    from paper_2311_15393_b200._lib import kp_history, kp_solver_options
+    L = lib()
+    check(L.kp_init(local))
+
+    t0 = time.time()
+    cfg = build_problem(args.config, rank, args.n, device_apply=True)
+    t_problem = time.time() - t0
+    t1 = time.time()
+    svd_r, svd_c = svd_pair(cfg.term, args.svd)
+    t_svd = time.time() - t1
+    fmt = K.PrecisionFormat.fp16()
+    m = K.build_preconditioner_from_svd(svd_r, svd_c, cfg.lambda_, fmt)
+    op = cfg.problem.a.handle()
+    setup_s = time.time() - t0
+    n = cfg.n
+    nn = n * n
+
+    # ---- device-resident inputs (value) ----
+    def dalloc(count):
+        p = C.c_void_p()
+        check(L.kp_device_alloc(count * 8, C.byref(p)))
+        return p
+
+    def halloc(count):
+        p = C.c_void_p()
+        check(L.kp_host_alloc(count * 8, C.byref(p)))
+        return p, np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), shape=(count,))
+
+    d_b, d_x, d_xt = dalloc(nn), dalloc(nn), dalloc(nn)
+    check(L.kp_memcpy_h2d(d_b, ptr(cfg.problem.b), nn * 8))
+    check(L.kp_memcpy_h2d(d_xt, ptr(cfg.problem.x_true), nn * 8))
+    hp_b, h_b = halloc(nn)
+    hp_x, h_x = halloc(nn)
+    hp_xt, h_xt = halloc(nn)
+    h_b[:] = cfg.problem.b
+    h_xt[:] = cfg.problem.x_true
+
+    cap = 101
+    hist_bufs = [np.zeros(cap) for _ in range(4)]
+
+    def solve(device: bool):
+        h = kp_history(capacity=cap, relative_error=ptr(hist_bufs[0]), residual_norm=ptr(hist_bufs[1]),
+                       work_units=ptr(hist_bufs[2]), residual_cosines=ptr(hist_bufs[3]))
+        o = kp_solver_options(lambda_=cfg.lambda_, max_iterations=100, rel_residual_tol=cfg.tol,
+                              x_true=(d_xt.value if device else hp_xt.value),
+                              device_pointers=int(device))
+        if device:
+            check(L.kp_fpcg(op, d_b, m.handle(), C.byref(o), d_x, C.byref(h)))
+        else:
+            check(L.kp_fpcg(op, hp_b, m.handle(), C.byref(o), hp_x, C.byref(h)))
+        return h.iterations_used, float(hist_bufs[0][h.rows - 1]), h.abort_reason.decode()
+
+    for _ in range(args.warmup):
+        its_w, rel_w, ab_w = solve(True)
+
+    def barrier():
+        check(L.kp_synchronize())
+        if dist:
+            dist.barrier()
+
+    # ---- timed region: device-resident (value) with per-kernel-class events ----
+    check(L.kp_profile_reset())
+    check(L.kp_profile_enable(1))
+    launches0 = L.kp_launch_count()
+    barrier()
+    iters = 0
+    rel_last = None
+    with ClockSampler(local) as clk:
+        check(L.kp_event_record(0))
+        for _ in range(args.steps):
+            it, rel_last, abort = solve(True)
+            iters += it
+        check(L.kp_event_record(1))
+        ms = C.c_float()
+        check(L.kp_event_elapsed(0, 1, C.byref(ms)))
+    barrier()
+    launches = L.kp_launch_count() - launches0
+    elapsed = ms.value / 1e3
+    prof = {}
+    for cls, name in enumerate(["operator_gemm_f64", "precond_gemm_f16ref", "vector", "spectral"]):
+        t = C.c_double()
+        c = C.c_longlong()
+        check(L.kp_profile_read(cls, C.byref(t), C.byref(c)))
+        prof[name] = (t.value, c.value)
+    check(L.kp_profile_enable(0))
+
+    # ---- e2e: the same solves through host (pinned) buffers ----
+    barrier()
+    check(L.kp_event_record(2))
+    e2e_iters = 0
+    for _ in range(args.steps):
+        it, _, _ = solve(False)
+        e2e_iters += it
+    check(L.kp_event_record(3))
+    e2e_ms = C.c_float()
+    check(L.kp_event_elapsed(2, 3, C.byref(e2e_ms)))
+    barrier()
+    e2e_elapsed = e2e_ms.value / 1e3
+
+    if dist:
+        t = torch.tensor([elapsed, e2e_elapsed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed, e2e_elapsed = float(t[0]), float(t[1])
+        c = torch.tensor([iters, e2e_iters], device="cuda", dtype=torch.float64)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        iters, e2e_iters = int(c[0]), int(c[1])
+        g = [None] * ws
+        dist.all_gather_object(g, {"rank": rank, "rel_err": rel_last})
+
+    value = iters / elapsed
+    e2e_value = e2e_iters / e2e_elapsed
+    r = len(cfg.problem.a.terms)
+    op_ms, op_launches = prof["operator_gemm_f64"]
+    flops_per_launch = 2.0 * r * float(n) ** 3  # each of the two GEMMs of an apply
+    achieved = flops_per_launch / (op_ms / op_launches / 1e3) / 1e12 if op_launches else 0.0
+    pm_ms, pm_launches = prof["precond_gemm_f16ref"]
+    half_ops = 2.0 * float(n) ** 3  # n^3 products + n^3 tree adds per GEMM
+    pm_achieved = half_ops / (pm_ms / pm_launches / 1e3) / 1e12 if pm_launches else 0.0
+    total_prof = sum(v[0] for v in prof.values())
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if ws == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            try:
+                tc = cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads)
+                cpu = {"value": 1.0 / tc, "unit": "iterations/s", "cores": threads, "kind": "port",
+                       "sample": "one FPCG iteration's normal_matvec + precond_solve at C5 "
+                                 "(oracle: OpenBLAS FP64 + streamed reference-exact fp16)"}
+            except Exception as e:  # noqa: BLE001
+                cpu = {"value": None, "unit": "iterations/s", "cores": threads, "kind": "port",
+                       "sample": f"failed: {e}"}
+        out = {
+            "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 (operator, vectors) + f16 (preconditioner, reference-exact)",
+            "data": "synthetic (seeded blob images, BASELINE C5 PSF)",
+            "config": {**workload_config(cfg), "parallelism": f"replicas x{ws}",
+                       "iterations_per_solve": iters // max(1, args.steps * ws),
+                       "final_rel_err": rel_last},
+            "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": 2 * nn * 8,
+                    "d2h_bytes_per_step": nn * 8 + 4 * cap * 8},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": DMMA_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": None,
+                         "kernel": "gemm_f64_kernel (DMMA m16n8k16, operator apply)",
+                         "peak_source": "measured DMMA f64 peak, profiles/r01_microbench_peaks.txt "
+                                        "(MEASURED_PEAKS.json has no FP64 entry)"},
+            "kernels": {k: {"ms": v[0], "launches": v[1],
+                            "share": v[0] / total_prof if total_prof else None}
+                        for k, v in prof.items()},
+            "precond_roofline": {"bound": "f16x2 CUDA-core pipe", "achieved": pm_achieved,
+                                 "peak": F16X2_PEAK_TOPS, "unit": "T half-ops/s",
+                                 "frac": pm_achieved / F16X2_PEAK_TOPS},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+            "setup_s": {"total": setup_s, "problem": t_problem, "svd": t_svd, "svd_backend": args.svd},
+        }
+        print(json.dumps(out), flush=True)
+    for p in (d_b, d_x, d_xt):
+        L.kp_device_free(p)
+    for p in (hp_b, hp_x, hp_xt):
+        L.kp_host_free(p)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -124,6 +124,13 @@ int kp_profile_enable(int on);
 int kp_profile_read(int kernel_class, double* total_ms, long long* launches);
 int kp_profile_reset(void);
 long long kp_launch_count(void);   /* kernels launched by this library */
+/* Device timestamps on the library stream (slots 0..15), for callers that
+ * time whole solves on the device. */
+int kp_event_record(int slot);
+int kp_event_elapsed(int slot_start, int slot_end, float* ms);
+/* Page-locked host buffers (fast H2D / D2H for host-pointer calls). */
+int kp_host_alloc(size_t bytes, void** hptr);
+int kp_host_free(void* hptr);
 
 /* ---- operator: kron.hpp / kron.cpp ------------------------------------ */
 /* row_factors / col_factors: r consecutive n-by-n column-major matrices,

@@ -64,7 +64,7 @@ EXPORTS = [
     "kp_precond_destroy", "kp_precond_solve", "kp_precond_export", "kp_precond_info",
     "kp_cgls", "kp_pcg", "kp_fpcg", "kp_spectral_create", "kp_spectral_destroy",
     "kp_spectral_export", "kp_gcv_objective", "kp_discrepancy_gap", "kp_gcv_grid", "kp_gcv",
-    "kp_discrepancy",
+    "kp_discrepancy", "kp_event_record", "kp_event_elapsed", "kp_host_alloc", "kp_host_free",
 ]
 
 _lib = None
@@ -110,6 +110,10 @@ def lib() -> C.CDLL:
             "kp_gcv_grid": ([P, P, I, P, C.POINTER(kp_param_choice)], I),
             "kp_gcv": ([P, C.POINTER(kp_param_choice)], I),
             "kp_discrepancy": ([P, D, D, C.POINTER(kp_param_choice)], I),
+            "kp_event_record": ([I], I),
+            "kp_event_elapsed": ([I, I, C.POINTER(C.c_float)], I),
+            "kp_host_alloc": ([C.c_size_t, C.POINTER(C.c_void_p)], I),
+            "kp_host_free": ([P], I),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

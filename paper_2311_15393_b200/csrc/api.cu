@@ -829,6 +829,25 @@ int kp_profile_read(int cls, double* total_ms, long long* launches) {
   })
 }
 long long kp_launch_count(void) { return ctx().launches; }
+int kp_event_record(int slot) {
+  KP_API({
+    static cudaEvent_t ev[16] = {};
+    if (slot < 0 || slot >= 16) throw InvalidArgument("event slot out of range");
+    if (!ev[slot]) KP_CUDA(cudaEventCreate(&ev[slot]));
+    KP_CUDA(cudaEventRecord(ev[slot], ctx().stream));
+    ctx().events[slot] = ev[slot];
+  })
+}
+int kp_event_elapsed(int a, int b, float* ms) {
+  KP_API({
+    if (a < 0 || a >= 16 || b < 0 || b >= 16 || !ctx().events[a] || !ctx().events[b])
+      throw InvalidArgument("event slot not recorded");
+    KP_CUDA(cudaEventSynchronize(ctx().events[b]));
+    KP_CUDA(cudaEventElapsedTime(ms, ctx().events[a], ctx().events[b]));
+  })
+}
+int kp_host_alloc(size_t bytes, void** hptr) { KP_API(KP_CUDA(cudaMallocHost(hptr, bytes))) }
+int kp_host_free(void* hptr) { KP_API(KP_CUDA(cudaFreeHost(hptr))) }
 
 // ---- operator ------------------------------------------------------------
 int kp_operator_create(int n, int r, const double* row_factors, const double* col_factors,

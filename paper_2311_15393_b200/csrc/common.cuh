@@ -46,6 +46,7 @@ struct Ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
   double total_ms[KC_COUNT] = {0, 0, 0, 0};
   long long count[KC_COUNT] = {0, 0, 0, 0};
+  cudaEvent_t events[16] = {};
 };
 
 Ctx& ctx();            // lazily initialised on first use (device 0)

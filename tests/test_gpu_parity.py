@@ -1,0 +1,380 @@
+"""Parity of the sm_100a path (through the C ABI) with the CPU oracle, plus
+the reference's hot-path known-answer tests re-run on the device.
+
+Tolerances (BASELINE north star): fp16 preconditioner solves bit-exact
+(same per-op rounding as the reference); FP64 operator products 1e-13
+relative; FP64 Krylov iterates 1e-10 over a prefix window; preconditioned
+runs: same iteration count (allowed +-2) and final relative error within 1e-3;
+lambda selection: identical grid index."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2311_15393_b200 as K
+from oracle import pyoracle as O
+from paper_2311_15393_b200 import problems as P
+from paper_2311_15393_b200.kronprec import KronTerm, KroneckerSum, SolverOptions, SvdTriple
+
+pytestmark = pytest.mark.gpu
+
+H = K.PrecisionFormat.fp16()
+D = K.PrecisionFormat.fp64()
+
+
+def same_bits(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    if a.shape != b.shape:
+        return False
+    nan = np.isnan(a)
+    return (np.array_equal(nan, np.isnan(b)) and np.array_equal(a[~nan], b[~nan])
+            and np.array_equal(np.signbit(a[~nan]), np.signbit(b[~nan])))
+
+
+def rsum(n, r, seed):
+    rng = np.random.default_rng(seed)
+    return KroneckerSum([KronTerm(rng.standard_normal((n, n)), rng.standard_normal((n, n)))
+                         for _ in range(r)], n)
+
+
+def pair_from(term):
+    sr = SvdTriple(*P.host_svd(term.row_factor))
+    sc = SvdTriple(*P.host_svd(term.col_factor))
+    return sr, sc
+
+
+def both_preconds(term, lam, fmt):
+    sr, sc = pair_from(term)
+    g = K.build_preconditioner_from_svd(sr, sc, lam, fmt)
+    o = O.build_preconditioner_from_svd((sr.u, sr.s, sr.v), (sc.u, sc.s, sc.v), lam, fmt)
+    return g, o
+
+
+# ---- operator -------------------------------------------------------------
+@pytest.mark.parametrize("n,r", [(4, 1), (8, 2), (13, 3), (32, 1), (64, 5), (100, 2), (256, 3)])
+def test_kronsum_apply_matches_oracle(n, r):
+    a = rsum(n, r, n * 10 + r)
+    y = np.random.default_rng(1).standard_normal(n * n)
+    for g, o in ((K.kronsum_apply, O.kronsum_apply),
+                 (K.kronsum_apply_transpose, O.kronsum_apply_transpose)):
+        got, want = g(a, y), o(a, y)
+        assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
+
+
+def test_operator_is_zero_bc_convolution():
+    """kronsum_apply == brute-force zero-boundary 2-D convolution
+    (test_deblur.cpp:18-55, acceptance criterion 4)."""
+    n = 16
+    psf = P.make_psf("speckle", 5, blob_count=4, seed=3)
+    a, _ = P.psf_to_kronsum(psf, n, truncation_tol=0.0)
+    x = np.random.default_rng(2).standard_normal((n, n))
+    want = np.zeros((n, n))
+    c = 2
+    for i in range(n):
+        for j in range(n):
+            s = 0.0
+            for k in range(5):
+                for l in range(5):
+                    ii, jj = i - (k - c), j - (l - c)
+                    if 0 <= ii < n and 0 <= jj < n:
+                        s += psf.values[k, l] * x[ii, jj]
+            want[i, j] = s
+    got = K.kronsum_apply(a, x.reshape(-1, order="F")).reshape(n, n, order="F")
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+
+
+def test_normal_matvec_vs_dense():  # test_krylov.cpp:91-108
+    a = rsum(4, 2, 7)
+    ad = sum(np.kron(t.row_factor, t.col_factor) for t in a.terms)
+    p = np.random.default_rng(3).standard_normal(16)
+    for lam in (0.0, 0.7):
+        want = ad.T @ (ad @ p) + lam * lam * p
+        assert np.linalg.norm(K.normal_matvec(a, lam, p) - want) <= 1e-12 * np.linalg.norm(want)
+    eye = KroneckerSum([KronTerm(np.eye(4), np.eye(4))], 4)
+    assert np.array_equal(K.normal_matvec(eye, 0.0, p), p)
+    with pytest.raises(ValueError):
+        K.normal_matvec(a, 0.0, np.ones(5))
+
+
+def test_operator_validation():
+    with pytest.raises(ValueError):
+        K.kronsum_apply(KroneckerSum([], 4), np.ones(16))
+    with pytest.raises(ValueError):
+        K.kronsum_apply(KroneckerSum([KronTerm(np.eye(4), np.eye(3))], 4), np.ones(16))
+
+
+# ---- preconditioner: bit-exact fp16 ---------------------------------------------------
+@pytest.mark.parametrize("n", [4, 8, 13, 16, 33, 64, 100, 128, 256])
+def test_precond_solve_fp16_bitwise(n):
+    psf = P.make_psf("gaussian", 3 if n < 5 else 5, sigma=1.5)
+    term = P.nearest_kron(psf, n)
+    for lam in (0.05, 0.004):  # 0.004: weights near the fp16 overflow threshold
+        g, o = both_preconds(term, lam, H)
+        assert same_bits(g.s_lp, o.s_lp)
+        assert same_bits(g.vr_lp, o.vr_lp) and same_bits(g.vc_lp, o.vc_lp)
+        rng = np.random.default_rng(n)
+        for scale in (1.0, 1e-6, 3e4):
+            r = rng.uniform(-1, 1, n * n) * scale
+            assert same_bits(K.precond_solve(g, r), O.precond_solve(o, r)), (lam, scale)
+
+
+def test_precond_identity_halves_rounded_residual():  # test_factor.cpp:245-252
+    g = K.build_preconditioner(np.eye(4), np.eye(4), 1.0, H)
+    r = np.random.default_rng(11).uniform(-1, 1, 16)
+    assert same_bits(K.precond_solve(g, r), 0.5 * O.round_array(r, H))
+
+
+def test_precond_fp64_inverts_m():  # test_factor.cpp:256-270
+    t = P.nearest_kron(P.make_psf("gaussian", 5, sigma=1.5), 8)
+    g = K.build_preconditioner(t.row_factor, t.col_factor, 0.01, D)
+    r = np.random.default_rng(5).uniform(-1, 1, 64)
+    z = K.precond_solve(g, r)
+    ah = np.kron(t.row_factor, t.col_factor)
+    zs = np.linalg.solve(ah.T @ ah + 1e-4 * np.eye(64), r)
+    assert np.linalg.norm(z - zs) <= 1e-10 * np.linalg.norm(zs)
+
+
+def test_precond_fp64_matches_oracle():
+    t = P.nearest_kron(P.make_psf("gaussian", 9, sigma=2.0), 96)
+    g, o = both_preconds(t, 0.01, D)
+    r = np.random.default_rng(9).standard_normal(96 * 96)
+    zg, zo = K.precond_solve(g, r), O.precond_solve(o, r)
+    assert np.linalg.norm(zg - zo) <= 1e-12 * np.linalg.norm(zo)
+
+
+def test_build_preconditioner_device_vs_oracle():
+    """kp_precond_build (host LAPACK inside the library) == oracle build."""
+    t = P.nearest_kron(P.make_psf("gaussian", 7, sigma=1.7), 24)
+    g = K.build_preconditioner(t.row_factor, t.col_factor, 0.03, H)
+    o = O.build_preconditioner(t.row_factor, t.col_factor, 0.03, H)
+    assert np.array_equal(g.s_weights, o.s_weights)
+    assert same_bits(g.s_lp, o.s_lp)
+    r = np.random.default_rng(4).uniform(-1, 1, 24 * 24)
+    assert same_bits(K.precond_solve(g, r), O.precond_solve(o, r))
+    q = K.with_lambda(g, 0.1)
+    qo = O.with_lambda(o, 0.1)
+    assert np.array_equal(q.s_weights, qo.s_weights)
+    assert same_bits(K.precond_solve(q, r), O.precond_solve(qo, r))
+
+
+def test_preconditioner_validation():  # test_factor.cpp:199-212
+    with pytest.raises(ValueError):
+        K.build_preconditioner(np.diag([1.0, 0.0]), np.eye(2), 0.0, D)
+    with pytest.raises(ValueError):
+        K.build_preconditioner(np.eye(2), np.eye(2), -1.0, D)
+    with pytest.raises(ValueError):
+        K.build_preconditioner(np.eye(2), np.eye(3), 1.0, D)
+    g = K.build_preconditioner(np.eye(4), np.eye(4), 1.0, H)
+    with pytest.raises(ValueError):
+        K.precond_solve(g, np.ones(15))
+
+
+# ---- solvers ---------------------------------------------------------------------
+def desk(kind, n, noise, seed):  # test_krylov.cpp:41-54
+    psf = P.make_psf(kind, 7, sigma=1.2, radius=2.0, seed=seed + 1)
+    tp = P.make_test_problem(P.default_test_image(n), psf, noise, seed)
+    return tp, P.nearest_kron(psf, n)
+
+
+def test_cgls_kats_on_device():  # test_krylov.cpp:110-206
+    eye = KroneckerSum([KronTerm(np.eye(4), np.eye(4))], 4)
+    b = P.rng_normals(21, 16)
+    r = K.cgls(eye, b, SolverOptions(lambda_=0.0, x_true=b))
+    assert r.history.converged and r.history.iterations_used == 1
+    assert np.linalg.norm(r.x - b) <= 1e-14 * np.linalg.norm(b)
+    assert r.history.relative_error[0] == 1.0
+    a = rsum(4, 2, 31)
+    ad = sum(np.kron(t.row_factor, t.col_factor) for t in a.terms)
+    b = P.rng_normals(35, 16)
+    lam = 0.3 * np.linalg.svd(ad, compute_uv=False)[0]
+    want = np.linalg.solve(ad.T @ ad + lam * lam * np.eye(16), ad.T @ b)
+    r = K.cgls(a, b, SolverOptions(lambda_=lam, max_iterations=16, rel_residual_tol=1e-10))
+    assert r.history.converged and np.linalg.norm(r.x - want) <= 1e-8 * np.linalg.norm(want)
+    tp, _ = desk("defocus", 8, 0.05, 11)
+    r = K.cgls(tp.a, tp.b, SolverOptions(lambda_=0.05, max_iterations=5, rel_residual_tol=1e-14,
+                                         x_true=tp.x_true))
+    h = r.history
+    assert not h.converged and h.abort_reason == "" and h.iterations_used == 5
+    assert len(h.residual_norm) == 6 and len(h.relative_error) == 6
+    assert h.work_units == [2.0 * k for k in range(6)]
+    assert h.residual_norm[0] == pytest.approx(np.linalg.norm(K.kronsum_apply_transpose(tp.a, tp.b)))
+    tp, _ = desk("gaussian", 8, 0.01, 9)
+    r = K.cgls(tp.a, tp.b, SolverOptions(lambda_=10.0, rel_residual_tol=1e-12, max_iterations=200))
+    bound = np.linalg.norm(K.kronsum_apply_transpose(tp.a, tp.b)) / 100.0
+    assert np.linalg.norm(r.x) <= bound * (1 + 1e-10)
+    with pytest.raises(ValueError):
+        K.cgls(eye, np.ones(5), SolverOptions())
+    with pytest.raises(ValueError):
+        K.cgls(eye, np.ones(16), SolverOptions(max_iterations=0))
+    with pytest.raises(ValueError):
+        K.cgls(eye, np.ones(16), SolverOptions(rel_residual_tol=0.0))
+    with pytest.raises(ValueError):
+        K.cgls(eye, np.ones(16), SolverOptions(x_true=np.ones(3)))
+
+
+def test_pcg_kats_on_device():  # test_krylov.cpp:208-351
+    tp, best = desk("gaussian", 8, 0.01, 41)
+    m = K.build_preconditioner(best.row_factor, best.col_factor, 0.05, D)
+    r = K.pcg(tp.a, tp.b, m, SolverOptions(lambda_=0.05, rel_residual_tol=1e-8))
+    assert r.history.converged and r.history.iterations_used == 1  # exact inverse
+    tp, best = desk("gaussian", 16, 0.01, 45)
+    m64 = K.build_preconditioner(best.row_factor, best.col_factor, 0.04, D)
+    m16 = K.build_preconditioner(best.row_factor, best.col_factor, 0.04, H)
+    opts = SolverOptions(lambda_=0.04, max_iterations=40, rel_residual_tol=1e-9, x_true=tp.x_true)
+    r64, r16 = K.pcg(tp.a, tp.b, m64, opts), K.pcg(tp.a, tp.b, m16, opts)
+    assert abs(r64.history.relative_error[-1] - r16.history.relative_error[-1]) <= 1e-2
+    tp, best = desk("gaussian", 8, 0.01, 49)  # energy norm monotone
+    lam = 0.05
+    m = K.build_preconditioner(best.row_factor, best.col_factor, lam, D)
+    r = K.pcg(tp.a, tp.b, m, SolverOptions(lambda_=lam, max_iterations=30, rel_residual_tol=1e-12,
+                                           record_iterates=True))
+    ad = sum(np.kron(t.row_factor, t.col_factor) for t in tp.a.terms)
+    g = ad.T @ ad + lam * lam * np.eye(64)
+    xs = np.linalg.solve(g, ad.T @ tp.b)
+    prev = math.inf
+    e0 = None
+    for xk in r.history.iterates:
+        e = xk - xs
+        en = e @ (g @ e)
+        e0 = en if e0 is None else e0
+        assert en <= prev + 1e-12 * e0
+        prev = en
+    tp, best = desk("defocus", 8, 0.01, 51)  # residual orthogonality diagnostics
+    m = K.build_preconditioner(best.row_factor, best.col_factor, 0.05, D)
+    r = K.pcg(tp.a, tp.b, m, SolverOptions(lambda_=0.05, max_iterations=6, rel_residual_tol=1e-13,
+                                           track_search_direction_orthogonality=True))
+    h = r.history
+    assert len(h.residual_cosines) == h.iterations_used
+    checked = 0
+    for k, c in enumerate(h.residual_cosines):
+        if h.residual_norm[k + 1] < 1e-8 * h.residual_norm[0]:
+            continue
+        assert c <= 1e-8
+        checked += 1
+    assert checked >= 2
+    tp, best = desk("gaussian", 8, 0.01, 53)  # fp16 overflow aborts with diagnostics
+    m16 = K.build_preconditioner(best.row_factor, best.col_factor, 0.05, H)
+    r = K.pcg(tp.a, np.full(64, 1e300), m16, SolverOptions(lambda_=0.05))
+    assert not r.history.converged and "non-finite" in r.history.abort_reason
+
+
+def test_abort_messages_match_oracle():
+    tp, best = desk("gaussian", 8, 0.01, 53)
+    for lam_m, b in ((0.05, np.full(64, 1e300)), (1e-4, tp.b)):  # overflow, S = inf
+        g, o = both_preconds(best, lam_m, H)
+        opts = SolverOptions(lambda_=0.05, max_iterations=20)
+        rg = K.pcg(tp.a, b, g, opts)
+        xo, ho = O.pcg(tp.a, b, o, opts)
+        assert rg.history.abort_reason == ho.abort_reason
+        assert rg.history.iterations_used == ho.iterations_used
+        assert rg.history.msolve_count == ho.msolve_count
+
+
+def test_scalar_preconditioner_is_plain_cg():  # test_krylov.cpp:222-239, 389-406
+    tp, _ = desk("gaussian", 8, 0.01, 43)
+    m = K.build_preconditioner(np.eye(8), np.eye(8), 1.0, D)
+    opts = SolverOptions(lambda_=0.07, max_iterations=12, rel_residual_tol=1e-13,
+                         record_iterates=True)
+    for solver in (K.pcg, K.fpcg):
+        r = solver(tp.a, tp.b, m, opts)
+        x = np.zeros(64)
+        res = K.kronsum_apply_transpose(tp.a, tp.b)
+        p = res.copy()
+        gma = res @ res
+        want = [x.copy()]
+        for _ in range(r.history.iterations_used):
+            q = K.normal_matvec(tp.a, 0.07, p)
+            al = gma / (p @ q)
+            x = x + al * p
+            res = res - al * q
+            want.append(x.copy())
+            gn = res @ res
+            p = res + (gn / gma) * p
+            gma = gn
+        for k, xk in enumerate(r.history.iterates):
+            assert np.linalg.norm(xk - want[k]) <= 1e-8 * max(1.0, np.linalg.norm(want[k]))
+
+
+def test_fpcg_kats_on_device():  # test_krylov.cpp:353-388
+    tp, best = desk("gaussian", 8, 0.01, 61)
+    m = K.build_preconditioner(best.row_factor, best.col_factor, 0.06, D)
+    opts = SolverOptions(lambda_=0.06, max_iterations=6, rel_residual_tol=1e-13, record_iterates=True)
+    rp, rf = K.pcg(tp.a, tp.b, m, opts), K.fpcg(tp.a, tp.b, m, opts)
+    for a, b in zip(rp.history.iterates, rf.history.iterates):
+        assert np.linalg.norm(a - b) <= 1e-8 * max(1.0, np.linalg.norm(a))
+    tp, best = desk("defocus", 16, 0.01, 63)
+    m16 = K.build_preconditioner(best.row_factor, best.col_factor, 0.03, H)
+    opts = SolverOptions(lambda_=0.03, max_iterations=40, rel_residual_tol=1e-9, x_true=tp.x_true)
+    rp, rf = K.pcg(tp.a, tp.b, m16, opts), K.fpcg(tp.a, tp.b, m16, opts)
+    assert abs(K.plateau_iteration(rp.history) - K.plateau_iteration(rf.history)) <= 2
+
+
+def blob_problem(n, sigma=2.0, np_=9, noise=0.01, seed=3):
+    psf = P.make_psf("gaussian", np_, sigma=sigma)
+    tp = P.make_test_problem(P.blob_image(n, seed + 100), psf, noise, seed)
+    return tp, P.nearest_kron(psf, n)
+
+
+@pytest.mark.parametrize("solver", ["pcg", "fpcg"])
+@pytest.mark.parametrize("n,fmt", [(32, "fp16"), (64, "fp16"), (100, "fp16"), (64, "fp64")])
+def test_preconditioned_solver_parity(solver, n, fmt):
+    fm = H if fmt == "fp16" else D
+    tp, term = blob_problem(n)
+    g, o = both_preconds(term, 0.01, fm)
+    opts = SolverOptions(lambda_=0.01, max_iterations=60, rel_residual_tol=1e-6, x_true=tp.x_true)
+    rg = getattr(K, solver)(tp.a, tp.b, g, opts)
+    xo, ho = getattr(O, solver)(tp.a, tp.b, o, opts)
+    hg = rg.history
+    assert abs(hg.iterations_used - ho.iterations_used) <= 2
+    assert hg.converged == ho.converged and hg.abort_reason == ho.abort_reason
+    assert abs(hg.relative_error[-1] - ho.relative_error[-1]) <= 1e-3
+    assert hg.work_units == [2.25 * k for k in range(len(hg.work_units))]
+    # FP64 steps: the first iterations agree to 1e-10
+    for k in range(min(3, len(hg.residual_norm), len(ho.residual_norm))):
+        assert hg.residual_norm[k] == pytest.approx(ho.residual_norm[k], rel=1e-10)
+
+
+def test_cgls_parity_prefix_window():
+    tp, _ = blob_problem(64)
+    opts = SolverOptions(lambda_=0.01, max_iterations=400, rel_residual_tol=1e-6, x_true=tp.x_true,
+                         record_iterates=True)
+    rg = K.cgls(tp.a, tp.b, opts)
+    xo, ho = O.cgls(tp.a, tp.b, opts)
+    window = 20
+    for k in range(window):
+        a, b = rg.history.iterates[k], ho.iterates[k]
+        assert np.linalg.norm(a - b) <= 1e-10 * max(np.linalg.norm(b), 1e-300), k
+    assert abs(rg.history.iterations_used - ho.iterations_used) <= 2
+    assert abs(rg.history.relative_error[-1] - ho.relative_error[-1]) <= 1e-3
+
+
+# ---- lambda selection ------------------------------------------------------------------
+def test_spectral_data_and_selectors_match_oracle():
+    n = 48
+    tp, term = blob_problem(n, noise=0.01)
+    g, o = both_preconds(term, 1.0, H)
+    sd = K.make_spectral_data(g, tp.b)
+    sg, bg = sd.exported()
+    so, bo = O.spectral(o, tp.b)
+    assert np.array_equal(sg, so)
+    assert np.abs(bg - bo).max() <= 1e-12 * np.abs(bo).max()
+    for lam in (1e-3, 1e-2, 0.3):
+        assert K.gcv_objective(sd, lam) == pytest.approx(O.gcv_objective(so, bo, lam), rel=1e-11)
+        assert K.discrepancy_gap(sd, 0.1, lam) == pytest.approx(
+            O.discrepancy_gap(so, bo, 0.1, lam), rel=1e-11, abs=1e-14)
+    grid = 10.0 ** (-4.0 + 4.0 * np.arange(64) / 63.0)
+    cg, vg = K.gcv_grid(sd, grid)
+    co, vo = O.gcv_grid(so, bo, grid)
+    assert cg.grid_index == co["grid_index"]
+    assert np.allclose(vg, vo, rtol=1e-11)
+    c = K.gcv(sd)
+    oc = O.select("gcv", so, bo)
+    assert c.lambda_ == pytest.approx(oc["lambda"], rel=1e-6)
+    nn = float(np.linalg.norm(tp.noise))
+    d = K.discrepancy(sd, nn, 1.01)
+    do = O.discrepancy(so, bo, nn, 1.01)
+    assert d.lambda_ == pytest.approx(do["lambda"], rel=1e-9)
+    with pytest.raises(K.NoRootError, match="too large"):
+        K.discrepancy(sd, 1e6, 1.0)
+    with pytest.raises(K.NoRootError, match="too small"):
+        K.discrepancy(sd, 1e-30, 1.0)
