@@ -500,9 +500,13 @@ void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
     per_iter_launches = c.launches - before;
     c.launches = before;
   }
+  // Poll after every iteration while an iteration is long (overshoot would
+  // cost real no-op launches); batch up to 16 iterations per poll once an
+  // iteration is shorter than ~1 ms, where the host round trip dominates.
   int done = 0, chunk = 1;
   while (done < maxit) {
     const int todo = std::min(chunk, maxit - done);
+    const auto t0 = std::chrono::steady_clock::now();
     for (int i = 0; i < todo; ++i) {
       if (exec) {
         KP_CUDA(cudaGraphLaunch(exec, c.stream));
@@ -516,7 +520,10 @@ void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
                             c.stream));
     sync();
     if (hst.p->status != ST_RUNNING) break;
-    chunk = std::min(chunk * 2, 16);
+    const double per_iter_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() /
+        todo;
+    chunk = per_iter_ms > 1.0 ? 1 : std::min(chunk * 2, 16);
   }
   if (exec) cudaGraphExecDestroy(exec);
 }
