@@ -1,0 +1,60 @@
+// C++ consumer of include/kronprec_b200.hpp — reads like the reference's
+// doctest cases (test_krylov.cpp "exact inverse converges in one iteration",
+// test_factor.cpp "identity factors halve the rounded residual").
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+
+#include "kronprec_b200.hpp"
+
+using namespace kronprec_b200;
+
+static int fails = 0;
+#define CHECK(c) do { if (!(c)) { std::printf("FAIL %s:%d %s\n", __FILE__, __LINE__, #c); ++fails; } } while (0)
+
+static Vec eye(int n) {
+  Vec m(size_t(n) * n, 0.0);
+  for (int i = 0; i < n; ++i) m[size_t(i) * n + i] = 1.0;
+  return m;
+}
+
+int main() {
+  // identity operator: CGLS converges in one step
+  const int n = 4;
+  KroneckerSum I({KronTerm{eye(n), eye(n)}}, n);
+  Vec b(16);
+  for (int i = 0; i < 16; ++i) b[i] = std::sin(1.0 + i);
+  SolverOptions o;
+  o.lambda = 0.0;
+  o.x_true = &b;
+  SolveResult r = cgls(I, b, o);
+  CHECK(r.history.converged && r.history.iterations_used == 1);
+  CHECK(std::fabs(r.history.relative_error.back()) <= 1e-14);
+
+  // identity preconditioner at lambda 1 halves the fp16-rounded residual
+  KronSvdPreconditioner m = build_preconditioner(eye(n), eye(n), n, 1.0, fp16());
+  Vec z = precond_solve(m, Vec(16, 0.1));
+  CHECK(z[0] == 0.5 * 0.0999755859375);
+
+  // exact-inverse preconditioner: PCG converges in one iteration
+  Vec t(size_t(n) * n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) t[size_t(j) * n + i] = (i == j) ? 0.5 : (std::abs(i - j) == 1 ? 0.25 : 0.0);
+  KroneckerSum A({KronTerm{t, t}}, n);
+  KronSvdPreconditioner mx = build_preconditioner(t, t, n, 0.05, fp64());
+  SolverOptions po;
+  po.lambda = 0.05;
+  SolveResult rp = pcg(A, b, mx, po);
+  CHECK(rp.history.converged && rp.history.iterations_used == 1);
+
+  // errors surface as the reference's exception types
+  bool threw = false;
+  try { build_preconditioner(eye(2), eye(2), 2, -1.0, fp64()); } catch (const std::invalid_argument&) { threw = true; }
+  CHECK(threw);
+  SpectralData sd = make_spectral_data(mx, b);
+  threw = false;
+  try { discrepancy(sd, 1e6, 1.0); } catch (const NoRootError&) { threw = true; }
+  CHECK(threw);
+  std::printf(fails ? "cpp api: %d failures\n" : "cpp api: ok\n", fails);
+  return fails ? 1 : 0;
+}

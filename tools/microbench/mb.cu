@@ -37,18 +37,18 @@ __global__ void dmma_k16(double* out, int iters) {
   double a[8], b[4];
   for (int i=0;i<8;i++) a[i]=threadIdx.x*1e-3+i;
   for (int i=0;i<4;i++) b[i]=0.25*i;
-  double c[4][4];
+  double c[12][4];
   #pragma unroll
-  for (int t=0;t<4;t++) for(int i=0;i<4;i++) c[t][i]=0;
+  for (int t=0;t<12;t++) for(int i=0;i<4;i++) c[t][i]=0;
   for (int it=0; it<iters; ++it) {
     #pragma unroll
-    for (int t=0;t<4;t++)
+    for (int t=0;t<12;t++)
       asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
         : "+d"(c[t][0]),"+d"(c[t][1]),"+d"(c[t][2]),"+d"(c[t][3])
         : "d"(a[0]),"d"(a[1]),"d"(a[2]),"d"(a[3]),"d"(a[4]),"d"(a[5]),"d"(a[6]),"d"(a[7]),
           "d"(b[0]),"d"(b[1]),"d"(b[2]),"d"(b[3]));
   }
-  double s=0; for(int t=0;t<4;t++) for(int i=0;i<4;i++) s+=c[t][i];
+  double s=0; for(int t=0;t<12;t++) for(int i=0;i<4;i++) s+=c[t][i];
   if (s == 12345.678) out[0]=s;
 }
 
@@ -111,7 +111,7 @@ int main() {
     printf("%-28s %9.2f T/s  (%.3f ms)\n", name, 3*flops/(ms*1e-3)/1e12, ms/3);
   };
   int iters = 4096;
-  for (int bpsm : {1,2,4}) for (int thr : {256, 512}) {
+  for (int bpsm : {1,2,4}) for (int thr : {128, 256, 512}) {
     long blocks = (long)sms*bpsm;
     char nm[64];
     snprintf(nm, 64, "DFMA ilp8 b%d t%d", bpsm, thr);
@@ -119,7 +119,7 @@ int main() {
     snprintf(nm, 64, "DMMA k4 b%d t%d", bpsm, thr);
     run(nm, [&]{ dmma_k4<<<blocks,thr>>>(d, iters/4); }, 2.0*blocks*(thr/32)*8*(iters/4)*16*8*4);
     snprintf(nm, 64, "DMMA k16 b%d t%d", bpsm, thr);
-    run(nm, [&]{ dmma_k16<<<blocks,thr>>>(d, iters/8); }, 2.0*blocks*(thr/32)*4*(iters/8)*16*8*16);
+    run(nm, [&]{ dmma_k16<<<blocks,thr>>>(d, iters/8); }, 2.0*blocks*(thr/32)*12*(iters/8)*16*8*16);
     snprintf(nm, 64, "HMUL2+HADD2 b%d t%d", bpsm, thr);
     run(nm, [&]{ h2_k<8><<<blocks,thr>>>(d, iters); }, 4.0*blocks*thr*8*iters);
     snprintf(nm, 64, "FFMA b%d t%d", bpsm, thr);
