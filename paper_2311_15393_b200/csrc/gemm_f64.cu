@@ -14,6 +14,8 @@
 // reorders the exact FP64 sum.
 #include "gemm_f64.cuh"
 
+#include <cstdlib>
+
 namespace kp {
 namespace {
 
@@ -54,13 +56,15 @@ __device__ __forceinline__ void dmma16(double (&c)[4], const double (&a)[8], con
 // of CTAs shares A and B tiles in L2.
 constexpr int GROUP_M = 16;
 
-template <int BM, int BN, int WM, int WN, int STAGES, bool VEC16>
+template <int BM, int BN, int WM, int WN, int STAGES, int KSUB, bool VEC16>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     gemm_f64_kernel(const F64GemmArgs args) {
   constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   constexpr int THREADS = WARPS_M * WARPS_N * 32;
   constexpr int MT = WM / 16, NT = WN / 8;
-  constexpr int STAGE_DOUBLES = (BM + BN) * BK;
+  constexpr int KT_DEPTH = BK * KSUB;                 // K per pipeline stage
+  constexpr int SUB_DOUBLES = (BM + BN) * BK;         // one 16-deep sub-tile
+  constexpr int STAGE_DOUBLES = SUB_DOUBLES * KSUB;
 
   if (args.status && *args.status != 0) return;
 
@@ -81,26 +85,28 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
   const int g = lane >> 2, t = lane & 3;
 
   const int Kb = args.Kb;
-  const int kt_per_batch = (Kb + BK - 1) / BK;
+  const int kt_per_batch = (Kb + KT_DEPTH - 1) / KT_DEPTH;
   const int total_kt = args.nb * kt_per_batch;
 
   const uint32_t smem_base = smem_u32(smem);
 
   auto load_tile = [&](int kt, int stage) {
     const int b = kt / kt_per_batch;
-    const int k0 = (kt % kt_per_batch) * BK;
-    const uint32_t sa = smem_base + uint32_t(stage * STAGE_DOUBLES) * 8u;
-    const uint32_t sb = sa + uint32_t(BM * BK) * 8u;
-    constexpr int CHUNKS_A = BM * 8, CHUNKS_B = BN * 8;
+    const int k0 = (kt % kt_per_batch) * KT_DEPTH;
+    constexpr int CHUNKS_A = BM * 8, CHUNKS_B = BN * 8, CHUNKS = (CHUNKS_A + CHUNKS_B) * KSUB;
 #pragma unroll
-    for (int id = tid; id < CHUNKS_A + CHUNKS_B; id += THREADS) {
-      const bool isA = id < CHUNKS_A;
-      const int cid = isA ? id : id - CHUNKS_A;
+    for (int id = tid; id < CHUNKS; id += THREADS) {
+      const int sub = id / (CHUNKS_A + CHUNKS_B);
+      const int rid = id % (CHUNKS_A + CHUNKS_B);
+      const bool isA = rid < CHUNKS_A;
+      const int cid = isA ? rid : rid - CHUNKS_A;
       const int row = cid >> 3, ch = cid & 7;
       const int grow = (isA ? m_base : n_base) + row;
       const int rows = isA ? M : N;
       const F64Operand& op = isA ? args.A : args.B;
-      const int kk = k0 + ch * 2;
+      const int kk = k0 + sub * BK + ch * 2;
+      const uint32_t sa = smem_base + uint32_t(stage * STAGE_DOUBLES + sub * SUB_DOUBLES) * 8u;
+      const uint32_t sb = sa + uint32_t(BM * BK) * 8u;
       const uint32_t dst = (isA ? sa : sb) + uint32_t(row * 128 + ((ch ^ (row & 7)) << 4));
       const double* src = op.p + long(b) * op.bstride + long(grow) * op.ld + kk;
       if (VEC16) {
@@ -138,29 +144,31 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
       cp_async_commit();
     }
     const int stage = kt % STAGES;
-    const uint32_t sa = smem_base + uint32_t(stage * STAGE_DOUBLES) * 8u;
-    const uint32_t sb = sa + uint32_t(BM * BK) * 8u;
-
-    double bf[NT][4];
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-      const int row = wn * WN + j * 8 + g;
-      const uint32_t rb = sb + uint32_t(row * 128);
-      lds128(rb + uint32_t(((2 * t) ^ (row & 7)) << 4), bf[j][0], bf[j][1]);
-      lds128(rb + uint32_t(((2 * t + 1) ^ (row & 7)) << 4), bf[j][2], bf[j][3]);
-    }
+    for (int sub = 0; sub < KSUB; ++sub) {
+      const uint32_t sa = smem_base + uint32_t(stage * STAGE_DOUBLES + sub * SUB_DOUBLES) * 8u;
+      const uint32_t sb = sa + uint32_t(BM * BK) * 8u;
+      double bf[NT][4];
 #pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      double af[8];
-      const int r0 = wm * WM + i * 16 + g, r1 = r0 + 8;
-      const uint32_t ra0 = sa + uint32_t(r0 * 128), ra1 = sa + uint32_t(r1 * 128);
-      // a[v0 + 2 v1] = A[g + 8 v0][4t + v1]
-      lds128(ra0 + uint32_t(((2 * t) ^ (r0 & 7)) << 4), af[0], af[2]);
-      lds128(ra0 + uint32_t(((2 * t + 1) ^ (r0 & 7)) << 4), af[4], af[6]);
-      lds128(ra1 + uint32_t(((2 * t) ^ (r1 & 7)) << 4), af[1], af[3]);
-      lds128(ra1 + uint32_t(((2 * t + 1) ^ (r1 & 7)) << 4), af[5], af[7]);
+      for (int j = 0; j < NT; ++j) {
+        const int row = wn * WN + j * 8 + g;
+        const uint32_t rb = sb + uint32_t(row * 128);
+        lds128(rb + uint32_t(((2 * t) ^ (row & 7)) << 4), bf[j][0], bf[j][1]);
+        lds128(rb + uint32_t(((2 * t + 1) ^ (row & 7)) << 4), bf[j][2], bf[j][3]);
+      }
 #pragma unroll
-      for (int j = 0; j < NT; ++j) dmma16(acc[i][j], af, bf[j]);
+      for (int i = 0; i < MT; ++i) {
+        double af[8];
+        const int r0 = wm * WM + i * 16 + g, r1 = r0 + 8;
+        const uint32_t ra0 = sa + uint32_t(r0 * 128), ra1 = sa + uint32_t(r1 * 128);
+        // a[v0 + 2 v1] = A[g + 8 v0][4t + v1]
+        lds128(ra0 + uint32_t(((2 * t) ^ (r0 & 7)) << 4), af[0], af[2]);
+        lds128(ra0 + uint32_t(((2 * t + 1) ^ (r0 & 7)) << 4), af[4], af[6]);
+        lds128(ra1 + uint32_t(((2 * t) ^ (r1 & 7)) << 4), af[1], af[3]);
+        lds128(ra1 + uint32_t(((2 * t + 1) ^ (r1 & 7)) << 4), af[5], af[7]);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma16(acc[i][j], af, bf[j]);
+      }
     }
   }
   cp_async_wait<0>();
@@ -208,17 +216,17 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
   }
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES>
+template <int BM, int BN, int WM, int WN, int STAGES, int KSUB>
 void launch_cfg(const F64GemmArgs& a) {
   constexpr int THREADS = (BM / WM) * (BN / WN) * 32;
-  constexpr size_t SMEM = size_t(STAGES) * (BM + BN) * BK * sizeof(double);
+  constexpr size_t SMEM = size_t(STAGES) * KSUB * (BM + BN) * BK * sizeof(double);
   const unsigned grid = cdiv(a.M, BM) * cdiv(a.N, BN);
   const bool vec16 = (a.Kb % 2 == 0) && (a.A.ld % 2 == 0) && (a.B.ld % 2 == 0) &&
                      (a.A.bstride % 2 == 0) && (a.B.bstride % 2 == 0) &&
                      (reinterpret_cast<uintptr_t>(a.A.p) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(a.B.p) % 16 == 0);
   if (vec16) {
-    auto k = gemm_f64_kernel<BM, BN, WM, WN, STAGES, true>;
+    auto k = gemm_f64_kernel<BM, BN, WM, WN, STAGES, KSUB, true>;
     static bool attr = false;
     if (!attr) {
       KP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM)));
@@ -226,7 +234,7 @@ void launch_cfg(const F64GemmArgs& a) {
     }
     k<<<grid, THREADS, SMEM, ctx().stream>>>(a);
   } else {
-    auto k = gemm_f64_kernel<BM, BN, WM, WN, STAGES, false>;
+    auto k = gemm_f64_kernel<BM, BN, WM, WN, STAGES, KSUB, false>;
     static bool attr = false;
     if (!attr) {
       KP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM)));
@@ -236,15 +244,38 @@ void launch_cfg(const F64GemmArgs& a) {
   }
 }
 
+// Big-tile variant (experiment switch KP_F64_CFG, default 0).
+int big_cfg() {
+  static int cfg = [] {
+    const char* e = getenv("KP_F64_CFG");
+    return e ? atoi(e) : 0;
+  }();
+  return cfg;
+}
+
 bool use_big_tiles(int M, int N) {
   // 128x128 tiles once they still give at least ~one CTA per SM.
   return long(cdiv(M, 128)) * cdiv(N, 128) >= ctx().num_sms;
 }
 
+void launch_big(const F64GemmArgs& a) {
+  // Measured at C5 (profiles/r01_sweep_f64.txt): 0: 30.5, 1: 30.6, 2: 32.2,
+  // 3: 31.6, 4: 27.7 TF/s; all variants are bitwise identical.
+  switch (big_cfg()) {
+    case 1: launch_cfg<128, 128, 32, 32, 4, 1>(a); break;   // 16 warps of 32x32
+    case 3: launch_cfg<128, 128, 32, 32, 3, 2>(a); break;   // 16 warps, 32-deep stages
+    case 4: launch_cfg<128, 64, 32, 32, 4, 1>(a); break;    // 8 warps, 2 CTAs/SM
+    case 5: launch_cfg<128, 128, 64, 32, 4, 1>(a); break;   // 8 warps, 16-deep stages
+    default: launch_cfg<128, 128, 64, 32, 3, 2>(a); break;  // 8 warps, 32-deep stages
+  }
+}
+
+int big_tile_n() { return big_cfg() == 4 ? 64 : 128; }
+
 }  // namespace
 
 int gemm_f64_num_ctas(int M, int N) {
-  if (use_big_tiles(M, N)) return int(cdiv(M, 128) * cdiv(N, 128));
+  if (use_big_tiles(M, N)) return int(cdiv(M, 128) * cdiv(N, big_tile_n()));
   return int(cdiv(M, 64) * cdiv(N, 64));
 }
 
@@ -252,9 +283,9 @@ void gemm_f64(const F64GemmArgs& a, int kernel_class) {
   if (a.M <= 0 || a.N <= 0) return;
   LaunchScope scope(kernel_class);
   if (use_big_tiles(a.M, a.N))
-    launch_cfg<128, 128, 64, 32, 4>(a);
+    launch_big(a);
   else
-    launch_cfg<64, 64, 32, 32, 4>(a);
+    launch_cfg<64, 64, 32, 32, 4, 1>(a);
   check_launch("gemm_f64");
 }
 
