@@ -184,6 +184,57 @@ def run_reference(args):
 
 
 METRIC = "PCG iterations/s at 4096^2 image"
+METRIC_C4 = "solves/s over image batch (64 x 1024^2, discrepancy lambda + PCG fp16)"
+
+
+def run_c4(args):
+    """BASELINE C4: 64 independent 1024^2 images sharded across the ranks;
+    per image: spectral data, discrepancy lambda, with_lambda, PCG (fp16)."""
+    ws, rank, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2311_15393_b200._lib import check, lib
+    from paper_2311_15393_b200.batch import C4Shard, gather_results, reduce_timing, shard
+    L = lib()
+    check(L.kp_init(local))
+    images = 64
+    mine = list(shard(images, ws, rank))
+    sh = C4Shard(n=args.n, svd=args.svd)
+    probs = {i: sh.problem(i) for i in mine}  # input generation is not timed
+    for i in mine[: max(1, args.warmup)]:
+        sh.solve(i, probs[i])
+    if dist:
+        dist.barrier()
+    launches0 = L.kp_launch_count()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        results = [sh.solve(i, probs[i]) for i in mine]  # each call ends synchronised
+        elapsed = time.perf_counter() - t0
+    launches = L.kp_launch_count() - launches0
+    elapsed, solved = reduce_timing(elapsed, float(len(results)), dist, device="cuda")
+    allres = gather_results(results, dist)
+    if rank == 0:
+        its = [r["iterations"] for r in allres]
+        out = {"metric": METRIC_C4, "value": solved / elapsed, "unit": "solves/s", "n_gpus": ws,
+               "steps": 1, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+               "dtype": "f64 + f16 (reference-exact)", "data": "synthetic (seeded blob images)",
+               "config": {"workload": "C4: 64 x n=1024, Gaussian sigma=2.5, noise 0.1/1/5 %, "
+                                      "discrepancy eta=1.01, PCG fp16 tol 1e-6",
+                          "parallelism": f"images sharded over {ws} GPU(s), NCCL gather",
+                          "mean_iterations": float(np.mean(its)), "images": len(allres),
+                          "no_root": sum(r["no_root"] for r in allres)},
+               "clocks": clk.summary(), "gpu_launches": int(launches),
+               "results": [{k: r[k] for k in ("image", "lam", "iterations", "rel_err")}
+                           for r in allres[:6]]}
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
 
 
 def workload_config(cfg) -> dict:
@@ -204,9 +255,13 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override image side (quick runs)")
     ap.add_argument("--svd", default="gpu", choices=["gpu", "host"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tensor", action="store_true", help="skip the tensor-mode secondary run")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+
+    if args.config == "C4":
+        return run_c4(args)
 
     ws, rank, local = dist_env()
     import torch
@@ -258,16 +313,16 @@ def main():
     cap = 101
     hist_bufs = [np.zeros(cap) for _ in range(4)]
 
-    def solve(device: bool):
+    def solve(device: bool, mm=None):
         h = kp_history(capacity=cap, relative_error=ptr(hist_bufs[0]), residual_norm=ptr(hist_bufs[1]),
                        work_units=ptr(hist_bufs[2]), residual_cosines=ptr(hist_bufs[3]))
         o = kp_solver_options(lambda_=cfg.lambda_, max_iterations=100, rel_residual_tol=cfg.tol,
                               x_true=(d_xt.value if device else hp_xt.value),
                               device_pointers=int(device))
         if device:
-            check(L.kp_fpcg(op, d_b, m.handle(), C.byref(o), d_x, C.byref(h)))
+            check(L.kp_fpcg(op, d_b, (mm or m).handle(), C.byref(o), d_x, C.byref(h)))
         else:
-            check(L.kp_fpcg(op, hp_b, m.handle(), C.byref(o), hp_x, C.byref(h)))
+            check(L.kp_fpcg(op, hp_b, (mm or m).handle(), C.byref(o), hp_x, C.byref(h)))
         return h.iterations_used, float(hist_bufs[0][h.rows - 1]), h.abort_reason.decode()
 
     for _ in range(args.warmup):
@@ -303,6 +358,25 @@ def main():
         check(L.kp_profile_read(cls, C.byref(t), C.byref(c)))
         prof[name] = (t.value, c.value)
     check(L.kp_profile_enable(0))
+
+    # ---- secondary: tcgen05 tensor-mode preconditioner (north-star variant) ----
+    tensor = None
+    if not args.no_tensor:
+        mt = K.build_preconditioner_from_svd(svd_r, svd_c, cfg.lambda_, fmt, accum="tensor")
+        solve(True, mt)
+        barrier()
+        check(L.kp_event_record(4))
+        t_iters, t_rel = 0, None
+        for _ in range(args.steps):
+            it, t_rel, _ = solve(True, mt)
+            t_iters += it
+        check(L.kp_event_record(5))
+        t_ms = C.c_float()
+        check(L.kp_event_elapsed(4, 5, C.byref(t_ms)))
+        tensor = {"value": t_iters / (t_ms.value / 1e3), "unit": "iterations/s",
+                  "solves_per_s": args.steps / (t_ms.value / 1e3),
+                  "iterations_per_solve": t_iters // args.steps, "final_rel_err": t_rel,
+                  "note": "KP_ACCUM_TENSOR: tcgen05 kind::f16, fp32 accumulation (not bit-exact)"}
 
     # ---- e2e: the same solves through host (pinned) buffers ----
     barrier()
@@ -373,6 +447,8 @@ def main():
             "precond_roofline": {"bound": "f16x2 CUDA-core pipe", "achieved": pm_achieved,
                                  "peak": F16X2_PEAK_TOPS, "unit": "T half-ops/s",
                                  "frac": pm_achieved / F16X2_PEAK_TOPS},
+            "solves_per_s": args.steps * ws / elapsed,
+            "tensor_mode": tensor,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),

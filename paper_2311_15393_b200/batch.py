@@ -1,0 +1,110 @@
+"""Batches of independent solves sharded across GPUs (BASELINE config C4).
+
+A single solve does not shard; batches of independent images
+do. Each rank takes a contiguous block of image indices, runs the full
+reference pipeline per image on its own GPU — spectral data, discrepancy-
+principle lambda (regparam.cpp:288-327, eta = 1.01), with_lambda, PCG with the
+fp16 preconditioner — and the per-image results are gathered with one
+collective (NCCL on GPUs, gloo in the CPU tests). No data-path collective.
+"""
+from __future__ import annotations
+
+from dataclasses import asdict, dataclass
+
+
+def shard(num_items: int, world: int, rank: int) -> range:
+    """Contiguous, balanced block of item indices for `rank`."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("shard: bad world/rank")
+    base, extra = divmod(num_items, world)
+    start = rank * base + min(rank, extra)
+    return range(start, start + base + (1 if rank < extra else 0))
+
+
+@dataclass
+class ImageResult:
+    image: int
+    noise_level: float
+    lam: float
+    iterations: int
+    converged: bool
+    rel_err: float
+    abort_reason: str = ""
+    no_root: bool = False
+
+
+def gather_results(local: list, dist=None) -> list:
+    """All ranks' results, sorted by image (all_gather_object)."""
+    items = [asdict(r) if isinstance(r, ImageResult) else dict(r) for r in local]
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return sorted(items, key=lambda d: d["image"])
+    bucket = [None] * dist.get_world_size()
+    dist.all_gather_object(bucket, items)
+    return sorted((d for part in bucket for d in part), key=lambda d: d["image"])
+
+
+def reduce_timing(elapsed_s: float, units: float, dist=None, device=None) -> tuple[float, float]:
+    """(max elapsed over ranks, sum of units over ranks) — the whole-job
+    throughput is units / elapsed."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return elapsed_s, units
+    import torch
+    t = torch.tensor([elapsed_s], dtype=torch.float64, device=device)
+    u = torch.tensor([units], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u.item())
+
+
+class C4Shard:
+    """Shared operator / preconditioner factors for the C4 batch on one GPU
+    (all 64 images share the PSF, hence A and the Kronecker factors)."""
+
+    def __init__(self, n: int | None = None, svd: str = "host"):
+        import numpy as np
+
+        from . import configs
+        from . import kronprec as K
+        from . import problems as P
+        from .kronprec import SvdTriple
+
+        self.K, self.P, self.np = K, P, np
+        base = configs.build("C4", image=0, n=n)
+        self.n = base.n
+        self.a = base.problem.a
+        self.psf = base.problem.psf
+        self.eta = base.eta
+        self.tol = base.tol
+        if svd == "gpu":
+            import torch
+            pair = []
+            for f in (base.term.row_factor, base.term.col_factor):
+                u, s, vh = torch.linalg.svd(torch.from_numpy(np.ascontiguousarray(f)).cuda())
+                pair.append(SvdTriple(np.asfortranarray(u.cpu().numpy()), s.cpu().numpy().copy(),
+                                      np.asfortranarray(vh.T.cpu().numpy())))
+            self.m0 = K.build_preconditioner_from_svd(pair[0], pair[1], 1.0, K.PrecisionFormat.fp16())
+        else:
+            self.m0 = K.build_preconditioner(base.term.row_factor, base.term.col_factor, 1.0,
+                                             K.PrecisionFormat.fp16())
+
+    def problem(self, image: int):
+        P, np = self.P, self.np
+        noise = [0.001, 0.01, 0.05][image % 3]
+        return P.make_test_problem(P.blob_image(self.n, 4000 + image), self.psf, noise, 5000 + image,
+                                   a=self.a)
+
+    def solve(self, image: int, tp=None) -> ImageResult:
+        K, np = self.K, self.np
+        tp = tp or self.problem(image)
+        sd = K.make_spectral_data(self.m0, tp.b)
+        try:
+            lam = K.discrepancy(sd, float(np.linalg.norm(tp.noise)), self.eta).lambda_
+        except K.NoRootError:
+            return ImageResult(image, tp.noise_level, float("nan"), 0, False, float("nan"),
+                               "", True)
+        m = K.with_lambda(self.m0, lam)
+        r = K.pcg(self.a, tp.b, m, K.SolverOptions(lambda_=lam, max_iterations=100,
+                                                   rel_residual_tol=self.tol, x_true=tp.x_true))
+        h = r.history
+        return ImageResult(image, tp.noise_level, lam, h.iterations_used, h.converged,
+                           h.relative_error[-1], h.abort_reason)

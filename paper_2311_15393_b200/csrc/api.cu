@@ -23,6 +23,7 @@
 #include "../../include/kronprec_b200.h"
 #include "common.cuh"
 #include "gemm_f16ref.cuh"
+#include "gemm_f16tc.cuh"
 #include "gemm_f64.cuh"
 #include "host_la.h"
 #include "vec.cuh"
@@ -234,6 +235,12 @@ void op_apply(kp_operator* op, const double* in, double* out, bool transpose,
 
 int op_partials_ctas(const kp_operator* op) { return gemm_f64_num_ctas(op->n, op->n); }
 
+int msolve_partials_ctas(const kp_precond* p) {
+  if (covers_double(p->fmt)) return gemm_f64_num_ctas(p->n, p->n);
+  return p->accum == KP_ACCUM_TENSOR ? gemm_f16tc_num_ctas(p->n, p->n)
+                                     : gemm_f16ref_num_ctas(p->n, p->n);
+}
+
 void ensure_ws(kp_precond* p) {
   const int n = p->n;
   const size_t nn = size_t(n) * n;
@@ -250,12 +257,8 @@ void ensure_ws(kp_precond* p) {
       fill_u16(p->t1h.p, p->t1h.n, 0x8000);  // A operands: -0 padding
       fill_u16(p->t3h.p, p->t3h.n, 0x8000);
     }
-    if (!p->part.p) p->part.alloc(size_t(gemm_f16ref_num_ctas(n, n)) * 4);
+    if (!p->part.p) p->part.alloc(size_t(msolve_partials_ctas(p)) * 4);
   }
-}
-
-int msolve_partials_ctas(const kp_precond* p) {
-  return covers_double(p->fmt) ? gemm_f64_num_ctas(p->n, p->n) : gemm_f16ref_num_ctas(p->n, p->n);
 }
 
 // precond_solve (factor.cpp:117-132). In fp16 mode r16 must already hold
@@ -287,25 +290,25 @@ void msolve(kp_precond* p, const double* r, double* z, const double* d0, const d
     return;
   }
   if (!is_fp16(p->fmt)) throw Unsupported("precond_solve: only fp16 and double-covering formats run on the B200 path");
-  if (p->accum != KP_ACCUM_REFERENCE) throw Unsupported("precond_solve: tensor accumulation not built");
   const long ldh = sh->ldh;
+  auto gemm = p->accum == KP_ACCUM_TENSOR ? gemm_f16tc : gemm_f16ref;
   F16GemmArgs g;
   g.M = n, g.N = n, g.K = n, g.status = status;
   g.A = {sh->vc_a.p, ldh}, g.B = {p->r16.p, ldh};  // t1 = lp(V_c^T R)
   g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = ldh, g.epi.cn = 1;
-  gemm_f16ref(g, KC_PRECOND);
+  gemm(g, KC_PRECOND);
   g.A = {p->t1h.p, ldh}, g.B = {sh->vr_b.p, ldh};  // w = round(S .* lp(t1 V_r))
   g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF_SCALED, g.epi.Ch = p->wh.p, g.epi.cm = 1,
   g.epi.cn = ldh, g.epi.scale = p->s16.p, g.epi.sm = 1, g.epi.sn = n;
-  gemm_f16ref(g, KC_PRECOND);
+  gemm(g, KC_PRECOND);
   g.A = {sh->vct_a.p, ldh}, g.B = {p->wh.p, ldh};  // t3 = lp(V_c w)
   g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t3h.p, g.epi.cm = ldh, g.epi.cn = 1;
-  gemm_f16ref(g, KC_PRECOND);
+  gemm(g, KC_PRECOND);
   g.A = {p->t3h.p, ldh}, g.B = {sh->vrt_b.p, ldh};  // z = lp(t3 V_r^T)
   g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z, g.epi.cm = 1, g.epi.cn = n;
   g.epi.vm = 1, g.epi.vn = n, g.epi.d0 = d0, g.epi.d1a = d1a, g.epi.d1b = d1b;
   g.epi.partials = p->part.p;
-  gemm_f16ref(g, KC_PRECOND);
+  gemm(g, KC_PRECOND);
 }
 
 void cast_r16(kp_precond* p, const double* r, const int* status) {
@@ -361,7 +364,6 @@ kp_precond* precond_from_svd(int n, std::vector<double> ur, std::vector<double> 
     throw Unsupported("build_preconditioner: the B200 path stores fp16 or FP64 factors only");
   if (accum == KP_ACCUM_TENSOR && !is_fp16(fmt))
     throw InvalidArgument("build_preconditioner: tensor accumulation requires fp16");
-  if (accum == KP_ACCUM_TENSOR) throw Unsupported("build_preconditioner: tensor accumulation not built");
   auto sh = std::make_shared<PrecondShared>();
   sh->n = n;
   sh->u_r = std::move(ur), sh->s_r = std::move(sr), sh->v_r = std::move(vr);

@@ -1,0 +1,105 @@
+"""Generate the config goldens with the CPU oracle (test infrastructure).
+
+The reference cannot be built here (Eigen absent), so the goldens for the
+BASELINE configs come from the oracle restatement, run on the
+same seeded inputs the device tests build (paper_2311_15393_b200.configs).
+Full sizes where the oracle finishes in minutes; C5 (n=4096) as a prefix of
+iterations. Output: tests/golden/<config>.json (histories, iteration counts,
+lambda choices, solution checksums). Usage:
+
+    python tests/golden/gen_goldens.py C1 C2 C3 C4 C5 [--threads 8]
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from oracle import pyoracle as O  # noqa: E402
+from paper_2311_15393_b200 import configs  # noqa: E402
+from paper_2311_15393_b200 import PrecisionFormat as PF  # noqa: E402
+from paper_2311_15393_b200.kronprec import SolverOptions  # noqa: E402
+
+FMT = {"fp16": PF.fp16(), "fp64": PF.fp64()}
+
+
+def hist_dict(x, h):
+    return {"iterations_used": h.iterations_used, "converged": h.converged,
+            "abort_reason": h.abort_reason, "msolve_count": h.msolve_count,
+            "residual_norm": h.residual_norm, "relative_error": h.relative_error,
+            "x_sum": float(np.sum(x)), "x_norm": float(np.linalg.norm(x))}
+
+
+def run_solver(cfg, solver, fmt, maxit, lam, m0):
+    opts = SolverOptions(lambda_=lam, max_iterations=maxit, rel_residual_tol=cfg.tol,
+                         x_true=cfg.problem.x_true)
+    t0 = time.time()
+    if solver == "cgls":
+        x, h = O.cgls(cfg.problem.a, cfg.problem.b, opts)
+    else:
+        m = O.with_lambda(m0[fmt], lam)
+        x, h = getattr(O, solver)(cfg.problem.a, cfg.problem.b, m, opts)
+    d = hist_dict(x, h)
+    d.update(solver=solver, fmt=fmt, max_iterations=maxit, seconds=time.time() - t0)
+    return d
+
+
+def gen(name: str, prefix: int | None = None, images=(0,)):
+    out = {"config": name, "generator": "oracle/kp_oracle.cpp via tests/golden/gen_goldens.py",
+           "images": []}
+    for img in images:
+        cfg = configs.build(name, image=img)
+        m0 = {}
+        fmts = {f for _, f, _ in cfg.solvers if f}
+        for f in fmts:  # build_preconditioner at lambda = 1 (cli.cpp:192-198)
+            m0[f] = O.build_preconditioner(cfg.term.row_factor, cfg.term.col_factor, 1.0, FMT[f])
+        rec = {"image": img, "n": cfg.n, "rank": len(cfg.problem.a.terms),
+               "noise_level": cfg.problem.noise_level,
+               "noise_norm": float(np.linalg.norm(cfg.problem.noise)),
+               "b_norm": float(np.linalg.norm(cfg.problem.b)), "select": cfg.select}
+        lam = cfg.lambda_
+        if cfg.select != "fixed":
+            s, bh = O.spectral(m0["fp16"], cfg.problem.b)
+            if cfg.select == "gcv_grid":
+                c, vals = O.gcv_grid(s, bh, configs.GCV_GRID)
+                rec["gcv_index"] = c["grid_index"]
+                rec["gcv_values"] = list(map(float, vals))
+            else:
+                c = O.discrepancy(s, bh, float(np.linalg.norm(cfg.problem.noise)), cfg.eta)
+            lam = c["lambda"]
+        rec["lambda"] = lam
+        rec["runs"] = []
+        for solver, fmt, maxit in cfg.solvers:
+            mi = min(maxit, prefix) if prefix else maxit
+            rec["runs"].append(run_solver(cfg, solver, fmt, mi, lam, m0))
+            print(name, img, solver, fmt, rec["runs"][-1]["iterations_used"],
+                  f"{rec['runs'][-1]['seconds']:.1f}s", flush=True)
+        out["images"].append(rec)
+    path = os.path.join(HERE, f"{name}.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print("wrote", path, flush=True)
+
+
+if __name__ == "__main__":
+    threads = 8
+    args = [a for a in sys.argv[1:]]
+    if "--threads" in args:
+        i = args.index("--threads")
+        threads = int(args[i + 1])
+        del args[i:i + 2]
+    O.set_threads(threads)
+    for name in args:
+        if name == "C4":
+            gen("C4", images=(0, 1, 2, 3, 4, 5))
+        elif name == "C5":
+            gen("C5", prefix=3)
+        else:
+            gen(name)

@@ -1,0 +1,123 @@
+"""BASELINE configurations on the device vs the oracle.
+
+C1 (n=256) runs the oracle at test time; C2-C5 compare against the committed
+oracle goldens (tests/golden/*.json, made by tests/golden/gen_goldens.py;
+C5 as a 3-iteration prefix). Bounds from the north star: reference-exact
+preconditioned runs within +-2 iterations and 1e-3 final relative error of
+the reference, identical GCV grid index, FP64 histories 1e-10 over a prefix."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2311_15393_b200 as K
+from oracle import pyoracle as O
+from paper_2311_15393_b200 import configs
+from paper_2311_15393_b200.kronprec import SolverOptions, SvdTriple
+from paper_2311_15393_b200 import problems as P
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+FMT = {"fp16": K.PrecisionFormat.fp16(), "fp64": K.PrecisionFormat.fp64()}
+
+
+def golden(name):
+    path = os.path.join(HERE, "golden", f"{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"golden {name}.json not generated (tests/golden/gen_goldens.py)")
+    with open(path) as f:
+        return json.load(f)
+
+
+def device_runs(cfg, lam, solvers, accum="reference", prefix=None):
+    m0 = {}
+    out = []
+    for solver, fmt, maxit in solvers:
+        opts = SolverOptions(lambda_=lam, max_iterations=min(maxit, prefix or maxit),
+                             rel_residual_tol=cfg.tol, x_true=cfg.problem.x_true)
+        if solver == "cgls":
+            r = K.cgls(cfg.problem.a, cfg.problem.b, opts)
+        else:
+            if fmt not in m0:
+                m0[fmt] = K.build_preconditioner(cfg.term.row_factor, cfg.term.col_factor, 1.0,
+                                                 FMT[fmt], accum=accum if fmt == "fp16" else "reference")
+            m = K.with_lambda(m0[fmt], lam)
+            r = getattr(K, solver)(cfg.problem.a, cfg.problem.b, m, opts)
+        out.append(r)
+    return out
+
+
+def check_against(run, ref, prefix_rows=3, final=True):
+    h = run.history
+    assert abs(h.iterations_used - ref["iterations_used"]) <= 2
+    assert h.converged == ref["converged"]
+    if final:
+        assert abs(h.relative_error[-1] - ref["relative_error"][-1]) <= 1e-3
+    for k in range(min(prefix_rows, len(h.residual_norm), len(ref["residual_norm"]))):
+        assert h.residual_norm[k] == pytest.approx(ref["residual_norm"][k], rel=1e-10)
+        assert h.relative_error[k] == pytest.approx(ref["relative_error"][k], rel=1e-10)
+
+
+def test_c1_vs_oracle_now():
+    cfg = configs.build("C1")
+    g = golden("C1")["images"][0]
+    runs = device_runs(cfg, cfg.lambda_, cfg.solvers)
+    for run, ref in zip(runs, g["runs"]):
+        check_against(run, ref)
+    # and against an oracle run made here with the same SVD (bit-exact M)
+    sr = SvdTriple(*P.host_svd(cfg.term.row_factor))
+    sc = SvdTriple(*P.host_svd(cfg.term.col_factor))
+    mg = K.build_preconditioner_from_svd(sr, sc, cfg.lambda_, FMT["fp16"])
+    mo = O.build_preconditioner_from_svd((sr.u, sr.s, sr.v), (sc.u, sc.s, sc.v), cfg.lambda_, FMT["fp16"])
+    opts = SolverOptions(lambda_=cfg.lambda_, max_iterations=100, rel_residual_tol=cfg.tol,
+                         x_true=cfg.problem.x_true)
+    rg = K.pcg(cfg.problem.a, cfg.problem.b, mg, opts)
+    _, ho = O.pcg(cfg.problem.a, cfg.problem.b, mo, opts)
+    assert rg.history.iterations_used == ho.iterations_used
+    assert abs(rg.history.relative_error[-1] - ho.relative_error[-1]) <= 1e-6
+
+
+def test_c2_fpcg_vs_golden():
+    cfg = configs.build("C2")
+    g = golden("C2")["images"][0]
+    (run,) = device_runs(cfg, cfg.lambda_, cfg.solvers)
+    ref = g["runs"][0]
+    check_against(run, ref, prefix_rows=5)
+    assert run.history.abort_reason.split(" at ")[0] == ref["abort_reason"].split(" at ")[0]
+
+
+def test_c3_gcv_index_and_pcg():
+    g = golden("C3")["images"][0]
+    cfg = configs.build("C3")
+    m0 = K.build_preconditioner(cfg.term.row_factor, cfg.term.col_factor, 1.0, FMT["fp16"])
+    sd = K.make_spectral_data(m0, cfg.problem.b)
+    c, vals = K.gcv_grid(sd, configs.GCV_GRID)
+    assert c.grid_index == g["gcv_index"]
+    assert np.allclose(vals, g["gcv_values"], rtol=1e-10)
+    (run,) = device_runs(cfg, c.lambda_, cfg.solvers)
+    check_against(run, g["runs"][0])
+
+
+def test_c4_discrepancy_and_pcg_subset():
+    from paper_2311_15393_b200.batch import C4Shard
+    g = golden("C4")
+    sh = C4Shard()
+    for rec in g["images"]:
+        res = sh.solve(rec["image"])
+        assert res.lam == pytest.approx(rec["lambda"], rel=1e-9)
+        ref = rec["runs"][0]
+        assert abs(res.iterations - ref["iterations_used"]) <= 2
+        assert res.converged == ref["converged"]
+        assert abs(res.rel_err - ref["relative_error"][-1]) <= 1e-3
+
+
+def test_c5_prefix_vs_golden():
+    g = golden("C5")["images"][0]
+    cfg = configs.build("C5")
+    runs = device_runs(cfg, cfg.lambda_, cfg.solvers, prefix=3)
+    for run, ref in zip(runs, g["runs"]):
+        assert run.history.iterations_used == ref["iterations_used"]
+        for k in range(len(ref["residual_norm"])):
+            assert run.history.residual_norm[k] == pytest.approx(ref["residual_norm"][k], rel=1e-8)
+            assert run.history.relative_error[k] == pytest.approx(ref["relative_error"][k], rel=1e-8)

@@ -1,0 +1,65 @@
+"""Host logic of the sharded batch path with world_size 2 over gloo (CPU)."""
+import os
+import socket
+
+import pytest
+
+from paper_2311_15393_b200.batch import ImageResult, gather_results, reduce_timing, shard
+
+
+def test_shard_covers_everything_once():
+    for n in (0, 1, 7, 64, 65):
+        for world in (1, 2, 3, 8):
+            seen = [i for r in range(world) for i in shard(n, world, r)]
+            assert seen == list(range(n))
+            sizes = [len(shard(n, world, r)) for r in range(world)]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard(4, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = [ImageResult(i, [0.001, 0.01, 0.05][i % 3], 0.01 * (i + 1), 10 + i, True, 0.1)
+            for i in shard(64, world, rank)]
+    allres = gather_results(mine, dist)
+    elapsed, units = reduce_timing(1.0 + rank, float(len(mine)), dist)
+    q.put((rank, [d["image"] for d in allres], elapsed, units))
+    dist.destroy_process_group()
+
+
+def test_gather_and_reduce_world2():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, images, elapsed, units in out:
+        assert images == list(range(64))  # every rank sees the full, ordered batch
+        assert elapsed == 2.0  # max over ranks
+        assert units == 64.0  # sum over ranks
+
+
+def test_single_process_fallbacks():
+    res = [ImageResult(3, 0.01, 0.1, 5, True, 0.2), ImageResult(1, 0.001, 0.1, 4, True, 0.2)]
+    assert [d["image"] for d in gather_results(res)] == [1, 3]
+    assert reduce_timing(2.5, 7.0) == (2.5, 7.0)

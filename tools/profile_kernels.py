@@ -22,7 +22,7 @@ if a.what == "op":
     x = np.random.default_rng(0).standard_normal(n * n)
     for _ in range(a.reps):
         t = time.time(); y = K.kronsum_apply(op, x); print("apply", time.time() - t, flush=True)
-else:
+elif a.what == "msolve":
     q = np.linalg.qr(np.random.default_rng(1).standard_normal((n, n)))[0]
     s = np.linspace(1.0, 1e-3, n)
     sv = SvdTriple(np.asfortranarray(q), s, np.asfortranarray(q))
@@ -30,3 +30,11 @@ else:
     r = np.random.default_rng(2).standard_normal(n * n)
     for _ in range(a.reps):
         t = time.time(); z = K.precond_solve(m, r); print("msolve", time.time() - t, flush=True)
+if a.what == "msolve_tc":
+    q = np.linalg.qr(np.random.default_rng(1).standard_normal((n, n)))[0]
+    s = np.linspace(1.0, 1e-3, n)
+    sv = SvdTriple(np.asfortranarray(q), s, np.asfortranarray(q))
+    m = K.build_preconditioner_from_svd(sv, sv, 0.01, K.PrecisionFormat.fp16(), accum="tensor")
+    r = np.random.default_rng(2).standard_normal(n * n)
+    for _ in range(a.reps):
+        t = time.time(); z = K.precond_solve(m, r); print("msolve_tc", time.time() - t, flush=True)
