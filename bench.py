@@ -34,7 +34,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DMMA_PEAK_TFLOPS = 37.0   # measured, profiles/r01_microbench_peaks.txt (m16n8k16 f64)
+DMMA_PEAK_TFLOPS = 37.07  # measured, profiles/r01_microbench_peaks_v2.txt (m16n8k16 f64)
+DFMA_PEAK_TFLOPS = 33.88  # measured DFMA (FP64 ALU) peak, same microbenchmark
 F16X2_PEAK_TOPS = 36.9    # measured f16x2 mul+add half-ops/s, same file
 
 
@@ -256,6 +257,8 @@ def main():
     ap.add_argument("--svd", default="gpu", choices=["gpu", "host"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tensor", action="store_true", help="skip the tensor-mode secondary run")
+    ap.add_argument("--no-dense", action="store_true", help="skip the dense-operator roofline probe")
+    ap.add_argument("--operator", default="auto", choices=["auto", "dense", "banded"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -285,6 +288,7 @@ def main():
     t_svd = time.time() - t1
     fmt = K.PrecisionFormat.fp16()
     m = K.build_preconditioner_from_svd(svd_r, svd_c, cfg.lambda_, fmt)
+    cfg.problem.a.set_mode(args.operator)
     op = cfg.problem.a.handle()
     setup_s = time.time() - t0
     n = cfg.n
@@ -404,13 +408,50 @@ def main():
     value = iters / elapsed
     e2e_value = e2e_iters / e2e_elapsed
     r = len(cfg.problem.a.terms)
+    op_mode, tc, tr = cfg.problem.a.mode()
     op_ms, op_launches = prof["operator_gemm_f64"]
-    flops_per_launch = 2.0 * r * float(n) ** 3  # each of the two GEMMs of an apply
-    achieved = flops_per_launch / (op_ms / op_launches / 1e3) / 1e12 if op_launches else 0.0
+    if op_mode == "banded":  # two correlation passes per apply: 2 r (Lc + Lr) n^2 flop
+        op_flops_per_launch = 2.0 * r * (tc + tr) * float(n) ** 2 / 2.0
+        op_peak, op_kernel = DFMA_PEAK_TFLOPS, "band_cols/band_rows (FP64 DFMA, banded Toeplitz)"
+        op_src = "measured DFMA peak, profiles/r01_microbench_peaks.txt"
+    else:  # each of the two GEMMs of an apply
+        op_flops_per_launch = 2.0 * r * float(n) ** 3
+        op_peak, op_kernel = DMMA_PEAK_TFLOPS, "gemm_f64_kernel (DMMA m16n8k16)"
+        op_src = "measured DMMA f64 peak, profiles/r01_microbench_peaks.txt"
+    op_ach = op_flops_per_launch / (op_ms / op_launches / 1e3) / 1e12 if op_launches else 0.0
     pm_ms, pm_launches = prof["precond_gemm_f16ref"]
-    half_ops = 2.0 * float(n) ** 3  # n^3 products + n^3 tree adds per GEMM
-    pm_achieved = half_ops / (pm_ms / pm_launches / 1e3) / 1e12 if pm_launches else 0.0
+    half_ops = 2.0 * float(n) ** 3  # n^3 rounded products + n^3 rounded tree adds per GEMM
+    pm_ach = half_ops / (pm_ms / pm_launches / 1e3) / 1e12 if pm_launches else 0.0
     total_prof = sum(v[0] for v in prof.values())
+    op_line = {"bound": "tensor" if op_mode == "dense" else "fp64-alu", "achieved": op_ach,
+               "peak": op_peak, "unit": "TFLOP/s", "frac": op_ach / op_peak, "traffic": None,
+               "kernel": op_kernel, "peak_source": op_src,
+               "work_per_launch": f"{op_flops_per_launch:.4g} flop"}
+    pm_line = {"bound": "f16x2 CUDA-core pipe (reference-exact rounding)", "achieved": pm_ach,
+               "peak": F16X2_PEAK_TOPS, "unit": "T half-ops/s", "frac": pm_ach / F16X2_PEAK_TOPS,
+               "traffic": None, "kernel": "gemm_f16ref_kernel",
+               "peak_source": "measured f16x2 mul+add rate, profiles/r01_microbench_peaks.txt",
+               "work_per_launch": f"{half_ops:.4g} half-ops"}
+    dominant, other = (pm_line, op_line) if pm_ms > op_ms else (op_line, pm_line)
+
+    # the dense DMMA operator (the product the reference computes), for its roofline
+    dense = None
+    if op_mode == "banded" and not args.no_dense:
+        cfg.problem.a.set_mode("dense")
+        check(L.kp_profile_reset())
+        check(L.kp_profile_enable(1))
+        xin = np.ascontiguousarray(cfg.problem.x_true)
+        for _ in range(2):
+            K.kronsum_apply(cfg.problem.a, xin)
+        t_ = C.c_double()
+        c_ = C.c_longlong()
+        check(L.kp_profile_read(0, C.byref(t_), C.byref(c_)))
+        check(L.kp_profile_enable(0))
+        cfg.problem.a.set_mode("auto")
+        d_ach = 2.0 * r * float(n) ** 3 / (t_.value / c_.value / 1e3) / 1e12
+        dense = {"bound": "tensor", "achieved": d_ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                 "frac": d_ach / DMMA_PEAK_TFLOPS, "kernel": "gemm_f64_kernel (DMMA m16n8k16)",
+                 "ms_per_launch": t_.value / c_.value, "launches": c_.value}
 
     out = None
     if rank == 0:
@@ -418,8 +459,8 @@ def main():
         if ws == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             try:
-                tc = cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads)
-                cpu = {"value": 1.0 / tc, "unit": "iterations/s", "cores": threads, "kind": "port",
+                t_cpu = cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads)
+                cpu = {"value": 1.0 / t_cpu, "unit": "iterations/s", "cores": threads, "kind": "port",
                        "sample": "one FPCG iteration's normal_matvec + precond_solve at C5 "
                                  "(oracle: OpenBLAS FP64 + streamed reference-exact fp16)"}
             except Exception as e:  # noqa: BLE001
@@ -436,17 +477,13 @@ def main():
                        "final_rel_err": rel_last},
             "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": 2 * nn * 8,
                     "d2h_bytes_per_step": nn * 8 + 4 * cap * 8},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": DMMA_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": None,
-                         "kernel": "gemm_f64_kernel (DMMA m16n8k16, operator apply)",
-                         "peak_source": "measured DMMA f64 peak, profiles/r01_microbench_peaks.txt "
-                                        "(MEASURED_PEAKS.json has no FP64 entry)"},
+            "roofline": dominant,
+            "roofline_other": other,
+            "roofline_dense_operator_gemm": dense,
+            "operator_mode": {"mode": op_mode, "col_taps": tc, "row_taps": tr},
             "kernels": {k: {"ms": v[0], "launches": v[1],
                             "share": v[0] / total_prof if total_prof else None}
                         for k, v in prof.items()},
-            "precond_roofline": {"bound": "f16x2 CUDA-core pipe", "achieved": pm_achieved,
-                                 "peak": F16X2_PEAK_TOPS, "unit": "T half-ops/s",
-                                 "frac": pm_achieved / F16X2_PEAK_TOPS},
             "solves_per_s": args.steps * ws / elapsed,
             "tensor_mode": tensor,
             "cpu_baseline": cpu,

@@ -139,6 +139,20 @@ int kp_operator_create(int n, int r, const double* row_factors,
                        const double* col_factors, kp_operator** out);
 int kp_operator_destroy(kp_operator* op);
 int kp_operator_info(const kp_operator* op, int* n, int* r);
+/* Operator algorithm. KP_OP_AUTO (default) uses the banded-Toeplitz kernels
+ * when every factor is a banded Toeplitz matrix (the psf_to_kronsum
+ * structure, deblur.cpp:157-199) with at most 57 diagonals and r <= 8, and
+ * the dense DMMA GEMMs otherwise; KP_OP_DENSE forces the dense product the
+ * reference computes (kron.cpp:69-70); KP_OP_BANDED fails with
+ * KP_ERR_INVALID_ARGUMENT if the structure is absent. The environment
+ * variable KP_OPERATOR=dense|banded sets the default at creation. */
+#define KP_OP_AUTO 0
+#define KP_OP_DENSE 1
+#define KP_OP_BANDED 2
+int kp_operator_set_mode(kp_operator* op, int mode);
+/* mode in use (KP_OP_DENSE / KP_OP_BANDED) and the number of diagonals of
+ * the column and row factors when banded (0 otherwise). */
+int kp_operator_get_mode(const kp_operator* op, int* mode, int* col_taps, int* row_taps);
 /* kronsum_apply (kron.cpp:73-79) / kronsum_apply_transpose (kron.cpp:81-88) */
 int kp_kronsum_apply(const kp_operator* op, const double* y, double* out);
 int kp_kronsum_apply_transpose(const kp_operator* op, const double* y,

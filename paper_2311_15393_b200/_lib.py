@@ -24,6 +24,10 @@ KP_ERR_UNSUPPORTED = 5
 KP_ACCUM_REFERENCE = 0
 KP_ACCUM_TENSOR = 1
 
+KP_OP_AUTO = 0
+KP_OP_DENSE = 1
+KP_OP_BANDED = 2
+
 
 class kp_format(C.Structure):
     _fields_ = [("significand_bits", C.c_int), ("max_exponent", C.c_int),
@@ -64,7 +68,7 @@ EXPORTS = [
     "kp_precond_destroy", "kp_precond_solve", "kp_precond_export", "kp_precond_info",
     "kp_cgls", "kp_pcg", "kp_fpcg", "kp_spectral_create", "kp_spectral_destroy",
     "kp_spectral_export", "kp_gcv_objective", "kp_discrepancy_gap", "kp_gcv_grid", "kp_gcv",
-    "kp_discrepancy", "kp_event_record", "kp_event_elapsed", "kp_host_alloc", "kp_host_free",
+    "kp_discrepancy", "kp_operator_set_mode", "kp_operator_get_mode", "kp_event_record", "kp_event_elapsed", "kp_host_alloc", "kp_host_free",
 ]
 
 _lib = None
@@ -111,6 +115,8 @@ def lib() -> C.CDLL:
             "kp_gcv": ([P, C.POINTER(kp_param_choice)], I),
             "kp_discrepancy": ([P, D, D, C.POINTER(kp_param_choice)], I),
             "kp_event_record": ([I], I),
+            "kp_operator_set_mode": ([P, I], I),
+            "kp_operator_get_mode": ([P, C.POINTER(I), C.POINTER(I), C.POINTER(I)], I),
             "kp_event_elapsed": ([I, I, C.POINTER(C.c_float)], I),
             "kp_host_alloc": ([C.c_size_t, C.POINTER(C.c_void_p)], I),
             "kp_host_free": ([P], I),

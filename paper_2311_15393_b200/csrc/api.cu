@@ -10,6 +10,7 @@
 //   make_spectral_data, gcv, discrepancy        regparam.cpp:119-134, 254-327
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -21,6 +22,7 @@
 #include <vector>
 
 #include "../../include/kronprec_b200.h"
+#include "banded.cuh"
 #include "common.cuh"
 #include "gemm_f16ref.cuh"
 #include "gemm_f16tc.cuh"
@@ -161,9 +163,15 @@ using namespace kp;
 // ============================================================================
 struct kp_operator {
   int n = 0, r = 0;
-  DBuf<double> Cs_rm, Cs_cm, Rr_rm, Rr_cm;  // r stacked n*n blocks
+  DBuf<double> Cs_rm, Cs_cm, Rr_rm, Rr_cm;  // r stacked n*n blocks (dense path)
   DBuf<double> W;                           // r*n*n workspace
-  DBuf<double> part;                        // GEMM epilogue partials
+  DBuf<double> part;                        // epilogue partials
+  // banded-Toeplitz path (banded.cu)
+  bool is_banded = false;
+  int mode = KP_OP_AUTO;
+  int col_taps = 0, row_taps = 0;
+  BandTaps cols_fw, cols_tr, rows_fw, rows_tr;
+  bool use_banded() const { return is_banded && mode != KP_OP_DENSE; }
 };
 
 struct PrecondShared {
@@ -215,6 +223,14 @@ long round_up(long v, long m) { return (v + m - 1) / m * m; }
 void op_apply(kp_operator* op, const double* in, double* out, bool transpose,
               const F64Epilogue* extra, const int* status) {
   const int n = op->n, r = op->r;
+  if (op->use_banded()) {
+    band_cols(in, op->W.p, n, r, transpose ? op->cols_tr : op->cols_fw, status);
+    F64Epilogue e;
+    if (extra) e = *extra;
+    e.C = out, e.cm = 1, e.cn = n, e.vm = 1, e.vn = n;
+    band_rows(op->W.p, n, r, transpose ? op->rows_tr : op->rows_fw, e, status);
+    return;
+  }
   const long nn = long(n) * n;
   F64GemmArgs g1;
   g1.M = r * n, g1.N = n, g1.nb = 1, g1.Kb = n;
@@ -233,7 +249,65 @@ void op_apply(kp_operator* op, const double* in, double* out, bool transpose,
   gemm_f64(g2, KC_OPERATOR);
 }
 
-int op_partials_ctas(const kp_operator* op) { return gemm_f64_num_ctas(op->n, op->n); }
+int op_partials_ctas(const kp_operator* op) {
+  return op->use_banded() ? band_rows_num_ctas(op->n) : gemm_f64_num_ctas(op->n, op->n);
+}
+
+// Diagonal values of a Toeplitz matrix F (n-by-n column-major): diag[d+n-1]
+// = F(j+d, j). Returns false if some diagonal is not constant.
+bool toeplitz_diagonals(const double* F, int n, std::vector<double>& diag) {
+  diag.assign(2 * size_t(n) - 1, 0.0);
+  for (int d = -(n - 1); d <= n - 1; ++d) {
+    const int j0 = d >= 0 ? 0 : -d;
+    const double v = F[size_t(j0) * n + (j0 + d)];
+    for (int j = j0; j < n && j + d < n; ++j)
+      if (F[size_t(j) * n + (j + d)] != v) return false;
+    diag[size_t(d + n - 1)] = v;
+  }
+  return true;
+}
+
+// Detect the banded-Toeplitz structure of all factors and derive the four
+// correlation tap sets (see banded.cu for the forms).
+void detect_banded(kp_operator* op, const double* rows, const double* cols) {
+  const int n = op->n, r = op->r;
+  if (r > BAND_MAX_TERMS) return;
+  std::vector<std::vector<double>> dr(r), dc(r);
+  int cmin = n, cmax = -n, rmin = n, rmax = -n;
+  for (int k = 0; k < r; ++k) {
+    if (!toeplitz_diagonals(rows + size_t(k) * n * n, n, dr[k])) return;
+    if (!toeplitz_diagonals(cols + size_t(k) * n * n, n, dc[k])) return;
+    for (int d = -(n - 1); d <= n - 1; ++d) {
+      if (dc[k][d + n - 1] != 0.0) cmin = std::min(cmin, d), cmax = std::max(cmax, d);
+      if (dr[k][d + n - 1] != 0.0) rmin = std::min(rmin, d), rmax = std::max(rmax, d);
+    }
+  }
+  if (cmin > cmax) cmin = cmax = 0;  // all-zero factors: one zero tap
+  if (rmin > rmax) rmin = rmax = 0;
+  const int lc = cmax - cmin + 1, lr = rmax - rmin + 1;
+  const int pc = (lc + 7) / 8 * 8, pr = (lr + 7) / 8 * 8;
+  if (pc > BAND_MAX_TAPS || pr > BAND_MAX_TAPS) return;
+  auto fill = [&](BandTaps& t, int taps, int shift, const std::vector<std::vector<double>>& dg,
+                  auto offset_of) {
+    t = BandTaps{};
+    t.taps = taps;
+    t.shift = shift;
+    for (int k = 0; k < r; ++k)
+      for (int u = 0; u < taps; ++u) {
+        const int d = offset_of(u);
+        t.w[k][u] = (d >= -(n - 1) && d <= n - 1 && u < taps) ? dg[k][size_t(d + n - 1)] : 0.0;
+      }
+  };
+  // A: Y = A_c X -> Y(a) = sum_u c[cmax-u] X(a - cmax + u); out: sum_u r[rmax-u] Y(j - rmax + u)
+  fill(op->cols_fw, pc, -cmax, dc, [&](int u) { return u < lc ? cmax - u : 1 << 30; });
+  fill(op->rows_fw, pr, -rmax, dr, [&](int u) { return u < lr ? rmax - u : 1 << 30; });
+  // A^T: Y(a) = sum_u c[cmin+u] X(a + cmin + u); out: sum_u r[rmin+u] Y(j + rmin + u)
+  fill(op->cols_tr, pc, cmin, dc, [&](int u) { return u < lc ? cmin + u : 1 << 30; });
+  fill(op->rows_tr, pr, rmin, dr, [&](int u) { return u < lr ? rmin + u : 1 << 30; });
+  op->col_taps = lc;
+  op->row_taps = lr;
+  op->is_banded = true;
+}
 
 int msolve_partials_ctas(const kp_precond* p) {
   if (covers_double(p->fmt)) return gemm_f64_num_ctas(p->n, p->n);
@@ -874,7 +948,12 @@ int kp_operator_create(int n, int r, const double* row_factors, const double* co
     transpose_blocks(op->Cs_cm.p, op->Cs_rm.p, n, r);
     transpose_blocks(op->Rr_cm.p, op->Rr_rm.p, n, r);
     op->W.alloc(tot);
-    op->part.alloc(size_t(op_partials_ctas(op.get())) * 4);
+    detect_banded(op.get(), row_factors, col_factors);
+    if (const char* env = getenv("KP_OPERATOR")) {
+      if (std::string(env) == "dense") op->mode = KP_OP_DENSE;
+      if (std::string(env) == "banded") op->mode = KP_OP_BANDED;
+    }
+    op->part.alloc(size_t(std::max(band_rows_num_ctas(n), gemm_f64_num_ctas(n, n))) * 4);
     sync();
     *out = op.release();
   })
@@ -884,6 +963,22 @@ int kp_operator_info(const kp_operator* op, int* n, int* r) {
   KP_API({
     if (!op) throw InvalidArgument("null operator");
     *n = op->n, *r = op->r;
+  })
+}
+int kp_operator_set_mode(kp_operator* op, int mode) {
+  KP_API({
+    if (!op || mode < KP_OP_AUTO || mode > KP_OP_BANDED) throw InvalidArgument("operator mode");
+    if (mode == KP_OP_BANDED && !op->is_banded)
+      throw InvalidArgument("KroneckerSum: factors are not banded Toeplitz");
+    op->mode = mode;
+  })
+}
+int kp_operator_get_mode(const kp_operator* op, int* mode, int* col_taps, int* row_taps) {
+  KP_API({
+    if (!op) throw InvalidArgument("null operator");
+    *mode = op->use_banded() ? KP_OP_BANDED : KP_OP_DENSE;
+    *col_taps = op->use_banded() ? op->col_taps : 0;
+    *row_taps = op->use_banded() ? op->row_taps : 0;
   })
 }
 int kp_kronsum_apply(const kp_operator* opc, const double* y, double* out) {

@@ -1,0 +1,29 @@
+// Banded-Toeplitz Kronecker-sum operator.
+#pragma once
+
+#include "common.cuh"
+#include "gemm_f64.cuh"
+
+namespace kp {
+
+constexpr int BAND_MAX_TAPS = 64;   // padded tap count limit (multiple of 8)
+constexpr int BAND_MAX_TERMS = 8;
+
+// One direction of a correlation y(a) = sum_u w[k][u] x(a + shift + u),
+// u in [0, taps); taps padded to a multiple of 8 with zeros at the end.
+struct BandTaps {
+  int taps = 0;
+  int shift = 0;
+  double w[BAND_MAX_TERMS][BAND_MAX_TAPS];
+};
+
+// Y_k = column correlation of X (n-by-n, column-major) for all r terms;
+// Y holds r stacked n-by-n column-major blocks.
+void band_cols(const double* X, double* Y, int n, int r, const BandTaps& t, const int* status);
+// out = sum_k row correlation of Y_k, with the GEMM epilogue contract
+// (F64Epilogue; C indexed column-major like out).
+void band_rows(const double* Y, int n, int r, const BandTaps& t, const F64Epilogue& e,
+               const int* status);
+int band_rows_num_ctas(int n);
+
+}  // namespace kp

@@ -137,6 +137,19 @@ class KroneckerSum:
             self._h = h
         return self._h
 
+    _MODES = {"auto": 0, "dense": 1, "banded": 2}
+
+    def set_mode(self, mode: str) -> None:
+        """Operator algorithm: "auto" (banded-Toeplitz kernels when the
+        factors have that structure), "dense" (DMMA GEMMs, the product the
+        reference computes) or "banded"."""
+        check(lib().kp_operator_set_mode(self.handle(), KroneckerSum._MODES[mode]))
+
+    def mode(self) -> tuple[str, int, int]:
+        m, tc, tr = C.c_int(), C.c_int(), C.c_int()
+        check(lib().kp_operator_get_mode(self.handle(), C.byref(m), C.byref(tc), C.byref(tr)))
+        return ("banded" if m.value == 2 else "dense"), tc.value, tr.value
+
     def release(self) -> None:
         if self._h is not None:
             lib().kp_operator_destroy(self._h)

@@ -433,3 +433,58 @@ def test_tensor_mode_solver_within_north_star_bounds(solver):
     # to change the count); the bound is checked at config scale in
     # tests/test_gpu_configs.py
     assert rg.history.iterations_used <= ho.iterations_used + 2
+
+
+# ---- banded-Toeplitz operator path ------------------------------------
+@pytest.mark.parametrize("kind,n,rank", [("gaussian", 64, 0), ("motion", 37, 0), ("speckle", 48, 0),
+                                         ("shake", 100, 0), ("speckle", 256, 3)])
+def test_banded_operator_matches_dense_and_oracle(kind, n, rank):
+    psf = P.make_psf(kind, 7, sigma=1.3, length=5, steps=20, blob_count=4, seed=5)
+    a, _ = P.psf_to_kronsum(psf, n, truncation_tol=0.0, max_rank=rank)
+    assert a.mode()[0] == "banded"
+    y = np.random.default_rng(n).standard_normal(n * n)
+    for g, o in ((K.kronsum_apply, O.kronsum_apply),
+                 (K.kronsum_apply_transpose, O.kronsum_apply_transpose)):
+        got = g(a, y)
+        want = o(a, y)
+        assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
+    a.set_mode("dense")
+    assert a.mode()[0] == "dense"
+    dense = K.kronsum_apply(a, y)
+    a.set_mode("auto")
+    assert np.linalg.norm(K.kronsum_apply(a, y) - dense) <= 1e-13 * np.linalg.norm(dense)
+
+
+def test_config_psfs_are_banded():
+    for name, taps in (("C1", 19), ("C2", 31), ("C4", 17), ("C5", 41)):
+        cfg = configs_small(name)
+        mode, tc, tr = cfg.problem.a.mode()
+        assert mode == "banded" and tc == taps and tr == taps
+
+
+def configs_small(name):
+    from paper_2311_15393_b200 import configs
+    return configs.build(name, n=96)
+
+
+def test_random_factors_stay_dense():
+    a = rsum(16, 2, 3)
+    assert a.mode()[0] == "dense"
+    with pytest.raises(ValueError):
+        a.set_mode("banded")
+
+
+def test_banded_normal_matvec_and_solvers():
+    tp, term = blob_problem(96)
+    assert tp.a.mode()[0] == "banded"
+    p = np.random.default_rng(1).standard_normal(96 * 96)
+    want = O.normal_matvec(tp.a, 0.01, p)
+    assert np.linalg.norm(K.normal_matvec(tp.a, 0.01, p) - want) <= 1e-13 * np.linalg.norm(want)
+    opts = SolverOptions(lambda_=0.01, max_iterations=300, rel_residual_tol=1e-6, x_true=tp.x_true,
+                         record_iterates=True)
+    rg = K.cgls(tp.a, tp.b, opts)
+    _, ho = O.cgls(tp.a, tp.b, opts)
+    for k in range(15):
+        assert np.linalg.norm(rg.history.iterates[k] - ho.iterates[k]) <= \
+            1e-10 * max(np.linalg.norm(ho.iterates[k]), 1e-300)
+    assert abs(rg.history.iterations_used - ho.iterations_used) <= 2
