@@ -19,10 +19,12 @@
 // k, so A is broadcast (PRMT) and all tree adds are vertical.
 #include "gemm_f16ref.cuh"
 
+#include <cstdlib>
+
 namespace kp {
 namespace {
 
-constexpr int BM = 32, BN = 64, BKH = 64, THREADS = 128, STAGES = 3;
+constexpr int BM = 32, BN = 64, BKH = 64, THREADS = 128;
 constexpr int ROW_BYTES = BKH * 2;  // 128
 constexpr int STAGE_BYTES = (BM + BN) * ROW_BYTES;
 constexpr int NACC = 8;  // 4 m-rows x 2 n-pairs per thread
@@ -66,6 +68,10 @@ __device__ __forceinline__ uint32_t part(const uint4& v, int q) {
   return q == 0 ? v.x : q == 1 ? v.y : q == 2 ? v.z : v.w;
 }
 
+// STAGES: cp.async pipeline depth. UNIT: leaves per value pushed into the
+// shared-memory counter stack (16: levels >= 4 in smem; 32: level 4 also in
+// registers, one smem level less).
+template <int STAGES, int UNIT>
 __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs args, int levels) {
   if (args.status && *args.status != 0) return;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -112,8 +118,14 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
     cp_async_commit();
   }
 
-  uint32_t l3[NACC];
-  int c16 = 0;  // 16-leaf values pushed so far
+  uint32_t l3[NACC], l4[NACC];
+  int c16 = 0;  // UNIT-leaf values pushed so far
+  // Per-thread constants: rows tm + 8i (A) all share (row & 7) = tm, rows
+  // tn + 16j (B) share tn & 7, so the swizzled chunk offset of sub-chunk s is
+  // (s << 4) ^ x for one x per operand; the row offsets are immediates.
+  const uint32_t a_off = uint32_t(tm * ROW_BYTES), b_off = uint32_t(BM * ROW_BYTES + tn * ROW_BYTES);
+  const uint32_t xa = uint32_t((tm & 7) << 4), xb = uint32_t((tn & 7) << 4);
+  uint32_t* const my_stack = stack + tid;
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
@@ -122,21 +134,16 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
       if (nk < KT) load_tile(nk, nk % STAGES);
       cp_async_commit();
     }
-    const uint32_t sa = sbase + uint32_t((kt % STAGES) * STAGE_BYTES);
-    const uint32_t sb = sa + uint32_t(BM * ROW_BYTES);
-#pragma unroll 1
+    const uint32_t st = sbase + uint32_t((kt % STAGES) * STAGE_BYTES);
+    const uint32_t sa = st + a_off, sb = st + b_off;
+#pragma unroll
     for (int sub = 0; sub < 8; ++sub) {  // 8-leaf sub-chunk = one 16-byte smem chunk
+      const uint32_t ca = uint32_t(sub << 4) ^ xa, cb = uint32_t(sub << 4) ^ xb;
       uint4 af[4], bfr[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int row = tm + 8 * i;
-        af[i] = lds128(sa + uint32_t(row * ROW_BYTES + ((sub ^ (row & 7)) << 4)));
-      }
+      for (int i = 0; i < 4; ++i) af[i] = lds128(sa + ca + uint32_t(i * 8 * ROW_BYTES));
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int row = tn + 16 * j;
-        bfr[j] = lds128(sb + uint32_t(row * ROW_BYTES + ((sub ^ (row & 7)) << 4)));
-      }
+      for (int j = 0; j < 4; ++j) bfr[j] = lds128(sb + cb + uint32_t(j * 16 * ROW_BYTES));
       uint32_t v8[NACC];
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
@@ -148,33 +155,41 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          uint32_t s[4];
+          uint32_t s4[4];
 #pragma unroll
           for (int kp = 0; kp < 4; ++kp) {
             const uint32_t a = part(af[i], kp);
             const uint32_t p0 = hmul2(bcast_lo(a), blo[kp]);  // leaf k = 2kp
             const uint32_t p1 = hmul2(bcast_hi(a), bhi[kp]);  // leaf k = 2kp+1
-            s[kp] = hadd2(p0, p1);
+            s4[kp] = hadd2(p0, p1);
           }
-          v8[i * 2 + p] = hadd2(hadd2(s[0], s[1]), hadd2(s[2], s[3]));
+          v8[i * 2 + p] = hadd2(hadd2(s4[0], s4[1]), hadd2(s4[2], s4[3]));
         }
       }
       if ((sub & 1) == 0) {
 #pragma unroll
         for (int q = 0; q < NACC; ++q) l3[q] = v8[q];
+      } else if (UNIT == 32 && (sub & 3) == 1) {
+#pragma unroll
+        for (int q = 0; q < NACC; ++q) l4[q] = hadd2(l3[q], v8[q]);
       } else {
         uint32_t v[NACC];
 #pragma unroll
         for (int q = 0; q < NACC; ++q) v[q] = hadd2(l3[q], v8[q]);
-        int L = 0, cnt = c16;
+        if (UNIT == 32) {
+#pragma unroll
+          for (int q = 0; q < NACC; ++q) v[q] = hadd2(l4[q], v[q]);
+        }
+        uint32_t* lvl = my_stack;
+        int cnt = c16;
         while (cnt & 1) {  // uniform across the CTA
 #pragma unroll
-          for (int q = 0; q < NACC; ++q) v[q] = hadd2(stack[(L * NACC + q) * THREADS + tid], v[q]);
+          for (int q = 0; q < NACC; ++q) v[q] = hadd2(lvl[q * THREADS], v[q]);
           cnt >>= 1;
-          ++L;
+          lvl += NACC * THREADS;
         }
 #pragma unroll
-        for (int q = 0; q < NACC; ++q) stack[(L * NACC + q) * THREADS + tid] = v[q];
+        for (int q = 0; q < NACC; ++q) lvl[q * THREADS] = v[q];
         ++c16;
       }
     }
@@ -255,6 +270,33 @@ __global__ void fill_u16_kernel(unsigned short* p, size_t n, unsigned short bits
     p[i] = bits;
 }
 
+template <int STAGES, int UNIT>
+void launch_f16ref(const F16GemmArgs& a, int kernel_class) {
+  const int kt = (a.K + BKH - 1) / BKH;
+  const int units = kt * (BKH / UNIT);
+  int levels = 1;
+  while ((1 << levels) <= units) ++levels;
+  const size_t smem = size_t(STAGES) * STAGE_BYTES + size_t(levels) * NACC * THREADS * 4;
+  auto kern = gemm_f16ref_kernel<STAGES, UNIT>;
+  static size_t attr_smem = 0;
+  if (smem > attr_smem) {
+    KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_smem = smem;
+  }
+  LaunchScope scope(kernel_class);
+  const unsigned grid = cdiv(a.M, BM) * cdiv(a.N, BN);
+  kern<<<grid, THREADS, smem, ctx().stream>>>(a, levels);
+  check_launch("gemm_f16ref");
+}
+
+int f16ref_cfg() {
+  static int cfg = [] {
+    const char* e = getenv("KP_F16REF_CFG");
+    return e ? atoi(e) : 0;
+  }();
+  return cfg;
+}
+
 }  // namespace
 
 int gemm_f16ref_num_ctas(int M, int N) { return int(cdiv(M, BM) * cdiv(N, BN)); }
@@ -264,21 +306,14 @@ void gemm_f16ref(const F16GemmArgs& a, int kernel_class) {
   if (a.K <= 0) throw InvalidArgument("lp_matmul: empty input");
   if (a.A.ld % BKH || a.B.ld % BKH || a.A.ld < a.K || a.B.ld < a.K)
     throw InvalidArgument("gemm_f16ref: operand leading dimension must be a multiple of 64 >= K");
-  const int kt = (a.K + BKH - 1) / BKH;
-  const int c16 = kt * (BKH / 16);
-  int levels = 1;
-  while ((1 << levels) <= c16) ++levels;
-  const size_t smem = size_t(STAGES) * STAGE_BYTES + size_t(levels) * NACC * THREADS * 4;
-  static size_t attr_smem = 0;
-  if (smem > attr_smem) {
-    KP_CUDA(cudaFuncSetAttribute(gemm_f16ref_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)));
-    attr_smem = smem;
+  // n=4096 (profiles/r01_sweep_f16ref.txt): <3,16> 30.45, <2,32> 31.21,
+  // <3,32> 31.38, <2,16> 30.51 T half-ops/s; all bit-identical.
+  switch (f16ref_cfg()) {
+    case 1: launch_f16ref<2, 32>(a, kernel_class); break;
+    case 3: launch_f16ref<2, 16>(a, kernel_class); break;
+    case 4: launch_f16ref<3, 16>(a, kernel_class); break;
+    default: launch_f16ref<3, 32>(a, kernel_class); break;
   }
-  LaunchScope scope(kernel_class);
-  const unsigned grid = cdiv(a.M, BM) * cdiv(a.N, BN);
-  gemm_f16ref_kernel<<<grid, THREADS, smem, ctx().stream>>>(a, levels);
-  check_launch("gemm_f16ref");
 }
 
 void fill_u16(__half* p, size_t count, uint16_t bits) {
