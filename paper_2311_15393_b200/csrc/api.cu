@@ -16,6 +16,7 @@
 #include <cstring>
 #include <functional>
 #include <limits>
+#include <map>
 #include <memory>
 #include <numeric>
 #include <string>
@@ -161,8 +162,34 @@ using namespace kp;
 // ============================================================================
 // handle types
 // ============================================================================
+// Solver workspace cached per operator: device vectors, partial-sum arrays,
+// history rows, the DevState and a pinned status word, reused across solves
+// (a C5 solve would otherwise spend ~0.1 s in cudaMalloc / cudaFree).
+struct SolverWorkspace {
+  std::map<std::string, DBuf<double>> bufs;
+  DBuf<DevState> state;
+  DevState* host_state = nullptr;
+  double* get(const std::string& key, size_t count) {
+    auto& b = bufs[key];
+    if (b.n < count) b.alloc(count);
+    return b.p;
+  }
+  DevState* dev_state() {
+    if (!state.p) state.alloc(1);
+    return state.p;
+  }
+  DevState* pinned_state() {
+    if (!host_state) KP_CUDA(cudaMallocHost(&host_state, sizeof(DevState)));
+    return host_state;
+  }
+  ~SolverWorkspace() {
+    if (host_state) cudaFreeHost(host_state);
+  }
+};
+
 struct kp_operator {
   int n = 0, r = 0;
+  SolverWorkspace ws;
   DBuf<double> Cs_rm, Cs_cm, Rr_rm, Rr_cm;  // r stacked n*n blocks (dense path)
   DBuf<double> W;                           // r*n*n workspace
   DBuf<double> part;                        // epilogue partials
@@ -490,11 +517,25 @@ kp_precond* precond_from_svd(int n, std::vector<double> ur, std::vector<double> 
 struct Solve {
   kp_operator* op;
   size_t nn;
-  DBuf<DevState> st;
-  DBuf<double> resid, relerr, cosines, iterates;
+  DevState* st = nullptr;  // device
+  double *resid = nullptr, *relerr = nullptr, *cosines = nullptr, *iterates = nullptr;
   DevHistory dh{};
   int capacity = 0;
 };
+
+struct Vec {
+  double* p;
+};
+
+// Device view of a solver input: the caller's device pointer, or a copy of
+// the host buffer into the cached workspace slot `key`.
+const double* stage_vec(SolverWorkspace& ws, const char* key, const double* src, size_t nn,
+                        bool device) {
+  if (device) return src;
+  double* d = ws.get(key, nn);
+  KP_CUDA(cudaMemcpyAsync(d, src, nn * sizeof(double), cudaMemcpyHostToDevice, ctx().stream));
+  return d;
+}
 
 void check_common(const kp_operator* op, const kp_solver_options* o, kp_history* h) {
   if (!op) throw InvalidArgument("solver: null operator");
@@ -535,17 +576,18 @@ void setup_state(Solve& s, const kp_solver_options* o, bool has_xt, bool flexibl
   h.tol = o->rel_residual_tol;
   h.l2 = o->lambda * o->lambda;
   h.work_per_iter = work;
-  s.st.alloc(1);
-  s.st.upload(&h, 1);
+  SolverWorkspace& ws = s.op->ws;
+  s.st = ws.dev_state();
+  KP_CUDA(cudaMemcpyAsync(s.st, &h, sizeof(DevState), cudaMemcpyHostToDevice, ctx().stream));
   s.capacity = o->max_iterations + 1;
-  s.resid.alloc(s.capacity);
-  s.relerr.alloc(s.capacity);
-  s.cosines.alloc(s.capacity);
-  if (o->record_iterates) s.iterates.alloc(size_t(s.capacity) * s.nn);
-  s.dh.resid = s.resid.p;
-  s.dh.relerr = s.relerr.p;
-  s.dh.cosines = s.cosines.p;
-  s.dh.iterates = s.iterates.p;
+  s.resid = ws.get("h_resid", s.capacity);
+  s.relerr = ws.get("h_relerr", s.capacity);
+  s.cosines = ws.get("h_cos", s.capacity);
+  s.iterates = o->record_iterates ? ws.get("h_iterates", size_t(s.capacity) * s.nn) : nullptr;
+  s.dh.resid = s.resid;
+  s.dh.relerr = s.relerr;
+  s.dh.cosines = s.cosines;
+  s.dh.iterates = s.iterates;
   s.dh.capacity = s.capacity;
 }
 
@@ -555,7 +597,7 @@ void setup_state(Solve& s, const kp_solver_options* o, bool has_xt, bool flexibl
 // device no-ops).
 void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
   Ctx& c = ctx();
-  Pinned<DevState> hst(1);
+  DevState* hst = s.op->ws.pinned_state();
   cudaGraphExec_t exec = nullptr;
   long long per_iter_launches = 0;
   if (!c.profile) {
@@ -592,10 +634,10 @@ void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
       }
     }
     done += todo;
-    KP_CUDA(cudaMemcpyAsync(&hst.p->status, &s.st.p->status, sizeof(int), cudaMemcpyDeviceToHost,
+    KP_CUDA(cudaMemcpyAsync(&hst->status, &s.st->status, sizeof(int), cudaMemcpyDeviceToHost,
                             c.stream));
     sync();
-    if (hst.p->status != ST_RUNNING) break;
+    if (hst->status != ST_RUNNING) break;
     const double per_iter_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() /
         todo;
@@ -605,30 +647,23 @@ void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
 }
 
 void finish(Solve& s, const kp_solver_options* o, kp_history* h, double work) {
-  DevState st;
-  s.st.download(&st, 1);
+  auto d2h = [](void* dst, const void* src, size_t bytes) {
+    if (bytes) KP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx().stream));
+  };
+  DevState* pst = s.op->ws.pinned_state();
+  d2h(pst, s.st, sizeof(DevState));
   sync();
+  const DevState st = *pst;
   const int rows = std::min(st.rows, h->capacity);
-  std::vector<double> buf(std::max(rows, 1));
-  s.resid.download(buf.data(), rows);
-  sync();
-  std::memcpy(h->residual_norm, buf.data(), rows * sizeof(double));
-  if (o->x_true && h->relative_error) {
-    s.relerr.download(buf.data(), rows);
-    sync();
-    std::memcpy(h->relative_error, buf.data(), rows * sizeof(double));
-  }
-  for (int k = 0; k < rows; ++k) h->work_units[k] = work * k;
   const int ncos = std::min(st.ncos, h->capacity);
-  if (o->track_search_direction_orthogonality && h->residual_cosines && ncos > 0) {
-    s.cosines.download(h->residual_cosines, ncos);
-    sync();
-  }
-  if (o->record_iterates && h->iterates) {
-    KP_CUDA(cudaMemcpyAsync(h->iterates, s.iterates.p, size_t(rows) * s.nn * sizeof(double),
-                            cudaMemcpyDeviceToHost, ctx().stream));
-    sync();
-  }
+  d2h(h->residual_norm, s.resid, rows * sizeof(double));
+  if (o->x_true && h->relative_error) d2h(h->relative_error, s.relerr, rows * sizeof(double));
+  if (o->track_search_direction_orthogonality && h->residual_cosines && ncos > 0)
+    d2h(h->residual_cosines, s.cosines, ncos * sizeof(double));
+  if (o->record_iterates && h->iterates)
+    d2h(h->iterates, s.iterates, size_t(rows) * s.nn * sizeof(double));
+  sync();
+  for (int k = 0; k < rows; ++k) h->work_units[k] = work * k;
   h->rows = rows;
   h->n_cosines = ncos;
   h->iterations_used = st.iterations_used;
@@ -647,24 +682,21 @@ void run_pcg(kp_operator* op, const double* b_in, kp_precond* m, const kp_solver
   const int n = op->n;
   const size_t nn = size_t(n) * n;
   const bool dev = o->device_pointers != 0;
-  VecArg b(b_in, nn, dev), xt(o->x_true, nn, dev);
+  SolverWorkspace& ws = op->ws;
+  const double* b = stage_vec(ws, "b", b_in, nn, dev);
+  const double* xt = o->x_true ? stage_vec(ws, "xt", o->x_true, nn, dev) : nullptr;
   Solve s;
   s.op = op;
   s.nn = nn;
-  setup_state(s, o, xt.d != nullptr, flexible, 2.25);
-  int* status = &s.st.p->status;
-  DBuf<double> xown;
-  double* x;
-  if (dev) {
-    x = x_out;
-  } else {
-    xown.alloc(nn);
-    x = xown.p;
-  }
-  DBuf<double> r(nn), p(nn), q(nn), z(nn), rprev(flexible ? nn : 0);
+  setup_state(s, o, xt != nullptr, flexible, 2.25);
+  int* status = &s.st->status;
+  double* x = dev ? x_out : ws.get("x", nn);
+  Vec r{ws.get("r", nn)}, p{ws.get("p", nn)}, q{ws.get("q", nn)}, z{ws.get("z", nn)};
+  Vec rprev{flexible ? ws.get("rprev", nn) : nullptr}, ap{ws.get("ap", nn)};
   const int nop = op_partials_ctas(op);
   const int nms = msolve_partials_ctas(m);
-  DBuf<double> part_op(size_t(nop) * 4), part_vec(size_t(VEC_CTAS) * 4), part_xt(size_t(VEC_CTAS) * 4);
+  Vec part_op{ws.get("part_op", size_t(nop) * 4)}, part_vec{ws.get("part_vec", size_t(VEC_CTAS) * 4)};
+  Vec part_xt{ws.get("part_xt", size_t(VEC_CTAS) * 4)};
   const bool fp16 = !covers_double(m->fmt);
 
   vec_zero(x, nn);
@@ -672,15 +704,14 @@ void run_pcg(kp_operator* op, const double* b_in, kp_precond* m, const kp_solver
   e.d0_self = 1;
   e.d0 = r.p;  // any non-null: self product
   e.partials = part_op.p;
-  op_apply(op, b.d, r.p, true, &e, status);  // r = A^T b, ||r||^2 partials
-  if (xt.d) vec_dot_partials(xt.d, xt.d, nn, part_xt.p);
-  pcg_init_scalar(s.st.p, s.dh, part_op.p, nop, part_xt.p, VEC_CTAS);
+  op_apply(op, b, r.p, true, &e, status);  // r = A^T b, ||r||^2 partials
+  if (xt) vec_dot_partials(xt, xt, nn, part_xt.p);
+  pcg_init_scalar(s.st, s.dh, part_op.p, nop, part_xt.p, VEC_CTAS);
   if (fp16) cast_r16(m, r.p, status);
   msolve(m, r.p, z.p, r.p, nullptr, nullptr, status);
-  pcg_init_msolve_scalar(s.st.p, m->part.p, nms);
+  pcg_init_msolve_scalar(s.st, m->part.p, nms);
   vec_copy(p.p, z.p, nn, status);
 
-  DBuf<double> ap(nn);
   auto iteration = [&]() {
     // q = A^T (A p) + lambda^2 p, with p.q partials (normal_matvec)
     op_apply(op, p.p, ap.p, false, nullptr, status);
@@ -688,18 +719,18 @@ void run_pcg(kp_operator* op, const double* b_in, kp_precond* m, const kp_solver
     ne.addv = p.p, ne.addc = o->lambda * o->lambda;
     ne.d0 = p.p, ne.partials = part_op.p;
     op_apply(op, ap.p, q.p, true, &ne, status);
-    pcg_alpha_scalar(s.st.p, part_op.p, nop);
-    pcg_update(s.st.p, s.dh, x, r.p, flexible ? rprev.p : nullptr, p.p, q.p, z.p, xt.d,
+    pcg_alpha_scalar(s.st, part_op.p, nop);
+    pcg_update(s.st, s.dh, x, r.p, flexible ? rprev.p : nullptr, p.p, q.p, z.p, xt,
                fp16 ? m->r16.p : nullptr, n, fp16 ? m->sh->ldh : 0, part_vec.p);
-    pcg_resid_scalar(s.st.p, s.dh, part_vec.p, VEC_CTAS);
+    pcg_resid_scalar(s.st, s.dh, part_vec.p, VEC_CTAS);
     msolve(m, r.p, z.p, r.p, flexible ? r.p : nullptr, flexible ? rprev.p : nullptr, status);
-    pcg_beta_scalar(s.st.p, m->part.p, nms);
-    pcg_p_update(s.st.p, p.p, z.p, nn);
+    pcg_beta_scalar(s.st, m->part.p, nms);
+    pcg_p_update(s.st, p.p, z.p, nn);
   };
   drive(s, o->max_iterations, iteration);
   finish(s, o, hist, 2.25);
   if (!dev) {
-    xown.download(x_out, nn);
+    KP_CUDA(cudaMemcpyAsync(x_out, x, nn * sizeof(double), cudaMemcpyDeviceToHost, ctx().stream));
     sync();
   }
 }
@@ -711,33 +742,30 @@ void run_cgls(kp_operator* op, const double* b_in, const kp_solver_options* o, d
   const int n = op->n;
   const size_t nn = size_t(n) * n;
   const bool dev = o->device_pointers != 0;
-  VecArg b(b_in, nn, dev), xt(o->x_true, nn, dev);
+  SolverWorkspace& ws = op->ws;
+  const double* b = stage_vec(ws, "b", b_in, nn, dev);
+  const double* xt = o->x_true ? stage_vec(ws, "xt", o->x_true, nn, dev) : nullptr;
   Solve s;
   s.op = op;
   s.nn = nn;
-  setup_state(s, o, xt.d != nullptr, false, 2.0);
-  int* status = &s.st.p->status;
-  DBuf<double> xown;
-  double* x;
-  if (dev) {
-    x = x_out;
-  } else {
-    xown.alloc(nn);
-    x = xown.p;
-  }
+  setup_state(s, o, xt != nullptr, false, 2.0);
+  int* status = &s.st->status;
+  double* x = dev ? x_out : ws.get("x", nn);
   const bool track = o->track_search_direction_orthogonality != 0;
-  DBuf<double> rt(nn), sv(nn), p(nn), q(nn), sprev(track ? nn : 0);
+  Vec rt{ws.get("r", nn)}, sv{ws.get("z", nn)}, p{ws.get("p", nn)}, q{ws.get("q", nn)};
+  Vec sprev{track ? ws.get("rprev", nn) : nullptr};
   const int nop = op_partials_ctas(op);
-  DBuf<double> part_q(size_t(nop) * 4), part_s(size_t(nop) * 4), part_vec(size_t(VEC_CTAS) * 4),
-      part_p(size_t(VEC_CTAS) * 4), part_xt(size_t(VEC_CTAS) * 4);
+  Vec part_q{ws.get("part_op", size_t(nop) * 4)}, part_s{ws.get("part_s", size_t(nop) * 4)};
+  Vec part_vec{ws.get("part_vec", size_t(VEC_CTAS) * 4)}, part_p{ws.get("part_p", size_t(VEC_CTAS) * 4)};
+  Vec part_xt{ws.get("part_xt", size_t(VEC_CTAS) * 4)};
 
   vec_zero(x, nn);
-  vec_copy(rt.p, b.d, nn, nullptr);
+  vec_copy(rt.p, b, nn, nullptr);
   F64Epilogue e;
   e.d0_self = 1, e.d0 = sv.p, e.partials = part_s.p;
   op_apply(op, rt.p, sv.p, true, &e, status);  // s = A^T rt
-  if (xt.d) vec_dot_partials(xt.d, xt.d, nn, part_xt.p);
-  cgls_init_scalar(s.st.p, s.dh, part_s.p, nop, part_xt.p, VEC_CTAS);
+  if (xt) vec_dot_partials(xt, xt, nn, part_xt.p);
+  cgls_init_scalar(s.st, s.dh, part_s.p, nop, part_xt.p, VEC_CTAS);
   vec_copy(p.p, sv.p, nn, status);
   if (track) vec_copy(sprev.p, sv.p, nn, status);
 
@@ -745,21 +773,21 @@ void run_cgls(kp_operator* op, const double* b_in, const kp_solver_options* o, d
     F64Epilogue qe;
     qe.d0_self = 1, qe.d0 = q.p, qe.partials = part_q.p;
     op_apply(op, p.p, q.p, false, &qe, status);  // q = A p, ||q||^2
-    cgls_alpha_scalar(s.st.p, part_q.p, nop, part_p.p, VEC_CTAS);
-    cgls_update(s.st.p, s.dh, x, rt.p, p.p, q.p, xt.d, nn, part_vec.p);
+    cgls_alpha_scalar(s.st, part_q.p, nop, part_p.p, VEC_CTAS);
+    cgls_update(s.st, s.dh, x, rt.p, p.p, q.p, xt, nn, part_vec.p);
     F64Epilogue se;  // s = A^T rt - lambda^2 x, ||s||^2 and s.s_prev
     se.addv = x, se.addc = -(o->lambda * o->lambda);
     se.d0_self = 1, se.d0 = sv.p;
     se.d1a = track ? sprev.p : nullptr;
     se.partials = part_s.p;
     op_apply(op, rt.p, sv.p, true, &se, status);
-    cgls_resid_scalar(s.st.p, s.dh, part_s.p, nop, part_vec.p, VEC_CTAS);
-    cgls_p_update(s.st.p, p.p, sv.p, track ? sprev.p : nullptr, nn, part_p.p);
+    cgls_resid_scalar(s.st, s.dh, part_s.p, nop, part_vec.p, VEC_CTAS);
+    cgls_p_update(s.st, p.p, sv.p, track ? sprev.p : nullptr, nn, part_p.p);
   };
   drive(s, o->max_iterations, iteration);
   finish(s, o, hist, 2.0);
   if (!dev) {
-    xown.download(x_out, nn);
+    KP_CUDA(cudaMemcpyAsync(x_out, x, nn * sizeof(double), cudaMemcpyDeviceToHost, ctx().stream));
     sync();
   }
 }
