@@ -193,11 +193,15 @@ def run_c4(args):
     per image: spectral data, discrepancy lambda, with_lambda, PCG (fp16)."""
     ws, rank, local = dist_env()
     import torch
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     from paper_2311_15393_b200._lib import check, lib
     from paper_2311_15393_b200.batch import C4Shard, gather_results, reduce_timing, shard
     L = lib()
@@ -216,7 +220,8 @@ def run_c4(args):
         results = [sh.solve(i, probs[i]) for i in mine]  # each call ends synchronised
         elapsed = time.perf_counter() - t0
     launches = L.kp_launch_count() - launches0
-    elapsed, solved = reduce_timing(elapsed, float(len(results)), dist, device="cuda")
+    elapsed, solved = reduce_timing(elapsed, float(len(results)), dist,
+                                    device="cuda" if args.dist_backend == "nccl" else "cpu")
     allres = gather_results(results, dist)
     if rank == 0:
         its = [r["iterations"] for r in allres]
@@ -259,6 +264,8 @@ def main():
     ap.add_argument("--no-tensor", action="store_true", help="skip the tensor-mode secondary run")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense-operator roofline probe")
     ap.add_argument("--operator", default="auto", choices=["auto", "dense", "banded"])
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="collective backend for timing reduction / result gather")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -268,11 +275,15 @@ def main():
 
     ws, rank, local = dist_env()
     import torch
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     import paper_2311_15393_b200 as K
     from paper_2311_15393_b200._lib import check, lib, ptr
@@ -395,16 +406,16 @@ def main():
     barrier()
     e2e_elapsed = e2e_ms.value / 1e3
 
-    if dist:
-        t = torch.tensor([elapsed, e2e_elapsed], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed, e2e_elapsed = float(t[0]), float(t[1])
-        c = torch.tensor([iters, e2e_iters], device="cuda", dtype=torch.float64)
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
-        iters, e2e_iters = int(c[0]), int(c[1])
-        g = [None] * ws
-        dist.all_gather_object(g, {"rank": rank, "rel_err": rel_last})
+    if dist:  # max time over ranks, summed work; per-image results gathered to all
+        from paper_2311_15393_b200.batch import gather_results, reduce_timing
+        dev = "cuda" if args.dist_backend == "nccl" else "cpu"
+        elapsed, iters = reduce_timing(elapsed, float(iters), dist, device=dev)
+        e2e_elapsed, e2e_iters = reduce_timing(e2e_elapsed, float(e2e_iters), dist, device=dev)
+        iters, e2e_iters = int(iters), int(e2e_iters)
+        per_rank = gather_results([{"image": rank, "rel_err": rel_last}], dist)
 
+    if not dist:
+        per_rank = None
     value = iters / elapsed
     e2e_value = e2e_iters / e2e_elapsed
     r = len(cfg.problem.a.terms)
@@ -473,6 +484,7 @@ def main():
             "dtype": "f64 (operator, vectors) + f16 (preconditioner, reference-exact)",
             "data": "synthetic (seeded blob images, BASELINE C5 PSF)",
             "config": {**workload_config(cfg), "parallelism": f"replicas x{ws}",
+                       "per_rank_final_rel_err": ([d["rel_err"] for d in per_rank] if dist else None),
                        "iterations_per_solve": iters // max(1, args.steps * ws),
                        "final_rel_err": rel_last},
             "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": 2 * nn * 8,

@@ -61,7 +61,7 @@ def build(name: str, image: int = 0, n: int | None = None) -> Config:
         xs, ns = 4000 + image, 5000 + image
         noise = [0.001, 0.01, 0.05][image % 3]
     else:
-        xs, ns = 1000 + cfg_id, 2000 + cfg_id
+        xs, ns = 1000 + cfg_id + 100 * image, 2000 + cfg_id + 100 * image  # image>0: replicas
         noise = {"C1": 0.01, "C2": 0.01, "C3": 0.005, "C5": 0.01}[name]
     tp = P.make_test_problem(P.blob_image(n, xs), psf, noise, ns, a=a)
     if name == "C1":

@@ -395,15 +395,27 @@ void msolve(kp_precond* p, const double* r, double* z, const double* d0, const d
   auto gemm = p->accum == KP_ACCUM_TENSOR ? gemm_f16tc : gemm_f16ref;
   F16GemmArgs g;
   g.M = n, g.N = n, g.K = n, g.status = status;
-  g.A = {sh->vc_a.p, ldh}, g.B = {p->r16.p, ldh};  // t1 = lp(V_c^T R)
-  g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = ldh, g.epi.cn = 1;
+  if (p->accum == KP_ACCUM_TENSOR) {
+    // tcgen05 epilogue threads own output rows (TMEM lanes): compute t1^T =
+    // R^T V_c so the row-major t1 is written M-contiguous (coalesced).
+    g.A = {p->r16.p, ldh}, g.B = {sh->vc_a.p, ldh};
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = 1, g.epi.cn = ldh;
+  } else {
+    g.A = {sh->vc_a.p, ldh}, g.B = {p->r16.p, ldh};  // t1 = lp(V_c^T R)
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = ldh, g.epi.cn = 1;
+  }
   gemm(g, KC_PRECOND);
   g.A = {p->t1h.p, ldh}, g.B = {sh->vr_b.p, ldh};  // w = round(S .* lp(t1 V_r))
   g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF_SCALED, g.epi.Ch = p->wh.p, g.epi.cm = 1,
   g.epi.cn = ldh, g.epi.scale = p->s16.p, g.epi.sm = 1, g.epi.sn = n;
   gemm(g, KC_PRECOND);
-  g.A = {sh->vct_a.p, ldh}, g.B = {p->wh.p, ldh};  // t3 = lp(V_c w)
-  g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t3h.p, g.epi.cm = ldh, g.epi.cn = 1;
+  if (p->accum == KP_ACCUM_TENSOR) {  // t3^T = w^T V_c^T, M-contiguous
+    g.A = {p->wh.p, ldh}, g.B = {sh->vct_a.p, ldh};
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t3h.p, g.epi.cm = 1, g.epi.cn = ldh;
+  } else {
+    g.A = {sh->vct_a.p, ldh}, g.B = {p->wh.p, ldh};  // t3 = lp(V_c w)
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t3h.p, g.epi.cm = ldh, g.epi.cn = 1;
+  }
   gemm(g, KC_PRECOND);
   g.A = {p->t3h.p, ldh}, g.B = {sh->vrt_b.p, ldh};  // z = lp(t3 V_r^T)
   g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z, g.epi.cm = 1, g.epi.cn = n;
