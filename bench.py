@@ -158,7 +158,7 @@ def run_reference(args):
     import paper_2311_15393_b200 as K
     threads = os.cpu_count() or 1
     t0 = time.time()
-    cfg = build_problem(args.config, 0, args.n, device_apply=False)
+    cfg = build_problem(args.config, 0, args.size, device_apply=False)
     svd_r, svd_c = svd_pair(cfg.term, "host")
     setup_s = time.time() - t0
     fmt = K.PrecisionFormat.fp16()
@@ -208,7 +208,7 @@ def run_c4(args):
     check(L.kp_init(local))
     images = 64
     mine = list(shard(images, ws, rank))
-    sh = C4Shard(n=args.n, svd=args.svd)
+    sh = C4Shard(n=args.size, svd=args.svd)
     probs = {i: sh.problem(i) for i in mine}  # input generation is not timed
     for i in mine[: max(1, args.warmup)]:
         sh.solve(i, probs[i])
@@ -258,7 +258,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--n", type=int, default=None, help="override image side (quick runs)")
+    ap.add_argument("--size", type=int, default=None, help="override image side n (quick runs)")
     ap.add_argument("--svd", default="gpu", choices=["gpu", "host"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tensor", action="store_true", help="skip the tensor-mode secondary run")
@@ -292,7 +292,7 @@ def main():
     check(L.kp_init(local))
 
     t0 = time.time()
-    cfg = build_problem(args.config, rank, args.n, device_apply=True)
+    cfg = build_problem(args.config, rank, args.size, device_apply=True)
     t_problem = time.time() - t0
     t1 = time.time()
     svd_r, svd_c = svd_pair(cfg.term, args.svd)

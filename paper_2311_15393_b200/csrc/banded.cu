@@ -92,37 +92,59 @@ __global__ void __launch_bounds__(A_THREADS) band_cols_kernel(const double* __re
   }
 }
 
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src),
+               "r"(valid ? 8 : 0));
+}
+
+// Pass B. The Y_k tiles (B_TJ + taps - 1 columns of B_TA rows) are
+// double-buffered with cp.async so term k+1 streams in while term k's
+// correlation runs.
 __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __restrict__ Y, int n,
                                                               int r, const __grid_constant__ BandTaps t,
                                                               const F64Epilogue e,
                                                               const int* status) {
   if (stopped(status)) return;
   extern __shared__ double sm[];
-  double* Ys = sm;  // [B_TJ + taps - 1][B_TA]
-  const int a0 = blockIdx.y * B_TA, j0 = blockIdx.x * B_TJ;
   const int rows = B_TJ + t.taps - 1;
+  const int buf_doubles = (rows + 1) * B_TA;  // +1 row: corr8 prefetch slack
+  const int a0 = blockIdx.y * B_TA, j0 = blockIdx.x * B_TJ;
   const int a = threadIdx.x % B_TA, jq = threadIdx.x / B_TA;  // jq in [0, 4)
   const size_t nn = size_t(n) * n;
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+  auto load = [&](int k, int buf) {
+    const double* Yk = Y + k * nn;
+    const uint32_t dst0 = sbase + uint32_t(buf * buf_doubles) * 8u;
+    for (int idx = threadIdx.x; idx < rows * B_TA; idx += B_THREADS) {
+      const int jw = idx / B_TA, aa = idx % B_TA;
+      const int j = j0 + t.shift + jw, ai = a0 + aa;
+      const bool v = j >= 0 && j < n && ai < n;
+      cp_async8(dst0 + uint32_t(idx) * 8u, v ? Yk + size_t(j) * n + ai : Y, v);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
   double acc[2][8];
 #pragma unroll
   for (int h = 0; h < 2; ++h)
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[h][q] = 0.0;
+  load(0, 0);
   for (int k = 0; k < r; ++k) {
-    const double* Yk = Y + k * nn;
-    for (int idx = threadIdx.x; idx < rows * B_TA; idx += B_THREADS) {
-      const int jw = idx / B_TA, aa = idx % B_TA;
-      const int j = j0 + t.shift + jw, ai = a0 + aa;
-      Ys[jw * B_TA + aa] = (j >= 0 && j < n && ai < n) ? Yk[size_t(j) * n + ai] : 0.0;
+    if (k + 1 < r) {
+      load(k + 1, (k + 1) & 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
     }
     __syncthreads();
+    const double* Ys = sm + (k & 1) * buf_doubles;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int jb = jq + 4 * h;  // 8-column block
       const double* base = Ys + (8 * jb) * B_TA + a;
       corr8(acc[h], t.w[k], t.taps, [&](int i) { return base[i * B_TA]; });
     }
-    __syncthreads();
+    __syncthreads();  // buffer (k & 1) is refilled at iteration k + 1
   }
   // epilogue (same contract as the GEMM epilogue)
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -184,8 +206,8 @@ int band_rows_num_ctas(int n) { return int(cdiv(n, B_TJ) * cdiv(n, B_TA)); }
 
 void band_rows(const double* Y, int n, int r, const BandTaps& t, const F64Epilogue& e,
                const int* status) {
-  // +1 row: the register window of corr8 prefetches one value past the taps
-  const size_t smem = size_t(B_TJ + t.taps) * B_TA * sizeof(double);
+  // two buffers; +1 row each: corr8 prefetches one value past the taps
+  const size_t smem = 2 * size_t(B_TJ + t.taps) * B_TA * sizeof(double);
   static size_t attr = 0;
   if (smem > attr) {
     KP_CUDA(cudaFuncSetAttribute(band_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
