@@ -219,6 +219,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t v[32];
         tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + uint32_t(acc * BN + c0), v);
         if (m >= M) continue;
+        if (e.mode == F16OUT_F64) {
+          // Batches of 8 columns: all vector loads of a batch are issued
+          // before any store, so their latencies overlap.
+          double* __restrict__ Cd = e.Cd;
+          const double* __restrict__ d0 = e.d0;
+          const double* __restrict__ d1a = e.d1a;
+          const double* __restrict__ d1b = e.d1b;
+          const bool part = e.partials != nullptr;
+#pragma unroll
+          for (int j0 = 0; j0 < 32; j0 += 8) {
+            double a0[8], a1[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int n = nb + c0 + j0 + j;
+              const long vi = long(m) * e.vm + long(n) * e.vn;
+              const bool ok = part && n < N;
+              a0[j] = (ok && d0) ? d0[vi] : 0.0;
+              a1[j] = (ok && d1a) ? (d1b ? d1a[vi] - d1b[vi] : d1a[vi]) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int n = nb + c0 + j0 + j;
+              if (n < N) {
+                const double z = double(__half2float(__float2half_rn(__uint_as_float(v[j0 + j]))));
+                Cd[long(m) * e.cm + long(n) * e.cn] = z;
+                if (part) {
+                  if (d0) s0 += z * a0[j];
+                  if (d1a) s1 += z * a1[j];
+                  if (!isfinite(z)) s2 += 1.0;
+                }
+              }
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int n = nb + c0 + j;
@@ -226,18 +261,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const __half h = __float2half_rn(__uint_as_float(v[j]));  // the result in binary16
           if (e.mode == F16OUT_HALF) {
             e.Ch[long(m) * e.cm + long(n) * e.cn] = h;
-          } else if (e.mode == F16OUT_HALF_SCALED) {  // w = round16(S .* t2), as the reference
+          } else {  // F16OUT_HALF_SCALED: w = round16(S .* t2), as the reference
             const __half sc = e.scale[long(m) * e.sm + long(n) * e.sn];
             e.Ch[long(m) * e.cm + long(n) * e.cn] = __hmul_rn(sc, h);
-          } else {
-            const double z = double(__half2float(h));
-            e.Cd[long(m) * e.cm + long(n) * e.cn] = z;
-            if (e.partials) {
-              const long vi = long(m) * e.vm + long(n) * e.vn;
-              if (e.d0) s0 += z * e.d0[vi];
-              if (e.d1a) s1 += z * (e.d1b ? (e.d1a[vi] - e.d1b[vi]) : e.d1a[vi]);
-              if (!isfinite(z)) s2 += 1.0;
-            }
           }
         }
       }

@@ -138,6 +138,11 @@ __global__ void pcg_alpha_scalar_kernel(DevState* st, const double* part, int n)
   st->alpha = st->rho / pq;
 }
 
+// Elements are processed in pairs (16-byte vector accesses) when n is even
+// and every pointer is 16-byte aligned (VEC2), else one at a time. Both
+// elements of a pair lie in the same column, so the binary16 copy of r is a
+// single half2 store into the padded B-operand layout (row l, ldh stride).
+template <bool VEC2>
 __global__ void pcg_update_kernel(const DevState* st, DevHistory h, double* x, double* r,
                                   double* r_prev, const double* p, const double* q,
                                   const double* z, const double* xt, __half* r16, int n,
@@ -146,28 +151,72 @@ __global__ void pcg_update_kernel(const DevState* st, DevHistory h, double* x, d
   __shared__ double red[VEC_THREADS / 32][4];
   const double alpha = st->alpha;
   const bool has_xt = st->has_xt, cos = st->track_cos;
+  const unsigned un = unsigned(n);
   double* it = (st->record && h.iterates) ? h.iterates + size_t(st->rows) * n * n : nullptr;
   const size_t nn = size_t(n) * n;
   double v[4] = {0.0, 0.0, 0.0, 0.0};
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
-       i += size_t(gridDim.x) * blockDim.x) {
-    const double ri = r[i];
-    if (r_prev) r_prev[i] = ri;
-    const double xi = x[i] + alpha * p[i];
-    const double rn = ri - alpha * q[i];
-    x[i] = xi;
-    r[i] = rn;
-    if (it) it[i] = xi;
-    if (r16) r16[(i / n) * ldh + (i % n)] = __double2half(rn);
-    v[0] += rn * rn;
-    if (has_xt) {
-      const double d = xi - xt[i];
-      v[1] += d * d;
+  if (VEC2) {
+    const size_t np = nn / 2;
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < np;
+         k += size_t(gridDim.x) * blockDim.x) {
+      const size_t i = 2 * k;
+      const double2 ri = reinterpret_cast<const double2*>(r)[k];
+      const double2 pi = reinterpret_cast<const double2*>(p)[k];
+      const double2 qi = reinterpret_cast<const double2*>(q)[k];
+      double2 xi = reinterpret_cast<const double2*>(x)[k];
+      if (r_prev) reinterpret_cast<double2*>(r_prev)[k] = ri;
+      xi.x += alpha * pi.x, xi.y += alpha * pi.y;
+      const double2 rn = make_double2(ri.x - alpha * qi.x, ri.y - alpha * qi.y);
+      reinterpret_cast<double2*>(x)[k] = xi;
+      reinterpret_cast<double2*>(r)[k] = rn;
+      if (it) reinterpret_cast<double2*>(it)[k] = xi;
+      if (r16) {
+        const unsigned l = unsigned(i) / un, row = unsigned(i) - l * un;
+        __half2 hv;
+        hv.x = __double2half(rn.x);
+        hv.y = __double2half(rn.y);
+        *reinterpret_cast<__half2*>(r16 + size_t(l) * ldh + row) = hv;
+      }
+      v[0] += rn.x * rn.x;
+      v[0] += rn.y * rn.y;
+      if (has_xt) {
+        const double2 ti = reinterpret_cast<const double2*>(xt)[k];
+        const double d0 = xi.x - ti.x, d1 = xi.y - ti.y;
+        v[1] += d0 * d0;
+        v[1] += d1 * d1;
+      }
+      if (cos) {
+        const double2 zi = reinterpret_cast<const double2*>(z)[k];
+        v[2] += rn.x * zi.x;
+        v[2] += rn.y * zi.y;
+        v[3] += zi.x * zi.x;
+        v[3] += zi.y * zi.y;
+      }
     }
-    if (cos) {
-      const double zi = z[i];
-      v[2] += rn * zi;
-      v[3] += zi * zi;
+  } else {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
+         i += size_t(gridDim.x) * blockDim.x) {
+      const double ri = r[i];
+      if (r_prev) r_prev[i] = ri;
+      const double xi = x[i] + alpha * p[i];
+      const double rn = ri - alpha * q[i];
+      x[i] = xi;
+      r[i] = rn;
+      if (it) it[i] = xi;
+      if (r16) {
+        const unsigned l = unsigned(i) / un, row = unsigned(i) - l * un;
+        r16[size_t(l) * ldh + row] = __double2half(rn);
+      }
+      v[0] += rn * rn;
+      if (has_xt) {
+        const double d = xi - xt[i];
+        v[1] += d * d;
+      }
+      if (cos) {
+        const double zi = z[i];
+        v[2] += rn * zi;
+        v[3] += zi * zi;
+      }
     }
   }
   block_sum<4>(v, red);
@@ -229,12 +278,22 @@ __global__ void pcg_beta_scalar_kernel(DevState* st, const double* part, int n) 
 }
 
 // p = z + beta p, then rho = rz with the positivity check (krylov.cpp:133-138)
-__global__ void pcg_p_update_kernel(DevState* st, double* p, const double* z, size_t nn) {
+__global__ void pcg_p_update_kernel(DevState* st, double* p, const double* z, size_t nn, bool vec2) {
   if (stopped(st)) return;
   const double beta = st->beta;
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
-       i += size_t(gridDim.x) * blockDim.x)
-    p[i] = z[i] + beta * p[i];
+  if (vec2) {
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < nn / 2;
+         k += size_t(gridDim.x) * blockDim.x) {
+      const double2 zi = reinterpret_cast<const double2*>(z)[k];
+      double2 pi = reinterpret_cast<const double2*>(p)[k];
+      pi.x = zi.x + beta * pi.x, pi.y = zi.y + beta * pi.y;
+      reinterpret_cast<double2*>(p)[k] = pi;
+    }
+  } else {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
+         i += size_t(gridDim.x) * blockDim.x)
+      p[i] = z[i] + beta * p[i];
+  }
 }
 __global__ void pcg_rho_scalar_kernel(DevState* st) {
   if (stopped(st) || threadIdx.x) return;
@@ -286,6 +345,7 @@ __global__ void cgls_alpha_scalar_kernel(DevState* st, const double* part_q, int
   st->alpha = st->gamma / delta;
 }
 
+template <bool VEC2>
 __global__ void cgls_update_kernel(const DevState* st, DevHistory h, double* x, double* rt,
                                    const double* p, const double* q, const double* xt, size_t nn,
                                    double* part) {
@@ -295,15 +355,36 @@ __global__ void cgls_update_kernel(const DevState* st, DevHistory h, double* x, 
   const bool has_xt = st->has_xt;
   double* it = (st->record && h.iterates) ? h.iterates + size_t(st->rows) * nn : nullptr;
   double v[1] = {0.0};
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
-       i += size_t(gridDim.x) * blockDim.x) {
-    const double xi = x[i] + alpha * p[i];
-    x[i] = xi;
-    rt[i] = rt[i] - alpha * q[i];
-    if (it) it[i] = xi;
-    if (has_xt) {
-      const double d = xi - xt[i];
-      v[0] += d * d;
+  if (VEC2) {
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < nn / 2;
+         k += size_t(gridDim.x) * blockDim.x) {
+      const double2 pi = reinterpret_cast<const double2*>(p)[k];
+      const double2 qi = reinterpret_cast<const double2*>(q)[k];
+      double2 xi = reinterpret_cast<const double2*>(x)[k];
+      double2 ri = reinterpret_cast<const double2*>(rt)[k];
+      xi.x += alpha * pi.x, xi.y += alpha * pi.y;
+      ri.x -= alpha * qi.x, ri.y -= alpha * qi.y;
+      reinterpret_cast<double2*>(x)[k] = xi;
+      reinterpret_cast<double2*>(rt)[k] = ri;
+      if (it) reinterpret_cast<double2*>(it)[k] = xi;
+      if (has_xt) {
+        const double2 ti = reinterpret_cast<const double2*>(xt)[k];
+        const double d0 = xi.x - ti.x, d1 = xi.y - ti.y;
+        v[0] += d0 * d0;
+        v[0] += d1 * d1;
+      }
+    }
+  } else {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
+         i += size_t(gridDim.x) * blockDim.x) {
+      const double xi = x[i] + alpha * p[i];
+      x[i] = xi;
+      rt[i] = rt[i] - alpha * q[i];
+      if (it) it[i] = xi;
+      if (has_xt) {
+        const double d = xi - xt[i];
+        v[0] += d * d;
+      }
     }
   }
   block_sum<1>(v, red);
@@ -351,19 +432,33 @@ __global__ void cgls_resid_scalar_kernel(DevState* st, DevHistory h, const doubl
   }
 }
 
+template <bool VEC2>
 __global__ void cgls_p_update_kernel(DevState* st, double* p, const double* s, double* s_prev,
                                      size_t nn, double* part) {
   if (stopped(st)) return;
   __shared__ double red[VEC_THREADS / 32][1];
   const double beta = st->beta;
   double v[1] = {0.0};
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
-       i += size_t(gridDim.x) * blockDim.x) {
-    const double si = s[i];
-    const double pi = si + beta * p[i];
-    p[i] = pi;
-    if (s_prev) s_prev[i] = si;
-    v[0] += pi * pi;
+  if (VEC2) {
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < nn / 2;
+         k += size_t(gridDim.x) * blockDim.x) {
+      const double2 si = reinterpret_cast<const double2*>(s)[k];
+      double2 pi = reinterpret_cast<const double2*>(p)[k];
+      pi.x = si.x + beta * pi.x, pi.y = si.y + beta * pi.y;
+      reinterpret_cast<double2*>(p)[k] = pi;
+      if (s_prev) reinterpret_cast<double2*>(s_prev)[k] = si;
+      v[0] += pi.x * pi.x;
+      v[0] += pi.y * pi.y;
+    }
+  } else {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
+         i += size_t(gridDim.x) * blockDim.x) {
+      const double si = s[i];
+      const double pi = si + beta * p[i];
+      p[i] = pi;
+      if (s_prev) s_prev[i] = si;
+      v[0] += pi * pi;
+    }
   }
   block_sum<1>(v, red);
   if (threadIdx.x == 0) {
@@ -497,11 +592,19 @@ void pcg_init_msolve_scalar(DevState* st, const double* part_z, int nz) {
 void pcg_alpha_scalar(DevState* st, const double* part_pq, int n) {
   KP_LAUNCH(KC_VECTOR, pcg_alpha_scalar_kernel, 1, VEC_THREADS, st, part_pq, n);
 }
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 void pcg_update(DevState* st, DevHistory h, double* x, double* r, double* r_prev, const double* p,
                 const double* q, const double* z, const double* xt, __half* r16, int n, long ldh,
                 double* partials) {
-  KP_LAUNCH(KC_VECTOR, pcg_update_kernel, VEC_CTAS, VEC_THREADS, st, h, x, r, r_prev, p, q, z, xt,
-            r16, n, ldh, partials);
+  const bool vec2 = n % 2 == 0 && al16(x) && al16(r) && al16(r_prev) && al16(p) && al16(q) &&
+                    al16(z) && al16(xt) && al16(h.iterates) && ldh % 2 == 0;
+  if (vec2)
+    KP_LAUNCH(KC_VECTOR, pcg_update_kernel<true>, VEC_CTAS, VEC_THREADS, st, h, x, r, r_prev, p, q,
+              z, xt, r16, n, ldh, partials);
+  else
+    KP_LAUNCH(KC_VECTOR, pcg_update_kernel<false>, VEC_CTAS, VEC_THREADS, st, h, x, r, r_prev, p,
+              q, z, xt, r16, n, ldh, partials);
 }
 void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n) {
   KP_LAUNCH(KC_VECTOR, pcg_resid_scalar_kernel, 1, VEC_THREADS, st, h, part, n);
@@ -510,7 +613,8 @@ void pcg_beta_scalar(DevState* st, const double* part_z, int n) {
   KP_LAUNCH(KC_VECTOR, pcg_beta_scalar_kernel, 1, VEC_THREADS, st, part_z, n);
 }
 void pcg_p_update(DevState* st, double* p, const double* z, size_t nn) {
-  KP_LAUNCH(KC_VECTOR, pcg_p_update_kernel, vec_grid(nn), VEC_THREADS, st, p, z, nn);
+  const bool vec2 = nn % 2 == 0 && al16(p) && al16(z);
+  KP_LAUNCH(KC_VECTOR, pcg_p_update_kernel, vec_grid(nn), VEC_THREADS, st, p, z, nn, vec2);
   KP_LAUNCH(KC_VECTOR, pcg_rho_scalar_kernel, 1, 32, st);
 }
 
@@ -523,8 +627,12 @@ void cgls_alpha_scalar(DevState* st, const double* part_q, int nq, const double*
 }
 void cgls_update(DevState* st, DevHistory h, double* x, double* rt, const double* p,
                  const double* q, const double* xt, size_t nn, double* partials) {
-  KP_LAUNCH(KC_VECTOR, cgls_update_kernel, VEC_CTAS, VEC_THREADS, st, h, x, rt, p, q, xt, nn,
-            partials);
+  if (nn % 2 == 0 && al16(x) && al16(rt) && al16(p) && al16(q) && al16(xt) && al16(h.iterates))
+    KP_LAUNCH(KC_VECTOR, cgls_update_kernel<true>, VEC_CTAS, VEC_THREADS, st, h, x, rt, p, q, xt,
+              nn, partials);
+  else
+    KP_LAUNCH(KC_VECTOR, cgls_update_kernel<false>, VEC_CTAS, VEC_THREADS, st, h, x, rt, p, q, xt,
+              nn, partials);
 }
 void cgls_resid_scalar(DevState* st, DevHistory h, const double* part_s, int ns,
                        const double* part_x, int nx) {
@@ -532,8 +640,12 @@ void cgls_resid_scalar(DevState* st, DevHistory h, const double* part_s, int ns,
 }
 void cgls_p_update(DevState* st, double* p, const double* s, double* s_prev, size_t nn,
                    double* partials) {
-  KP_LAUNCH(KC_VECTOR, cgls_p_update_kernel, VEC_CTAS, VEC_THREADS, st, p, s, s_prev, nn,
-            partials);
+  if (nn % 2 == 0 && al16(p) && al16(s) && al16(s_prev))
+    KP_LAUNCH(KC_VECTOR, cgls_p_update_kernel<true>, VEC_CTAS, VEC_THREADS, st, p, s, s_prev, nn,
+              partials);
+  else
+    KP_LAUNCH(KC_VECTOR, cgls_p_update_kernel<false>, VEC_CTAS, VEC_THREADS, st, p, s, s_prev, nn,
+              partials);
   KP_LAUNCH(KC_VECTOR, cgls_next_kernel, 1, 32, st);
 }
 

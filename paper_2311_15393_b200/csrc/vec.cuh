@@ -50,13 +50,13 @@ struct DevHistory {
 };
 
 // Partial-sum buffers are [ctas][4] doubles.
-constexpr int VEC_CTAS = 296;   // fixed grid of the vector kernels (2 x 148 SMs)
+constexpr int VEC_CTAS = 1184;  // fixed grid of the vector kernels (8 x 148 SMs)
 constexpr int VEC_THREADS = 256;
 
 // ---- generic helpers -------------------------------------------------------
 void vec_copy(double* dst, const double* src, size_t n, const int* status);
 void vec_zero(double* dst, size_t n);
-// partials[cta*4+0] = sum x*y over a fixed 296-CTA grid
+// partials[cta*4+0] = sum x*y over the fixed VEC_CTAS grid
 void vec_dot_partials(const double* x, const double* y, size_t n, double* partials);
 // dst16[l*ldh + i] = round16(src[l*n + i]) (RNE binary16, overflow -> inf)
 void cast_f64_to_f16_padded(const double* src, __half* dst, int rows, int cols, long ld_src,

@@ -31,6 +31,10 @@ def same_bits(a, b):
             and np.array_equal(np.signbit(a[~nan]), np.signbit(b[~nan])))
 
 
+def ref_matrix(n, seed):  # test_krylov.cpp:21-27 (column-major fill from Rng(seed))
+    return P.rng_normals(seed, n * n).reshape(n, n, order="F")
+
+
 def rsum(n, r, seed):
     rng = np.random.default_rng(seed)
     return KroneckerSum([KronTerm(rng.standard_normal((n, n)), rng.standard_normal((n, n)))
@@ -183,13 +187,15 @@ def test_cgls_kats_on_device():  # test_krylov.cpp:110-206
     assert r.history.converged and r.history.iterations_used == 1
     assert np.linalg.norm(r.x - b) <= 1e-14 * np.linalg.norm(b)
     assert r.history.relative_error[0] == 1.0
-    a = rsum(4, 2, 31)
+    a = KroneckerSum([KronTerm(ref_matrix(4, 31), ref_matrix(4, 32)),  # test_krylov.cpp:125-128
+                      KronTerm(0.4 * ref_matrix(4, 33), ref_matrix(4, 34))], 4)
     ad = sum(np.kron(t.row_factor, t.col_factor) for t in a.terms)
     b = P.rng_normals(35, 16)
     lam = 0.3 * np.linalg.svd(ad, compute_uv=False)[0]
     want = np.linalg.solve(ad.T @ ad + lam * lam * np.eye(16), ad.T @ b)
     r = K.cgls(a, b, SolverOptions(lambda_=lam, max_iterations=16, rel_residual_tol=1e-10))
-    assert r.history.converged and np.linalg.norm(r.x - want) <= 1e-8 * np.linalg.norm(want)
+    assert r.history.converged and r.history.iterations_used <= 16
+    assert np.linalg.norm(r.x - want) <= 1e-8 * np.linalg.norm(want)
     tp, _ = desk("defocus", 8, 0.05, 11)
     r = K.cgls(tp.a, tp.b, SolverOptions(lambda_=0.05, max_iterations=5, rel_residual_tol=1e-14,
                                          x_true=tp.x_true))
