@@ -54,7 +54,15 @@ void ensure_init() {
   KP_CUDA(cudaSetDevice(0));
   KP_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
   KP_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, 0));
+  init_pool(0);
   c.device = 0;
+}
+
+void init_pool(int device) {
+  cudaMemPool_t pool;
+  KP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t threshold = ~uint64_t(0);
+  KP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
 }
 
 void check_launch(const char* what) {
@@ -210,6 +218,9 @@ struct PrecondShared {
   DBuf<__half> vc_a, vr_b, vct_a, vrt_b;
   // FP64 operands (fmt covers double)
   DBuf<double> vc, vr, vct, vrt;
+  // extremes of s_r(j) s_c(i) over all (i, j), computed once (spectral data)
+  bool have_range = false;
+  double smin = 0.0, smax = 0.0;
 };
 
 struct kp_precond {
@@ -218,7 +229,6 @@ struct kp_precond {
   double lambda = 0.0;
   kp_format fmt{};
   int accum = KP_ACCUM_REFERENCE;
-  std::vector<double> s_weights;  // host FP64 (factor.cpp:62-76)
   DBuf<double> s64;               // fp64 format
   DBuf<__half> s16;               // fp16 format (col-major n*n)
   // workspace
@@ -447,16 +457,24 @@ std::vector<double> weight_matrix(const PrecondShared& sh, double lambda) {
 void set_weights(kp_precond* p) {
   const int n = p->n;
   const size_t nn = size_t(n) * n;
-  p->s_weights = weight_matrix(*p->sh, p->lambda);
+  const auto& sh = *p->sh;
+  // denominators are monotone in s_r(j) s_c(i) >= 0, so the smallest one is
+  // zero iff any is (the reference's per-element check, factor.cpp:70-72)
+  auto amin = [](const std::vector<double>& v) {
+    double m = std::numeric_limits<double>::infinity();
+    for (double x : v) m = std::min(m, std::fabs(x));
+    return m;
+  };
+  const double pmin = amin(sh.s_r) * amin(sh.s_c);
+  const double l2 = p->lambda * p->lambda;
+  if (pmin * pmin + l2 == 0.0)
+    throw InvalidArgument("build_preconditioner: singular factors need lambda > 0");
   if (covers_double(p->fmt)) {
     p->s64.alloc(nn);
-    p->s64.upload(p->s_weights.data(), nn);
+    precond_weights(sh.d_s_r.p, sh.d_s_c.p, n, l2, p->s64.p, nullptr);
   } else {
-    DBuf<double> tmp(nn);
-    tmp.upload(p->s_weights.data(), nn);
     p->s16.alloc(nn);
-    cast_f64_to_f16_padded(tmp.p, p->s16.p, n, n, n, n, nullptr);  // round_array(s_weights)
-    sync();
+    precond_weights(sh.d_s_r.p, sh.d_s_c.p, n, l2, nullptr, p->s16.p);  // round_array(S)
   }
 }
 
@@ -596,6 +614,8 @@ void setup_state(Solve& s, const kp_solver_options* o, bool has_xt, bool flexibl
   s.relerr = ws.get("h_relerr", s.capacity);
   s.cosines = ws.get("h_cos", s.capacity);
   s.iterates = o->record_iterates ? ws.get("h_iterates", size_t(s.capacity) * s.nn) : nullptr;
+  if (s.iterates)  // row 0 is the starting guess x0 = 0
+    KP_CUDA(cudaMemsetAsync(s.iterates, 0, s.nn * sizeof(double), ctx().stream));
   s.dh.resid = s.resid;
   s.dh.relerr = s.relerr;
   s.dh.cosines = s.cosines;
@@ -923,6 +943,7 @@ int kp_init(int device) {
       if (c.stream) cudaStreamDestroy(c.stream);
       KP_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
       KP_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
+      init_pool(device);
       c.device = device;
     }
   })
@@ -1122,9 +1143,9 @@ int kp_precond_export(const kp_precond* p, int field, double* out) {
         }
     };
     switch (field) {
-      case 0: put(p->s_weights); break;
+      case 0: put(weight_matrix(*sh, p->lambda)); break;
       case 1:
-        if (covers_double(p->fmt)) put(p->s_weights);
+        if (covers_double(p->fmt)) put(weight_matrix(*sh, p->lambda));
         else put_half(p->s16.p, n, false);
         break;
       case 2:
@@ -1188,14 +1209,19 @@ int kp_spectral_create(const kp_precond* p, const double* b, kp_spectral** out) 
     g.epi = F64Epilogue{}, g.epi.C = sd->bhat.p, g.epi.cm = 1, g.epi.cn = n;
     gemm_f64(g, KC_SPECTRAL);
     sync();
-    const auto& sr = sd->sh->s_r;
-    const auto& sc = sd->sh->s_c;
-    sd->smax = sr[0] * sc[0];
-    sd->smin = std::numeric_limits<double>::infinity();
-    for (int j = 0; j < n; ++j)
-      for (int i = 0; i < n; ++i) sd->smin = std::min(sd->smin, sr[j] * sc[i]);
-    for (int j = 0; j < n; ++j)
-      for (int i = 0; i < n; ++i) sd->smax = std::max(sd->smax, sr[j] * sc[i]);
+    auto& sh = *sd->sh;
+    if (!sh.have_range) {
+      const auto& sr = sh.s_r;
+      const auto& sc = sh.s_c;
+      sh.smax = sr[0] * sc[0];
+      sh.smin = std::numeric_limits<double>::infinity();
+      for (int j = 0; j < n; ++j)
+        for (int i = 0; i < n; ++i) sh.smin = std::min(sh.smin, sr[j] * sc[i]);
+      for (int j = 0; j < n; ++j)
+        for (int i = 0; i < n; ++i) sh.smax = std::max(sh.smax, sr[j] * sc[i]);
+      sh.have_range = true;
+    }
+    sd->smin = sh.smin, sd->smax = sh.smax;
     *out = sd.release();
   })
 }

@@ -51,6 +51,7 @@ struct Ctx {
 
 Ctx& ctx();            // lazily initialised on first use (device 0)
 void ensure_init();
+void init_pool(int device);  // keep freed pool blocks cached (release threshold = max)
 void check_launch(const char* what);
 
 // RAII launch bracket: counts the launch and, when profiling, records events.
@@ -70,11 +71,13 @@ struct DBuf {
   explicit DBuf(size_t count) { alloc(count); }
   void alloc(size_t count) {
     free();
-    if (count) KP_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    // Stream-ordered pool allocation (the pool keeps freed blocks; see
+    // init_pool), so per-call scratch costs no device synchronisation.
+    if (count) KP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), ctx().stream));
     n = count;
   }
   void free() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, ctx().stream);
     p = nullptr;
     n = 0;
   }

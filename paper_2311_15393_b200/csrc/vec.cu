@@ -90,6 +90,23 @@ __global__ void cast_f16_kernel(const double* src, __half* dst, int rows, int co
   }
 }
 
+// S(i,j) = 1 / ((s_r(j) s_c(i))^2 + lambda^2) at j*n + i (factor.cpp:62-76),
+// unfused IEEE operations so it equals the host formula bit for bit; stored
+// as FP64 or rounded once to binary16 (round_array of the FP64 weights).
+__global__ void weights_kernel(const double* s_r, const double* s_c, int n, double l2,
+                               double* s64, __half* s16) {
+  const size_t nn = size_t(n) * n;
+  const unsigned un = unsigned(n);
+  for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < nn;
+       idx += size_t(gridDim.x) * blockDim.x) {
+    const unsigned j = unsigned(idx / un), i = unsigned(idx - size_t(j) * un);
+    const double prod = __dmul_rn(s_r[j], s_c[i]);
+    const double w = __ddiv_rn(1.0, __dadd_rn(__dmul_rn(prod, prod), l2));
+    if (s64) s64[idx] = w;
+    if (s16) s16[idx] = __double2half(w);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // PCG (pcg_core, krylov.cpp:58-142)
 __global__ void pcg_init_scalar_kernel(DevState* st, DevHistory h, const double* part_r, int nr,
@@ -569,6 +586,11 @@ unsigned vec_grid(size_t nn) {
 
 void vec_copy(double* dst, const double* src, size_t n, const int* status) {
   KP_LAUNCH(KC_VECTOR, copy_kernel, vec_grid(n), VEC_THREADS, dst, src, n, status);
+}
+void precond_weights(const double* s_r, const double* s_c, int n, double l2, double* s64,
+                     __half* s16) {
+  KP_LAUNCH(KC_PRECOND, weights_kernel, vec_grid(size_t(n) * n), VEC_THREADS, s_r, s_c, n, l2, s64,
+            s16);
 }
 void vec_zero(double* dst, size_t n) {
   KP_LAUNCH(KC_VECTOR, zero_kernel, vec_grid(n), VEC_THREADS, dst, n);

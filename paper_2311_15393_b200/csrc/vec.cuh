@@ -62,6 +62,11 @@ void vec_dot_partials(const double* x, const double* y, size_t n, double* partia
 void cast_f64_to_f16_padded(const double* src, __half* dst, int rows, int cols, long ld_src,
                             long ld_dst, const int* status);
 
+// S weights of the Kronecker-SVD preconditioner (factor.cpp:62-76) into s64
+// (FP64) and/or s16 (binary16), column-major n x n.
+void precond_weights(const double* s_r, const double* s_c, int n, double l2, double* s64,
+                     __half* s16);
+
 // ---- PCG -------------------------------------------------------------------
 // init after r = A^T b (partials_r: [ctas] of ||r||^2) and xnorm partials.
 void pcg_init_scalar(DevState* st, DevHistory h, const double* part_r, int nr,
