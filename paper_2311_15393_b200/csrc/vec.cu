@@ -489,37 +489,40 @@ __global__ void cgls_next_kernel(DevState* st) {
 }
 
 // ---------------------------------------------------------------------------
-// Spectral sums. sigma(i,j) = s_r[j] * s_c[i] at linear index j*n + i.
-constexpr int LCHUNK = 16;
-
+// Spectral sums. sigma(i,j) = s_r[j] * s_c[i] at linear index j*n + i. LC
+// lambdas per pass over b_hat (LC = 1 for the single-lambda probes of the
+// root finders, 16 for grids).
+template <int LC>
 __global__ void gcv_sums_kernel(const double* s_r, const double* s_c, const double* bhat, int n,
                                 const double* lambdas, int m, double* part) {
-  __shared__ double red[VEC_THREADS / 32][2 * LCHUNK];
+  __shared__ double red[VEC_THREADS / 32][2 * LC];
   const size_t nn = size_t(n) * n;
-  for (int q0 = 0; q0 < m; q0 += LCHUNK) {
-    double l2[LCHUNK];
-    double v[2 * LCHUNK];
+  const unsigned un = unsigned(n);
+  for (int q0 = 0; q0 < m; q0 += LC) {
+    double l2[LC];
+    double v[2 * LC];
 #pragma unroll
-    for (int c = 0; c < LCHUNK; ++c) {
+    for (int c = 0; c < LC; ++c) {
       const double l = (q0 + c < m) ? lambdas[q0 + c] : 1.0;
       l2[c] = l * l;
       v[2 * c] = 0.0, v[2 * c + 1] = 0.0;
     }
     for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < nn;
          idx += size_t(gridDim.x) * blockDim.x) {
-      const double s = s_r[idx / n] * s_c[idx % n];
+      const unsigned j = unsigned(idx / un), i = unsigned(idx - size_t(j) * un);
+      const double s = s_r[j] * s_c[i];
       const double s2 = s * s, b = bhat[idx];
 #pragma unroll
-      for (int c = 0; c < LCHUNK; ++c) {
+      for (int c = 0; c < LC; ++c) {
         const double d = s2 + l2[c];
         const double t = b / d;
         v[2 * c] += t * t;
         v[2 * c + 1] += 1.0 / d;
       }
     }
-    block_sum<2 * LCHUNK>(v, red);
+    block_sum<2 * LC>(v, red);
     if (threadIdx.x == 0)
-      for (int c = 0; c < LCHUNK && q0 + c < m; ++c) {
+      for (int c = 0; c < LC && q0 + c < m; ++c) {
         part[(size_t(q0 + c) * gridDim.x + blockIdx.x) * 2 + 0] = v[2 * c];
         part[(size_t(q0 + c) * gridDim.x + blockIdx.x) * 2 + 1] = v[2 * c + 1];
       }
@@ -527,47 +530,56 @@ __global__ void gcv_sums_kernel(const double* s_r, const double* s_c, const doub
   }
 }
 
+template <int LC>
 __global__ void resid_sums_kernel(const double* s_r, const double* s_c, const double* bhat, int n,
                                   const double* lambdas, int m, double* part) {
-  __shared__ double red[VEC_THREADS / 32][LCHUNK];
+  __shared__ double red[VEC_THREADS / 32][LC];
   const size_t nn = size_t(n) * n;
-  for (int q0 = 0; q0 < m; q0 += LCHUNK) {
-    double l2[LCHUNK];
-    double v[LCHUNK];
+  const unsigned un = unsigned(n);
+  for (int q0 = 0; q0 < m; q0 += LC) {
+    double l2[LC];
+    double v[LC];
 #pragma unroll
-    for (int c = 0; c < LCHUNK; ++c) {
+    for (int c = 0; c < LC; ++c) {
       const double l = (q0 + c < m) ? lambdas[q0 + c] : 1.0;
       l2[c] = l * l;
       v[c] = 0.0;
     }
     for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < nn;
          idx += size_t(gridDim.x) * blockDim.x) {
-      const double s = s_r[idx / n] * s_c[idx % n];
+      const unsigned j = unsigned(idx / un), i = unsigned(idx - size_t(j) * un);
+      const double s = s_r[j] * s_c[i];
       const double s2 = s * s, b = bhat[idx];
 #pragma unroll
-      for (int c = 0; c < LCHUNK; ++c) {
+      for (int c = 0; c < LC; ++c) {
         const double t = l2[c] * b / (s2 + l2[c]);
         v[c] += t * t;
       }
     }
-    block_sum<LCHUNK>(v, red);
+    block_sum<LC>(v, red);
     if (threadIdx.x == 0)
-      for (int c = 0; c < LCHUNK && q0 + c < m; ++c)
+      for (int c = 0; c < LC && q0 + c < m; ++c)
         part[size_t(q0 + c) * gridDim.x + blockIdx.x] = v[c];
     __syncthreads();
   }
 }
 
-// out[q*stride_out + j] = sum over ctas of part[(q*ctas + cta)*width + j]
+// out[q*width + j] = sum over ctas of part[(q*ctas + cta)*width + j]; one
+// block per q, fixed-order strided partial sums + tree (deterministic).
 __global__ void finish_sums_kernel(const double* part, int ctas, int width, int m, double* out) {
+  __shared__ double red[VEC_THREADS / 32][1];
   const int q = blockIdx.x;
   if (q >= m) return;
-  for (int j = threadIdx.x; j < width; j += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < ctas; ++c) s += part[(size_t(q) * ctas + c) * width + j];
-    out[size_t(q) * width + j] = s;
+  for (int j = 0; j < width; ++j) {
+    double v[1] = {0.0};
+    for (int c = threadIdx.x; c < ctas; c += blockDim.x) v[0] += part[(size_t(q) * ctas + c) * width + j];
+    block_sum<1>(v, red);
+    if (threadIdx.x == 0) out[size_t(q) * width + j] = v[0];
+    __syncthreads();
   }
 }
+
+constexpr int LCHUNK = 16;
 
 unsigned vec_grid(size_t nn) {
   return unsigned(std::min<size_t>(VEC_CTAS, std::max<size_t>(1, (nn + VEC_THREADS - 1) / VEC_THREADS)));
@@ -674,17 +686,25 @@ void cgls_p_update(DevState* st, double* p, const double* s, double* s_prev, siz
 void spectral_gcv_sums(const double* s_r, const double* s_c, const double* bhat, int n,
                        const double* lambdas, int m, double* out) {
   DBuf<double> part(size_t(m) * VEC_CTAS * 2);
-  KP_LAUNCH(KC_SPECTRAL, gcv_sums_kernel, VEC_CTAS, VEC_THREADS, s_r, s_c, bhat, n, lambdas, m,
-            part.p);
-  KP_LAUNCH(KC_SPECTRAL, finish_sums_kernel, m, 32, part.p, VEC_CTAS, 2, m, out);
+  if (m == 1)
+    KP_LAUNCH(KC_SPECTRAL, gcv_sums_kernel<1>, VEC_CTAS, VEC_THREADS, s_r, s_c, bhat, n, lambdas,
+              m, part.p);
+  else
+    KP_LAUNCH(KC_SPECTRAL, gcv_sums_kernel<LCHUNK>, VEC_CTAS, VEC_THREADS, s_r, s_c, bhat, n,
+              lambdas, m, part.p);
+  KP_LAUNCH(KC_SPECTRAL, finish_sums_kernel, m, VEC_THREADS, part.p, VEC_CTAS, 2, m, out);
   KP_CUDA(cudaStreamSynchronize(ctx().stream));
 }
 void spectral_resid_sums(const double* s_r, const double* s_c, const double* bhat, int n,
                          const double* lambdas, int m, double* out) {
   DBuf<double> part(size_t(m) * VEC_CTAS);
-  KP_LAUNCH(KC_SPECTRAL, resid_sums_kernel, VEC_CTAS, VEC_THREADS, s_r, s_c, bhat, n, lambdas, m,
-            part.p);
-  KP_LAUNCH(KC_SPECTRAL, finish_sums_kernel, m, 32, part.p, VEC_CTAS, 1, m, out);
+  if (m == 1)
+    KP_LAUNCH(KC_SPECTRAL, resid_sums_kernel<1>, VEC_CTAS, VEC_THREADS, s_r, s_c, bhat, n, lambdas,
+              m, part.p);
+  else
+    KP_LAUNCH(KC_SPECTRAL, resid_sums_kernel<LCHUNK>, VEC_CTAS, VEC_THREADS, s_r, s_c, bhat, n,
+              lambdas, m, part.p);
+  KP_LAUNCH(KC_SPECTRAL, finish_sums_kernel, m, VEC_THREADS, part.p, VEC_CTAS, 1, m, out);
   KP_CUDA(cudaStreamSynchronize(ctx().stream));
 }
 
