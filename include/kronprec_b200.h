@@ -199,11 +199,21 @@ int kp_fpcg(const kp_operator* op, const double* b, const kp_precond* m,
  * s_r(j) s_c(i) and b_hat = vec(U_c^T B U_r) from the FP64 SVD factors. */
 int kp_spectral_create(const kp_precond* p, const double* b,
                        kp_spectral** out);
+/* make_spectral_data(p, b, x_true) (regparam.cpp:127-134): also x_hat =
+ * vec(V_c^T X_true V_r), required by kp_lambda_opt / kp_opt_objective. */
+int kp_spectral_create_x(const kp_precond* p, const double* b,
+                         const double* x_true, kp_spectral** out);
 int kp_spectral_destroy(kp_spectral* sd);
 /* Sorted nonincreasing like approx_spectrum/project_b (factor.cpp:134-177). */
 int kp_spectral_export(const kp_spectral* sd, double* sigma_hat,
                        double* b_hat);
+/* x_hat in the same (sorted) order as kp_spectral_export. */
+int kp_spectral_export_xhat(const kp_spectral* sd, double* x_hat);
+/* Pointwise criteria (regparam.cpp:216-246). */
 int kp_gcv_objective(const kp_spectral* sd, double lambda, double* value);
+int kp_opt_objective(const kp_spectral* sd, double lambda, double* value);
+int kp_wgcv_objective(const kp_spectral* sd, double omega, double lambda,
+                      double* value);
 int kp_discrepancy_gap(const kp_spectral* sd, double epsilon, double lambda,
                        double* value);
 /* GCV over an explicit lambda grid (one batched reduction); argmin is the
@@ -212,6 +222,14 @@ int kp_gcv_grid(const kp_spectral* sd, const double* lambdas, int m,
                 double* values, kp_param_choice* choice);
 /* gcv (regparam.cpp:254-258): 1024-point log grid + golden refinement. */
 int kp_gcv(const kp_spectral* sd, kp_param_choice* choice);
+/* lambda_opt (regparam.cpp:248-252): needs kp_spectral_create_x. */
+int kp_lambda_opt(const kp_spectral* sd, kp_param_choice* choice);
+/* wgcv (regparam.cpp:260-286), omega > 0. */
+int kp_wgcv(const kp_spectral* sd, double omega, kp_param_choice* choice);
+/* filtered_solution (regparam.cpp:329-349): direct Tikhonov solution for
+ * the Kronecker approximation, FP64 on the device; x is n*n (host). */
+int kp_filtered_solution(const kp_precond* p, const double* b, double lambda,
+                         double* x);
 /* discrepancy (regparam.cpp:288-327); KP_ERR_NO_ROOT when no root. */
 int kp_discrepancy(const kp_spectral* sd, double noise_norm, double eta,
                    kp_param_choice* choice);

@@ -203,9 +203,9 @@ inline SolveResult fpcg(const KroneckerSum& a, const Vec& b, const KronSvdPrecon
 // SpectralData + selectors (regparam.hpp:19-90)
 class SpectralData {
  public:
-  SpectralData(const KronSvdPreconditioner& p, const Vec& b) {
+  SpectralData(const KronSvdPreconditioner& p, const Vec& b, const Vec* x_true = nullptr) {
     kp_spectral* s = nullptr;
-    check(kp_spectral_create(p.handle(), b.data(), &s));
+    check(kp_spectral_create_x(p.handle(), b.data(), x_true ? x_true->data() : nullptr, &s));
     s_.reset(s, [](kp_spectral* q) { kp_spectral_destroy(q); });
   }
   const kp_spectral* handle() const { return s_.get(); }
@@ -215,6 +215,35 @@ class SpectralData {
 };
 inline SpectralData make_spectral_data(const KronSvdPreconditioner& p, const Vec& b) {
   return SpectralData(p, b);
+}
+inline SpectralData make_spectral_data(const KronSvdPreconditioner& p, const Vec& b,
+                                       const Vec& x_true) {
+  return SpectralData(p, b, &x_true);
+}
+inline double opt_objective(const SpectralData& sd, double lambda) {
+  double v;
+  check(kp_opt_objective(sd.handle(), lambda, &v));
+  return v;
+}
+inline double wgcv_objective(const SpectralData& sd, double omega, double lambda) {
+  double v;
+  check(kp_wgcv_objective(sd.handle(), omega, lambda, &v));
+  return v;
+}
+inline kp_param_choice lambda_opt(const SpectralData& sd) {
+  kp_param_choice c;
+  check(kp_lambda_opt(sd.handle(), &c));
+  return c;
+}
+inline kp_param_choice wgcv(const SpectralData& sd, double omega) {
+  kp_param_choice c;
+  check(kp_wgcv(sd.handle(), omega, &c));
+  return c;
+}
+inline Vec filtered_solution(const KronSvdPreconditioner& p, const Vec& b, double lambda) {
+  Vec x(b.size());
+  check(kp_filtered_solution(p.handle(), b.data(), lambda, x.data()));
+  return x;
 }
 inline double gcv_objective(const SpectralData& sd, double lambda) {
   double v;

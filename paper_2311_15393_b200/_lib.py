@@ -69,6 +69,8 @@ EXPORTS = [
     "kp_cgls", "kp_pcg", "kp_fpcg", "kp_spectral_create", "kp_spectral_destroy",
     "kp_spectral_export", "kp_gcv_objective", "kp_discrepancy_gap", "kp_gcv_grid", "kp_gcv",
     "kp_discrepancy", "kp_operator_set_mode", "kp_operator_get_mode", "kp_event_record", "kp_event_elapsed", "kp_host_alloc", "kp_host_free",
+    "kp_spectral_create_x", "kp_spectral_export_xhat", "kp_opt_objective", "kp_wgcv_objective",
+    "kp_lambda_opt", "kp_wgcv", "kp_filtered_solution",
 ]
 
 _lib = None
@@ -113,6 +115,13 @@ def lib() -> C.CDLL:
             "kp_discrepancy_gap": ([P, D, D, C.POINTER(D)], I),
             "kp_gcv_grid": ([P, P, I, P, C.POINTER(kp_param_choice)], I),
             "kp_gcv": ([P, C.POINTER(kp_param_choice)], I),
+            "kp_spectral_create_x": ([P, P, P, C.POINTER(V)], I),
+            "kp_spectral_export_xhat": ([P, P], I),
+            "kp_opt_objective": ([P, D, C.POINTER(D)], I),
+            "kp_wgcv_objective": ([P, D, D, C.POINTER(D)], I),
+            "kp_lambda_opt": ([P, C.POINTER(kp_param_choice)], I),
+            "kp_wgcv": ([P, D, C.POINTER(kp_param_choice)], I),
+            "kp_filtered_solution": ([P, P, D, P], I),
             "kp_discrepancy": ([P, D, D, C.POINTER(kp_param_choice)], I),
             "kp_event_record": ([I], I),
             "kp_operator_set_mode": ([P, I], I),

@@ -213,6 +213,8 @@ struct PrecondShared {
   int n = 0;
   std::vector<double> u_r, s_r, v_r, u_c, s_c, v_c;  // FP64 SVDs (host)
   DBuf<double> d_u_r, d_u_c, d_s_r, d_s_c;            // for spectral data
+  DBuf<double> d_v_r, d_v_c;                          // x_true projection (col-major)
+  DBuf<double> d_vc_rm, d_vr_rm;                      // filtered solution (row-major)
   // binary16 operands (padded, K-major), exact / tensor modes
   long ldh = 0;
   DBuf<__half> vc_a, vr_b, vct_a, vrt_b;
@@ -241,6 +243,7 @@ struct kp_spectral {
   int n = 0;
   std::shared_ptr<PrecondShared> sh;
   DBuf<double> bhat;
+  DBuf<double> xhat;  // optional: coordinates of x_true (regparam.hpp:23)
   double smax = 0.0, smin = 0.0;
 };
 
@@ -832,29 +835,45 @@ double probe(const std::function<double(double)>& f, double x, const char* who) 
   return v;
 }
 
-void gcv_values(const kp_spectral* sd, const double* lambdas, int m, double* values) {
+// Objective values for m lambdas in one batched device reduction
+// (regparam.cpp:216-246): kind SK_GCV -> gcv_objective, SK_RESID ->
+// discrepancy_gap (+ eps^2), SK_OPT -> opt_objective, SK_WGCV ->
+// wgcv_objective, SK_WTRACE -> the wgcv trace term.
+void spectral_values(const kp_spectral* sd, int kind, const double* lambdas, int m, double omega,
+                     double eps, double* values) {
+  if (kind == SK_OPT && !sd->xhat.p) throw InvalidArgument("opt_objective: x coordinates missing");
   DBuf<double> dl(m), out(size_t(m) * 2);
   dl.upload(lambdas, m);
-  spectral_gcv_sums(sd->sh->d_s_r.p, sd->sh->d_s_c.p, sd->bhat.p, sd->n, dl.p, m, out.p);
+  spectral_sums(kind, sd->sh->d_s_r.p, sd->sh->d_s_c.p, sd->bhat.p, sd->xhat.p, sd->n, dl.p, m,
+                omega, out.p);
   std::vector<double> h(size_t(m) * 2);
   out.download(h.data(), h.size());
   sync();
   const double N = double(sd->n) * sd->n;
-  for (int q = 0; q < m; ++q) values[q] = N * h[2 * q] / (h[2 * q + 1] * h[2 * q + 1]);
+  for (int q = 0; q < m; ++q) {
+    const double a = h[2 * q], b = h[2 * q + 1];
+    switch (kind) {
+      case SK_GCV: values[q] = N * a / (b * b); break;
+      case SK_RESID: values[q] = a - eps * eps; break;
+      case SK_WGCV:
+        values[q] = b == 0.0 ? std::numeric_limits<double>::infinity() : (a * N) / (b * b);
+        break;
+      default: values[q] = a; break;  // SK_OPT, SK_WTRACE
+    }
+  }
 }
-double gcv_value(const kp_spectral* sd, double lambda) {
+double spectral_value(const kp_spectral* sd, int kind, double lambda, double omega = 0.0,
+                      double eps = 0.0) {
   double v;
-  gcv_values(sd, &lambda, 1, &v);
+  spectral_values(sd, kind, &lambda, 1, omega, eps, &v);
   return v;
 }
+void gcv_values(const kp_spectral* sd, const double* lambdas, int m, double* values) {
+  spectral_values(sd, SK_GCV, lambdas, m, 0.0, 0.0, values);
+}
+double gcv_value(const kp_spectral* sd, double lambda) { return spectral_value(sd, SK_GCV, lambda); }
 double gap_value(const kp_spectral* sd, double eps, double lambda) {
-  DBuf<double> dl(1), out(1);
-  dl.upload(&lambda, 1);
-  spectral_resid_sums(sd->sh->d_s_r.p, sd->sh->d_s_c.p, sd->bhat.p, sd->n, dl.p, 1, out.p);
-  double h;
-  out.download(&h, 1);
-  sync();
-  return h - eps * eps;
+  return spectral_value(sd, SK_RESID, lambda, 0.0, eps);
 }
 
 // minimize_1d (regparam.cpp:149-181)
@@ -902,6 +921,75 @@ double find_root(const std::function<double(double)>& f, double lo, double hi, d
     }
   }
   return a + 0.5 * (b - a);
+}
+
+// check_spectral (regparam.cpp:16-28): singular values are products of the
+// factor SVDs' values, never negative; reject an all-zero spectrum.
+void check_spectral(const kp_spectral* sd, bool need_x) {
+  if (!sd) throw InvalidArgument("spectral data: null");
+  if (need_x && !sd->xhat.p) throw InvalidArgument("selector requires x coordinates");
+  if (!(sd->smax > 0.0)) throw InvalidArgument("spectral data: all singular values zero");
+}
+
+// minimize_log (regparam.cpp:54-88): 1024-point log grid (one batched
+// launch), then golden-section refinement around the best grid point.
+kp_param_choice minimize_log(const kp_spectral* sd, int kind, double omega, double lo, double hi,
+                             int method) {
+  auto g = [&](double l) { return spectral_value(sd, kind, l, omega); };
+  kp_param_choice c{};
+  c.method = method, c.bracket_lo = lo, c.bracket_hi = hi, c.grid_index = -1;
+  if (hi <= lo * (1.0 + 1e-12)) {
+    c.lambda = lo, c.objective_value = probe(g, lo, "minimize_log"), c.flat_objective = 1;
+    return c;
+  }
+  const double ulo = std::log(lo), uhi = std::log(hi);
+  const int grid = 1024;
+  std::vector<double> ls(grid), vs(grid);
+  for (int k = 0; k < grid; ++k) ls[k] = std::exp(ulo + (uhi - ulo) * k / (grid - 1));
+  spectral_values(sd, kind, ls.data(), grid, omega, 0.0, vs.data());
+  int best_k = -1;
+  double best_v = std::numeric_limits<double>::infinity();
+  double vmin = best_v, vmax = -best_v;
+  for (int k = 0; k < grid; ++k) {
+    const double v = vs[k];
+    if (std::isnan(v)) throw std::runtime_error("minimize_log: objective is NaN");
+    if (!std::isfinite(v)) continue;
+    vmin = std::min(vmin, v), vmax = std::max(vmax, v);
+    if (v < best_v) best_v = v, best_k = k;
+  }
+  if (best_k < 0) throw std::runtime_error("minimize_log: objective infinite everywhere");
+  const double scale = std::max({std::abs(vmin), std::abs(vmax), 1e-300});
+  if (vmax - vmin <= 1e-14 * scale) {
+    const double mid = std::exp(0.5 * (ulo + uhi));
+    c.lambda = mid, c.objective_value = probe(g, mid, "minimize_log"), c.flat_objective = 1;
+    return c;
+  }
+  const double step = (uhi - ulo) / (grid - 1);
+  const double a = std::max(ulo, ulo + (best_k - 1) * step);
+  const double b = std::min(uhi, ulo + (best_k + 1) * step);
+  const auto r = minimize_1d([&](double u) { return g(std::exp(u)); }, a, b, 1e-12);
+  c.lambda = std::exp(r.first), c.objective_value = r.second;
+  return c;
+}
+
+// selector bracket [max(sigma_min, 1e-10 sigma_max), sigma_max] (regparam.cpp:30-34)
+std::pair<double, double> selector_bracket(const kp_spectral* sd) {
+  return {std::max(sd->smin, 1e-10 * sd->smax), sd->smax};
+}
+
+// vec(Ul^T X Ur) for n x n column-major X (device), FP64 DMMA GEMMs
+// (project_b, factor.cpp:157-177; the x_true projection uses the V factors).
+void project_dev(int n, const double* ul, const double* ur, const double* x, double* out) {
+  const size_t nn = size_t(n) * n;
+  DBuf<double> t(nn);
+  F64GemmArgs g;
+  g.M = n, g.N = n, g.nb = 1, g.Kb = n;
+  g.A = {ul, n, 0}, g.B = {x, n, 0};
+  g.epi.C = t.p, g.epi.cm = n, g.epi.cn = 1;
+  gemm_f64(g, KC_SPECTRAL);
+  g.A = {t.p, n, 0}, g.B = {ur, n, 0};
+  g.epi = F64Epilogue{}, g.epi.C = out, g.epi.cm = 1, g.epi.cn = n;
+  gemm_f64(g, KC_SPECTRAL);
 }
 
 }  // namespace
@@ -1189,7 +1277,10 @@ int kp_fpcg(const kp_operator* op, const double* b, const kp_precond* m,
 }
 
 // ---- lambda selection ------------------------------------------------------------
-int kp_spectral_create(const kp_precond* p, const double* b, kp_spectral** out) {
+// make_spectral_data (regparam.cpp:119-134): b_hat = vec(U_c^T B U_r) and,
+// with x_true, x_hat = vec(V_c^T X V_r) on the device.
+int kp_spectral_create_x(const kp_precond* p, const double* b, const double* x_true,
+                         kp_spectral** out) {
   KP_API({
     if (!p || !b) throw InvalidArgument("make_spectral_data: null argument");
     const int n = p->n;
@@ -1197,19 +1288,23 @@ int kp_spectral_create(const kp_precond* p, const double* b, kp_spectral** out) 
     auto sd = std::make_unique<kp_spectral>();
     sd->n = n;
     sd->sh = p->sh;
-    sd->bhat.alloc(nn);
-    DBuf<double> db(nn), t(nn);
-    db.upload(b, nn);
-    F64GemmArgs g;  // b_hat = vec(U_c^T B U_r)  (factor.cpp:157-177)
-    g.M = n, g.N = n, g.nb = 1, g.Kb = n;
-    g.A = {sd->sh->d_u_c.p, n, 0}, g.B = {db.p, n, 0};
-    g.epi.C = t.p, g.epi.cm = n, g.epi.cn = 1;
-    gemm_f64(g, KC_SPECTRAL);
-    g.A = {t.p, n, 0}, g.B = {sd->sh->d_u_r.p, n, 0};
-    g.epi = F64Epilogue{}, g.epi.C = sd->bhat.p, g.epi.cm = 1, g.epi.cn = n;
-    gemm_f64(g, KC_SPECTRAL);
-    sync();
     auto& sh = *sd->sh;
+    sd->bhat.alloc(nn);
+    {
+      DBuf<double> db(nn);
+      db.upload(b, nn);
+      project_dev(n, sh.d_u_c.p, sh.d_u_r.p, db.p, sd->bhat.p);
+      if (x_true) {
+        if (!sh.d_v_r.p) {
+          sh.d_v_r.alloc(nn), sh.d_v_r.upload(sh.v_r.data(), nn);
+          sh.d_v_c.alloc(nn), sh.d_v_c.upload(sh.v_c.data(), nn);
+        }
+        sd->xhat.alloc(nn);
+        db.upload(x_true, nn);
+        project_dev(n, sh.d_v_c.p, sh.d_v_r.p, db.p, sd->xhat.p);
+      }
+      sync();
+    }
     if (!sh.have_range) {
       const auto& sr = sh.s_r;
       const auto& sc = sh.s_c;
@@ -1223,6 +1318,67 @@ int kp_spectral_create(const kp_precond* p, const double* b, kp_spectral** out) 
     }
     sd->smin = sh.smin, sd->smax = sh.smax;
     *out = sd.release();
+  })
+}
+int kp_spectral_create(const kp_precond* p, const double* b, kp_spectral** out) {
+  return kp_spectral_create_x(p, b, nullptr, out);
+}
+// filtered_solution (regparam.cpp:329-349): X = V_c (F .* (U_c^T B U_r)) V_r^T
+// with F(i,j) = sigma / (sigma^2 + lambda^2), sigma = s_r(j) s_c(i); FP64.
+int kp_filtered_solution(const kp_precond* p, const double* b, double lambda, double* x) {
+  KP_API({
+    if (!p || !b || !x) throw InvalidArgument("filtered_solution: null argument");
+    if (lambda < 0.0) throw InvalidArgument("filtered_solution: negative lambda");
+    const int n = p->n;
+    const size_t nn = size_t(n) * n;
+    auto& sh = *p->sh;
+    if (lambda == 0.0) {
+      double mn = std::numeric_limits<double>::infinity();
+      for (double v : sh.s_r) mn = std::min(mn, std::fabs(v));
+      double mc = std::numeric_limits<double>::infinity();
+      for (double v : sh.s_c) mc = std::min(mc, std::fabs(v));
+      if ((mn * mc) * (mn * mc) == 0.0)
+        throw InvalidArgument("filtered_solution: zero singular value with lambda = 0");
+    }
+    if (!sh.d_v_r.p) {
+      sh.d_v_r.alloc(nn), sh.d_v_r.upload(sh.v_r.data(), nn);
+      sh.d_v_c.alloc(nn), sh.d_v_c.upload(sh.v_c.data(), nn);
+    }
+    DBuf<double> db(nn), bh(nn), t(nn);
+    db.upload(b, nn);
+    project_dev(n, sh.d_u_c.p, sh.d_u_r.p, db.p, bh.p);
+    spectral_filter(sh.d_s_r.p, sh.d_s_c.p, n, lambda * lambda, bh.p);  // coef in place
+    if (!sh.d_vc_rm.p) {  // row-major copies of V_c, V_r (K-major operands below)
+      sh.d_vc_rm.alloc(nn), sh.d_vc_rm.upload(host_transpose(sh.v_c, n).data(), nn);
+      sh.d_vr_rm.alloc(nn), sh.d_vr_rm.upload(host_transpose(sh.v_r, n).data(), nn);
+      sync();
+    }
+    F64GemmArgs g;  // t = V_c coef ; X = t V_r^T
+    g.M = n, g.N = n, g.nb = 1, g.Kb = n;
+    g.A = {sh.d_vc_rm.p, n, 0}, g.B = {bh.p, n, 0};
+    g.epi.C = t.p, g.epi.cm = n, g.epi.cn = 1;
+    gemm_f64(g, KC_SPECTRAL);
+    g.A = {t.p, n, 0}, g.B = {sh.d_vr_rm.p, n, 0};
+    g.epi = F64Epilogue{}, g.epi.C = db.p, g.epi.cm = 1, g.epi.cn = n;
+    gemm_f64(g, KC_SPECTRAL);
+    db.download(x, nn);
+    sync();
+  })
+}
+int kp_spectral_export_xhat(const kp_spectral* sd, double* x_hat) {
+  KP_API({
+    if (!sd || !sd->xhat.p) throw InvalidArgument("spectral data: x coordinates missing");
+    const int n = sd->n;
+    const size_t nn = size_t(n) * n;
+    std::vector<double> prod(nn), xh(nn);
+    for (long j = 0; j < n; ++j)
+      for (long i = 0; i < n; ++i) prod[j * n + i] = sd->sh->s_r[j] * sd->sh->s_c[i];
+    sd->xhat.download(xh.data(), nn);
+    sync();
+    std::vector<long> perm(nn);
+    std::iota(perm.begin(), perm.end(), 0L);
+    std::stable_sort(perm.begin(), perm.end(), [&](long a, long b) { return prod[a] > prod[b]; });
+    for (size_t k = 0; k < nn; ++k) x_hat[k] = xh[perm[k]];
   })
 }
 int kp_spectral_destroy(kp_spectral* sd) { KP_API(delete sd) }
@@ -1278,43 +1434,44 @@ int kp_gcv_grid(const kp_spectral* sd, const double* lambdas, int m, double* val
 // gcv (regparam.cpp:254-258) = run_selector(minimize_log)
 int kp_gcv(const kp_spectral* sd, kp_param_choice* choice) {
   KP_API({
-    const double lo = std::max(sd->smin, 1e-10 * sd->smax), hi = sd->smax;
-    auto g = [&](double l) { return gcv_value(sd, l); };
-    kp_param_choice c{};
-    c.method = 1, c.bracket_lo = lo, c.bracket_hi = hi, c.grid_index = -1;
-    if (hi <= lo * (1.0 + 1e-12)) {
-      c.lambda = lo, c.objective_value = probe(g, lo, "minimize_log"), c.flat_objective = 1;
-    } else {  // minimize_log (regparam.cpp:54-88), grid evaluated in one batched launch
-      const double ulo = std::log(lo), uhi = std::log(hi);
-      const int grid = 1024;
-      std::vector<double> ls(grid), vs(grid);
-      for (int k = 0; k < grid; ++k) ls[k] = std::exp(ulo + (uhi - ulo) * k / (grid - 1));
-      gcv_values(sd, ls.data(), grid, vs.data());
-      int best_k = -1;
-      double best_v = std::numeric_limits<double>::infinity();
-      double vmin = best_v, vmax = -best_v;
-      for (int k = 0; k < grid; ++k) {
-        const double v = vs[k];
-        if (std::isnan(v)) throw std::runtime_error("minimize_log: objective is NaN");
-        if (!std::isfinite(v)) continue;
-        vmin = std::min(vmin, v), vmax = std::max(vmax, v);
-        if (v < best_v) best_v = v, best_k = k;
-      }
-      if (best_k < 0) throw std::runtime_error("minimize_log: objective infinite everywhere");
-      const double scale = std::max({std::abs(vmin), std::abs(vmax), 1e-300});
-      if (vmax - vmin <= 1e-14 * scale) {
-        const double mid = std::exp(0.5 * (ulo + uhi));
-        c.lambda = mid, c.objective_value = probe(g, mid, "minimize_log"), c.flat_objective = 1;
-      } else {
-        const double step = (uhi - ulo) / (grid - 1);
-        const double a = std::max(ulo, ulo + (best_k - 1) * step);
-        const double b = std::min(uhi, ulo + (best_k + 1) * step);
-        const auto r = minimize_1d([&](double u) { return g(std::exp(u)); }, a, b, 1e-12);
-        c.lambda = std::exp(r.first), c.objective_value = r.second;
-      }
-    }
-    *choice = c;
+    check_spectral(sd, false);
+    const auto br = selector_bracket(sd);
+    *choice = minimize_log(sd, SK_GCV, 0.0, br.first, br.second, 1);
   })
+}
+// lambda_opt (regparam.cpp:248-252)
+int kp_lambda_opt(const kp_spectral* sd, kp_param_choice* choice) {
+  KP_API({
+    check_spectral(sd, true);
+    const auto br = selector_bracket(sd);
+    *choice = minimize_log(sd, SK_OPT, 0.0, br.first, br.second, 0);
+  })
+}
+// wgcv (regparam.cpp:260-286): for omega > 1 start where the trace term
+// turns positive (log-bisection to 1e-13 relative width)
+int kp_wgcv(const kp_spectral* sd, double omega, kp_param_choice* choice) {
+  KP_API({
+    check_spectral(sd, false);
+    if (!(omega > 0.0)) throw InvalidArgument("wgcv: omega must be positive");
+    auto [lo, hi] = selector_bracket(sd);
+    auto tr = [&](double l) { return spectral_value(sd, SK_WTRACE, l, omega); };
+    if (omega > 1.0 && tr(lo) < 0.0 && tr(hi) > 0.0) {
+      double a = std::log(lo), b = std::log(hi);
+      while (b - a > 1e-13 * (1.0 + std::abs(b))) {
+        const double m = 0.5 * (a + b);
+        (tr(std::exp(m)) > 0.0 ? b : a) = m;
+      }
+      lo = std::exp(b);
+    }
+    *choice = minimize_log(sd, SK_WGCV, omega, lo, hi, 2);
+    choice->omega = omega;
+  })
+}
+int kp_opt_objective(const kp_spectral* sd, double lambda, double* value) {
+  KP_API(*value = spectral_value(sd, SK_OPT, lambda))
+}
+int kp_wgcv_objective(const kp_spectral* sd, double omega, double lambda, double* value) {
+  KP_API(*value = spectral_value(sd, SK_WGCV, lambda, omega))
 }
 // discrepancy (regparam.cpp:288-327)
 int kp_discrepancy(const kp_spectral* sd, double noise_norm, double eta, kp_param_choice* choice) {

@@ -489,15 +489,18 @@ __global__ void cgls_next_kernel(DevState* st) {
 }
 
 // ---------------------------------------------------------------------------
-// Spectral sums. sigma(i,j) = s_r[j] * s_c[i] at linear index j*n + i. LC
-// lambdas per pass over b_hat (LC = 1 for the single-lambda probes of the
+// Spectral sums (regparam.cpp:216-246). sigma(i,j) = s_r[j] * s_c[i] at
+// linear index j*n + i; two sums per lambda (see SpectralKind in vec.cuh).
+// LC lambdas per pass over b_hat (LC = 1 for the single-lambda probes of the
 // root finders, 16 for grids).
-template <int LC>
-__global__ void gcv_sums_kernel(const double* s_r, const double* s_c, const double* bhat, int n,
-                                const double* lambdas, int m, double* part) {
+template <int LC, int KIND>
+__global__ void spectral_sums_kernel(const double* s_r, const double* s_c, const double* bhat,
+                                     const double* xhat, int n, const double* lambdas, int m,
+                                     double omega, double* part) {
   __shared__ double red[VEC_THREADS / 32][2 * LC];
   const size_t nn = size_t(n) * n;
   const unsigned un = unsigned(n);
+  const double om1 = 1.0 - omega;
   for (int q0 = 0; q0 < m; q0 += LC) {
     double l2[LC];
     double v[2 * LC];
@@ -512,12 +515,27 @@ __global__ void gcv_sums_kernel(const double* s_r, const double* s_c, const doub
       const unsigned j = unsigned(idx / un), i = unsigned(idx - size_t(j) * un);
       const double s = s_r[j] * s_c[i];
       const double s2 = s * s, b = bhat[idx];
+      const double x = (KIND == SK_OPT) ? xhat[idx] : 0.0;
 #pragma unroll
       for (int c = 0; c < LC; ++c) {
         const double d = s2 + l2[c];
-        const double t = b / d;
-        v[2 * c] += t * t;
-        v[2 * c + 1] += 1.0 / d;
+        if (KIND == SK_GCV) {  // (b/d)^2, 1/d
+          const double t = b / d;
+          v[2 * c] += t * t;
+          v[2 * c + 1] += 1.0 / d;
+        } else if (KIND == SK_RESID) {  // (l^2 b/d)^2
+          const double t = l2[c] * b / d;
+          v[2 * c] += t * t;
+        } else if (KIND == SK_OPT) {  // (s b/d - x)^2
+          const double t = s * b / d - x;
+          v[2 * c] += t * t;
+        } else if (KIND == SK_WGCV) {  // (l^2 b/d)^2, ((1-w) s^2 + l^2)/d
+          const double t = l2[c] * b / d;
+          v[2 * c] += t * t;
+          v[2 * c + 1] += (om1 * s2 + l2[c]) / d;
+        } else {  // SK_WTRACE: ((1-w) s^2 + l^2)/d
+          v[2 * c] += (om1 * s2 + l2[c]) / d;
+        }
       }
     }
     block_sum<2 * LC>(v, red);
@@ -530,37 +548,18 @@ __global__ void gcv_sums_kernel(const double* s_r, const double* s_c, const doub
   }
 }
 
-template <int LC>
-__global__ void resid_sums_kernel(const double* s_r, const double* s_c, const double* bhat, int n,
-                                  const double* lambdas, int m, double* part) {
-  __shared__ double red[VEC_THREADS / 32][LC];
+// Tikhonov filter in place: c(i,j) = sigma / (sigma^2 + l2) * c(i,j)
+// (regparam.cpp:329-349).
+__global__ void spectral_filter_kernel(const double* s_r, const double* s_c, int n, double l2,
+                                       double* c) {
   const size_t nn = size_t(n) * n;
   const unsigned un = unsigned(n);
-  for (int q0 = 0; q0 < m; q0 += LC) {
-    double l2[LC];
-    double v[LC];
-#pragma unroll
-    for (int c = 0; c < LC; ++c) {
-      const double l = (q0 + c < m) ? lambdas[q0 + c] : 1.0;
-      l2[c] = l * l;
-      v[c] = 0.0;
-    }
-    for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < nn;
-         idx += size_t(gridDim.x) * blockDim.x) {
-      const unsigned j = unsigned(idx / un), i = unsigned(idx - size_t(j) * un);
-      const double s = s_r[j] * s_c[i];
-      const double s2 = s * s, b = bhat[idx];
-#pragma unroll
-      for (int c = 0; c < LC; ++c) {
-        const double t = l2[c] * b / (s2 + l2[c]);
-        v[c] += t * t;
-      }
-    }
-    block_sum<LC>(v, red);
-    if (threadIdx.x == 0)
-      for (int c = 0; c < LC && q0 + c < m; ++c)
-        part[size_t(q0 + c) * gridDim.x + blockIdx.x] = v[c];
-    __syncthreads();
+  for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < nn;
+       idx += size_t(gridDim.x) * blockDim.x) {
+    const unsigned j = unsigned(idx / un), i = unsigned(idx - size_t(j) * un);
+    const double s = __dmul_rn(s_r[j], s_c[i]);
+    const double den = __dadd_rn(__dmul_rn(s, s), l2);
+    c[idx] = __dmul_rn(__ddiv_rn(s, den), c[idx]);
   }
 }
 
@@ -683,29 +682,35 @@ void cgls_p_update(DevState* st, double* p, const double* s, double* s_prev, siz
   KP_LAUNCH(KC_VECTOR, cgls_next_kernel, 1, 32, st);
 }
 
-void spectral_gcv_sums(const double* s_r, const double* s_c, const double* bhat, int n,
-                       const double* lambdas, int m, double* out) {
-  DBuf<double> part(size_t(m) * VEC_CTAS * 2);
-  if (m == 1)
-    KP_LAUNCH(KC_SPECTRAL, gcv_sums_kernel<1>, VEC_CTAS, VEC_THREADS, s_r, s_c, bhat, n, lambdas,
-              m, part.p);
-  else
-    KP_LAUNCH(KC_SPECTRAL, gcv_sums_kernel<LCHUNK>, VEC_CTAS, VEC_THREADS, s_r, s_c, bhat, n,
-              lambdas, m, part.p);
-  KP_LAUNCH(KC_SPECTRAL, finish_sums_kernel, m, VEC_THREADS, part.p, VEC_CTAS, 2, m, out);
-  KP_CUDA(cudaStreamSynchronize(ctx().stream));
+void spectral_filter(const double* s_r, const double* s_c, int n, double l2, double* c) {
+  KP_LAUNCH(KC_SPECTRAL, spectral_filter_kernel, vec_grid(size_t(n) * n), VEC_THREADS, s_r, s_c, n,
+            l2, c);
 }
-void spectral_resid_sums(const double* s_r, const double* s_c, const double* bhat, int n,
-                         const double* lambdas, int m, double* out) {
-  DBuf<double> part(size_t(m) * VEC_CTAS);
+
+template <int KIND>
+void launch_sums(const double* s_r, const double* s_c, const double* bhat, const double* xhat,
+                 int n, const double* lambdas, int m, double omega, double* part) {
   if (m == 1)
-    KP_LAUNCH(KC_SPECTRAL, resid_sums_kernel<1>, VEC_CTAS, VEC_THREADS, s_r, s_c, bhat, n, lambdas,
-              m, part.p);
+    KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<1, KIND>), VEC_CTAS, VEC_THREADS, s_r, s_c, bhat,
+              xhat, n, lambdas, m, omega, part);
   else
-    KP_LAUNCH(KC_SPECTRAL, resid_sums_kernel<LCHUNK>, VEC_CTAS, VEC_THREADS, s_r, s_c, bhat, n,
-              lambdas, m, part.p);
-  KP_LAUNCH(KC_SPECTRAL, finish_sums_kernel, m, VEC_THREADS, part.p, VEC_CTAS, 1, m, out);
-  KP_CUDA(cudaStreamSynchronize(ctx().stream));
+    KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<LCHUNK, KIND>), VEC_CTAS, VEC_THREADS, s_r, s_c,
+              bhat, xhat, n, lambdas, m, omega, part);
+}
+
+void spectral_sums(int kind, const double* s_r, const double* s_c, const double* bhat,
+                   const double* xhat, int n, const double* lambdas, int m, double omega,
+                   double* out) {
+  DBuf<double> part(size_t(m) * VEC_CTAS * 2);
+  switch (kind) {
+    case SK_GCV: launch_sums<SK_GCV>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p); break;
+    case SK_RESID: launch_sums<SK_RESID>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p); break;
+    case SK_OPT: launch_sums<SK_OPT>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p); break;
+    case SK_WGCV: launch_sums<SK_WGCV>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p); break;
+    case SK_WTRACE: launch_sums<SK_WTRACE>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p); break;
+    default: throw InvalidArgument("spectral_sums: bad kind");
+  }
+  KP_LAUNCH(KC_SPECTRAL, finish_sums_kernel, m, VEC_THREADS, part.p, VEC_CTAS, 2, m, out);
 }
 
 }  // namespace kp

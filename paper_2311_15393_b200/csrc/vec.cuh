@@ -98,12 +98,19 @@ void cgls_p_update(DevState* st, double* p, const double* s, double* s_prev, siz
                    double* partials);
 
 // ---- spectral ----------------------------------------------------------------
-// For each lambda_q: num_q = sum (bhat/d)^2, den_q = sum 1/d, d = sigma^2 +
-// lambda^2, sigma(i,j) = s_r[j] s_c[i]. out[q*2+{0,1}] (device).
-void spectral_gcv_sums(const double* s_r, const double* s_c, const double* bhat, int n,
-                       const double* lambdas, int m, double* out);
-// out[q] = sum (lambda^2 bhat / d)^2 for each lambda_q (device).
-void spectral_resid_sums(const double* s_r, const double* s_c, const double* bhat, int n,
-                         const double* lambdas, int m, double* out);
+// Per-lambda sums over sigma(i,j) = s_r[j] s_c[i], d = sigma^2 + lambda^2
+// (regparam.cpp:216-246), written to out[q*2 + {0,1}] (device):
+enum SpectralKind {
+  SK_GCV = 0,     // sum (bhat/d)^2,          sum 1/d
+  SK_RESID = 1,   // sum (lambda^2 bhat/d)^2, 0
+  SK_OPT = 2,     // sum (sigma bhat/d - xhat)^2, 0
+  SK_WGCV = 3,    // sum (lambda^2 bhat/d)^2, sum ((1-omega) sigma^2 + lambda^2)/d
+  SK_WTRACE = 4,  // sum ((1-omega) sigma^2 + lambda^2)/d, 0
+};
+// c(i,j) *= sigma / (sigma^2 + l2) (filtered_solution coefficients), device
+void spectral_filter(const double* s_r, const double* s_c, int n, double l2, double* c);
+void spectral_sums(int kind, const double* s_r, const double* s_c, const double* bhat,
+                   const double* xhat, int n, const double* lambdas, int m, double omega,
+                   double* out);
 
 }  // namespace kp

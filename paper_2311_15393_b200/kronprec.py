@@ -26,8 +26,8 @@ __all__ = [
     "build_preconditioner", "build_preconditioner_from_svd", "with_lambda", "precond_solve",
     "SolverOptions", "ConvergenceHistory", "SolveResult", "cgls", "pcg", "fpcg",
     "plateau_iteration", "WorkReport", "work_report", "SpectralData", "make_spectral_data",
-    "ParamChoice", "gcv_objective", "discrepancy_gap", "gcv", "gcv_grid", "discrepancy",
-    "NoRootError",
+    "ParamChoice", "gcv_objective", "opt_objective", "wgcv_objective", "discrepancy_gap", "gcv",
+    "gcv_grid", "lambda_opt", "wgcv", "discrepancy", "filtered_solution", "NoRootError",
 ]
 
 
@@ -453,10 +453,11 @@ def _choice(c: kp_param_choice) -> ParamChoice:
 class SpectralData:
     """Device-resident sigma_hat = s_r(j) s_c(i) and b_hat = vec(U_c^T B U_r)."""
 
-    def __init__(self, handle, n: int):
+    def __init__(self, handle, n: int, has_x: bool = False):
         self._h = handle
         self.n = n * n
         self._side = n
+        self._has_x = has_x
 
     def handle(self):
         return self._h
@@ -473,6 +474,15 @@ class SpectralData:
         return self.exported()[0]
 
     @property
+    def x_hat(self) -> np.ndarray | None:
+        """Coordinates of x_true (same order as exported()), or None."""
+        if not self._has_x:
+            return None
+        x = np.empty(self.n)
+        check(lib().kp_spectral_export_xhat(self._h, ptr(x)))
+        return x
+
+    @property
     def b_hat(self) -> np.ndarray:
         return self.exported()[1]
 
@@ -485,19 +495,60 @@ class SpectralData:
             pass
 
 
-def make_spectral_data(p: KronSvdPreconditioner, b) -> SpectralData:  # regparam.cpp:119-126
+def make_spectral_data(p: KronSvdPreconditioner, b, x_true=None) -> SpectralData:
+    """regparam.cpp:119-134 (x_true: the overload with x coordinates)."""
     b = np.ascontiguousarray(np.asarray(b, dtype=np.float64).reshape(-1))
     if b.size != p.n * p.n:
         raise ValueError("project: vector length is not n^2")
     h = C.c_void_p()
-    check(lib().kp_spectral_create(p.handle(), ptr(b), C.byref(h)))
-    return SpectralData(h, p.n)
+    if x_true is None:
+        check(lib().kp_spectral_create(p.handle(), ptr(b), C.byref(h)))
+        return SpectralData(h, p.n)
+    x = np.ascontiguousarray(np.asarray(x_true, dtype=np.float64).reshape(-1))
+    if x.size != p.n * p.n:
+        raise ValueError("project: vector length is not n^2")
+    check(lib().kp_spectral_create_x(p.handle(), ptr(b), ptr(x), C.byref(h)))
+    return SpectralData(h, p.n, True)
 
 
 def gcv_objective(sd: SpectralData, lambda_: float) -> float:  # regparam.cpp:224-229
     v = C.c_double()
     check(lib().kp_gcv_objective(sd.handle(), float(lambda_), C.byref(v)))
     return v.value
+
+
+def opt_objective(sd: SpectralData, lambda_: float) -> float:  # regparam.cpp:216-222
+    v = C.c_double()
+    check(lib().kp_opt_objective(sd.handle(), float(lambda_), C.byref(v)))
+    return v.value
+
+
+def wgcv_objective(sd: SpectralData, omega: float, lambda_: float) -> float:  # :231-240
+    v = C.c_double()
+    check(lib().kp_wgcv_objective(sd.handle(), float(omega), float(lambda_), C.byref(v)))
+    return v.value
+
+
+def lambda_opt(sd: SpectralData) -> ParamChoice:  # regparam.cpp:248-252
+    c = kp_param_choice()
+    check(lib().kp_lambda_opt(sd.handle(), C.byref(c)))
+    return _choice(c)
+
+
+def wgcv(sd: SpectralData, omega: float) -> ParamChoice:  # regparam.cpp:260-286
+    c = kp_param_choice()
+    check(lib().kp_wgcv(sd.handle(), float(omega), C.byref(c)))
+    return _choice(c)
+
+
+def filtered_solution(p: KronSvdPreconditioner, b, lambda_: float) -> np.ndarray:
+    """Direct Tikhonov solution for the Kronecker approximation (regparam.cpp:329-349)."""
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64).reshape(-1))
+    if b.size != p.n * p.n:
+        raise ValueError("filtered_solution: vector length is not n^2")
+    x = np.empty_like(b)
+    check(lib().kp_filtered_solution(p.handle(), ptr(b), float(lambda_), ptr(x)))
+    return x
 
 
 def discrepancy_gap(sd: SpectralData, epsilon: float, lambda_: float) -> float:  # :242-246

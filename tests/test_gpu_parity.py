@@ -390,6 +390,39 @@ def test_spectral_data_and_selectors_match_oracle():
         K.discrepancy(sd, 1e-30, 1.0)
 
 
+def test_opt_wgcv_filtered_match_oracle():  # regparam.cpp:216-286, 329-349
+    n = 40
+    tp, term = blob_problem(n, noise=0.01)
+    g, o = both_preconds(term, 1.0, H)
+    sd = K.make_spectral_data(g, tp.b, tp.x_true)
+    so, bo, xo = O.spectral(o, tp.b, tp.x_true)
+    sg, bg = sd.exported()
+    xg = sd.x_hat
+    assert np.array_equal(sg, so)
+    assert np.abs(xg - xo).max() <= 1e-12 * np.abs(xo).max()
+    for lam in (1e-3, 3e-2, 0.5):
+        assert K.opt_objective(sd, lam) == pytest.approx(O.opt_objective(so, bo, xo, lam), rel=1e-10)
+        for om in (0.5, 1.0, 1.7):
+            assert K.wgcv_objective(sd, om, lam) == pytest.approx(
+                O.wgcv_objective(so, bo, om, lam), rel=1e-10)
+    c, oc = K.lambda_opt(sd), O.select("opt", so, bo, xo)
+    assert c.method == "opt" and c.lambda_ == pytest.approx(oc["lambda"], rel=1e-6)
+    assert c.bracket_lo == pytest.approx(oc["bracket_lo"], rel=1e-15)
+    for om in (0.7, 1.5):
+        c, oc = K.wgcv(sd, om), O.select("wgcv", so, bo, omega=om)
+        assert c.omega == om and c.lambda_ == pytest.approx(oc["lambda"], rel=1e-6)
+        assert c.bracket_lo == pytest.approx(oc["bracket_lo"], rel=1e-9)
+    with pytest.raises(ValueError):
+        K.lambda_opt(K.make_spectral_data(g, tp.b))  # no x coordinates
+    with pytest.raises(ValueError):
+        K.wgcv(sd, 0.0)
+    for lam in (1e-3, 0.05):
+        xf, xof = K.filtered_solution(g, tp.b, lam), O.filtered_solution(o, tp.b, lam)
+        assert np.linalg.norm(xf - xof) <= 1e-11 * np.linalg.norm(xof)
+    with pytest.raises(ValueError):
+        K.filtered_solution(g, tp.b, -1.0)
+
+
 # ---- tcgen05 tensor mode (KP_ACCUM_TENSOR) -------------------------------------------
 def tensor_mode_emulation(sr, sc, lam, r):
     """fp16 operands, wide accumulation, one binary16 rounding per product
