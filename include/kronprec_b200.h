@@ -186,6 +186,19 @@ int kp_precond_export(const kp_precond* p, int field, double* out);
 int kp_precond_info(const kp_precond* p, int* n, double* lambda,
                     kp_format* fmt, int* accum);
 
+/* ---- emulated low-precision BLAS: precision.hpp / lpblas.hpp ----------- */
+/* round_array (precision.cpp:82-95) for any format; host arrays. */
+int kp_round_array(const double* x, long count, kp_format fmt, double* out);
+/* lp_matmul (lpblas.cpp:59-70): c = tree_k round(a(:,k) b(k,:)), one
+ * rounding per pairwise stage; a m x k, b k x n, c m x n, column-major host
+ * arrays. Bit-identical to the reference for every format. */
+int kp_lp_matmul(int m, int k, int n, const double* a, const double* b,
+                 kp_format fmt, double* c);
+/* round_leaves = 0: the products are taken as pre-rounded addends, which
+ * with b = ones gives pairwise_sum (lpblas.cpp:34-37). */
+int kp_lp_matmul_ex(int m, int k, int n, const double* a, const double* b,
+                    kp_format fmt, int round_leaves, double* c);
+
 /* ---- solvers: krylov.hpp / krylov.cpp --------------------------------- */
 int kp_cgls(const kp_operator* op, const double* b,
             const kp_solver_options* opts, double* x, kp_history* hist);

@@ -70,7 +70,8 @@ EXPORTS = [
     "kp_spectral_export", "kp_gcv_objective", "kp_discrepancy_gap", "kp_gcv_grid", "kp_gcv",
     "kp_discrepancy", "kp_operator_set_mode", "kp_operator_get_mode", "kp_event_record", "kp_event_elapsed", "kp_host_alloc", "kp_host_free",
     "kp_spectral_create_x", "kp_spectral_export_xhat", "kp_opt_objective", "kp_wgcv_objective",
-    "kp_lambda_opt", "kp_wgcv", "kp_filtered_solution",
+    "kp_lambda_opt", "kp_wgcv", "kp_filtered_solution", "kp_round_array", "kp_lp_matmul",
+    "kp_lp_matmul_ex",
 ]
 
 _lib = None
@@ -122,6 +123,9 @@ def lib() -> C.CDLL:
             "kp_lambda_opt": ([P, C.POINTER(kp_param_choice)], I),
             "kp_wgcv": ([P, D, C.POINTER(kp_param_choice)], I),
             "kp_filtered_solution": ([P, P, D, P], I),
+            "kp_round_array": ([P, C.c_long, kp_format, P], I),
+            "kp_lp_matmul": ([I, I, I, P, P, kp_format, P], I),
+            "kp_lp_matmul_ex": ([I, I, I, P, P, kp_format, I, P], I),
             "kp_discrepancy": ([P, D, D, C.POINTER(kp_param_choice)], I),
             "kp_event_record": ([I], I),
             "kp_operator_set_mode": ([P, I], I),

@@ -27,6 +27,7 @@
 #include "common.cuh"
 #include "gemm_f16ref.cuh"
 #include "gemm_f16tc.cuh"
+#include "lp_generic.cuh"
 #include "gemm_f64.cuh"
 #include "host_la.h"
 #include "vec.cuh"
@@ -236,6 +237,7 @@ struct kp_precond {
   // workspace
   DBuf<__half> r16, t1h, wh, t3h;
   DBuf<double> t1d, wd, t3d;
+  DBuf<double> rlp;  // generic formats: round_array(unvec(r), fmt)
   DBuf<double> part;
 };
 
@@ -254,6 +256,19 @@ bool covers_double(const kp_format& f) {
 }
 bool is_fp16(const kp_format& f) {
   return f.significand_bits == 11 && f.max_exponent == 15 && f.subnormals_enabled;
+}
+// Neither fp16 (f16x2 GEMMs) nor double-covering (DMMA GEMMs): the generic
+// emulation path (lp_generic.cu), exact for any (t, emax, subnormals).
+bool is_generic(const kp_format& f) { return !covers_double(f) && !is_fp16(f); }
+LpFormat lp_format(const kp_format& f) {
+  LpFormat l;
+  l.t = f.significand_bits, l.emax = f.max_exponent, l.sub = f.subnormals_enabled != 0;
+  return l;
+}
+void check_format(const kp_format& f) {
+  if (f.significand_bits < 2 || f.significand_bits > 53 || f.max_exponent < 1 ||
+      f.max_exponent > 1023)
+    throw InvalidArgument("precision format: need 2 <= t <= 53 and 1 <= emax <= 1023");
 }
 long round_up(long v, long m) { return (v + m - 1) / m * m; }
 
@@ -350,6 +365,7 @@ void detect_banded(kp_operator* op, const double* rows, const double* cols) {
 }
 
 int msolve_partials_ctas(const kp_precond* p) {
+  if (is_generic(p->fmt)) return LP_PART_CTAS;
   if (covers_double(p->fmt)) return gemm_f64_num_ctas(p->n, p->n);
   return p->accum == KP_ACCUM_TENSOR ? gemm_f16tc_num_ctas(p->n, p->n)
                                      : gemm_f16ref_num_ctas(p->n, p->n);
@@ -358,7 +374,10 @@ int msolve_partials_ctas(const kp_precond* p) {
 void ensure_ws(kp_precond* p) {
   const int n = p->n;
   const size_t nn = size_t(n) * n;
-  if (covers_double(p->fmt)) {
+  if (is_generic(p->fmt)) {
+    if (!p->t1d.p) p->t1d.alloc(nn), p->wd.alloc(nn), p->t3d.alloc(nn), p->rlp.alloc(nn);
+    if (!p->part.p) p->part.alloc(size_t(LP_PART_CTAS) * 4);
+  } else if (covers_double(p->fmt)) {
     if (!p->t1d.p) p->t1d.alloc(nn), p->wd.alloc(nn), p->t3d.alloc(nn);
     if (!p->part.p) p->part.alloc(size_t(gemm_f64_num_ctas(n, n)) * 4);
   } else {
@@ -383,6 +402,28 @@ void msolve(kp_precond* p, const double* r, double* z, const double* d0, const d
   const int n = p->n;
   auto* sh = p->sh.get();
   ensure_ws(p);
+  if (is_generic(p->fmt)) {  // precond_solve (factor.cpp:117-132), every rounding explicit
+    const size_t nn = size_t(n) * n;
+    const LpFormat f = lp_format(p->fmt);
+    lp_round_array(r, nn, f, p->rlp.p, KC_PRECOND);  // round_inplace(rm)
+    LpGemmArgs g;
+    g.M = n, g.N = n, g.K = n, g.f = f, g.status = status, g.ldc = n;
+    g.a = sh->vc.p, g.ai = n, g.ak = 1;  // t1 = lp(vc_lp^T, rm)
+    g.b = p->rlp.p, g.bk = 1, g.bj = n, g.c = p->t1d.p;
+    lp_gemm_generic(g, KC_PRECOND);
+    g.a = p->t1d.p, g.ai = 1, g.ak = n;  // w = round(s_lp .* lp(t1, vr_lp))
+    g.b = sh->vr.p, g.bk = 1, g.bj = n, g.c = p->wd.p, g.scale = p->s64.p, g.ls = n;
+    lp_gemm_generic(g, KC_PRECOND);
+    g.scale = nullptr;
+    g.a = sh->vc.p, g.ai = 1, g.ak = n;  // t3 = lp(vc_lp, w)
+    g.b = p->wd.p, g.bk = 1, g.bj = n, g.c = p->t3d.p;
+    lp_gemm_generic(g, KC_PRECOND);
+    g.a = p->t3d.p, g.ai = 1, g.ak = n;  // z = lp(t3, vr_lp^T)
+    g.b = sh->vr.p, g.bk = n, g.bj = 1, g.c = z;
+    lp_gemm_generic(g, KC_PRECOND);
+    lp_vector_partials(z, nn, d0, d1a, d1b, p->part.p, status, KC_PRECOND);
+    return;
+  }
   if (covers_double(p->fmt)) {
     F64GemmArgs g;
     g.M = n, g.N = n, g.nb = 1, g.Kb = n, g.status = status;
@@ -472,9 +513,10 @@ void set_weights(kp_precond* p) {
   const double l2 = p->lambda * p->lambda;
   if (pmin * pmin + l2 == 0.0)
     throw InvalidArgument("build_preconditioner: singular factors need lambda > 0");
-  if (covers_double(p->fmt)) {
+  if (covers_double(p->fmt) || is_generic(p->fmt)) {
     p->s64.alloc(nn);
     precond_weights(sh.d_s_r.p, sh.d_s_c.p, n, l2, p->s64.p, nullptr);
+    if (is_generic(p->fmt)) lp_round_array(p->s64.p, nn, lp_format(p->fmt), p->s64.p, KC_PRECOND);
   } else {
     p->s16.alloc(nn);
     precond_weights(sh.d_s_r.p, sh.d_s_c.p, n, l2, nullptr, p->s16.p);  // round_array(S)
@@ -494,8 +536,7 @@ kp_precond* precond_from_svd(int n, std::vector<double> ur, std::vector<double> 
                              kp_format fmt, int accum) {
   if (n < 1) throw InvalidArgument("build_preconditioner: empty factors");
   if (lambda < 0.0) throw InvalidArgument("build_preconditioner: negative lambda");
-  if (!covers_double(fmt) && !is_fp16(fmt))
-    throw Unsupported("build_preconditioner: the B200 path stores fp16 or FP64 factors only");
+  check_format(fmt);
   if (accum == KP_ACCUM_TENSOR && !is_fp16(fmt))
     throw InvalidArgument("build_preconditioner: tensor accumulation requires fp16");
   auto sh = std::make_shared<PrecondShared>();
@@ -508,7 +549,12 @@ kp_precond* precond_from_svd(int n, std::vector<double> ur, std::vector<double> 
   sh->d_s_r.alloc(n), sh->d_s_r.upload(sh->s_r.data(), n);
   sh->d_s_c.alloc(n), sh->d_s_c.upload(sh->s_c.data(), n);
   const std::vector<double> vct = host_transpose(sh->v_c, n), vrt = host_transpose(sh->v_r, n);
-  if (covers_double(fmt)) {
+  if (is_generic(fmt)) {  // vr_lp, vc_lp = round_array(V, fmt), FP64 col-major
+    sh->vc.alloc(nn), sh->vc.upload(sh->v_c.data(), nn);
+    sh->vr.alloc(nn), sh->vr.upload(sh->v_r.data(), nn);
+    lp_round_array(sh->vc.p, nn, lp_format(fmt), sh->vc.p, KC_PRECOND);
+    lp_round_array(sh->vr.p, nn, lp_format(fmt), sh->vr.p, KC_PRECOND);
+  } else if (covers_double(fmt)) {
     sh->vc.alloc(nn), sh->vc.upload(sh->v_c.data(), nn);
     sh->vr.alloc(nn), sh->vr.upload(sh->v_r.data(), nn);
     sh->vct.alloc(nn), sh->vct.upload(vct.data(), nn);
@@ -732,7 +778,7 @@ void run_pcg(kp_operator* op, const double* b_in, kp_precond* m, const kp_solver
   const int nms = msolve_partials_ctas(m);
   Vec part_op{ws.get("part_op", size_t(nop) * 4)}, part_vec{ws.get("part_vec", size_t(VEC_CTAS) * 4)};
   Vec part_xt{ws.get("part_xt", size_t(VEC_CTAS) * 4)};
-  const bool fp16 = !covers_double(m->fmt);
+  const bool fp16 = is_fp16(m->fmt);
 
   vec_zero(x, nn);
   F64Epilogue e;
@@ -1206,7 +1252,7 @@ int kp_precond_solve(const kp_precond* pc, const double* r, double* z) {
     const size_t nn = size_t(p->n) * p->n;
     DBuf<double> dr(nn), dz(nn);
     dr.upload(r, nn);
-    if (!covers_double(p->fmt)) cast_r16(p, dr.p, nullptr);
+    if (is_fp16(p->fmt)) cast_r16(p, dr.p, nullptr);
     msolve(p, dr.p, dz.p, nullptr, nullptr, nullptr, nullptr);
     dz.download(z, nn);
     sync();
@@ -1230,6 +1276,14 @@ int kp_precond_export(const kp_precond* p, int field, double* out) {
           else out[size_t(a) * n + i] = v;
         }
     };
+    auto put_dev = [&](const double* d) {
+      KP_CUDA(cudaMemcpyAsync(out, d, nn * sizeof(double), cudaMemcpyDeviceToHost, ctx().stream));
+      sync();
+    };
+    if (is_generic(p->fmt) && field >= 1 && field <= 3) {  // rounded copies on the device
+      put_dev(field == 1 ? p->s64.p : field == 2 ? sh->vr.p : sh->vc.p);
+      return KP_OK;
+    }
     switch (field) {
       case 0: put(weight_matrix(*sh, p->lambda)); break;
       case 1:
@@ -1252,7 +1306,6 @@ int kp_precond_export(const kp_precond* p, int field, double* out) {
       case 9: put(sh->v_c); break;
       default: throw InvalidArgument("precond_export: bad field");
     }
-    (void)nn;
   })
 }
 int kp_precond_info(const kp_precond* p, int* n, double* lambda, kp_format* fmt, int* accum) {
@@ -1260,6 +1313,61 @@ int kp_precond_info(const kp_precond* p, int* n, double* lambda, kp_format* fmt,
     if (!p) throw InvalidArgument("null preconditioner");
     *n = p->n, *lambda = p->lambda, *fmt = p->fmt, *accum = p->accum;
   })
+}
+
+// ---- emulated low-precision BLAS (precision.cpp, lpblas.cpp) ---------------------
+int kp_round_array(const double* x, long count, kp_format fmt, double* out) {
+  KP_API({
+    check_format(fmt);
+    if (count < 0 || (count && (!x || !out))) throw InvalidArgument("round_array: bad arguments");
+    if (!count) return KP_OK;
+    DBuf<double> d(static_cast<size_t>(count));
+    d.upload(x, size_t(count));
+    lp_round_array(d.p, size_t(count), lp_format(fmt), d.p, KC_PRECOND);
+    d.download(out, size_t(count));
+    sync();
+  })
+}
+// lp_matmul (lpblas.cpp:59-70): a is m x k, b is k x n, c is m x n, all
+// column-major host arrays. fp16 with binary16-representable inputs runs on
+// the f16x2 GEMM (gemm_f16ref); everything else on the generic emulation.
+// round_leaves = 0 treats the products as pre-rounded addends (pairwise_sum).
+int kp_lp_matmul_ex(int m, int k, int n, const double* a, const double* b, kp_format fmt,
+                    int round_leaves, double* c) {
+  KP_API({
+    check_format(fmt);
+    if (m < 0 || n < 0 || k < 0) throw InvalidArgument("lp_matmul: negative dimension");
+    if (k == 0) throw InvalidArgument("lp_matmul: empty input");
+    if (m == 0 || n == 0) return KP_OK;
+    const size_t na = size_t(m) * k, nb = size_t(k) * n, nc = size_t(m) * n;
+    DBuf<double> da(na), db(nb), dc(nc);
+    da.upload(a, na);
+    db.upload(b, nb);
+    if (is_fp16(fmt) && round_leaves && count_not_f16(da.p, na) + count_not_f16(db.p, nb) == 0) {
+      const long ldh = round_up(k, 64);
+      DBuf<__half> ha(size_t(m) * ldh), hb(size_t(n) * ldh);
+      pack_f16(da.p, 1, m, m, k, ha.p, ldh, 0x8000);  // A(i,kk) = a[i + kk m], -0 padding
+      pack_f16(db.p, k, 1, n, k, hb.p, ldh, 0x0000);  // B(j,kk) = b[kk + j k], +0 padding
+      F16GemmArgs g;
+      g.M = m, g.N = n, g.K = k;
+      g.A = {ha.p, ldh}, g.B = {hb.p, ldh};
+      g.epi.mode = F16OUT_F64, g.epi.Cd = dc.p, g.epi.cm = 1, g.epi.cn = m;
+      gemm_f16ref(g, KC_PRECOND);
+    } else {
+      LpGemmArgs g;
+      g.M = m, g.N = n, g.K = k, g.f = lp_format(fmt), g.round_leaves = round_leaves != 0;
+      g.a = da.p, g.ai = 1, g.ak = m;
+      g.b = db.p, g.bk = 1, g.bj = k;
+      g.c = dc.p, g.ldc = m;
+      lp_gemm_generic(g, KC_PRECOND);
+    }
+    dc.download(c, nc);
+    sync();
+  })
+}
+int kp_lp_matmul(int m, int k, int n, const double* a, const double* b, kp_format fmt,
+                 double* c) {
+  return kp_lp_matmul_ex(m, k, n, a, b, fmt, 1, c);
 }
 
 // ---- solvers --------------------------------------------------------------------

@@ -21,7 +21,8 @@ from ._lib import (KP_ACCUM_REFERENCE, KP_ACCUM_TENSOR, NoRootError, check, f64,
                    kp_history, kp_param_choice, kp_solver_options, lib, ptr)
 
 __all__ = [
-    "PrecisionFormat", "KronTerm", "KroneckerSum", "vec", "unvec", "kronsum_apply",
+    "PrecisionFormat", "round_value", "round_array", "lp_matmul", "lp_matvec", "lp_dot",
+    "pairwise_sum", "KronTerm", "KroneckerSum", "vec", "unvec", "kronsum_apply",
     "kronsum_apply_transpose", "normal_matvec", "KronSvdPreconditioner",
     "build_preconditioner", "build_preconditioner_from_svd", "with_lambda", "precond_solve",
     "SolverOptions", "ConvergenceHistory", "SolveResult", "cgls", "pcg", "fpcg",
@@ -86,6 +87,67 @@ class PrecisionFormat:
 
     def c(self) -> kp_format:
         return kp_format(self.significand_bits, self.max_exponent, int(self.subnormals_enabled))
+
+
+# ---------------------------------------------------------------------------
+# precision.hpp:39-51, lpblas.hpp:9-33 — device emulation, any format
+def round_value(x: float, fmt: PrecisionFormat) -> float:
+    return float(round_array(np.array([x], dtype=np.float64), fmt)[0])
+
+
+def round_array(a, fmt: PrecisionFormat) -> np.ndarray:
+    """round_array (precision.cpp:82-95), same shape as `a`."""
+    arr = np.asarray(a, dtype=np.float64)
+    x = np.ascontiguousarray(arr.reshape(-1))
+    out = np.empty_like(x)
+    check(lib().kp_round_array(ptr(x), x.size, fmt.c(), ptr(out)))
+    return out.reshape(arr.shape)
+
+
+def _lp(a, b, fmt: PrecisionFormat, round_leaves: bool) -> np.ndarray:
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.ndim != 2 or b.ndim != 2 or a.shape[1] != b.shape[0]:
+        raise ValueError("lp_matmul: shape mismatch")
+    m, k = a.shape
+    n = b.shape[1]
+    af = np.asfortranarray(a)
+    bf = np.asfortranarray(b)
+    c = np.empty((m, n), dtype=np.float64, order="F")
+    check(lib().kp_lp_matmul_ex(m, k, n, ptr(af), ptr(bf), fmt.c(), int(round_leaves), ptr(c)))
+    return np.ascontiguousarray(c)
+
+
+def lp_matmul(a, b, fmt: PrecisionFormat) -> np.ndarray:
+    """Pairwise-tree product with every product and stage sum rounded (lpblas.cpp:59-70)."""
+    return _lp(a, b, fmt, True)
+
+
+def lp_matvec(a, v, fmt: PrecisionFormat) -> np.ndarray:  # lpblas.cpp:48-57
+    v = np.asarray(v, dtype=np.float64).reshape(-1)
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim != 2 or a.shape[1] != v.size:
+        raise ValueError("lp_matvec: shape mismatch")
+    if v.size == 0:
+        raise ValueError("lp_matvec: empty input")
+    return _lp(a, v.reshape(-1, 1), fmt, True)[:, 0]
+
+
+def lp_dot(x, y, fmt: PrecisionFormat) -> float:  # lpblas.cpp:39-46
+    x = np.asarray(x, dtype=np.float64).reshape(-1)
+    y = np.asarray(y, dtype=np.float64).reshape(-1)
+    if x.size != y.size:
+        raise ValueError("lp_dot: length mismatch")
+    if x.size == 0:
+        raise ValueError("lp_dot: empty input")
+    return float(_lp(x.reshape(1, -1), y.reshape(-1, 1), fmt, True)[0, 0])
+
+
+def pairwise_sum(z, fmt: PrecisionFormat) -> float:  # lpblas.cpp:34-37 (pre-rounded addends)
+    z = np.asarray(z, dtype=np.float64).reshape(-1)
+    if z.size == 0:
+        raise ValueError("pairwise_sum: empty input")
+    return float(_lp(z.reshape(1, -1), np.ones((z.size, 1)), fmt, False)[0, 0])
 
 
 # ---------------------------------------------------------------------------
