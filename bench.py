@@ -160,22 +160,36 @@ def run_reference(args):
     t0 = time.time()
     cfg = build_problem(args.config, 0, args.size, device_apply=False)
     svd_r, svd_c = svd_pair(cfg.term, "host")
-    setup_s = time.time() - t0
     fmt = K.PrecisionFormat.fp16()
+    if cfg.lambda_ is None:  # C3 / C4: the config's lambda rule, on the oracle (cli.cpp:469-505)
+        from oracle import pyoracle as O
+        from paper_2311_15393_b200.configs import GCV_GRID
+        m0 = O.build_preconditioner_from_svd((svd_r.u, svd_r.s, svd_r.v),
+                                             (svd_c.u, svd_c.s, svd_c.v), 1.0, fmt)
+        so, bo = O.spectral(m0, cfg.problem.b)
+        if cfg.select == "gcv_grid":
+            cfg.lambda_ = O.gcv_grid(so, bo, GCV_GRID)[0]["lambda"]
+        else:
+            cfg.lambda_ = O.discrepancy(so, bo, float(np.linalg.norm(cfg.problem.noise)),
+                                        cfg.eta)["lambda"]
+    setup_s = time.time() - t0
+    solver_name = cfg.solvers[0][0]
     for _ in range(args.warmup):
         cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads)
     times = [cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads) for _ in range(args.steps)]
     total = sum(times)
     value = args.steps / total
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "iterations/s",
+        "impl": "reference",
+        "metric": METRIC if cfg.name == "C5" else f"PCG iterations/s at {cfg.n}^2 image ({cfg.name})",
+        "value": value, "unit": "iterations/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64+f16(emulated)", "data": "synthetic",
         "config": workload_config(cfg),
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": threads, "kind": "port",
-                         "sample": "one FPCG iteration's normal_matvec + precond_solve (fp16 "
-                                   "reference-exact emulation) per step"},
+                         "sample": f"one {solver_name.upper()} iteration's normal_matvec + "
+                                   "precond_solve (fp16 reference-exact emulation) per step"},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "setup_s": setup_s,
@@ -208,17 +222,23 @@ def run_c4(args):
     check(L.kp_init(local))
     images = 64
     mine = list(shard(images, ws, rank))
-    sh = C4Shard(n=args.size, svd=args.svd)
+    sh = C4Shard(n=args.size, svd=args.svd, device=local)
     probs = {i: sh.problem(i) for i in mine}  # input generation is not timed
-    for i in mine[: max(1, args.warmup)]:
-        sh.solve(i, probs[i])
+    warm = mine[: max(1, min(args.warmup, len(mine)))]
+    sh.solve_many(warm, probs, args.workers)
     if dist:
         dist.barrier()
+    import ctypes as C
     launches0 = L.kp_launch_count()
     with ClockSampler(local) as clk:
-        t0 = time.perf_counter()
-        results = [sh.solve(i, probs[i]) for i in mine]  # each call ends synchronised
-        elapsed = time.perf_counter() - t0
+        check(L.kp_synchronize())
+        check(L.kp_event_record(0))
+        # every solve ends synchronised on its worker's stream
+        results = sh.solve_many(mine, probs, args.workers)
+        check(L.kp_event_record(1))
+        ms = C.c_float()
+        check(L.kp_event_elapsed(0, 1, C.byref(ms)))
+        elapsed = ms.value / 1e3
     launches = L.kp_launch_count() - launches0
     elapsed, solved = reduce_timing(elapsed, float(len(results)), dist,
                                     device="cuda" if args.dist_backend == "nccl" else "cpu")
@@ -231,7 +251,8 @@ def run_c4(args):
                "dtype": "f64 + f16 (reference-exact)", "data": "synthetic (seeded blob images)",
                "config": {"workload": "C4: 64 x n=1024, Gaussian sigma=2.5, noise 0.1/1/5 %, "
                                       "discrepancy eta=1.01, PCG fp16 tol 1e-6",
-                          "parallelism": f"images sharded over {ws} GPU(s), NCCL gather",
+                          "parallelism": f"images sharded over {ws} GPU(s), NCCL gather; "
+                                         f"{args.workers} concurrent streams per GPU",
                           "mean_iterations": float(np.mean(its)), "images": len(allres),
                           "no_root": sum(r["no_root"] for r in allres)},
                "clocks": clk.summary(), "gpu_launches": int(launches),
@@ -244,9 +265,11 @@ def run_c4(args):
 
 
 def workload_config(cfg) -> dict:
-    return {"workload": f"{cfg.name}: n={cfg.n} r={len(cfg.problem.a.terms)} FPCG, fp16 "
+    solver, _, maxit = cfg.solvers[0]
+    lam = cfg.lambda_ if cfg.select == "fixed" else f"{cfg.select} ({cfg.lambda_:.6g})"
+    return {"workload": f"{cfg.name}: n={cfg.n} r={len(cfg.problem.a.terms)} {solver.upper()}, fp16 "
                         f"Kronecker-SVD preconditioner (reference-exact rounding), "
-                        f"lambda={cfg.lambda_}, tol={cfg.tol}, maxit 100",
+                        f"lambda={lam}, tol={cfg.tol}, maxit {maxit}",
             "unknowns": cfg.n * cfg.n,
             "l2": "working set (~4 GB) far larger than the 126 MB L2; no flush needed"}
 
@@ -264,6 +287,8 @@ def main():
     ap.add_argument("--no-tensor", action="store_true", help="skip the tensor-mode secondary run")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense-operator roofline probe")
     ap.add_argument("--operator", default="auto", choices=["auto", "dense", "banded"])
+    ap.add_argument("--workers", type=int, default=4,
+                    help="C4: concurrent host threads / streams per GPU")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="collective backend for timing reduction / result gather")
     args = ap.parse_args()
@@ -298,7 +323,16 @@ def main():
     svd_r, svd_c = svd_pair(cfg.term, args.svd)
     t_svd = time.time() - t1
     fmt = K.PrecisionFormat.fp16()
+    solver_name, _, maxit = cfg.solvers[0]  # C1-C3, C5: the config's preconditioned run
+    lam_select = None
+    if cfg.lambda_ is None:  # C3: GCV over the 64-point grid with m0 at lambda = 1 (cli.cpp:469-505)
+        from paper_2311_15393_b200.configs import GCV_GRID
+        m0 = K.build_preconditioner_from_svd(svd_r, svd_c, 1.0, fmt)
+        choice, _ = K.gcv_grid(K.make_spectral_data(m0, cfg.problem.b), GCV_GRID)
+        cfg.lambda_ = choice.lambda_
+        lam_select = {"method": "gcv_grid", "grid_index": choice.grid_index, "lambda": choice.lambda_}
     m = K.build_preconditioner_from_svd(svd_r, svd_c, cfg.lambda_, fmt)
+    solve_fn = L.kp_fpcg if solver_name == "fpcg" else L.kp_pcg
     cfg.problem.a.set_mode(args.operator)
     op = cfg.problem.a.handle()
     setup_s = time.time() - t0
@@ -325,19 +359,19 @@ def main():
     h_b[:] = cfg.problem.b
     h_xt[:] = cfg.problem.x_true
 
-    cap = 101
+    cap = maxit + 1
     hist_bufs = [np.zeros(cap) for _ in range(4)]
 
     def solve(device: bool, mm=None):
         h = kp_history(capacity=cap, relative_error=ptr(hist_bufs[0]), residual_norm=ptr(hist_bufs[1]),
                        work_units=ptr(hist_bufs[2]), residual_cosines=ptr(hist_bufs[3]))
-        o = kp_solver_options(lambda_=cfg.lambda_, max_iterations=100, rel_residual_tol=cfg.tol,
+        o = kp_solver_options(lambda_=cfg.lambda_, max_iterations=maxit, rel_residual_tol=cfg.tol,
                               x_true=(d_xt.value if device else hp_xt.value),
                               device_pointers=int(device))
         if device:
-            check(L.kp_fpcg(op, d_b, (mm or m).handle(), C.byref(o), d_x, C.byref(h)))
+            check(solve_fn(op, d_b, (mm or m).handle(), C.byref(o), d_x, C.byref(h)))
         else:
-            check(L.kp_fpcg(op, hp_b, (mm or m).handle(), C.byref(o), hp_x, C.byref(h)))
+            check(solve_fn(op, hp_b, (mm or m).handle(), C.byref(o), hp_x, C.byref(h)))
         return h.iterations_used, float(hist_bufs[0][h.rows - 1]), h.abort_reason.decode()
 
     for _ in range(args.warmup):
@@ -348,9 +382,7 @@ def main():
         if dist:
             dist.barrier()
 
-    # ---- timed region: device-resident (value) with per-kernel-class events ----
-    check(L.kp_profile_reset())
-    check(L.kp_profile_enable(1))
+    # ---- timed region: device-resident (value); iterations replayed as CUDA graphs ----
     launches0 = L.kp_launch_count()
     barrier()
     iters = 0
@@ -366,6 +398,19 @@ def main():
     barrier()
     launches = L.kp_launch_count() - launches0
     elapsed = ms.value / 1e3
+
+    # ---- profiled pass: the same K solves with CUDA events around every launch
+    # (per kernel class, on the library stream) for the roofline and shares ----
+    check(L.kp_profile_reset())
+    check(L.kp_profile_enable(1))
+    check(L.kp_event_record(6))
+    prof_iters = 0
+    for _ in range(args.steps):
+        it, _, _ = solve(True)
+        prof_iters += it
+    check(L.kp_event_record(7))
+    prof_ms = C.c_float()
+    check(L.kp_event_elapsed(6, 7, C.byref(prof_ms)))
     prof = {}
     for cls, name in enumerate(["operator_gemm_f64", "precond_gemm_f16ref", "vector", "spectral"]):
         t = C.c_double()
@@ -472,20 +517,23 @@ def main():
             try:
                 t_cpu = cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads)
                 cpu = {"value": 1.0 / t_cpu, "unit": "iterations/s", "cores": threads, "kind": "port",
-                       "sample": "one FPCG iteration's normal_matvec + precond_solve at C5 "
-                                 "(oracle: OpenBLAS FP64 + streamed reference-exact fp16)"}
+                       "sample": f"one {solver_name.upper()} iteration's normal_matvec + "
+                                 f"precond_solve at {cfg.name} (oracle: OpenBLAS FP64 + "
+                                 "streamed reference-exact fp16)"}
             except Exception as e:  # noqa: BLE001
                 cpu = {"value": None, "unit": "iterations/s", "cores": threads, "kind": "port",
                        "sample": f"failed: {e}"}
         out = {
-            "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": ws,
+            "metric": METRIC if cfg.name == "C5" else f"PCG iterations/s at {n}^2 image ({cfg.name})",
+            "value": value, "unit": "iterations/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64 (operator, vectors) + f16 (preconditioner, reference-exact)",
-            "data": "synthetic (seeded blob images, BASELINE C5 PSF)",
+            "data": f"synthetic (seeded blob images, BASELINE {cfg.name} PSF)",
             "config": {**workload_config(cfg), "parallelism": f"replicas x{ws}",
                        "per_rank_final_rel_err": ([d["rel_err"] for d in per_rank] if dist else None),
                        "iterations_per_solve": iters // max(1, args.steps * ws),
+                       "lambda": cfg.lambda_, "lambda_selection": lam_select,
                        "final_rel_err": rel_last},
             "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": 2 * nn * 8,
                     "d2h_bytes_per_step": nn * 8 + 4 * cap * 8},
@@ -496,6 +544,9 @@ def main():
             "kernels": {k: {"ms": v[0], "launches": v[1],
                             "share": v[0] / total_prof if total_prof else None}
                         for k, v in prof.items()},
+            "profiled_pass": {"value": prof_iters / (prof_ms.value / 1e3), "unit": "iterations/s",
+                              "note": "same solves with per-launch CUDA events and no graph "
+                                      "replay; source of roofline and kernel shares"},
             "solves_per_s": args.steps * ws / elapsed,
             "tensor_mode": tensor,
             "cpu_baseline": cpu,

@@ -58,9 +58,14 @@ def reduce_timing(elapsed_s: float, units: float, dist=None, device=None) -> tup
 
 class C4Shard:
     """Shared operator / preconditioner factors for the C4 batch on one GPU
-    (all 64 images share the PSF, hence A and the Kronecker factors)."""
+    (all 64 images share the PSF, hence A and the Kronecker factors).
 
-    def __init__(self, n: int | None = None, svd: str = "host"):
+    solve_many() runs `workers` host threads; each has its own library
+    context (stream) and its own operator handle, so independent images
+    overlap on the device (the kernels of one image at n = 1024 do not fill
+    the 148 SMs on their own)."""
+
+    def __init__(self, n: int | None = None, svd: str = "host", device: int = 0):
         import numpy as np
 
         from . import configs
@@ -69,6 +74,7 @@ class C4Shard:
         from .kronprec import SvdTriple
 
         self.K, self.P, self.np = K, P, np
+        self.device = device
         base = configs.build("C4", image=0, n=n)
         self.n = base.n
         self.a = base.problem.a
@@ -93,9 +99,39 @@ class C4Shard:
         return P.make_test_problem(P.blob_image(self.n, 4000 + image), self.psf, noise, 5000 + image,
                                    a=self.a)
 
-    def solve(self, image: int, tp=None) -> ImageResult:
+    def solve_many(self, images, probs: dict, workers: int = 1) -> list:
+        """Solve `images` (problems in `probs`) on `workers` concurrent streams."""
+        import threading
+
+        from ._lib import check, lib
+        images = list(images)
+        workers = max(1, min(workers, len(images)))
+        if workers == 1:
+            return [self.solve(i, probs[i]) for i in images]
+        out, errors = {}, []
+
+        def run(w):
+            try:
+                check(lib().kp_init(self.device))  # this thread's context and stream
+                a = self.K.KroneckerSum(list(self.a.terms), self.a.n)  # own operator handle
+                for i in images[w::workers]:
+                    out[i] = self.solve(i, probs[i], a=a)
+            except Exception as e:  # noqa: BLE001
+                errors.append(e)
+
+        threads = [threading.Thread(target=run, args=(w,)) for w in range(workers)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errors:
+            raise errors[0]
+        return [out[i] for i in images]
+
+    def solve(self, image: int, tp=None, a=None) -> ImageResult:
         K, np = self.K, self.np
         tp = tp or self.problem(image)
+        a = a if a is not None else self.a
         sd = K.make_spectral_data(self.m0, tp.b)
         try:
             lam = K.discrepancy(sd, float(np.linalg.norm(tp.noise)), self.eta).lambda_
@@ -103,7 +139,7 @@ class C4Shard:
             return ImageResult(image, tp.noise_level, float("nan"), 0, False, float("nan"),
                                "", True)
         m = K.with_lambda(self.m0, lam)
-        r = K.pcg(self.a, tp.b, m, K.SolverOptions(lambda_=lam, max_iterations=100,
+        r = K.pcg(a, tp.b, m, K.SolverOptions(lambda_=lam, max_iterations=100,
                                                    rel_residual_tol=self.tol, x_true=tp.x_true))
         h = r.history
         return ImageResult(image, tp.noise_level, lam, h.iterations_used, h.converged,

@@ -9,6 +9,8 @@
 //   pcg / fpcg (pcg_core), cgls                krylov.cpp:58-142, 154-208
 //   make_spectral_data, gcv, discrepancy        regparam.cpp:119-134, 254-327
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -39,10 +41,15 @@ namespace kp {
 
 static thread_local std::string g_last_error;
 
+// One context (device, stream, profiling state) per host thread: handles
+// follow the reference's "one handle per thread" rule, and independent solves
+// issued from different threads run concurrently on their own streams.
 Ctx& ctx() {
-  static Ctx c;
+  static thread_local Ctx c;
   return c;
 }
+
+std::atomic<long long> g_launches{0};
 
 void ensure_init() {
   Ctx& c = ctx();
@@ -52,11 +59,13 @@ void ensure_init() {
   if (e != cudaSuccess || count == 0)
     throw CudaError(std::string("no CUDA device available: ") + cudaGetErrorString(e) +
                     " (the B200 path has no CPU fallback)");
-  KP_CUDA(cudaSetDevice(0));
+  int dev = 0;
+  KP_CUDA(cudaGetDevice(&dev));  // the calling thread's current device
+  KP_CUDA(cudaSetDevice(dev));
   KP_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
-  KP_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, 0));
-  init_pool(0);
-  c.device = 0;
+  KP_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  init_pool(dev);
+  c.device = dev;
 }
 
 void init_pool(int device) {
@@ -74,6 +83,7 @@ void check_launch(const char* what) {
 LaunchScope::LaunchScope(int c) : cls(c) {
   Ctx& x = ctx();
   x.launches++;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   if (x.profile) {
     if (!x.pool.empty()) {
       ev = x.pool.back();
@@ -224,6 +234,7 @@ struct PrecondShared {
   // extremes of s_r(j) s_c(i) over all (i, j), computed once (spectral data)
   bool have_range = false;
   double smin = 0.0, smax = 0.0;
+  std::mutex lazy_mu;  // guards the lazily created members above (shared across handles)
 };
 
 struct kp_precond {
@@ -698,6 +709,7 @@ void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
     KP_CUDA(cudaGraphDestroy(graph));
     per_iter_launches = c.launches - before;
     c.launches = before;
+    g_launches.fetch_sub(per_iter_launches, std::memory_order_relaxed);  // captured, not launched
   }
   // Poll after every iteration while an iteration is long (overshoot would
   // cost real no-op launches); batch up to 16 iterations per poll once an
@@ -710,6 +722,7 @@ void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
       if (exec) {
         KP_CUDA(cudaGraphLaunch(exec, c.stream));
         c.launches += per_iter_launches;
+        g_launches.fetch_add(per_iter_launches, std::memory_order_relaxed);
       } else {
         iteration();
       }
@@ -1106,7 +1119,7 @@ int kp_profile_read(int cls, double* total_ms, long long* launches) {
     *launches = ctx().count[cls];
   })
 }
-long long kp_launch_count(void) { return ctx().launches; }
+long long kp_launch_count(void) { return kp::g_launches.load(); }
 int kp_event_record(int slot) {
   KP_API({
     static cudaEvent_t ev[16] = {};
@@ -1403,9 +1416,13 @@ int kp_spectral_create_x(const kp_precond* p, const double* b, const double* x_t
       db.upload(b, nn);
       project_dev(n, sh.d_u_c.p, sh.d_u_r.p, db.p, sd->bhat.p);
       if (x_true) {
-        if (!sh.d_v_r.p) {
-          sh.d_v_r.alloc(nn), sh.d_v_r.upload(sh.v_r.data(), nn);
-          sh.d_v_c.alloc(nn), sh.d_v_c.upload(sh.v_c.data(), nn);
+        {
+          std::lock_guard<std::mutex> lk(sh.lazy_mu);
+          if (!sh.d_v_r.p) {
+            sh.d_v_r.alloc(nn), sh.d_v_r.upload(sh.v_r.data(), nn);
+            sh.d_v_c.alloc(nn), sh.d_v_c.upload(sh.v_c.data(), nn);
+            sync();
+          }
         }
         sd->xhat.alloc(nn);
         db.upload(x_true, nn);
@@ -1413,6 +1430,7 @@ int kp_spectral_create_x(const kp_precond* p, const double* b, const double* x_t
       }
       sync();
     }
+    std::lock_guard<std::mutex> lk(sh.lazy_mu);
     if (!sh.have_range) {
       const auto& sr = sh.s_r;
       const auto& sc = sh.s_c;
@@ -1448,19 +1466,17 @@ int kp_filtered_solution(const kp_precond* p, const double* b, double lambda, do
       if ((mn * mc) * (mn * mc) == 0.0)
         throw InvalidArgument("filtered_solution: zero singular value with lambda = 0");
     }
-    if (!sh.d_v_r.p) {
-      sh.d_v_r.alloc(nn), sh.d_v_r.upload(sh.v_r.data(), nn);
-      sh.d_v_c.alloc(nn), sh.d_v_c.upload(sh.v_c.data(), nn);
-    }
-    DBuf<double> db(nn), bh(nn), t(nn);
-    db.upload(b, nn);
-    project_dev(n, sh.d_u_c.p, sh.d_u_r.p, db.p, bh.p);
-    spectral_filter(sh.d_s_r.p, sh.d_s_c.p, n, lambda * lambda, bh.p);  // coef in place
+    std::unique_lock<std::mutex> lk(sh.lazy_mu);
     if (!sh.d_vc_rm.p) {  // row-major copies of V_c, V_r (K-major operands below)
       sh.d_vc_rm.alloc(nn), sh.d_vc_rm.upload(host_transpose(sh.v_c, n).data(), nn);
       sh.d_vr_rm.alloc(nn), sh.d_vr_rm.upload(host_transpose(sh.v_r, n).data(), nn);
       sync();
     }
+    lk.unlock();
+    DBuf<double> db(nn), bh(nn), t(nn);
+    db.upload(b, nn);
+    project_dev(n, sh.d_u_c.p, sh.d_u_r.p, db.p, bh.p);
+    spectral_filter(sh.d_s_r.p, sh.d_s_c.p, n, lambda * lambda, bh.p);  // coef in place
     F64GemmArgs g;  // t = V_c coef ; X = t V_r^T
     g.M = n, g.N = n, g.nb = 1, g.Kb = n;
     g.A = {sh.d_vc_rm.p, n, 0}, g.B = {bh.p, n, 0};

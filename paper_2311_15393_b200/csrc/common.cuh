@@ -67,27 +67,31 @@ template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t s = nullptr;  // stream the block was allocated on (and is freed on)
   DBuf() = default;
   explicit DBuf(size_t count) { alloc(count); }
   void alloc(size_t count) {
     free();
     // Stream-ordered pool allocation (the pool keeps freed blocks; see
     // init_pool), so per-call scratch costs no device synchronisation.
-    if (count) KP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), ctx().stream));
+    if (count) {
+      s = ctx().stream;
+      KP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+    }
     n = count;
   }
   void free() {
-    if (p) cudaFreeAsync(p, ctx().stream);
+    if (p) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
   }
   ~DBuf() { free(); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr, o.n = 0; }
   DBuf& operator=(DBuf&& o) noexcept {
     free();
-    p = o.p, n = o.n;
+    p = o.p, n = o.n, s = o.s;
     o.p = nullptr, o.n = 0;
     return *this;
   }

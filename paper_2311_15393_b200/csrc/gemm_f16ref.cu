@@ -70,7 +70,8 @@ __device__ __forceinline__ uint32_t part(const uint4& v, int q) {
 
 // STAGES: cp.async pipeline depth. UNIT: leaves per value pushed into the
 // shared-memory counter stack (16: levels >= 4 in smem; 32: level 4 also in
-// registers, one smem level less).
+// registers; 64: levels 4 and 5 in registers — the whole 64-leaf k-tile is
+// reduced in registers and pushed once, the smallest stack).
 template <int STAGES, int UNIT>
 __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs args, int levels) {
   if (args.status && *args.status != 0) return;
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
     cp_async_commit();
   }
 
-  uint32_t l3[NACC], l4[NACC];
+  uint32_t l3[NACC], l4[NACC], l5[NACC];
   int c16 = 0;  // UNIT-leaf values pushed so far
   // Per-thread constants: rows tm + 8i (A) all share (row & 7) = tm, rows
   // tn + 16j (B) share tn & 7, so the swizzled chunk offset of sub-chunk s is
@@ -169,16 +170,23 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
       if ((sub & 1) == 0) {
 #pragma unroll
         for (int q = 0; q < NACC; ++q) l3[q] = v8[q];
-      } else if (UNIT == 32 && (sub & 3) == 1) {
+      } else if (UNIT >= 32 && (sub & 3) == 1) {
 #pragma unroll
         for (int q = 0; q < NACC; ++q) l4[q] = hadd2(l3[q], v8[q]);
+      } else if (UNIT == 64 && sub == 3) {  // 32-leaf value (subs 0-3) stays in registers
+#pragma unroll
+        for (int q = 0; q < NACC; ++q) l5[q] = hadd2(l4[q], hadd2(l3[q], v8[q]));
       } else {
         uint32_t v[NACC];
 #pragma unroll
         for (int q = 0; q < NACC; ++q) v[q] = hadd2(l3[q], v8[q]);
-        if (UNIT == 32) {
+        if (UNIT >= 32) {
 #pragma unroll
           for (int q = 0; q < NACC; ++q) v[q] = hadd2(l4[q], v[q]);
+        }
+        if (UNIT == 64) {  // one 64-leaf value per k-tile
+#pragma unroll
+          for (int q = 0; q < NACC; ++q) v[q] = hadd2(l5[q], v[q]);
         }
         uint32_t* lvl = my_stack;
         int cnt = c16;
@@ -307,12 +315,15 @@ void gemm_f16ref(const F16GemmArgs& a, int kernel_class) {
   if (a.A.ld % BKH || a.B.ld % BKH || a.A.ld < a.K || a.B.ld < a.K)
     throw InvalidArgument("gemm_f16ref: operand leading dimension must be a multiple of 64 >= K");
   // n=4096 (profiles/r01_sweep_f16ref.txt): <3,16> 30.45, <2,32> 31.21,
-  // <3,32> 31.38, <2,16> 30.51 T half-ops/s; all bit-identical.
+  // <3,32> 31.38, <2,16> 30.51, <2,64> 31.83, <3,64> 31.49 T half-ops/s; all
+  // bit-identical. <2,64> keeps the smallest counter stack (4 CTAs / SM).
   switch (f16ref_cfg()) {
     case 1: launch_f16ref<2, 32>(a, kernel_class); break;
+    case 2: launch_f16ref<3, 32>(a, kernel_class); break;
     case 3: launch_f16ref<2, 16>(a, kernel_class); break;
     case 4: launch_f16ref<3, 16>(a, kernel_class); break;
-    default: launch_f16ref<3, 32>(a, kernel_class); break;
+    case 6: launch_f16ref<3, 64>(a, kernel_class); break;
+    default: launch_f16ref<2, 64>(a, kernel_class); break;
   }
 }
 

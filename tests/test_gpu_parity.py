@@ -527,3 +527,17 @@ def test_banded_normal_matvec_and_solvers():
         assert np.linalg.norm(rg.history.iterates[k] - ho.iterates[k]) <= \
             1e-10 * max(np.linalg.norm(ho.iterates[k]), 1e-300)
     assert abs(rg.history.iterations_used - ho.iterations_used) <= 2
+
+
+def test_concurrent_streams_match_sequential():
+    """Per-thread contexts: images solved on concurrent streams give exactly
+    the sequential results (deterministic kernels, private handles)."""
+    from paper_2311_15393_b200.batch import C4Shard
+    sh = C4Shard(n=128)
+    imgs = list(range(6))
+    probs = {i: sh.problem(i) for i in imgs}
+    seq = sh.solve_many(imgs, probs, workers=1)
+    con = sh.solve_many(imgs, probs, workers=3)
+    for a, b in zip(seq, con):
+        assert (a.image, a.lam, a.iterations, a.converged, a.rel_err, a.abort_reason) == \
+               (b.image, b.lam, b.iterations, b.converged, b.rel_err, b.abort_reason)

@@ -24,7 +24,7 @@ for n in (1024, 4096):
     ms = t.value / c.value
     print("RESULT", os.environ.get("KP_F16REF_CFG", "0"), n, f"{ms:.4f} ms/GEMM", f"{2*n**3/(ms/1e3)/1e12:.2f} Tops", hashlib.md5(z.tobytes()).hexdigest(), flush=True)
 ''' % ROOT
-for cfg in ["0", "1", "2", "3"]:
+for cfg in sys.argv[1:] or ["0", "1", "5", "6"]:
     env = dict(os.environ, KP_F16REF_CFG=cfg)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     print([l for l in r.stdout.splitlines() if l.startswith("RESULT")] or r.stderr[-800:], flush=True)
