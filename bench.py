@@ -439,6 +439,8 @@ def main():
                   "note": "KP_ACCUM_TENSOR: tcgen05 kind::f16, fp32 accumulation (not bit-exact)"}
 
     # ---- e2e: the same solves through host (pinned) buffers ----
+    for _ in range(max(1, args.warmup)):  # warm the host-path staging buffers too
+        solve(False)
     barrier()
     check(L.kp_event_record(2))
     e2e_iters = 0

@@ -21,6 +21,7 @@ BUILD = os.path.join(PKG, "_build")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libkronprec_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+NO_FMAD = {"vec.cu"}
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -70,8 +71,12 @@ def build_library(verbose: bool = False, force: bool = False) -> str:
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         objs.append(obj)
         if force or _newer(obj, [src] + headers):
+            # vec.cu: the CG updates (x += alpha p, r -= alpha q, p = z + beta p)
+            # round the product and the sum separately, as the reference's Eigen
+            # expressions do (no FMA contraction)
+            extra = ["-fmad=false"] if os.path.basename(src) in NO_FMAD else []
             jobs.append([NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-                         "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
+                         "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3", *extra,
                          "-c", src, "-o", obj])
     for src in cpp:
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")

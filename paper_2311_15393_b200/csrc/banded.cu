@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
       double v = acc[h][q];
       const long vi = long(m) * e.vm + long(j) * e.vn;
       if (e.mul) v *= e.mul[vi];
-      if (e.addv) v += e.addc * e.addv[vi];
+      if (e.addv) v = __dadd_rn(v, __dmul_rn(e.addc, e.addv[vi]));  // + lambda^2 p, unfused as Eigen
       e.C[long(m) * e.cm + long(j) * e.cn] = v;
       if (e.partials) {
         if (e.d0) s0 += v * (e.d0_self ? v : e.d0[vi]);

@@ -188,7 +188,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
           double v = acc[i][j][q];
           const long vi = long(m) * e.vm + long(n) * e.vn;
           if (e.mul) v *= e.mul[vi];
-          if (e.addv) v += e.addc * e.addv[vi];
+          if (e.addv) v = __dadd_rn(v, __dmul_rn(e.addc, e.addv[vi]));  // + lambda^2 p, unfused as Eigen
           e.C[long(m) * e.cm + long(n) * e.cn] = v;
           if (e.partials) {
             if (e.d0) s0 += v * (e.d0_self ? v : e.d0[vi]);

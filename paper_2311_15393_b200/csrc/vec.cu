@@ -39,9 +39,12 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double (*red)[NV]) {
   }
 }
 
-// Sum of component q of a [n][4] partials array, fixed order, one block.
+// Sum of component q of a [n][4] partials array, fixed order, one block of
+// SCALAR_THREADS threads (wide, so the partials of an 8192-tile GEMM are read
+// with few dependent steps per thread).
+constexpr int SCALAR_THREADS = 1024;
 __device__ double sum_partials(const double* part, int n, int q) {
-  __shared__ double red[VEC_THREADS / 32][1];
+  __shared__ double red[SCALAR_THREADS / 32][1];
   double v[1] = {0.0};
   for (int i = threadIdx.x; i < n; i += blockDim.x) v[0] += part[size_t(i) * 4 + q];
   block_sum<1>(v, red);
@@ -617,13 +620,13 @@ void cast_f64_to_f16_padded(const double* src, __half* dst, int rows, int cols, 
 
 void pcg_init_scalar(DevState* st, DevHistory h, const double* part_r, int nr,
                      const double* part_xt, int nxt) {
-  KP_LAUNCH(KC_VECTOR, pcg_init_scalar_kernel, 1, VEC_THREADS, st, h, part_r, nr, part_xt, nxt);
+  KP_LAUNCH(KC_VECTOR, pcg_init_scalar_kernel, 1, SCALAR_THREADS, st, h, part_r, nr, part_xt, nxt);
 }
 void pcg_init_msolve_scalar(DevState* st, const double* part_z, int nz) {
-  KP_LAUNCH(KC_VECTOR, pcg_init_msolve_scalar_kernel, 1, VEC_THREADS, st, part_z, nz);
+  KP_LAUNCH(KC_VECTOR, pcg_init_msolve_scalar_kernel, 1, SCALAR_THREADS, st, part_z, nz);
 }
 void pcg_alpha_scalar(DevState* st, const double* part_pq, int n) {
-  KP_LAUNCH(KC_VECTOR, pcg_alpha_scalar_kernel, 1, VEC_THREADS, st, part_pq, n);
+  KP_LAUNCH(KC_VECTOR, pcg_alpha_scalar_kernel, 1, SCALAR_THREADS, st, part_pq, n);
 }
 static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -640,10 +643,10 @@ void pcg_update(DevState* st, DevHistory h, double* x, double* r, double* r_prev
               q, z, xt, r16, n, ldh, partials);
 }
 void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n) {
-  KP_LAUNCH(KC_VECTOR, pcg_resid_scalar_kernel, 1, VEC_THREADS, st, h, part, n);
+  KP_LAUNCH(KC_VECTOR, pcg_resid_scalar_kernel, 1, SCALAR_THREADS, st, h, part, n);
 }
 void pcg_beta_scalar(DevState* st, const double* part_z, int n) {
-  KP_LAUNCH(KC_VECTOR, pcg_beta_scalar_kernel, 1, VEC_THREADS, st, part_z, n);
+  KP_LAUNCH(KC_VECTOR, pcg_beta_scalar_kernel, 1, SCALAR_THREADS, st, part_z, n);
 }
 void pcg_p_update(DevState* st, double* p, const double* z, size_t nn) {
   const bool vec2 = nn % 2 == 0 && al16(p) && al16(z);
@@ -653,10 +656,10 @@ void pcg_p_update(DevState* st, double* p, const double* z, size_t nn) {
 
 void cgls_init_scalar(DevState* st, DevHistory h, const double* part_s, int ns,
                       const double* part_xt, int nxt) {
-  KP_LAUNCH(KC_VECTOR, cgls_init_scalar_kernel, 1, VEC_THREADS, st, h, part_s, ns, part_xt, nxt);
+  KP_LAUNCH(KC_VECTOR, cgls_init_scalar_kernel, 1, SCALAR_THREADS, st, h, part_s, ns, part_xt, nxt);
 }
 void cgls_alpha_scalar(DevState* st, const double* part_q, int nq, const double* part_p, int np) {
-  KP_LAUNCH(KC_VECTOR, cgls_alpha_scalar_kernel, 1, VEC_THREADS, st, part_q, nq, part_p, np);
+  KP_LAUNCH(KC_VECTOR, cgls_alpha_scalar_kernel, 1, SCALAR_THREADS, st, part_q, nq, part_p, np);
 }
 void cgls_update(DevState* st, DevHistory h, double* x, double* rt, const double* p,
                  const double* q, const double* xt, size_t nn, double* partials) {
@@ -669,7 +672,7 @@ void cgls_update(DevState* st, DevHistory h, double* x, double* rt, const double
 }
 void cgls_resid_scalar(DevState* st, DevHistory h, const double* part_s, int ns,
                        const double* part_x, int nx) {
-  KP_LAUNCH(KC_VECTOR, cgls_resid_scalar_kernel, 1, VEC_THREADS, st, h, part_s, ns, part_x, nx);
+  KP_LAUNCH(KC_VECTOR, cgls_resid_scalar_kernel, 1, SCALAR_THREADS, st, h, part_s, ns, part_x, nx);
 }
 void cgls_p_update(DevState* st, double* p, const double* s, double* s_prev, size_t nn,
                    double* partials) {
