@@ -10,7 +10,7 @@ Both arms (CUDA path and CPU oracle) consume these arrays.
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -33,6 +33,11 @@ class Psf:
     center_row: int
     center_col: int
     kind: str = "gaussian"
+    seed: int = 0
+    # BlurParams (deblur.hpp): sigma, radius, length, steps, blob_count, blob_sigma
+    params: dict = field(default_factory=lambda: {
+        "sigma": 2.0, "radius": 3.0, "length": 5, "steps": 64, "blob_count": 10,
+        "blob_sigma": 1.0})
 
 
 def rng_normals(seed: int, count: int) -> np.ndarray:
@@ -48,7 +53,9 @@ def make_psf(kind: str, n_p: int, sigma: float = 2.0, radius: float = 3.0, lengt
     L = lib()
     _chk(L.kpg_make_psf(BLUR_KINDS[kind], n_p, sigma, radius, length, steps, blob_count,
                         blob_sigma, seed, ptr(out)))
-    return Psf(out, n_p // 2, n_p // 2, kind)
+    return Psf(out, n_p // 2, n_p // 2, kind, seed,
+               {"sigma": sigma, "radius": radius, "length": length, "steps": steps,
+                "blob_count": blob_count, "blob_sigma": blob_sigma})
 
 
 def psf_aniso_gaussian(n_p: int, cov) -> Psf:
