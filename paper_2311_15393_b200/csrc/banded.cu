@@ -23,7 +23,7 @@ namespace kp {
 namespace {
 
 constexpr int A_TA = 128, A_TL = 32, A_THREADS = 256;   // pass A tile: 128 rows x 32 cols
-constexpr int B_TA = 64, B_TJ = 64, B_THREADS = 256;    // pass B tile: 64 rows x 64 cols
+constexpr int B_TA = 32, B_TJ = 64, B_THREADS = 256;    // pass B tile: 32 rows x 64 cols
 
 __device__ __forceinline__ bool stopped(const int* status) { return status && *status != 0; }
 
@@ -54,47 +54,51 @@ __global__ void __launch_bounds__(A_THREADS) band_cols_kernel(const double* __re
                                                               const int* status) {
   if (stopped(status)) return;
   extern __shared__ double sm[];
-  const int S = (A_TA + t.taps - 1) | 1;  // odd column stride
-  double* Xs = sm;                        // [A_TL][S]
-  double* Os = sm + A_TL * S + 1;         // [A_TL][A_TA + 1] (+1: corr8 prefetch slack)
-  constexpr int OS = A_TA + 1;
+  const int S = (A_TA + t.taps) | 1;  // odd column stride; >= A_TA + taps (corr8 prefetch slack)
+  double* Xs = sm;                    // [A_TL][S]
   const int a0 = blockIdx.y * A_TA, l0 = blockIdx.x * A_TL;
-  const int rows = A_TA + t.taps - 1;
-  for (int idx = threadIdx.x; idx < A_TL * rows; idx += A_THREADS) {
-    const int c = idx / rows, v = idx % rows;
+  for (int idx = threadIdx.x; idx < A_TL * S; idx += A_THREADS) {
+    const int c = idx / S, v = idx % S;
     const int l = l0 + c, i = a0 + t.shift + v;
-    Xs[c * S + v] = (l < n && i >= 0 && i < n) ? X[size_t(l) * n + i] : 0.0;
-  }
-  for (int idx = threadIdx.x; idx < A_TL * (S - rows); idx += A_THREADS) {
-    const int c = idx / (S - rows), v = rows + idx % (S - rows);
-    Xs[c * S + v] = 0.0;
+    Xs[idx] = (l < n && i >= 0 && i < n && v < A_TA + t.taps - 1) ? X[size_t(l) * n + i] : 0.0;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t nn = size_t(n) * n;
+  const int l = l0 + lane;
+  const bool vec = (n & 1) == 0;
   for (int k = 0; k < r; ++k) {
+    double* Yk = Y + k * nn + size_t(l) * n;
 #pragma unroll
     for (int h = 0; h < A_TA / 8 / (A_THREADS / 32); ++h) {
       const int b = warp + h * (A_THREADS / 32);  // 8-row block
       double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       const double* base = Xs + lane * S + 8 * b;
       corr8(acc, t.w[k], t.taps, [&](int i) { return base[i]; });
+      // straight from registers: 8 consecutive rows of column l (64 contiguous bytes)
+      const int a = a0 + 8 * b;
+      if (l < n) {
+        if (vec && a + 8 <= n) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) Os[lane * OS + 8 * b + q] = acc[q];
+          for (int q = 0; q < 8; q += 2)
+            *reinterpret_cast<double2*>(Yk + a + q) = make_double2(acc[q], acc[q + 1]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (a + q < n) Yk[a + q] = acc[q];
+        }
+      }
     }
-    __syncthreads();
-    double* Yk = Y + k * nn;
-    for (int idx = threadIdx.x; idx < A_TL * A_TA; idx += A_THREADS) {
-      const int c = idx / A_TA, a = idx % A_TA;
-      if (l0 + c < n && a0 + a < n) Yk[size_t(l0 + c) * n + a0 + a] = Os[c * OS + a];
-    }
-    __syncthreads();
   }
 }
 
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src),
                "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0));
 }
 
 // Pass B. The Y_k tiles (B_TJ + taps - 1 columns of B_TA rows) are
@@ -109,25 +113,33 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
   const int rows = B_TJ + t.taps - 1;
   const int buf_doubles = (rows + 1) * B_TA;  // +1 row: corr8 prefetch slack
   const int a0 = blockIdx.y * B_TA, j0 = blockIdx.x * B_TJ;
-  const int a = threadIdx.x % B_TA, jq = threadIdx.x / B_TA;  // jq in [0, 4)
+  const int a = threadIdx.x % B_TA, jq = threadIdx.x / B_TA;  // jq in [0, 8): 8-column block
   const size_t nn = size_t(n) * n;
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+  const bool vec = (n & 1) == 0;  // 16-byte copies (pairs of rows) when n is even
   auto load = [&](int k, int buf) {
     const double* Yk = Y + k * nn;
     const uint32_t dst0 = sbase + uint32_t(buf * buf_doubles) * 8u;
-    for (int idx = threadIdx.x; idx < rows * B_TA; idx += B_THREADS) {
-      const int jw = idx / B_TA, aa = idx % B_TA;
-      const int j = j0 + t.shift + jw, ai = a0 + aa;
-      const bool v = j >= 0 && j < n && ai < n;
-      cp_async8(dst0 + uint32_t(idx) * 8u, v ? Yk + size_t(j) * n + ai : Y, v);
+    if (vec) {
+      for (int idx = threadIdx.x; idx < rows * (B_TA / 2); idx += B_THREADS) {
+        const int jw = idx / (B_TA / 2), aa = 2 * (idx % (B_TA / 2));
+        const int j = j0 + t.shift + jw, ai = a0 + aa;
+        const bool v = j >= 0 && j < n && ai < n;
+        cp_async16(dst0 + uint32_t(jw * B_TA + aa) * 8u, v ? Yk + size_t(j) * n + ai : Y, v);
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < rows * B_TA; idx += B_THREADS) {
+        const int jw = idx / B_TA, aa = idx % B_TA;
+        const int j = j0 + t.shift + jw, ai = a0 + aa;
+        const bool v = j >= 0 && j < n && ai < n;
+        cp_async8(dst0 + uint32_t(idx) * 8u, v ? Yk + size_t(j) * n + ai : Y, v);
+      }
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
-  double acc[2][8];
+  double acc[8];
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[h][q] = 0.0;
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
   load(0, 0);
   for (int k = 0; k < r; ++k) {
     if (k + 1 < r) {
@@ -138,34 +150,28 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
     }
     __syncthreads();
     const double* Ys = sm + (k & 1) * buf_doubles;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int jb = jq + 4 * h;  // 8-column block
-      const double* base = Ys + (8 * jb) * B_TA + a;
-      corr8(acc[h], t.w[k], t.taps, [&](int i) { return base[i * B_TA]; });
-    }
+    const double* base = Ys + (8 * jq) * B_TA + a;
+    corr8(acc, t.w[k], t.taps, [&](int i) { return base[i * B_TA]; });
     __syncthreads();  // buffer (k & 1) is refilled at iteration k + 1
   }
   // epilogue (same contract as the GEMM epilogue)
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   const int m = a0 + a;
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int j = j0 + 8 * (jq + 4 * h) + q;
-      if (m >= n || j >= n) continue;
-      double v = acc[h][q];
-      const long vi = long(m) * e.vm + long(j) * e.vn;
-      if (e.mul) v *= e.mul[vi];
-      if (e.addv) v = __dadd_rn(v, __dmul_rn(e.addc, e.addv[vi]));  // + lambda^2 p, unfused as Eigen
-      e.C[long(m) * e.cm + long(j) * e.cn] = v;
-      if (e.partials) {
-        if (e.d0) s0 += v * (e.d0_self ? v : e.d0[vi]);
-        if (e.d1a) s1 += v * (e.d1b ? (e.d1a[vi] - e.d1b[vi]) : e.d1a[vi]);
-        if (e.count_nonfinite && !isfinite(v)) s2 += 1.0;
-      }
+  for (int q = 0; q < 8; ++q) {
+    const int j = j0 + 8 * jq + q;
+    if (m >= n || j >= n) continue;
+    double v = acc[q];
+    const long vi = long(m) * e.vm + long(j) * e.vn;
+    if (e.mul) v *= e.mul[vi];
+    if (e.addv) v = __dadd_rn(v, __dmul_rn(e.addc, e.addv[vi]));  // + lambda^2 p, unfused as Eigen
+    e.C[long(m) * e.cm + long(j) * e.cn] = v;
+    if (e.partials) {
+      if (e.d0) s0 += v * (e.d0_self ? v : e.d0[vi]);
+      if (e.d1a) s1 += v * (e.d1b ? (e.d1a[vi] - e.d1b[vi]) : e.d1a[vi]);
+      if (e.count_nonfinite && !isfinite(v)) s2 += 1.0;
     }
+  }
   if (e.partials) {
     __shared__ double red[B_THREADS / 32][3];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -189,8 +195,8 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
 }  // namespace
 
 void band_cols(const double* X, double* Y, int n, int r, const BandTaps& t, const int* status) {
-  const int S = (A_TA + t.taps - 1) | 1;
-  const size_t smem = (size_t(A_TL) * S + size_t(A_TL) * (A_TA + 1) + 1) * sizeof(double);
+  const int S = (A_TA + t.taps) | 1;
+  const size_t smem = size_t(A_TL) * S * sizeof(double);
   static size_t attr = 0;
   if (smem > attr) {
     KP_CUDA(cudaFuncSetAttribute(band_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
