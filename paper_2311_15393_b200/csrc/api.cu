@@ -353,10 +353,11 @@ void detect_banded(kp_operator* op, const double* rows, const double* cols) {
   const int lc = cmax - cmin + 1, lr = rmax - rmin + 1;
   const int pc = (lc + 7) / 8 * 8, pr = (lr + 7) / 8 * 8;
   if (pc > BAND_MAX_TAPS || pr > BAND_MAX_TAPS) return;
-  auto fill = [&](BandTaps& t, int taps, int shift, const std::vector<std::vector<double>>& dg,
-                  auto offset_of) {
+  auto fill = [&](BandTaps& t, int taps, int real, int shift,
+                  const std::vector<std::vector<double>>& dg, auto offset_of) {
     t = BandTaps{};
     t.taps = taps;
+    t.real = real;
     t.shift = shift;
     for (int k = 0; k < r; ++k)
       for (int u = 0; u < taps; ++u) {
@@ -365,11 +366,11 @@ void detect_banded(kp_operator* op, const double* rows, const double* cols) {
       }
   };
   // A: Y = A_c X -> Y(a) = sum_u c[cmax-u] X(a - cmax + u); out: sum_u r[rmax-u] Y(j - rmax + u)
-  fill(op->cols_fw, pc, -cmax, dc, [&](int u) { return u < lc ? cmax - u : 1 << 30; });
-  fill(op->rows_fw, pr, -rmax, dr, [&](int u) { return u < lr ? rmax - u : 1 << 30; });
+  fill(op->cols_fw, pc, lc, -cmax, dc, [&](int u) { return u < lc ? cmax - u : 1 << 30; });
+  fill(op->rows_fw, pr, lr, -rmax, dr, [&](int u) { return u < lr ? rmax - u : 1 << 30; });
   // A^T: Y(a) = sum_u c[cmin+u] X(a + cmin + u); out: sum_u r[rmin+u] Y(j + rmin + u)
-  fill(op->cols_tr, pc, cmin, dc, [&](int u) { return u < lc ? cmin + u : 1 << 30; });
-  fill(op->rows_tr, pr, rmin, dr, [&](int u) { return u < lr ? rmin + u : 1 << 30; });
+  fill(op->cols_tr, pc, lc, cmin, dc, [&](int u) { return u < lc ? cmin + u : 1 << 30; });
+  fill(op->rows_tr, pr, lr, rmin, dr, [&](int u) { return u < lr ? rmin + u : 1 << 30; });
   op->col_taps = lc;
   op->row_taps = lr;
   op->is_banded = true;

@@ -48,6 +48,38 @@ __device__ __forceinline__ void corr8(double (&acc)[8], const double* w, int tap
   }
 }
 
+// corr8 over the actual tap count: full blocks of 8, then the remaining
+// taps % 8 one at a time (no DFMAs on the zero padding). Used by pass B,
+// where it is faster; pass A keeps the padded loop (fewer registers).
+// Reads src up to index taps + 7.
+template <typename Src>
+__device__ __forceinline__ void corr8_tail(double (&acc)[8], const double* w, int taps, Src src) {
+  double x[16];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) x[v] = src(v);
+  const int full = taps & ~7;
+  for (int u0 = 0; u0 < full; u0 += 8) {
+#pragma unroll
+    for (int v = 0; v < 8; ++v) x[8 + v] = src(u0 + 8 + v);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const double wv = w[u0 + v];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = fma(wv, x[q + v], acc[q]);
+    }
+#pragma unroll
+    for (int v = 0; v < 8; ++v) x[v] = x[8 + v];
+  }
+  for (int v = full; v < taps; ++v) {  // x[0..7] = src(v .. v + 7)
+    const double wv = w[v];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = fma(wv, x[q], acc[q]);
+#pragma unroll
+    for (int q = 0; q < 7; ++q) x[q] = x[q + 1];
+    x[7] = src(v + 8);
+  }
+}
+
 __global__ void __launch_bounds__(A_THREADS) band_cols_kernel(const double* __restrict__ X,
                                                               double* __restrict__ Y, int n, int r,
                                                               const __grid_constant__ BandTaps t,
@@ -151,7 +183,7 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
     __syncthreads();
     const double* Ys = sm + (k & 1) * buf_doubles;
     const double* base = Ys + (8 * jq) * B_TA + a;
-    corr8(acc, t.w[k], t.taps, [&](int i) { return base[i * B_TA]; });
+    corr8_tail(acc, t.w[k], t.real, [&](int i) { return base[i * B_TA]; });
     __syncthreads();  // buffer (k & 1) is refilled at iteration k + 1
   }
   // epilogue (same contract as the GEMM epilogue)

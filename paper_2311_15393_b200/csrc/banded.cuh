@@ -12,7 +12,8 @@ constexpr int BAND_MAX_TERMS = 8;
 // One direction of a correlation y(a) = sum_u w[k][u] x(a + shift + u),
 // u in [0, taps); taps padded to a multiple of 8 with zeros at the end.
 struct BandTaps {
-  int taps = 0;
+  int taps = 0;   // padded to a multiple of 8 (shared-memory halo sizing)
+  int real = 0;   // actual tap count (the correlation loops)
   int shift = 0;
   double w[BAND_MAX_TERMS][BAND_MAX_TAPS];
 };
