@@ -17,9 +17,10 @@
 //               issues tcgen05.mma.kind::f16 (M=128, N=BN, K=16) from smem
 //               descriptors, commits stage releases and accumulator-ready
 //               signals (tcgen05.commit -> mbarrier)
-//   warps 2..5  epilogue: tcgen05.ld the accumulator (warp w owns TMEM lanes
-//               32*(w%4)..), round to binary16, fuse S.* / FP64 output / dot
-//               partials, release the TMEM buffer
+//   warps 2..9  epilogue: tcgen05.ld the accumulator (warp w owns TMEM lanes
+//               32*(w%4)..; the two warps of a quadrant take alternate 32-column
+//               chunks, doubling the loads in flight), round to binary16, fuse
+//               S.* / FP64 output / dot partials, release the TMEM buffer
 // Tiles are distributed persistently over the grid with double-buffered
 // accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
 #include <cudaTypedefs.h>
@@ -34,7 +35,8 @@ namespace kp {
 namespace {
 
 constexpr int BM = 128, BKH = 64, STAGES = 4;
-constexpr int NUM_THREADS = 192;  // 6 warps
+constexpr int EPI_WARPS = 8;       // two warps per TMEM lane quadrant
+constexpr int NUM_THREADS = 32 * (2 + EPI_WARPS);
 constexpr int TILE_A_BYTES = BM * BKH * 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ double red[4][3];
+  __shared__ double red[EPI_WARPS][3];
 
   const int M = args.M, N = args.N;
   const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&full_bar[s]), 1), mbar_init(smem_u32(&empty_bar[s]), 1);
-    for (int s = 0; s < 2; ++s) mbar_init(smem_u32(&tfull_bar[s]), 1), mbar_init(smem_u32(&tempty_bar[s]), 4);
+    for (int s = 0; s < 2; ++s) mbar_init(smem_u32(&tfull_bar[s]), 1), mbar_init(smem_u32(&tempty_bar[s]), EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -202,8 +204,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         umma_commit(smem_u32(&tfull_bar[acc]));  // accumulator ready
       }
     }
-  } else {  // ===== epilogue warps 2..5 =====
-    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+  } else {  // ===== epilogue warps 2..9 =====
+    const int quad = warp & 3;          // TMEM lane quadrant this warp may access
+    const int ew = warp - 2;            // epilogue warp index 0..7
+    const int half = ew >> 2;           // which alternate 32-column chunks
     const F16Epilogue& e = args.epi;
     int local = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int m = mb + quad * 32 + lane;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = 32 * half; c0 < BN; c0 += 64) {
         uint32_t v[32];
         tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + uint32_t(acc * BN + c0), v);
         if (m >= M) continue;
@@ -254,16 +258,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           continue;
         }
+        __half* __restrict__ Ch = e.Ch;
+        if (e.mode == F16OUT_HALF_SCALED) {  // w = round16(S .* t2), as the reference
+          const __half* __restrict__ sc = e.scale;
+          __half sv[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = nb + c0 + j;
-          if (n >= N) break;
-          const __half h = __float2half_rn(__uint_as_float(v[j]));  // the result in binary16
-          if (e.mode == F16OUT_HALF) {
-            e.Ch[long(m) * e.cm + long(n) * e.cn] = h;
-          } else {  // F16OUT_HALF_SCALED: w = round16(S .* t2), as the reference
-            const __half sc = e.scale[long(m) * e.sm + long(n) * e.sn];
-            e.Ch[long(m) * e.cm + long(n) * e.cn] = __hmul_rn(sc, h);
+          for (int j = 0; j < 32; ++j) {  // all scale loads first
+            const int n = nb + c0 + j;
+            sv[j] = n < N ? sc[long(m) * e.sm + long(n) * e.sn] : __ushort_as_half(0);
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int n = nb + c0 + j;
+            if (n < N)
+              Ch[long(m) * e.cm + long(n) * e.cn] = __hmul_rn(sv[j], __float2half_rn(__uint_as_float(v[j])));
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int n = nb + c0 + j;
+            if (n < N) Ch[long(m) * e.cm + long(n) * e.cn] = __float2half_rn(__uint_as_float(v[j]));
           }
         }
       }
@@ -278,15 +292,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           s1 += __shfl_xor_sync(0xffffffffu, s1, off);
           s2 += __shfl_xor_sync(0xffffffffu, s2, off);
         }
-        if (lane == 0) red[quad][0] = s0, red[quad][1] = s1, red[quad][2] = s2;
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
-        if (warp == 2 && lane == 0) {
+        if (lane == 0) red[ew][0] = s0, red[ew][1] = s1, red[ew][2] = s2;
+        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * EPI_WARPS) : "memory");
+        if (ew == 0 && lane == 0) {
           double a0 = 0, a1 = 0, a2 = 0;
-          for (int w = 0; w < 4; ++w) a0 += red[w][0], a1 += red[w][1], a2 += red[w][2];
+          for (int w = 0; w < EPI_WARPS; ++w) a0 += red[w][0], a1 += red[w][1], a2 += red[w][2];
           double* o = e.partials + long(t) * 4;
           o[0] = a0, o[1] = a1, o[2] = a2, o[3] = 0.0;
         }
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        asm volatile("bar.sync 1, %0;\n" ::"n"(32 * EPI_WARPS) : "memory");
       }
     }
   }
