@@ -137,3 +137,22 @@ def test_c5_prefix_vs_golden():
     for run, ref in zip(runs, g["runs"]):
         assert run.history.iterations_used == ref["iterations_used"]
         check_against(run, ref, prefix_rows=len(ref["residual_norm"]), final=False)
+
+
+def test_c5_operator_full_size_properties():
+    """Size-independent checks at BASELINE size (n = 4096, r = 5): the banded
+    operator equals the dense DMMA product, is linear, and A^T is its adjoint."""
+    psf, cap = configs._psf("C5")
+    a, _ = P.psf_to_kronsum(psf, 4096, max_rank=cap)
+    assert a.mode()[0] == "banded"
+    rng = np.random.default_rng(55)
+    x, y = rng.standard_normal(4096 * 4096), rng.standard_normal(4096 * 4096)
+    ax = K.kronsum_apply(a, x)
+    aty = K.kronsum_apply_transpose(a, y)
+    assert abs(ax @ y - x @ aty) <= 1e-12 * np.linalg.norm(ax) * np.linalg.norm(y)
+    axy = K.kronsum_apply(a, 2.0 * x - 3.0 * y)
+    assert np.linalg.norm(axy - (2.0 * ax - 3.0 * K.kronsum_apply(a, y))) <= 1e-13 * np.linalg.norm(axy)
+    a.set_mode("dense")
+    dx = K.kronsum_apply(a, x)
+    a.set_mode("auto")
+    assert np.linalg.norm(ax - dx) <= 1e-13 * np.linalg.norm(dx)
