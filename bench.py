@@ -37,6 +37,15 @@ sys.path.insert(0, ROOT)
 DMMA_PEAK_TFLOPS = 37.07  # measured, profiles/r01_microbench_peaks_v2.txt (m16n8k16 f64)
 DFMA_PEAK_TFLOPS = 33.88  # measured DFMA (FP64 ALU) peak, same microbenchmark
 F16X2_PEAK_TOPS = 36.9    # measured f16x2 mul+add half-ops/s, same file
+BF16_PEAK_TFLOPS = 1653.4  # MEASURED_PEAKS.json bf16_tflops (burst; fp16 kind::f16 same rate)
+# DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the
+# committed ncu --set full captures (profiles/r01_ncu_key_metrics.txt)
+TRAFFIC = {
+    ("gemm_f16ref_kernel", 4096): 67.94e6 + 22.77e6,   # r01_gemm_f16ref_u64_n4096.ncu-rep
+    ("gemm_f16tc_kernel", 4096): (74.78e6 + 19.91e6 + 119.2e6 + 22.84e6 + 73.73e6 + 19.7e6
+                                  + 445.1e6 + 109e6) / 4,  # mean of the 4 products of a solve
+    ("band", 4096): (134.8e6 + 617.2e6 + 671.4e6 + 120.9e6) / 2,  # per pass, r01_band_vec
+}
 
 
 def peaks():
@@ -441,10 +450,24 @@ def main():
         check(L.kp_event_record(5))
         t_ms = C.c_float()
         check(L.kp_event_elapsed(4, 5, C.byref(t_ms)))
+        # one profiled solve for the tcgen05 kernel's roofline (per-launch events)
+        check(L.kp_profile_reset())
+        check(L.kp_profile_enable(1))
+        solve(True, mt)
+        tt, tcnt = C.c_double(), C.c_longlong()
+        check(L.kp_profile_read(1, C.byref(tt), C.byref(tcnt)))
+        check(L.kp_profile_enable(0))
+        tc_ach = 2.0 * float(n) ** 3 / (tt.value / tcnt.value / 1e3) / 1e12 if tcnt.value else 0.0
         tensor = {"value": t_iters / (t_ms.value / 1e3), "unit": "iterations/s",
                   "solves_per_s": args.steps / (t_ms.value / 1e3),
                   "iterations_per_solve": t_iters // args.steps, "final_rel_err": t_rel,
-                  "note": "KP_ACCUM_TENSOR: tcgen05 kind::f16, fp32 accumulation (not bit-exact)"}
+                  "note": "KP_ACCUM_TENSOR: tcgen05 kind::f16, fp32 accumulation (not bit-exact)",
+                  "roofline": {"bound": "tensor", "achieved": tc_ach, "peak": BF16_PEAK_TFLOPS,
+                               "unit": "TFLOP/s", "frac": tc_ach / BF16_PEAK_TFLOPS,
+                               "kernel": "gemm_f16tc_kernel (tcgen05 kind::f16, 4 per M-solve)",
+                               "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",
+                               "work_per_launch": f"{2.0 * float(n) ** 3:.4g} flop",
+                               "traffic": TRAFFIC.get(("gemm_f16tc_kernel", n))}}
 
     # ---- e2e: the same solves through host (pinned) buffers ----
     for _ in range(max(1, args.warmup)):  # warm the host-path staging buffers too
@@ -489,13 +512,17 @@ def main():
     half_ops = 2.0 * float(n) ** 3  # n^3 rounded products + n^3 rounded tree adds per GEMM
     pm_ach = half_ops / (pm_ms / pm_launches / 1e3) / 1e12 if pm_launches else 0.0
     total_prof = sum(v[0] for v in prof.values())
-    op_line = {"bound": "tensor" if op_mode == "dense" else "fp64-alu", "achieved": op_ach,
-               "peak": op_peak, "unit": "TFLOP/s", "frac": op_ach / op_peak, "traffic": None,
+    op_line = {"bound": "tensor" if op_mode == "dense" else "compute",
+               "pipe": "DMMA" if op_mode == "dense" else "FP64 DFMA", "achieved": op_ach,
+               "peak": op_peak, "unit": "TFLOP/s", "frac": op_ach / op_peak,
+               "traffic": TRAFFIC.get(("band", n)) if op_mode == "banded" else None,
                "kernel": op_kernel, "peak_source": op_src,
                "work_per_launch": f"{op_flops_per_launch:.4g} flop"}
-    pm_line = {"bound": "f16x2 CUDA-core pipe (reference-exact rounding)", "achieved": pm_ach,
+    pm_line = {"bound": "compute", "pipe": "f16x2 CUDA-core FMA pipe (reference-exact rounding "
+                                          "needs a binary16 rounding per product and per sum)",
+               "achieved": pm_ach,
                "peak": F16X2_PEAK_TOPS, "unit": "T half-ops/s", "frac": pm_ach / F16X2_PEAK_TOPS,
-               "traffic": None, "kernel": "gemm_f16ref_kernel",
+               "traffic": TRAFFIC.get(("gemm_f16ref_kernel", n)), "kernel": "gemm_f16ref_kernel",
                "peak_source": "measured f16x2 mul+add rate, profiles/r01_microbench_peaks.txt",
                "work_per_launch": f"{half_ops:.4g} half-ops"}
     dominant, other = (pm_line, op_line) if pm_ms > op_ms else (op_line, pm_line)
