@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const double* __restrict__ d1a = e.d1a;
           const double* __restrict__ d1b = e.d1b;
           const bool part = e.partials != nullptr;
+          const bool same = d0 != nullptr && d1a == d0;
 #pragma unroll
           for (int j0 = 0; j0 < 32; j0 += 8) {
             double a0[8], a1[8];
@@ -240,7 +241,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const long vi = long(m) * e.vm + long(n) * e.vn;
               const bool ok = part && n < N;
               a0[j] = (ok && d0) ? d0[vi] : 0.0;
-              a1[j] = (ok && d1a) ? (d1b ? d1a[vi] - d1b[vi] : d1a[vi]) : 0.0;
+              // FPCG passes d0 == d1a == r: load r once
+              const double ra = same ? a0[j] : ((ok && d1a) ? d1a[vi] : 0.0);
+              a1[j] = (ok && d1a) ? (d1b ? ra - d1b[vi] : ra) : 0.0;
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -354,18 +357,24 @@ void launch_tc(const F16GemmArgs& a) {
   k<<<grid, NUM_THREADS, SMEM, ctx().stream>>>(ma, mb, a);
 }
 
-int tc_bn() {
-  static int bn = [] {
+// Tile width: BN = 256 for the binary16-output products (half the A traffic
+// per flop: 97.6 vs 131.5 us per n = 4096 product), BN = 128 for the FP64
+// output + dot-partials product, whose epilogue is memory bound and needs the
+// finer tiles to overlap it with the MMAs (229.5 vs 261.8 us).
+// KP_F16TC_BN = 128 | 256 forces one width for all products.
+int tc_bn(int mode) {
+  static int forced = [] {
     const char* e = getenv("KP_F16TC_BN");
-    return (e && atoi(e) == 256) ? 256 : 128;
+    return e ? atoi(e) : 0;
   }();
-  return bn;
+  if (forced == 128 || forced == 256) return forced;
+  return mode == F16OUT_F64 ? 128 : 256;
 }
 
 }  // namespace
 
-// Partials are written per output tile.
-int gemm_f16tc_num_ctas(int M, int N) { return int(cdiv(M, BM) * cdiv(N, tc_bn())); }
+// Partials are written per output tile (FP64-output products only).
+int gemm_f16tc_num_ctas(int M, int N) { return int(cdiv(M, BM) * cdiv(N, tc_bn(F16OUT_F64))); }
 
 void gemm_f16tc(const F16GemmArgs& a, int kernel_class) {
   if (a.M <= 0 || a.N <= 0) return;
@@ -373,7 +382,7 @@ void gemm_f16tc(const F16GemmArgs& a, int kernel_class) {
   if (a.A.ld % BKH || a.B.ld % BKH || a.A.ld < a.K || a.B.ld < a.K)
     throw InvalidArgument("gemm_f16tc: operand leading dimension must be a multiple of 64 >= K");
   LaunchScope scope(kernel_class);
-  if (tc_bn() == 256)
+  if (tc_bn(a.epi.mode) == 256)
     launch_tc<256>(a);
   else
     launch_tc<128>(a);
