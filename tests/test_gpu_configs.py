@@ -156,3 +156,34 @@ def test_c5_operator_full_size_properties():
     dx = K.kronsum_apply(a, x)
     a.set_mode("auto")
     assert np.linalg.norm(ax - dx) <= 1e-13 * np.linalg.norm(dx)
+
+
+def test_setup_svd_backend_invariance():
+    """The factor SVDs may come from host LAPACK or cuSOLVER (bench / C4 setup);
+    their vectors differ in sign and last bits. M, the GCV sums and the
+    discrepancy lambda are invariant (SURVEY §7 'setup cost')."""
+    import torch
+    cfg = configs.build("C1")
+    term = cfg.term
+    host = [SvdTriple(*P.host_svd(f)) for f in (term.row_factor, term.col_factor)]
+    dev = []
+    for f in (term.row_factor, term.col_factor):
+        u, s, vh = torch.linalg.svd(torch.from_numpy(np.ascontiguousarray(f)).cuda())
+        dev.append(SvdTriple(np.asfortranarray(u.cpu().numpy()), s.cpu().numpy().copy(),
+                             np.asfortranarray(vh.T.cpu().numpy())))
+    r = np.random.default_rng(8).standard_normal(cfg.n * cfg.n)
+    for fmt, tol in ((K.PrecisionFormat.fp64(), 1e-10), (K.PrecisionFormat.fp16(), 2e-3)):
+        mh = K.build_preconditioner_from_svd(host[0], host[1], 0.01, fmt)
+        md = K.build_preconditioner_from_svd(dev[0], dev[1], 0.01, fmt)
+        zh, zd = K.precond_solve(mh, r), K.precond_solve(md, r)
+        assert np.linalg.norm(zh - zd) <= tol * np.linalg.norm(zh)
+    m0h = K.build_preconditioner_from_svd(host[0], host[1], 1.0, K.PrecisionFormat.fp16())
+    m0d = K.build_preconditioner_from_svd(dev[0], dev[1], 1.0, K.PrecisionFormat.fp16())
+    sh, sd = K.make_spectral_data(m0h, cfg.problem.b), K.make_spectral_data(m0d, cfg.problem.b)
+    ch, vh_ = K.gcv_grid(sh, configs.GCV_GRID)
+    cd, vd = K.gcv_grid(sd, configs.GCV_GRID)
+    assert ch.grid_index == cd.grid_index
+    assert np.allclose(vh_, vd, rtol=1e-10)
+    nn = float(np.linalg.norm(cfg.problem.noise))
+    assert K.discrepancy(sh, nn, 1.01).lambda_ == pytest.approx(K.discrepancy(sd, nn, 1.01).lambda_,
+                                                                 rel=1e-9)
