@@ -201,8 +201,21 @@ struct SolverWorkspace {
     if (!host_state) KP_CUDA(cudaMallocHost(&host_state, sizeof(DevState)));
     return host_state;
   }
+  // two pinned status slots + events for the pipelined status polls of drive()
+  int* poll_slots() {
+    if (!poll) {
+      KP_CUDA(cudaMallocHost(&poll, 2 * sizeof(int)));
+      for (auto& e : poll_ev) KP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    return poll;
+  }
+  int* poll = nullptr;
+  cudaEvent_t poll_ev[2] = {nullptr, nullptr};
   ~SolverWorkspace() {
     if (host_state) cudaFreeHost(host_state);
+    if (poll) cudaFreeHost(poll);
+    for (auto& e : poll_ev)
+      if (e) cudaEventDestroy(e);
   }
 };
 
@@ -690,7 +703,6 @@ void setup_state(Solve& s, const kp_solver_options* o, bool has_xt, bool flexibl
 // device no-ops).
 void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
   Ctx& c = ctx();
-  DevState* hst = s.op->ws.pinned_state();
   cudaGraphExec_t exec = nullptr;
   long long per_iter_launches = 0;
   if (!c.profile) {
@@ -712,13 +724,21 @@ void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
     c.launches = before;
     g_launches.fetch_sub(per_iter_launches, std::memory_order_relaxed);  // captured, not launched
   }
-  // Poll after every iteration while an iteration is long (overshoot would
-  // cost real no-op launches); batch up to 16 iterations per poll once an
-  // iteration is shorter than ~1 ms, where the host round trip dominates.
-  int done = 0, chunk = 1;
+  // Pipelined polling: after enqueueing a chunk of iterations the host reads
+  // the status the PREVIOUS chunk left (pinned slot + event), so the device
+  // always has the next chunk queued and never idles on the host round trip.
+  // Overshoot is at most one chunk of no-op iterations (every kernel returns
+  // once the status leaves RUNNING). A chunk is 1 iteration while an
+  // iteration is long (> 1 ms, where a no-op iteration still costs launches),
+  // else it doubles up to 16.
+  int* slot = s.op->ws.poll_slots();
+  cudaEvent_t* ev = s.op->ws.poll_ev;
+  int done = 0, chunk = 1, cur = 0;
+  bool pending = false;
+  auto t_prev = std::chrono::steady_clock::now();
+  int prev_todo = 1;
   while (done < maxit) {
     const int todo = std::min(chunk, maxit - done);
-    const auto t0 = std::chrono::steady_clock::now();
     for (int i = 0; i < todo; ++i) {
       if (exec) {
         KP_CUDA(cudaGraphLaunch(exec, c.stream));
@@ -729,14 +749,21 @@ void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
       }
     }
     done += todo;
-    KP_CUDA(cudaMemcpyAsync(&hst->status, &s.st->status, sizeof(int), cudaMemcpyDeviceToHost,
+    KP_CUDA(cudaMemcpyAsync(&slot[cur], &s.st->status, sizeof(int), cudaMemcpyDeviceToHost,
                             c.stream));
-    sync();
-    if (hst->status != ST_RUNNING) break;
-    const double per_iter_ms =
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() /
-        todo;
-    chunk = per_iter_ms > 1.0 ? 1 : std::min(chunk * 2, 16);
+    KP_CUDA(cudaEventRecord(ev[cur], c.stream));
+    if (pending) {  // the chunk before this one
+      KP_CUDA(cudaEventSynchronize(ev[cur ^ 1]));
+      if (slot[cur ^ 1] != ST_RUNNING) break;
+      const auto t = std::chrono::steady_clock::now();
+      const double per_iter_ms =
+          std::chrono::duration<double, std::milli>(t - t_prev).count() / prev_todo;
+      t_prev = t;
+      chunk = per_iter_ms > 1.0 ? 1 : std::min(chunk * 2, 16);
+    }
+    pending = true;
+    prev_todo = todo;
+    cur ^= 1;
   }
   if (exec) cudaGraphExecDestroy(exec);
 }
