@@ -95,22 +95,33 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
   const int KT = (args.K + BKH - 1) / BKH;
   const uint32_t sbase = smem_u32(smem);
 
+  // Per-thread copy plan, computed once: chunk i of every k-tile is the 16-byte
+  // piece id = tid + i * THREADS (ids < CA are A rows, the rest B rows), so
+  // the k-loop only advances 64-bit source pointers (ALU adds, no IMADs on
+  // the FMA pipe the f16x2 math needs).
+  constexpr int CA = BM * 8, CB = BN * 8, NCH = (CA + CB) / THREADS;
+  static_assert((CA + CB) % THREADS == 0 && CA % THREADS == 0, "copy plan");
+  const __half* src0[NCH];
+  uint32_t dst_off[NCH];
+  bool valid[NCH];
+#pragma unroll
+  for (int i = 0; i < NCH; ++i) {
+    const int id = tid + i * THREADS;
+    const bool isA = id < CA;  // compile-time per i (tid < THREADS)
+    const int cid = isA ? id : id - CA;
+    const int row = cid >> 3, ch = cid & 7;
+    const int grow = (isA ? m_base : n_base) + row;
+    valid[i] = grow < (isA ? M : N);
+    const F16Operand& op = isA ? args.A : args.B;
+    src0[i] = valid[i] ? op.p + long(grow) * op.ld + ch * 8 : op.p;
+    dst_off[i] = (isA ? 0u : uint32_t(BM * ROW_BYTES)) +
+                 uint32_t(row * ROW_BYTES + ((ch ^ (row & 7)) << 4));
+  }
   auto load_tile = [&](int kt, int stage) {
     const uint32_t sa = sbase + uint32_t(stage * STAGE_BYTES);
-    const uint32_t sb = sa + uint32_t(BM * ROW_BYTES);
-    constexpr int CA = BM * 8, CB = BN * 8;
 #pragma unroll
-    for (int id = tid; id < CA + CB; id += THREADS) {
-      const bool isA = id < CA;
-      const int cid = isA ? id : id - CA;
-      const int row = cid >> 3, ch = cid & 7;
-      const int grow = (isA ? m_base : n_base) + row;
-      const bool v = grow < (isA ? M : N);
-      const F16Operand& op = isA ? args.A : args.B;
-      const __half* src = op.p + long(grow) * op.ld + kt * BKH + ch * 8;
-      const uint32_t dst = (isA ? sa : sb) + uint32_t(row * ROW_BYTES + ((ch ^ (row & 7)) << 4));
-      cp_async16(dst, v ? src : op.p, v);
-    }
+    for (int i = 0; i < NCH; ++i)
+      cp_async16(sa + dst_off[i], valid[i] ? src0[i] + kt * BKH : src0[i], valid[i]);
   };
 
 #pragma unroll
