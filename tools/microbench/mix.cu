@@ -14,6 +14,27 @@ __device__ __forceinline__ float fmul(float a, float b) {
 __device__ __forceinline__ unsigned f2h2(float a, float b) {
   unsigned r; asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b)); return r; }
 
+__device__ __forceinline__ unsigned hfma2(unsigned a, unsigned b, unsigned c) {
+  unsigned r; asm volatile("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c)); return r; }
+
+// all f16x2 work as fma.rn.f16x2 (mul = fma(a, b, -0), add = fma(a, 1, b))
+__global__ void fma_only_k(unsigned* out, int iters) {
+  constexpr int ILP = 8;
+  unsigned h[ILP];
+  for (int i = 0; i < ILP; ++i) h[i] = 0x3c003c00u + threadIdx.x + i;
+  const unsigned m = 0x3c003c01u, one = 0x3c003c00u, nz = 0x80008000u;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) h[i] = (q & 1) ? hfma2(h[i], one, m) : hfma2(h[i], m, nz);
+    }
+  }
+  unsigned s = 0;
+  for (int i = 0; i < ILP; ++i) s ^= h[i];
+  if (s == 0x12345678u) out[0] = s;
+}
+
 // H: f16x2 ops per iteration per ILP slot, F: fmul, C: cvt packs
 template <int H, int F, int CV>
 __global__ void mix_k(unsigned* out, int iters) {
@@ -63,7 +84,26 @@ int run(const char* name) {
   return 0;
 }
 
+int run_fma() {
+  unsigned* d; CK(cudaMalloc(&d, 4));
+  int sms = 0; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  int clk = 0; CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0));
+  const int iters = 4096, blocks = sms * 8, threads = 256;
+  fma_only_k<<<blocks, threads>>>(d, 16);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  cudaEventRecord(a);
+  fma_only_k<<<blocks, threads>>>(d, iters);
+  cudaEventRecord(b); CK(cudaEventSynchronize(b));
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  const double warp_iters = double(blocks) * threads / 32 * iters * 8;
+  const double cycles = ms * 1e-3 * clk * 1e3 * sms;
+  printf("%-28s %8.3f ms  per SM-cycle: f16x2 %.2f warp-instr (%.1f T half-ops/s)\n", "fma.rn.f16x2 only", ms,
+         warp_iters * 8 / cycles, warp_iters * 8 * 64 / (ms * 1e-3) / 1e12);
+  return 0;
+}
+
 int main() {
+  run_fma();
   run<8, 0, 0>("f16x2 only");
   run<0, 8, 0>("fmul only");
   run<0, 1, 4>("cvt.f16x2.f32 (+1 fmul)");
