@@ -7,7 +7,9 @@ Full sizes where the oracle finishes in minutes; C5 (n=4096) as a prefix of
 iterations. Output: tests/golden/<config>.json (histories, iteration counts,
 lambda choices, solution checksums). Usage:
 
-    python tests/golden/gen_goldens.py C1 C2 C3 C4 C5 [--threads 8]
+    python tests/golden/gen_goldens.py C1 C2 C3 C4 C5 [C5fpcg] [--threads 8]
+
+C5fpcg writes C5_fpcg_full.json: the headline FPCG run to its end.
 """
 from __future__ import annotations
 
@@ -51,7 +53,7 @@ def run_solver(cfg, solver, fmt, maxit, lam, m0):
     return d
 
 
-def gen(name: str, prefix: int | None = None, images=(0,)):
+def gen(name: str, prefix: int | None = None, images=(0,), only=None, tag=None):
     out = {"config": name, "generator": "oracle/kp_oracle.cpp via tests/golden/gen_goldens.py",
            "images": []}
     for img in images:
@@ -77,12 +79,14 @@ def gen(name: str, prefix: int | None = None, images=(0,)):
         rec["lambda"] = lam
         rec["runs"] = []
         for solver, fmt, maxit in cfg.solvers:
+            if only and solver != only:
+                continue
             mi = min(maxit, prefix) if prefix else maxit
             rec["runs"].append(run_solver(cfg, solver, fmt, mi, lam, m0))
             print(name, img, solver, fmt, rec["runs"][-1]["iterations_used"],
                   f"{rec['runs'][-1]['seconds']:.1f}s", flush=True)
         out["images"].append(rec)
-    path = os.path.join(HERE, f"{name}.json")
+    path = os.path.join(HERE, f"{tag or name}.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
     print("wrote", path, flush=True)
@@ -101,5 +105,7 @@ if __name__ == "__main__":
             gen("C4", images=(0, 1, 2, 3, 4, 5))
         elif name == "C5":
             gen("C5", prefix=3)
+        elif name == "C5fpcg":  # the headline run in full (about 40 min on 16 threads)
+            gen("C5", only="fpcg", tag="C5_fpcg_full")
         else:
             gen(name)
