@@ -173,3 +173,46 @@ def test_ragged_sizes_fp16_bitwise(n):
     r = rng.standard_normal(n * n)
     zg, zo = K.precond_solve(g, r), O.precond_solve(o, r)
     assert np.array_equal(zg.view(np.uint64), zo.view(np.uint64))
+
+
+def test_device_pointer_mode_matches_host_mode():
+    """kp_solver_options.device_pointers = 1: b, x_true and x live in device
+    memory (the bench's value path); results equal the host-buffer path."""
+    import ctypes as C
+
+    from paper_2311_15393_b200._lib import check, kp_history, kp_solver_options, lib, ptr
+    tp, term = blur(32)
+    g, _ = preconds(term, 0.05, H)
+    L = lib()
+    nn = 32 * 32
+    opts = SolverOptions(lambda_=0.05, max_iterations=12, rel_residual_tol=1e-9, x_true=tp.x_true)
+
+    def dev(a):
+        p = C.c_void_p()
+        check(L.kp_device_alloc(nn * 8, C.byref(p)))
+        if a is not None:
+            check(L.kp_memcpy_h2d(p, ptr(np.ascontiguousarray(a)), nn * 8))
+        return p
+
+    for kind in ("cgls", "pcg", "fpcg"):
+        ref = K.cgls(tp.a, tp.b, opts) if kind == "cgls" else getattr(K, kind)(tp.a, tp.b, g, opts)
+        db, dxt, dx = dev(tp.b), dev(tp.x_true), dev(None)
+        cap = 13
+        bufs = [np.zeros(cap) for _ in range(4)]
+        h = kp_history(capacity=cap, relative_error=ptr(bufs[0]), residual_norm=ptr(bufs[1]),
+                       work_units=ptr(bufs[2]), residual_cosines=ptr(bufs[3]))
+        o = kp_solver_options(lambda_=0.05, max_iterations=12, rel_residual_tol=1e-9,
+                              x_true=dxt.value, device_pointers=1)
+        if kind == "cgls":
+            check(L.kp_cgls(tp.a.handle(), db, C.byref(o), dx, C.byref(h)))
+        else:
+            f = L.kp_pcg if kind == "pcg" else L.kp_fpcg
+            check(f(tp.a.handle(), db, g.handle(), C.byref(o), dx, C.byref(h)))
+        x = np.empty(nn)
+        check(L.kp_memcpy_d2h(ptr(x), dx, nn * 8))
+        assert h.iterations_used == ref.history.iterations_used
+        assert np.array_equal(x, ref.x)
+        assert np.array_equal(bufs[1][:h.rows], np.array(ref.history.residual_norm))
+        assert np.array_equal(bufs[0][:h.rows], np.array(ref.history.relative_error))
+        for p in (db, dxt, dx):
+            L.kp_device_free(p)
