@@ -211,7 +211,9 @@ struct SolverWorkspace {
   }
   int* poll = nullptr;
   cudaEvent_t poll_ev[2] = {nullptr, nullptr};
+  cudaGraphExec_t exec = nullptr;  // last solve's iteration graph (drive())
   ~SolverWorkspace() {
+    if (exec) cudaGraphExecDestroy(exec);
     if (host_state) cudaFreeHost(host_state);
     if (poll) cudaFreeHost(poll);
     for (auto& e : poll_ev)
@@ -718,7 +720,20 @@ void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
     }
     cudaGraph_t graph;
     KP_CUDA(cudaStreamEndCapture(c.stream, &graph));
-    KP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    // Reuse the workspace's executable graph when the new capture has the
+    // same topology (repeated solves on one operator): an in-place parameter
+    // update is much cheaper than instantiation.
+    SolverWorkspace& ws = s.op->ws;
+    if (ws.exec) {
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(ws.exec, graph, &info) != cudaSuccess) {
+        cudaGetLastError();  // clear the update failure
+        cudaGraphExecDestroy(ws.exec);
+        ws.exec = nullptr;
+      }
+    }
+    if (!ws.exec) KP_CUDA(cudaGraphInstantiate(&ws.exec, graph, 0));
+    exec = ws.exec;
     KP_CUDA(cudaGraphDestroy(graph));
     per_iter_launches = c.launches - before;
     c.launches = before;
@@ -765,7 +780,6 @@ void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
     prev_todo = todo;
     cur ^= 1;
   }
-  if (exec) cudaGraphExecDestroy(exec);
 }
 
 void finish(Solve& s, const kp_solver_options* o, kp_history* h, double work) {
