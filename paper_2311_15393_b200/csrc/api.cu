@@ -75,6 +75,13 @@ void init_pool(int device) {
   KP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
 }
 
+void set_smem_limit(const void* kernel, size_t bytes) {
+  auto& cur = ctx().smem_attr[kernel];
+  if (bytes <= cur) return;
+  KP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+  cur = bytes;
+}
+
 void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));

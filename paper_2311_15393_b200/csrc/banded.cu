@@ -229,11 +229,7 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
 void band_cols(const double* X, double* Y, int n, int r, const BandTaps& t, const int* status) {
   const int S = (A_TA + t.taps) | 1;
   const size_t smem = size_t(A_TL) * S * sizeof(double);
-  static size_t attr = 0;
-  if (smem > attr) {
-    KP_CUDA(cudaFuncSetAttribute(band_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = smem;
-  }
+  set_smem_limit(reinterpret_cast<const void*>(band_cols_kernel), smem);
   LaunchScope scope(KC_OPERATOR);
   dim3 grid(cdiv(n, A_TL), cdiv(n, A_TA));
   band_cols_kernel<<<grid, A_THREADS, smem, ctx().stream>>>(X, Y, n, r, t, status);
@@ -246,11 +242,7 @@ void band_rows(const double* Y, int n, int r, const BandTaps& t, const F64Epilog
                const int* status) {
   // two buffers; +1 row each: corr8 prefetches one value past the taps
   const size_t smem = 2 * size_t(B_TJ + t.taps) * B_TA * sizeof(double);
-  static size_t attr = 0;
-  if (smem > attr) {
-    KP_CUDA(cudaFuncSetAttribute(band_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = smem;
-  }
+  set_smem_limit(reinterpret_cast<const void*>(band_rows_kernel), smem);
   LaunchScope scope(KC_OPERATOR);
   dim3 grid(cdiv(n, B_TJ), cdiv(n, B_TA));
   band_rows_kernel<<<grid, B_THREADS, smem, ctx().stream>>>(Y, n, r, t, e, status);

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 namespace kp {
@@ -47,11 +48,17 @@ struct Ctx {
   double total_ms[KC_COUNT] = {0, 0, 0, 0};
   long long count[KC_COUNT] = {0, 0, 0, 0};
   cudaEvent_t events[16] = {};
+  // dynamic shared-memory limit already set per kernel on this thread's device
+  std::unordered_map<const void*, size_t> smem_attr;
 };
 
 Ctx& ctx();            // lazily initialised on first use (device 0)
 void ensure_init();
-void init_pool(int device);  // keep freed pool blocks cached (release threshold = max)
+void init_pool(int device);
+// Raise a kernel's dynamic shared-memory limit to `bytes` on the calling
+// thread's device (cached per thread: no shared mutable state, and a thread
+// per device sets it for every device it uses).
+void set_smem_limit(const void* kernel, size_t bytes);  // keep freed pool blocks cached (release threshold = max)
 void check_launch(const char* what);
 
 // RAII launch bracket: counts the launch and, when profiling, records events.

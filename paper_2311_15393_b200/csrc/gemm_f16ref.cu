@@ -297,11 +297,7 @@ void launch_f16ref(const F16GemmArgs& a, int kernel_class) {
   while ((1 << levels) <= units) ++levels;
   const size_t smem = size_t(STAGES) * STAGE_BYTES + size_t(levels) * NACC * THREADS * 4;
   auto kern = gemm_f16ref_kernel<STAGES, UNIT>;
-  static size_t attr_smem = 0;
-  if (smem > attr_smem) {
-    KP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_smem = smem;
-  }
+  set_smem_limit(reinterpret_cast<const void*>(kern), smem);
   LaunchScope scope(kernel_class);
   const unsigned grid = cdiv(a.M, BM) * cdiv(a.N, BN);
   kern<<<grid, THREADS, smem, ctx().stream>>>(a, levels);

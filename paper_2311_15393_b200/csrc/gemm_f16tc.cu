@@ -346,11 +346,7 @@ template <int BN>
 void launch_tc(const F16GemmArgs& a) {
   constexpr size_t SMEM = size_t(STAGES) * (TILE_A_BYTES + BN * BKH * 2) + 1024;
   auto k = gemm_f16tc_kernel<BN>;
-  static bool attr = false;
-  if (!attr) {
-    KP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM)));
-    attr = true;
-  }
+  set_smem_limit(reinterpret_cast<const void*>(k), SMEM);
   const CUtensorMap ma = make_map(a.A, a.M, BM), mb = make_map(a.B, a.N, BN);
   const int tiles = int(cdiv(a.M, BM) * cdiv(a.N, BN));
   const int grid = std::min(tiles, ctx().num_sms);

@@ -227,19 +227,11 @@ void launch_cfg(const F64GemmArgs& a) {
                      (reinterpret_cast<uintptr_t>(a.B.p) % 16 == 0);
   if (vec16) {
     auto k = gemm_f64_kernel<BM, BN, WM, WN, STAGES, KSUB, true>;
-    static bool attr = false;
-    if (!attr) {
-      KP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM)));
-      attr = true;
-    }
+    set_smem_limit(reinterpret_cast<const void*>(k), SMEM);
     k<<<grid, THREADS, SMEM, ctx().stream>>>(a);
   } else {
     auto k = gemm_f64_kernel<BM, BN, WM, WN, STAGES, KSUB, false>;
-    static bool attr = false;
-    if (!attr) {
-      KP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM)));
-      attr = true;
-    }
+    set_smem_limit(reinterpret_cast<const void*>(k), SMEM);
     k<<<grid, THREADS, SMEM, ctx().stream>>>(a);
   }
 }
