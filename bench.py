@@ -303,6 +303,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tensor", action="store_true", help="skip the tensor-mode secondary run")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense-operator roofline probe")
+    ap.add_argument("--no-other-runs", action="store_true",
+                    help="skip the config's other solver runs (C5: PCG fp64-precond, CGLS)")
     ap.add_argument("--operator", default="auto", choices=["auto", "dense", "banded"])
     ap.add_argument("--workers", type=int, default=4,
                     help="C4: concurrent host threads / streams per GPU")
@@ -469,6 +471,37 @@ def main():
                                "work_per_launch": f"{2.0 * float(n) ** 3:.4g} flop",
                                "traffic": TRAFFIC.get(("gemm_f16tc_kernel", n))}}
 
+    # ---- the config's other runs (C5: PCG with the FP64 preconditioner, CGLS),
+    # one device-resident solve each, for the record ----
+    other_runs = {}
+    if not args.no_other_runs:
+        for solver_o, fmt_o, maxit_o in cfg.solvers[1:]:
+            hb = [np.zeros(maxit_o + 1) for _ in range(4)]  # kept alive for the call
+            rel_o = hb[0]
+            ho = kp_history(capacity=maxit_o + 1, relative_error=ptr(hb[0]), residual_norm=ptr(hb[1]),
+                            work_units=ptr(hb[2]), residual_cosines=ptr(hb[3]))
+            oo = kp_solver_options(lambda_=cfg.lambda_, max_iterations=maxit_o,
+                                   rel_residual_tol=cfg.tol, x_true=d_xt.value, device_pointers=1)
+            mo = None
+            if solver_o != "cgls":
+                fmt_obj = K.PrecisionFormat.fp64() if fmt_o == "fp64" else fmt
+                mo = K.build_preconditioner_from_svd(svd_r, svd_c, cfg.lambda_, fmt_obj)
+            barrier()
+            check(L.kp_event_record(8))
+            if solver_o == "cgls":
+                check(L.kp_cgls(op, d_b, C.byref(oo), d_x, C.byref(ho)))
+            else:
+                fn = L.kp_fpcg if solver_o == "fpcg" else L.kp_pcg
+                check(fn(op, d_b, mo.handle(), C.byref(oo), d_x, C.byref(ho)))
+            check(L.kp_event_record(9))
+            o_ms = C.c_float()
+            check(L.kp_event_elapsed(8, 9, C.byref(o_ms)))
+            other_runs[f"{solver_o}_{fmt_o or 'none'}"] = {
+                "iterations_per_s": ho.iterations_used / (o_ms.value / 1e3),
+                "iterations": ho.iterations_used, "converged": bool(ho.converged),
+                "final_rel_err": float(rel_o[ho.rows - 1]), "ms": o_ms.value,
+                "abort_reason": ho.abort_reason.decode()}
+
     # ---- e2e: the same solves through host (pinned) buffers ----
     for _ in range(max(1, args.warmup)):  # warm the host-path staging buffers too
         solve(False)
@@ -586,6 +619,7 @@ def main():
                                       "replay; source of roofline and kernel shares"},
             "solves_per_s": args.steps * ws / elapsed,
             "tensor_mode": tensor,
+            "other_runs": other_runs,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
