@@ -29,6 +29,7 @@ __all__ = [
     "plateau_iteration", "WorkReport", "work_report", "SpectralData", "make_spectral_data",
     "ParamChoice", "gcv_objective", "opt_objective", "wgcv_objective", "discrepancy_gap", "gcv",
     "gcv_grid", "lambda_opt", "wgcv", "discrepancy", "filtered_solution", "NoRootError",
+    "MinimizeResult", "minimize_1d", "find_root", "param_method_name",
 ]
 
 
@@ -571,6 +572,89 @@ def make_spectral_data(p: KronSvdPreconditioner, b, x_true=None) -> SpectralData
         raise ValueError("project: vector length is not n^2")
     check(lib().kp_spectral_create_x(p.handle(), ptr(b), ptr(x), C.byref(h)))
     return SpectralData(h, p.n, True)
+
+
+def _probe(f, x: float, who: str) -> float:  # regparam.cpp:37-43
+    v = float(f(x))
+    if math.isnan(v):
+        raise RuntimeError(f"{who}: objective is NaN")
+    return v
+
+
+@dataclass
+class MinimizeResult:  # regparam.hpp:55-58
+    x: float = 0.0
+    fx: float = 0.0
+
+
+def minimize_1d(f, lo: float, hi: float, tol: float) -> MinimizeResult:
+    """Golden-section search (regparam.cpp:150-181); host arithmetic, same
+    IEEE double operations as the reference."""
+    if not lo < hi:
+        raise ValueError("minimize_1d: requires lo < hi")
+    if not tol > 0.0:
+        raise ValueError("minimize_1d: tol must be positive")
+    invphi = 0.6180339887498949
+    a, b = lo, hi
+    c = b - invphi * (b - a)
+    d = a + invphi * (b - a)
+    fc, fd = _probe(f, c, "minimize_1d"), _probe(f, d, "minimize_1d")
+    it = 0
+    while it < 300 and b - a > tol * (1.0 + min(abs(a), abs(b))):
+        if fc < fd:
+            b, d, fd = d, c, fc
+            c = b - invphi * (b - a)
+            if c <= a or c >= d:
+                break
+            fc = _probe(f, c, "minimize_1d")
+        else:
+            a, c, fc = c, d, fd
+            d = a + invphi * (b - a)
+            if d <= c or d >= b:
+                break
+            fd = _probe(f, d, "minimize_1d")
+        it += 1
+    return MinimizeResult(c, fc) if fc < fd else MinimizeResult(d, fd)
+
+
+def find_root(f, lo: float, hi: float, tol: float) -> float:
+    """Bisection (regparam.cpp:184-214)."""
+    if not lo < hi:
+        raise ValueError("find_root: requires lo < hi")
+    if not tol > 0.0:
+        raise ValueError("find_root: tol must be positive")
+    flo, fhi = _probe(f, lo, "find_root"), _probe(f, hi, "find_root")
+    if not (math.isfinite(flo) and math.isfinite(fhi)):
+        raise RuntimeError("find_root: endpoint value not finite")
+    if flo == 0.0:
+        return lo
+    if fhi == 0.0:
+        return hi
+    if (flo > 0.0) == (fhi > 0.0):
+        raise ValueError("find_root: no sign change over [lo, hi]")
+    a, b = lo, hi
+    while b - a > tol * (1.0 + 0.5 * (abs(a) + abs(b))):
+        m = a + 0.5 * (b - a)
+        if m <= a or m >= b:
+            break
+        fm = _probe(f, m, "find_root")
+        if not math.isfinite(fm):
+            raise RuntimeError("find_root: function value not finite")
+        if fm == 0.0:
+            return m
+        if (fm > 0.0) == (flo > 0.0):
+            a, flo = m, fm
+        else:
+            b = m
+    return a + 0.5 * (b - a)
+
+
+def param_method_name(method: str) -> str:  # regparam.cpp:136-148
+    names = {"opt": "opt", "gcv": "gcv", "wgcv": "wgcv", "discrepancy": "discrepancy",
+             "gcv_grid": "gcv_grid"}
+    if method not in names:
+        raise ValueError("unknown parameter method")
+    return names[method]
 
 
 def gcv_objective(sd: SpectralData, lambda_: float) -> float:  # regparam.cpp:224-229
