@@ -299,7 +299,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
     ap.add_argument("--size", type=int, default=None, help="override image side n (quick runs)")
-    ap.add_argument("--svd", default="gpu", choices=["gpu", "host"])
+    ap.add_argument("--svd", default="host", choices=["gpu", "host"],
+                    help="setup SVD of the factors: host LAPACK dgesdd (the oracle's routine; "
+                         "default) or cuSOLVER via torch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tensor", action="store_true", help="skip the tensor-mode secondary run")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense-operator roofline probe")

@@ -193,19 +193,16 @@ def test_c5_fpcg_full_solve_vs_golden():
     """The headline run end to end at BASELINE size: C5 FPCG with the fp16
     reference-exact preconditioner, against the oracle's complete run
     (tests/golden/C5_fpcg_full.json: iterations, stop / abort reason,
-    final relative error). Setup SVD from cuSOLVER, as the bench does."""
+    final relative error)."""
     path = os.path.join(os.path.dirname(__file__), "golden", "C5_fpcg_full.json")
     if not os.path.exists(path):
         pytest.skip("C5_fpcg_full.json not generated")
     ref = json.load(open(path))["images"][0]["runs"][0]
-    import torch
     cfg = configs.build("C5")
-    svd = []
-    for f in (cfg.term.row_factor, cfg.term.col_factor):
-        u, s, vh = torch.linalg.svd(torch.from_numpy(np.ascontiguousarray(f)).cuda())
-        svd.append(SvdTriple(np.asfortranarray(u.cpu().numpy()), s.cpu().numpy().copy(),
-                             np.asfortranarray(vh.T.cpu().numpy())))
-    m = K.build_preconditioner_from_svd(svd[0], svd[1], cfg.lambda_, FMT["fp16"])
+    # the library's LAPACK setup SVD (the oracle's routine); cuSOLVER factors
+    # move the stagnation-point abort by a few iterations (DESIGN.md §6)
+    m = K.build_preconditioner(cfg.term.row_factor, cfg.term.col_factor, cfg.lambda_,
+                               FMT["fp16"])
     opts = SolverOptions(lambda_=cfg.lambda_, max_iterations=100, rel_residual_tol=cfg.tol,
                          x_true=cfg.problem.x_true)
     run = K.fpcg(cfg.problem.a, cfg.problem.b, m, opts)
