@@ -9,7 +9,8 @@ lambda choices, solution checksums). Usage:
 
     python tests/golden/gen_goldens.py C1 C2 C3 C4 C5 [C5fpcg] [--threads 8]
 
-C5fpcg writes C5_fpcg_full.json: the headline FPCG run to its end.
+C5fpcg writes C5_fpcg_full.json: the headline FPCG run to its end;
+C5cgls writes C5_cgls_full.json: the CGLS run to convergence.
 """
 from __future__ import annotations
 
@@ -105,7 +106,9 @@ if __name__ == "__main__":
             gen("C4", images=(0, 1, 2, 3, 4, 5))
         elif name == "C5":
             gen("C5", prefix=3)
-        elif name == "C5fpcg":  # the headline run in full (about 40 min on 16 threads)
+        elif name == "C5fpcg":  # the headline run in full (about 45 min on 8 threads)
             gen("C5", only="fpcg", tag="C5_fpcg_full")
+        elif name == "C5cgls":  # CGLS to convergence (about 45 min on 8 threads)
+            gen("C5", only="cgls", tag="C5_cgls_full")
         else:
             gen(name)
