@@ -208,3 +208,17 @@ def test_c5_fpcg_full_solve_vs_golden():
     run = K.fpcg(cfg.problem.a, cfg.problem.b, m, opts)
     check_against(run, ref, prefix_rows=1)
     assert run.history.abort_reason.split(" at ")[0] == ref["abort_reason"].split(" at ")[0]
+
+
+def test_c5_cgls_full_solve_vs_golden():
+    """C5's CGLS run to convergence at BASELINE size (FP64 only) against the
+    oracle's complete run: iteration count, convergence, final error, and the
+    residual / error history over a 20-row prefix at 1e-8 (later rows drift
+    with FP64 re-association)."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "C5_cgls_full.json")
+    if not os.path.exists(path):
+        pytest.skip("C5_cgls_full.json not generated")
+    ref = json.load(open(path))["images"][0]["runs"][0]
+    cfg = configs.build("C5")
+    (run,) = device_runs(cfg, cfg.lambda_, [("cgls", None, 2000)])
+    check_against(run, ref, prefix_rows=20)
