@@ -111,7 +111,10 @@ typedef struct kp_spectral kp_spectral; /* SpectralData (regparam.hpp:19-24) */
 
 /* ---- context ---------------------------------------------------------- */
 const char* kp_last_error(void);
-int kp_init(int device);            /* selects the device, creates the stream */
+/* Every host thread has its own context: kp_init selects the device and
+ * creates the calling thread's stream (a thread that never calls it gets the
+ * device current for it). Handles are used by one thread at a time. */
+int kp_init(int device);
 int kp_synchronize(void);
 int kp_device_alloc(size_t bytes, void** dptr);
 int kp_device_free(void* dptr);
@@ -123,7 +126,7 @@ int kp_memcpy_d2h(void* dst, const void* src, size_t bytes);
 int kp_profile_enable(int on);
 int kp_profile_read(int kernel_class, double* total_ms, long long* launches);
 int kp_profile_reset(void);
-long long kp_launch_count(void);   /* kernels launched by this library */
+long long kp_launch_count(void);   /* kernels launched by this library (all threads) */
 /* Device timestamps on the library stream (slots 0..15), for callers that
  * time whole solves on the device. */
 int kp_event_record(int slot);
@@ -141,7 +144,7 @@ int kp_operator_destroy(kp_operator* op);
 int kp_operator_info(const kp_operator* op, int* n, int* r);
 /* Operator algorithm. KP_OP_AUTO (default) uses the banded-Toeplitz kernels
  * when every factor is a banded Toeplitz matrix (the psf_to_kronsum
- * structure, deblur.cpp:157-199) with at most 57 diagonals and r <= 8, and
+ * structure, deblur.cpp:157-199) with at most 64 diagonals and r <= 8, and
  * the dense DMMA GEMMs otherwise; KP_OP_DENSE forces the dense product the
  * reference computes (kron.cpp:69-70); KP_OP_BANDED fails with
  * KP_ERR_INVALID_ARGUMENT if the structure is absent. The environment
@@ -163,7 +166,10 @@ int kp_normal_matvec(const kp_operator* op, double lambda, const double* p,
 
 /* ---- preconditioner: factor.hpp / factor.cpp -------------------------- */
 /* build_preconditioner (factor.cpp:80-104): host LAPACK SVDs of a_r, a_c,
- * weights S(i,j)=1/((s_r(j) s_c(i))^2+lambda^2), rounded V_r, V_c, S. */
+ * weights S(i,j)=1/((s_r(j) s_c(i))^2+lambda^2), rounded V_r, V_c, S.
+ * Any format: binary16 runs on the f16x2 GEMMs (or tcgen05 with
+ * KP_ACCUM_TENSOR), double-covering formats on DMMA GEMMs, every other
+ * (t, emax, subnormals) on the exact generic emulation. */
 int kp_precond_build(const double* a_r, const double* a_c, int n,
                      double lambda, kp_format fmt, int accum,
                      kp_precond** out);
