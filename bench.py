@@ -41,10 +41,10 @@ BF16_PEAK_TFLOPS = 1653.4  # MEASURED_PEAKS.json bf16_tflops (burst; fp16 kind::
 # DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the
 # committed ncu --set full captures (profiles/r01_ncu_key_metrics.txt)
 TRAFFIC = {
-    ("gemm_f16ref_kernel", 4096): 67.94e6 + 22.77e6,   # r01_gemm_f16ref_u64_n4096.ncu-rep
-    ("gemm_f16tc_kernel", 4096): (74.78e6 + 19.91e6 + 119.2e6 + 22.84e6 + 73.73e6 + 19.7e6
-                                  + 445.1e6 + 109e6) / 4,  # mean of the 4 products of a solve
-    ("band", 4096): (134.8e6 + 617.2e6 + 671.4e6 + 120.9e6) / 2,  # per pass, r01_band_vec
+    ("gemm_f16ref_kernel", 4096): 68.37e6 + 22.35e6,   # r01_gemm_f16ref_u64_n4096.ncu-rep
+    ("gemm_f16tc_kernel", 4096): (74.24e6 + 13.7e6 + 118.3e6 + 17.75e6 + 72.9e6 + 14.26e6
+                                  + 440.1e6 + 109.1e6) / 4,  # mean of the 4 products of a solve
+    ("band", 4096): (134.6e6 + 619.9e6 + 671.2e6 + 123.5e6) / 2,  # per pass, r01_band_vec
 }
 
 
