@@ -24,10 +24,12 @@
 namespace kp {
 namespace {
 
-constexpr int BM = 32, BN = 64, BKH = 64, THREADS = 128;
+constexpr int BM = 32, BKH = 64, THREADS = 128;
 constexpr int ROW_BYTES = BKH * 2;  // 128
-constexpr int STAGE_BYTES = (BM + BN) * ROW_BYTES;
-constexpr int NACC = 8;  // 4 m-rows x 2 n-pairs per thread
+// BN = 64 (4 m-rows x 2 n-pairs = 8 packed accumulators per thread) or 32
+// (4 x 1; twice the CTAs and warps for problems too small to fill the SMs).
+constexpr int stage_bytes(int bn) { return (BM + bn) * ROW_BYTES; }
+constexpr int nacc(int bn) { return 4 * (bn / 32); }
 constexpr int GROUP_M = 8;
 
 __device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
@@ -72,8 +74,9 @@ __device__ __forceinline__ uint32_t part(const uint4& v, int q) {
 // shared-memory counter stack (16: levels >= 4 in smem; 32: level 4 also in
 // registers; 64: levels 4 and 5 in registers — the whole 64-leaf k-tile is
 // reduced in registers and pushed once, the smallest stack).
-template <int STAGES, int UNIT>
+template <int STAGES, int UNIT, int BN>
 __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs args, int levels) {
+  constexpr int NP = BN / 32, NACC = nacc(BN), STAGE_BYTES = stage_bytes(BN);
   if (args.status && *args.status != 0) return;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* stack = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES);
@@ -151,14 +154,14 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
 #pragma unroll
     for (int sub = 0; sub < 8; ++sub) {  // 8-leaf sub-chunk = one 16-byte smem chunk
       const uint32_t ca = uint32_t(sub << 4) ^ xa, cb = uint32_t(sub << 4) ^ xb;
-      uint4 af[4], bfr[4];
+      uint4 af[4], bfr[2 * NP];
 #pragma unroll
       for (int i = 0; i < 4; ++i) af[i] = lds128(sa + ca + uint32_t(i * 8 * ROW_BYTES));
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bfr[j] = lds128(sb + cb + uint32_t(j * 16 * ROW_BYTES));
+      for (int j = 0; j < 2 * NP; ++j) bfr[j] = lds128(sb + cb + uint32_t(j * 16 * ROW_BYTES));
       uint32_t v8[NACC];
 #pragma unroll
-      for (int p = 0; p < 2; ++p) {
+      for (int p = 0; p < NP; ++p) {
         uint32_t blo[4], bhi[4];
 #pragma unroll
         for (int kp = 0; kp < 4; ++kp) {
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
             const uint32_t p1 = hmul2(bcast_hi(a), bhi[kp]);  // leaf k = 2kp+1
             s4[kp] = hadd2(p0, p1);
           }
-          v8[i * 2 + p] = hadd2(hadd2(s4[0], s4[1]), hadd2(s4[2], s4[3]));
+          v8[i * NP + p] = hadd2(hadd2(s4[0], s4[1]), hadd2(s4[2], s4[3]));
         }
       }
       if ((sub & 1) == 0) {
@@ -238,13 +241,13 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int p = 0; p < 2; ++p)
+    for (int p = 0; p < NP; ++p)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int m = m_base + tm + 8 * i;
         const int n = n_base + tn + 32 * p + 16 * h;
         if (m >= M || n >= N) continue;
-        const uint32_t word = acc[i * 2 + p];
+        const uint32_t word = acc[i * NP + p];
         const unsigned short bits = h ? (unsigned short)(word >> 16) : (unsigned short)(word & 0xffffu);
         if (e.mode == F16OUT_HALF) {
           e.Ch[long(m) * e.cm + long(n) * e.cn] = __ushort_as_half(bits);
@@ -289,19 +292,38 @@ __global__ void fill_u16_kernel(unsigned short* p, size_t n, unsigned short bits
     p[i] = bits;
 }
 
-template <int STAGES, int UNIT>
-void launch_f16ref(const F16GemmArgs& a, int kernel_class) {
+// Tile width for an M x N product: BN = 32 when the 32 x 64 tiles alone would
+// give fewer than 8 CTAs per SM (n <= 1024), else 64.
+int f16ref_bn(int M, int N) {
+  static const int forced = [] {
+    const char* e = getenv("KP_F16REF_BN");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 32 || forced == 64) return forced;
+  return cdiv(M, BM) * cdiv(N, 64) < 8 * ctx().num_sms ? 32 : 64;
+}
+
+template <int STAGES, int UNIT, int BN>
+void launch_f16ref_bn(const F16GemmArgs& a, int kernel_class) {
   const int kt = (a.K + BKH - 1) / BKH;
   const int units = kt * (BKH / UNIT);
   int levels = 1;
   while ((1 << levels) <= units) ++levels;
-  const size_t smem = size_t(STAGES) * STAGE_BYTES + size_t(levels) * NACC * THREADS * 4;
-  auto kern = gemm_f16ref_kernel<STAGES, UNIT>;
+  const size_t smem = size_t(STAGES) * stage_bytes(BN) + size_t(levels) * nacc(BN) * THREADS * 4;
+  auto kern = gemm_f16ref_kernel<STAGES, UNIT, BN>;
   set_smem_limit(reinterpret_cast<const void*>(kern), smem);
   LaunchScope scope(kernel_class);
   const unsigned grid = cdiv(a.M, BM) * cdiv(a.N, BN);
   kern<<<grid, THREADS, smem, ctx().stream>>>(a, levels);
   check_launch("gemm_f16ref");
+}
+
+template <int STAGES, int UNIT>
+void launch_f16ref(const F16GemmArgs& a, int kernel_class) {
+  if (f16ref_bn(a.M, a.N) == 32)
+    launch_f16ref_bn<STAGES, UNIT, 32>(a, kernel_class);
+  else
+    launch_f16ref_bn<STAGES, UNIT, 64>(a, kernel_class);
 }
 
 int f16ref_cfg() {
@@ -314,7 +336,7 @@ int f16ref_cfg() {
 
 }  // namespace
 
-int gemm_f16ref_num_ctas(int M, int N) { return int(cdiv(M, BM) * cdiv(N, BN)); }
+int gemm_f16ref_num_ctas(int M, int N) { return int(cdiv(M, BM) * cdiv(N, f16ref_bn(M, N))); }
 
 void gemm_f16ref(const F16GemmArgs& a, int kernel_class) {
   if (a.M <= 0 || a.N <= 0) return;
