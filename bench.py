@@ -299,9 +299,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
     ap.add_argument("--size", type=int, default=None, help="override image side n (quick runs)")
-    ap.add_argument("--svd", default="host", choices=["gpu", "host"],
-                    help="setup SVD of the factors: host LAPACK dgesdd (the oracle's routine; "
-                         "default) or cuSOLVER via torch")
+    ap.add_argument("--svd", default="auto", choices=["auto", "gpu", "host"],
+                    help="setup SVD of the factors: host LAPACK dgesdd (the oracle's routine) or "
+                         "cuSOLVER via torch; auto = host on one GPU, cuSOLVER when several "
+                         "ranks would contend for the host cores")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tensor", action="store_true", help="skip the tensor-mode secondary run")
     ap.add_argument("--no-dense", action="store_true", help="skip the dense-operator roofline probe")
@@ -313,6 +314,8 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="collective backend for timing reduction / result gather")
     args = ap.parse_args()
+    if args.svd == "auto":
+        args.svd = "host" if dist_env()[0] == 1 else "gpu"
     if args.impl == "reference":
         return run_reference(args)
 
