@@ -22,7 +22,7 @@
 namespace kp {
 namespace {
 
-constexpr int A_TA = 128, A_TL = 32, A_THREADS = 256;   // pass A tile: 128 rows x 32 cols
+constexpr int A_TA = 64, A_TL = 32, A_THREADS = 256;    // pass A tile: 64 rows x 32 cols
 constexpr int B_TA = 32, B_TJ = 64, B_THREADS = 256;    // pass B tile: 32 rows x 64 cols
 
 __device__ __forceinline__ bool stopped(const int* status) { return status && *status != 0; }
