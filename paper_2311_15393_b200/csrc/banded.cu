@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(A_THREADS) band_cols_kernel(const double* __re
                                                               double* __restrict__ Y, int n, int r,
                                                               const __grid_constant__ BandTaps t,
                                                               const int* status) {
+  pdl_wait();
   if (stopped(status)) return;
   extern __shared__ double sm[];
   const int S = (A_TA + t.taps) | 1;  // odd column stride; >= A_TA + taps (corr8 prefetch slack)
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
                                                               int r, const __grid_constant__ BandTaps t,
                                                               const F64Epilogue e,
                                                               const int* status) {
+  pdl_wait();
   if (stopped(status)) return;
   extern __shared__ double sm[];
   const int rows = B_TJ + t.taps - 1;
@@ -232,7 +234,7 @@ void band_cols(const double* X, double* Y, int n, int r, const BandTaps& t, cons
   set_smem_limit(reinterpret_cast<const void*>(band_cols_kernel), smem);
   LaunchScope scope(KC_OPERATOR);
   dim3 grid(cdiv(n, A_TL), cdiv(n, A_TA));
-  band_cols_kernel<<<grid, A_THREADS, smem, ctx().stream>>>(X, Y, n, r, t, status);
+  launch_pdl(band_cols_kernel, grid, dim3(A_THREADS), smem, X, Y, n, r, t, status);
   check_launch("band_cols");
 }
 
@@ -245,7 +247,7 @@ void band_rows(const double* Y, int n, int r, const BandTaps& t, const F64Epilog
   set_smem_limit(reinterpret_cast<const void*>(band_rows_kernel), smem);
   LaunchScope scope(KC_OPERATOR);
   dim3 grid(cdiv(n, B_TJ), cdiv(n, B_TA));
-  band_rows_kernel<<<grid, B_THREADS, smem, ctx().stream>>>(Y, n, r, t, e, status);
+  launch_pdl(band_rows_kernel, grid, dim3(B_THREADS), smem, Y, n, r, t, e, status);
   check_launch("band_rows");
 }
 

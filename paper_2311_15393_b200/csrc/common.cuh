@@ -9,6 +9,7 @@
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
+#include <utility>
 #include <vector>
 
 namespace kp {
@@ -60,6 +61,32 @@ void init_pool(int device);
 // per device sets it for every device it uses).
 void set_smem_limit(const void* kernel, size_t bytes);  // keep freed pool blocks cached (release threshold = max)
 void check_launch(const char* what);
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx().stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KP_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
+// Programmatic dependent launch: every hot-path kernel starts with
+// pdl_wait() (griddepcontrol.wait) before touching memory, and is launched
+// with launch_pdl(), so consecutive kernels on the stream (and in the
+// captured iteration graphs) overlap one kernel's launch with the previous
+// one's tail while keeping full stream-order visibility of its results.
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 900)
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
+}
 
 // RAII launch bracket: counts the launch and, when profiling, records events.
 struct LaunchScope {

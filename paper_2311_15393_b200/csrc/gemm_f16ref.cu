@@ -76,6 +76,7 @@ __device__ __forceinline__ uint32_t part(const uint4& v, int q) {
 // reduced in registers and pushed once, the smallest stack).
 template <int STAGES, int UNIT, int BN>
 __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs args, int levels) {
+  pdl_wait();
   constexpr int NP = BN / 32, NACC = nacc(BN), STAGE_BYTES = stage_bytes(BN);
   if (args.status && *args.status != 0) return;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
 }
 
 __global__ void fill_u16_kernel(unsigned short* p, size_t n, unsigned short bits) {
+  pdl_wait();
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x)
     p[i] = bits;
@@ -314,7 +316,7 @@ void launch_f16ref_bn(const F16GemmArgs& a, int kernel_class) {
   set_smem_limit(reinterpret_cast<const void*>(kern), smem);
   LaunchScope scope(kernel_class);
   const unsigned grid = cdiv(a.M, BM) * cdiv(a.N, BN);
-  kern<<<grid, THREADS, smem, ctx().stream>>>(a, levels);
+  launch_pdl(kern, dim3(grid), dim3(THREADS), smem, a, levels);
   check_launch("gemm_f16ref");
 }
 

@@ -115,6 +115,7 @@ template <int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_f16tc_kernel(const __grid_constant__ CUtensorMap map_a,
                       const __grid_constant__ CUtensorMap map_b, const F16GemmArgs args) {
+  pdl_wait();
   constexpr int TILE_B_BYTES = BN * BKH * 2;
   constexpr int STAGE_BYTES = TILE_A_BYTES + TILE_B_BYTES;
   constexpr int TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulators
@@ -350,7 +351,7 @@ void launch_tc(const F16GemmArgs& a) {
   const CUtensorMap ma = make_map(a.A, a.M, BM), mb = make_map(a.B, a.N, BN);
   const int tiles = int(cdiv(a.M, BM) * cdiv(a.N, BN));
   const int grid = std::min(tiles, ctx().num_sms);
-  k<<<grid, NUM_THREADS, SMEM, ctx().stream>>>(ma, mb, a);
+  launch_pdl(k, dim3(grid), dim3(NUM_THREADS), SMEM, ma, mb, a);
 }
 
 // Tile width: BN = 256 for the binary16-output products (half the A traffic

@@ -59,6 +59,7 @@ constexpr int GROUP_M = 16;
 template <int BM, int BN, int WM, int WN, int STAGES, int KSUB, bool VEC16>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
     gemm_f64_kernel(const F64GemmArgs args) {
+  pdl_wait();
   constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   constexpr int THREADS = WARPS_M * WARPS_N * 32;
   constexpr int MT = WM / 16, NT = WN / 8;
@@ -228,11 +229,11 @@ void launch_cfg(const F64GemmArgs& a) {
   if (vec16) {
     auto k = gemm_f64_kernel<BM, BN, WM, WN, STAGES, KSUB, true>;
     set_smem_limit(reinterpret_cast<const void*>(k), SMEM);
-    k<<<grid, THREADS, SMEM, ctx().stream>>>(a);
+    launch_pdl(k, dim3(grid), dim3(THREADS), SMEM, a);
   } else {
     auto k = gemm_f64_kernel<BM, BN, WM, WN, STAGES, KSUB, false>;
     set_smem_limit(reinterpret_cast<const void*>(k), SMEM);
-    k<<<grid, THREADS, SMEM, ctx().stream>>>(a);
+    launch_pdl(k, dim3(grid), dim3(THREADS), SMEM, a);
   }
 }
 

@@ -59,17 +59,20 @@ __device__ __forceinline__ bool stopped(const DevState* st) { return st->status 
 
 // ---------------------------------------------------------------------------
 __global__ void copy_kernel(double* dst, const double* src, size_t n, const int* status) {
+  pdl_wait();
   if (status && *status) return;
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x)
     dst[i] = src[i];
 }
 __global__ void zero_kernel(double* dst, size_t n) {
+  pdl_wait();
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
        i += size_t(gridDim.x) * blockDim.x)
     dst[i] = 0.0;
 }
 __global__ void dot_partials_kernel(const double* x, const double* y, size_t n, double* part) {
+  pdl_wait();
   __shared__ double red[VEC_THREADS / 32][1];
   double v[1] = {0.0};
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
@@ -84,6 +87,7 @@ __global__ void dot_partials_kernel(const double* x, const double* y, size_t n, 
 
 __global__ void cast_f16_kernel(const double* src, __half* dst, int rows, int cols, long ld_src,
                                 long ld_dst, const int* status) {
+  pdl_wait();
   if (status && *status) return;
   const size_t total = size_t(rows) * cols;
   for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < total;
@@ -98,6 +102,7 @@ __global__ void cast_f16_kernel(const double* src, __half* dst, int rows, int co
 // as FP64 or rounded once to binary16 (round_array of the FP64 weights).
 __global__ void weights_kernel(const double* s_r, const double* s_c, int n, double l2,
                                double* s64, __half* s16) {
+  pdl_wait();
   const size_t nn = size_t(n) * n;
   const unsigned un = unsigned(n);
   for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < nn;
@@ -114,6 +119,7 @@ __global__ void weights_kernel(const double* s_r, const double* s_c, int n, doub
 // PCG (pcg_core, krylov.cpp:58-142)
 __global__ void pcg_init_scalar_kernel(DevState* st, DevHistory h, const double* part_r, int nr,
                                        const double* part_xt, int nxt) {
+  pdl_wait();
   if (stopped(st)) return;
   const double rr = sum_partials(part_r, nr, 0);
   const double xx = st->has_xt ? sum_partials(part_xt, nxt, 0) : 0.0;
@@ -129,6 +135,7 @@ __global__ void pcg_init_scalar_kernel(DevState* st, DevHistory h, const double*
 }
 
 __global__ void pcg_init_msolve_scalar_kernel(DevState* st, const double* part_z, int nz) {
+  pdl_wait();
   if (stopped(st)) return;
   const double rz = sum_partials(part_z, nz, 0);
   const double bad = sum_partials(part_z, nz, 2);
@@ -144,6 +151,7 @@ __global__ void pcg_init_msolve_scalar_kernel(DevState* st, const double* part_z
 }
 
 __global__ void pcg_alpha_scalar_kernel(DevState* st, const double* part, int n) {
+  pdl_wait();
   if (stopped(st)) return;
   const double pq = sum_partials(part, n, 0);
   if (threadIdx.x) return;
@@ -167,6 +175,7 @@ __global__ void pcg_update_kernel(const DevState* st, DevHistory h, double* x, d
                                   double* r_prev, const double* p, const double* q,
                                   const double* z, const double* xt, __half* r16, int n,
                                   long ldh, double* part) {
+  pdl_wait();
   if (stopped(st)) return;
   __shared__ double red[VEC_THREADS / 32][4];
   const double alpha = st->alpha;
@@ -247,6 +256,7 @@ __global__ void pcg_update_kernel(const DevState* st, DevHistory h, double* x, d
 }
 
 __global__ void pcg_resid_scalar_kernel(DevState* st, DevHistory h, const double* part, int n) {
+  pdl_wait();
   if (stopped(st)) return;
   const double rr = sum_partials(part, n, 0);
   const double ee = st->has_xt ? sum_partials(part, n, 1) : 0.0;
@@ -277,6 +287,7 @@ __global__ void pcg_resid_scalar_kernel(DevState* st, DevHistory h, const double
 }
 
 __global__ void pcg_beta_scalar_kernel(DevState* st, const double* part, int n) {
+  pdl_wait();
   if (stopped(st)) return;
   const double rz = sum_partials(part, n, 0);
   const double zdr = sum_partials(part, n, 1);
@@ -299,6 +310,7 @@ __global__ void pcg_beta_scalar_kernel(DevState* st, const double* part, int n) 
 
 // p = z + beta p, then rho = rz with the positivity check (krylov.cpp:133-138)
 __global__ void pcg_p_update_kernel(DevState* st, double* p, const double* z, size_t nn, bool vec2) {
+  pdl_wait();
   if (stopped(st)) return;
   const double beta = st->beta;
   if (vec2) {
@@ -316,6 +328,7 @@ __global__ void pcg_p_update_kernel(DevState* st, double* p, const double* z, si
   }
 }
 __global__ void pcg_rho_scalar_kernel(DevState* st) {
+  pdl_wait();
   if (stopped(st) || threadIdx.x) return;
   st->rho = st->rz;
   if (st->rho <= 0.0) {
@@ -329,6 +342,7 @@ __global__ void pcg_rho_scalar_kernel(DevState* st) {
 // CGLS (krylov.cpp:154-208)
 __global__ void cgls_init_scalar_kernel(DevState* st, DevHistory h, const double* part_s, int ns,
                                         const double* part_xt, int nxt) {
+  pdl_wait();
   if (stopped(st)) return;
   const double ss = sum_partials(part_s, ns, 0);
   const double xx = st->has_xt ? sum_partials(part_xt, nxt, 0) : 0.0;
@@ -348,6 +362,7 @@ __global__ void cgls_init_scalar_kernel(DevState* st, DevHistory h, const double
 
 __global__ void cgls_alpha_scalar_kernel(DevState* st, const double* part_q, int nq,
                                          const double* part_p, int np) {
+  pdl_wait();
   if (stopped(st)) return;
   const double qq = sum_partials(part_q, nq, 0);
   const double pp = (st->k > 1) ? sum_partials(part_p, np, 0) : 0.0;
@@ -369,6 +384,7 @@ template <bool VEC2>
 __global__ void cgls_update_kernel(const DevState* st, DevHistory h, double* x, double* rt,
                                    const double* p, const double* q, const double* xt, size_t nn,
                                    double* part) {
+  pdl_wait();
   if (stopped(st)) return;
   __shared__ double red[VEC_THREADS / 32][1];
   const double alpha = st->alpha;
@@ -417,6 +433,7 @@ __global__ void cgls_update_kernel(const DevState* st, DevHistory h, double* x, 
 // part_s from the s = A^T rt - l2 x GEMM epilogue: [0] ||s||^2, [1] s.s_prev
 __global__ void cgls_resid_scalar_kernel(DevState* st, DevHistory h, const double* part_s, int ns,
                                          const double* part_x, int nx) {
+  pdl_wait();
   if (stopped(st)) return;
   const double ss = sum_partials(part_s, ns, 0);
   const double sp = st->track_cos ? sum_partials(part_s, ns, 1) : 0.0;
@@ -455,6 +472,7 @@ __global__ void cgls_resid_scalar_kernel(DevState* st, DevHistory h, const doubl
 template <bool VEC2>
 __global__ void cgls_p_update_kernel(DevState* st, double* p, const double* s, double* s_prev,
                                      size_t nn, double* part) {
+  pdl_wait();
   if (stopped(st)) return;
   __shared__ double red[VEC_THREADS / 32][1];
   const double beta = st->beta;
@@ -487,6 +505,7 @@ __global__ void cgls_p_update_kernel(DevState* st, double* p, const double* s, d
   }
 }
 __global__ void cgls_next_kernel(DevState* st) {
+  pdl_wait();
   if (stopped(st) || threadIdx.x) return;
   st->k++;
 }
@@ -500,6 +519,7 @@ template <int LC, int KIND>
 __global__ void spectral_sums_kernel(const double* s_r, const double* s_c, const double* bhat,
                                      const double* xhat, int n, const double* lambdas, int m,
                                      double omega, double* part) {
+  pdl_wait();
   __shared__ double red[VEC_THREADS / 32][2 * LC];
   const size_t nn = size_t(n) * n;
   const unsigned un = unsigned(n);
@@ -555,6 +575,7 @@ __global__ void spectral_sums_kernel(const double* s_r, const double* s_c, const
 // (regparam.cpp:329-349).
 __global__ void spectral_filter_kernel(const double* s_r, const double* s_c, int n, double l2,
                                        double* c) {
+  pdl_wait();
   const size_t nn = size_t(n) * n;
   const unsigned un = unsigned(n);
   for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < nn;
@@ -569,6 +590,7 @@ __global__ void spectral_filter_kernel(const double* s_r, const double* s_c, int
 // out[q*width + j] = sum over ctas of part[(q*ctas + cta)*width + j]; one
 // block per q, fixed-order strided partial sums + tree (deterministic).
 __global__ void finish_sums_kernel(const double* part, int ctas, int width, int m, double* out) {
+  pdl_wait();
   __shared__ double red[VEC_THREADS / 32][1];
   const int q = blockIdx.x;
   if (q >= m) return;
@@ -594,7 +616,7 @@ unsigned vec_grid(size_t nn) {
 #define KP_LAUNCH(cls, kernel, grid, block, ...)                   \
   do {                                                             \
     LaunchScope scope_(cls);                                       \
-    kernel<<<(grid), (block), 0, ctx().stream>>>(__VA_ARGS__);     \
+    launch_pdl(kernel, dim3(grid), dim3(block), 0, __VA_ARGS__);   \
     check_launch(#kernel);                                         \
   } while (0)
 
