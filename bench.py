@@ -259,7 +259,8 @@ def run_c4(args):
     launches = L.kp_launch_count() - launches0
     elapsed, solved = reduce_timing(elapsed, float(len(results)), dist,
                                     device="cuda" if args.dist_backend == "nccl" else "cpu")
-    allres = gather_results(results, dist)
+    allres = gather_results(results, dist,
+                            device="cuda" if (dist and args.dist_backend == "nccl") else None)
     if rank == 0:
         its = [r["iterations"] for r in allres]
         metric = METRIC_C4 if sh.n == 1024 else METRIC_C4.replace("1024^2", f"{sh.n}^2")
@@ -529,7 +530,8 @@ def main():
         elapsed, iters = reduce_timing(elapsed, float(iters), dist, device=dev)
         e2e_elapsed, e2e_iters = reduce_timing(e2e_elapsed, float(e2e_iters), dist, device=dev)
         iters, e2e_iters = int(iters), int(e2e_iters)
-        per_rank = gather_results([{"image": rank, "rel_err": rel_last}], dist)
+        per_rank = gather_results([{"image": rank, "rel_err": rel_last}], dist, device=dev,
+                                  fields=("image", "rel_err"))
 
     if not dist:
         per_rank = None

@@ -33,14 +33,52 @@ class ImageResult:
     no_root: bool = False
 
 
-def gather_results(local: list, dist=None) -> list:
-    """All ranks' results, sorted by image (all_gather_object)."""
+RESULT_FIELDS = ("image", "noise_level", "lam", "iterations", "converged", "rel_err", "no_root")
+_INT_FIELDS = {"image", "iterations"}
+_BOOL_FIELDS = {"converged", "no_root"}
+
+
+def gather_results(local: list, dist=None, device=None, fields=RESULT_FIELDS) -> list:
+    """All ranks' results, sorted by image. The numeric fields travel as one
+    float64 tensor per rank (dist.all_gather: ncclAllGather on the NCCL
+    backend, `device` = "cuda"); abort-reason strings, when any rank has one,
+    follow in a small object gather."""
     items = [asdict(r) if isinstance(r, ImageResult) else dict(r) for r in local]
     if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
         return sorted(items, key=lambda d: d["image"])
-    bucket = [None] * dist.get_world_size()
-    dist.all_gather_object(bucket, items)
-    return sorted((d for part in bucket for d in part), key=lambda d: d["image"])
+    import torch
+    world = dist.get_world_size()
+    cnt = torch.tensor([len(items)], dtype=torch.int64, device=device)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(counts, cnt)
+    counts = [int(c.item()) for c in counts]
+    rows = max(1, max(counts))
+    buf = torch.full((rows, len(fields)), float("nan"), dtype=torch.float64)
+    for i, d in enumerate(items):
+        buf[i] = torch.tensor([float(d[f]) for f in fields], dtype=torch.float64)
+    buf = buf.to(device) if device else buf
+    bufs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(bufs, buf)
+    has_reason = torch.tensor([int(any(d.get("abort_reason") for d in items))], device=device)
+    dist.all_reduce(has_reason, op=dist.ReduceOp.MAX)
+    reasons = {}
+    if has_reason.item():
+        objs = [None] * world
+        dist.all_gather_object(objs, {d["image"]: d["abort_reason"] for d in items
+                                      if d.get("abort_reason")})
+        for o in objs:
+            reasons.update(o)
+    out = []
+    for r, b in enumerate(bufs):
+        for row in b[:counts[r]].cpu().tolist():
+            d = {}
+            for f, v in zip(fields, row):
+                d[f] = int(v) if f in _INT_FIELDS else bool(v) if f in _BOOL_FIELDS else v
+            if "image" in d and "abort_reason" in ImageResult.__dataclass_fields__ and \
+                    fields is RESULT_FIELDS:
+                d["abort_reason"] = reasons.get(d["image"], "")
+            out.append(d)
+    return sorted(out, key=lambda d: d["image"])
 
 
 def reduce_timing(elapsed_s: float, units: float, dist=None, device=None) -> tuple[float, float]:

@@ -32,11 +32,18 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    mine = [ImageResult(i, [0.001, 0.01, 0.05][i % 3], 0.01 * (i + 1), 10 + i, True, 0.1)
+    mine = [ImageResult(i, [0.001, 0.01, 0.05][i % 3], 0.01 * (i + 1), 10 + i, i % 5 != 0,
+                        0.1 + i / 1000, "curvature breakdown at iteration 3" if i == 40 else "",
+                        i == 63)
             for i in shard(64, world, rank)]
     allres = gather_results(mine, dist)
     elapsed, units = reduce_timing(1.0 + rank, float(len(mine)), dist)
-    q.put((rank, [d["image"] for d in allres], elapsed, units))
+    ok = all(d["lam"] == 0.01 * (d["image"] + 1) and d["iterations"] == 10 + d["image"]
+             and d["converged"] == (d["image"] % 5 != 0) and d["rel_err"] == 0.1 + d["image"] / 1000
+             and d["no_root"] == (d["image"] == 63)
+             and d["abort_reason"] == ("curvature breakdown at iteration 3" if d["image"] == 40 else "")
+             for d in allres)
+    q.put((rank, [d["image"] for d in allres], elapsed, units, ok))
     dist.destroy_process_group()
 
 
@@ -53,8 +60,9 @@ def test_gather_and_reduce_world2():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, images, elapsed, units in out:
+    for rank, images, elapsed, units, ok in out:
         assert images == list(range(64))  # every rank sees the full, ordered batch
+        assert ok  # every field survives the tensor gather
         assert elapsed == 2.0  # max over ranks
         assert units == 64.0  # sum over ranks
 
