@@ -37,7 +37,24 @@ inline void check(int status) {
 
 // PrecisionFormat presets (precision.cpp:45-48)
 inline kp_format fp16() { return {11, 15, 1}; }
+inline kp_format bfloat16() { return {8, 127, 1}; }
+inline kp_format fp32() { return {24, 127, 1}; }
 inline kp_format fp64() { return {53, 1023, 1}; }
+
+// round_array (precision.cpp:82-95)
+inline Vec round_array(const Vec& a, kp_format fmt) {
+  Vec out(a.size());
+  check(kp_round_array(a.data(), long(a.size()), fmt, out.data()));
+  return out;
+}
+// lp_matmul (lpblas.cpp:59-70): a m x k, b k x n, column-major
+inline Vec lp_matmul(const Vec& a, const Vec& b, int m, int k, int n, kp_format fmt) {
+  if (a.size() != size_t(m) * k || b.size() != size_t(k) * n)
+    throw std::invalid_argument("lp_matmul: shape mismatch");
+  Vec c(size_t(m) * n);
+  check(kp_lp_matmul(m, k, n, a.data(), b.data(), fmt, c.data()));
+  return c;
+}
 
 // KronTerm / KroneckerSum (kron.hpp:12-22): factors are n*n column-major.
 struct KronTerm {

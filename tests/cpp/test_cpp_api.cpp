@@ -47,6 +47,19 @@ int main() {
   SolveResult rp = pcg(A, b, mx, po);
   CHECK(rp.history.converged && rp.history.iterations_used == 1);
 
+  // emulated low-precision BLAS (test_lpblas.cpp pins)
+  CHECK(round_array(Vec{1.0 + 1.0 / 4096}, fp16())[0] == 1.0);
+  const Vec c = lp_matmul(Vec{1, 3, 2, 4}, Vec{5, 7, 6, 8}, 2, 2, 2, fp16());  // [[1,2],[3,4]] x [[5,6],[7,8]]
+  CHECK(c[0] == 19 && c[1] == 43 && c[2] == 22 && c[3] == 50);
+  CHECK(lp_matmul(Vec{2048, 1, 1, 1}, Vec{1, 1, 1, 1}, 1, 4, 1, fp16())[0] == 2050.0);
+
+  // optimal lambda and the filtered solution (regparam.cpp:248-252, 329-349)
+  SpectralData sdx = make_spectral_data(mx, b, b);
+  const kp_param_choice opt = lambda_opt(sdx);
+  CHECK(opt.lambda > 0.0 && std::isfinite(opt.objective_value));
+  const Vec xf = filtered_solution(mx, b, 0.05);
+  CHECK(xf.size() == b.size() && std::isfinite(xf[0]));
+
   // errors surface as the reference's exception types
   bool threw = false;
   try { build_preconditioner(eye(2), eye(2), 2, -1.0, fp64()); } catch (const std::invalid_argument&) { threw = true; }
