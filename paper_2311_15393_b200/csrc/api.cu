@@ -401,8 +401,7 @@ void detect_banded(kp_operator* op, const double* rows, const double* cols) {
 int msolve_partials_ctas(const kp_precond* p) {
   if (is_generic(p->fmt)) return LP_PART_CTAS;
   if (covers_double(p->fmt)) return gemm_f64_num_ctas(p->n, p->n);
-  return p->accum == KP_ACCUM_TENSOR ? gemm_f16tc_num_ctas(p->n, p->n)
-                                     : gemm_f16ref_num_ctas(p->n, p->n);
+  return p->accum == KP_ACCUM_TENSOR ? VEC_CTAS : gemm_f16ref_num_ctas(p->n, p->n);
 }
 
 void ensure_ws(kp_precond* p) {
@@ -506,6 +505,14 @@ void msolve(kp_precond* p, const double* r, double* z, const double* d0, const d
   }
   gemm(g, KC_PRECOND);
   g.A = {p->t3h.p, ldh}, g.B = {sh->vrt_b.p, ldh};  // z = lp(t3 V_r^T)
+  if (p->accum == KP_ACCUM_TENSOR) {
+    // binary16 z into t1h (free once the second product has consumed it),
+    // then one HBM pass widens it and forms the dot partials
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = 1, g.epi.cn = ldh;
+    gemm(g, KC_PRECOND);
+    msolve_finish_f16(p->t1h.p, ldh, n, z, d0, d1a, d1b, p->part.p, status);
+    return;
+  }
   g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z, g.epi.cm = 1, g.epi.cn = n;
   g.epi.vm = 1, g.epi.vn = n, g.epi.d0 = d0, g.epi.d1a = d1a, g.epi.d1b = d1b;
   g.epi.partials = p->part.p;

@@ -355,9 +355,10 @@ void launch_tc(const F16GemmArgs& a) {
 }
 
 // Tile width: BN = 256 for the binary16-output products (half the A traffic
-// per flop: 97.6 vs 131.5 us per n = 4096 product), BN = 128 for the FP64
-// output + dot-partials product, whose epilogue is memory bound and needs the
-// finer tiles to overlap it with the MMAs (229.5 vs 261.8 us).
+// per flop: 97.6 vs 131.5 us per n = 4096 product), BN = 128 for FP64 output
+// (lp_matmul's FP64 result), whose epilogue is memory bound and needs the
+// finer tiles to overlap it with the MMAs. The M-solve's last product stores
+// binary16 z and leaves widening + dots to msolve_finish_f16 (vec.cu).
 // KP_F16TC_BN = 128 | 256 forces one width for all products.
 int tc_bn(int mode) {
   static int forced = [] {

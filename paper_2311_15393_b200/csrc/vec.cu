@@ -97,6 +97,64 @@ __global__ void cast_f16_kernel(const double* src, __half* dst, int rows, int co
   }
 }
 
+// Tensor-mode M-solve tail: the last tcgen05 product stores binary16 z
+// (one rounding, as its FP64 epilogue did); this pass widens it to FP64 and
+// forms the dot partials pcg_beta needs, at HBM speed instead of inside the
+// GEMM's epilogue. Pairs of rows (half2 -> double2) when VEC2.
+template <bool VEC2>
+__global__ void msolve_finish_f16_kernel(const __half* z16, long ldh, int n, double* z,
+                                         const double* d0, const double* d1a, const double* d1b,
+                                         double* part, const int* status) {
+  pdl_wait();
+  if (status && *status) return;
+  __shared__ double red[VEC_THREADS / 32][3];
+  const unsigned un = unsigned(n);
+  const size_t nn = size_t(n) * n;
+  const bool same = d0 && d1a == d0;
+  double v[3] = {0.0, 0.0, 0.0};
+  if (VEC2) {
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < nn / 2;
+         k += size_t(gridDim.x) * blockDim.x) {
+      const unsigned i = unsigned(2 * k), l = i / un, row = i - l * un;
+      const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(z16 + size_t(l) * ldh + row));
+      const double2 zi = make_double2(double(hf.x), double(hf.y));
+      reinterpret_cast<double2*>(z)[k] = zi;
+      double2 a0 = make_double2(0.0, 0.0);
+      if (d0) {
+        a0 = reinterpret_cast<const double2*>(d0)[k];
+        v[0] += zi.x * a0.x;
+        v[0] += zi.y * a0.y;
+      }
+      if (d1a) {
+        double2 a1 = same ? a0 : reinterpret_cast<const double2*>(d1a)[k];
+        if (d1b) {
+          const double2 b1 = reinterpret_cast<const double2*>(d1b)[k];
+          a1.x -= b1.x, a1.y -= b1.y;
+        }
+        v[1] += zi.x * a1.x;
+        v[1] += zi.y * a1.y;
+      }
+      if (!isfinite(zi.x)) v[2] += 1.0;
+      if (!isfinite(zi.y)) v[2] += 1.0;
+    }
+  } else {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nn;
+         i += size_t(gridDim.x) * blockDim.x) {
+      const unsigned l = unsigned(i) / un, row = unsigned(i) - l * un;
+      const double zi = double(__half2float(z16[size_t(l) * ldh + row]));
+      z[i] = zi;
+      if (d0) v[0] += zi * d0[i];
+      if (d1a) v[1] += zi * (d1b ? d1a[i] - d1b[i] : d1a[i]);
+      if (!isfinite(zi)) v[2] += 1.0;
+    }
+  }
+  block_sum<3>(v, red);
+  if (threadIdx.x == 0) {
+    double* o = part + size_t(blockIdx.x) * 4;
+    o[0] = v[0], o[1] = v[1], o[2] = v[2], o[3] = 0.0;
+  }
+}
+
 // S(i,j) = 1 / ((s_r(j) s_c(i))^2 + lambda^2) at j*n + i (factor.cpp:62-76),
 // unfused IEEE operations so it equals the host formula bit for bit; stored
 // as FP64 or rounded once to binary16 (round_array of the FP64 weights).
@@ -640,6 +698,20 @@ void cast_f64_to_f16_padded(const double* src, __half* dst, int rows, int cols, 
             rows, cols, ld_src, ld_dst, status);
 }
 
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+void msolve_finish_f16(const __half* z16, long ldh, int n, double* z, const double* d0,
+                       const double* d1a, const double* d1b, double* partials,
+                       const int* status) {
+  const bool vec2 = n % 2 == 0 && ldh % 2 == 0 && al16(z) && al16(d0) && al16(d1a) && al16(d1b);
+  if (vec2)
+    KP_LAUNCH(KC_VECTOR, msolve_finish_f16_kernel<true>, VEC_CTAS, VEC_THREADS, z16, ldh, n, z, d0,
+              d1a, d1b, partials, status);
+  else
+    KP_LAUNCH(KC_VECTOR, msolve_finish_f16_kernel<false>, VEC_CTAS, VEC_THREADS, z16, ldh, n, z,
+              d0, d1a, d1b, partials, status);
+}
+
 void pcg_init_scalar(DevState* st, DevHistory h, const double* part_r, int nr,
                      const double* part_xt, int nxt) {
   KP_LAUNCH(KC_VECTOR, pcg_init_scalar_kernel, 1, SCALAR_THREADS, st, h, part_r, nr, part_xt, nxt);
@@ -650,7 +722,6 @@ void pcg_init_msolve_scalar(DevState* st, const double* part_z, int nz) {
 void pcg_alpha_scalar(DevState* st, const double* part_pq, int n) {
   KP_LAUNCH(KC_VECTOR, pcg_alpha_scalar_kernel, 1, SCALAR_THREADS, st, part_pq, n);
 }
-static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 void pcg_update(DevState* st, DevHistory h, double* x, double* r, double* r_prev, const double* p,
                 const double* q, const double* z, const double* xt, __half* r16, int n, long ldh,

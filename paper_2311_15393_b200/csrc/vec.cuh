@@ -67,6 +67,13 @@ void cast_f64_to_f16_padded(const double* src, __half* dst, int rows, int cols, 
 void precond_weights(const double* s_r, const double* s_c, int n, double l2, double* s64,
                      __half* s16);
 
+// Last step of the tensor-mode M-solve: z[l*n + i] = double(z16[l*ldh + i])
+// (exact) with the M-solve dot partials over the fixed VEC_CTAS grid:
+// [0] z.d0, [1] z.(d1a - d1b) (d1b optional), [2] #non-finite z.
+void msolve_finish_f16(const __half* z16, long ldh, int n, double* z, const double* d0,
+                       const double* d1a, const double* d1b, double* partials,
+                       const int* status);
+
 // ---- PCG -------------------------------------------------------------------
 // init after r = A^T b (partials_r: [ctas] of ||r||^2) and xnorm partials.
 void pcg_init_scalar(DevState* st, DevHistory h, const double* part_r, int nr,
