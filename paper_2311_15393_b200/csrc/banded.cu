@@ -19,6 +19,8 @@
 // lanes walking different columns never share a bank.
 #include "banded.cuh"
 
+#include <cstdlib>
+
 namespace kp {
 namespace {
 
@@ -80,35 +82,121 @@ __device__ __forceinline__ void corr8_tail(double (&acc)[8], const double* w, in
   }
 }
 
-__global__ void __launch_bounds__(A_THREADS) band_cols_kernel(const double* __restrict__ X,
+// Compile-time tap count: fully unrolled, exact taps (no zero padding), the
+// 8-value window kept as a register ring (src(i) in slot i % 8, refilled
+// right after its last use), weights as constant-bank DFMA operands.
+// Reads src(0 .. TAPS + 6).
+template <int TAPS, typename Src>
+__device__ __forceinline__ void corr8_fixed(double (&acc)[8], const double* w, Src src) {
+  double ring[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) ring[v] = src(v);
+#pragma unroll
+  for (int u = 0; u < TAPS; ++u) {
+    const double wv = w[u];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = fma(wv, ring[(u + q) & 7], acc[q]);
+    if (u + 8 <= TAPS + 6) ring[u & 7] = src(u + 8);
+  }
+}
+
+// Compile-time tap count with the register footprint of corr8 (pass A keeps
+// 4 CTAs per SM; the fully unrolled form hoists every load and drops to 2):
+// runtime loop over the full 8-tap blocks, then the TAPS % 8 remaining taps
+// unrolled with compile-time window indices. Reads src(0 .. TAPS + 6).
+template <int TAPS, typename Src>
+__device__ __forceinline__ void corr8_blocks(double (&acc)[8], const double* w, Src src) {
+  constexpr int FULL = TAPS & ~7, TAIL = TAPS & 7;
+  double x[16];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) x[v] = src(v);
+#pragma unroll 1
+  for (int u0 = 0; u0 < FULL; u0 += 8) {
+#pragma unroll
+    for (int v = 0; v < 8; ++v) x[8 + v] = src(u0 + 8 + v);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const double wv = w[u0 + v];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = fma(wv, x[q + v], acc[q]);
+    }
+#pragma unroll
+    for (int v = 0; v < 8; ++v) x[v] = x[8 + v];
+  }
+  if constexpr (TAIL > 0) {
+#pragma unroll
+    for (int v = 0; v + 1 < TAIL; ++v) x[8 + v] = src(FULL + 8 + v);
+#pragma unroll
+    for (int v = 0; v < TAIL; ++v) {
+      const double wv = w[FULL + v];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = fma(wv, x[q + v], acc[q]);
+    }
+  }
+}
+
+// TAPS > 0: kernels specialised for that exact tap count (the BASELINE PSF
+// supports); TAPS == 0: runtime tap count, padded to a multiple of 8.
+template <int TAPS>
+__host__ __device__ constexpr int cols_stride(int padded_taps) {
+  return (A_TA + (TAPS > 0 ? TAPS - 1 : padded_taps)) | 1;  // odd; generic keeps corr8's slack
+}
+template <int TAPS>
+__host__ __device__ constexpr int rows_halo(int padded_taps) {
+  return TAPS > 0 ? B_TJ + TAPS - 1 : B_TJ + padded_taps;  // generic: +1 row corr8 slack
+}
+
+#ifndef KP_BAND_A_STAGED
+#define KP_BAND_A_STAGED 1
+#endif
+constexpr int A_SO = A_TA + 2;  // staged output tile stride: 16-byte aligned, conflict-free 128-bit accesses
+#ifndef KP_BAND_A_MINB
+#define KP_BAND_A_MINB 4
+#endif
+template <int TAPS>
+__global__ void __launch_bounds__(A_THREADS, KP_BAND_A_MINB) band_cols_kernel(const double* __restrict__ X,
                                                               double* __restrict__ Y, int n, int r,
                                                               const __grid_constant__ BandTaps t,
                                                               const int* status) {
   pdl_wait();
   if (stopped(status)) return;
   extern __shared__ double sm[];
-  const int S = (A_TA + t.taps) | 1;  // odd column stride; >= A_TA + taps (corr8 prefetch slack)
-  double* Xs = sm;                    // [A_TL][S]
+  const int S = cols_stride<TAPS>(t.taps);  // odd column stride (no bank sharing across lanes)
+  double* Xs = sm;                          // [A_TL][S]
   const int a0 = blockIdx.y * A_TA, l0 = blockIdx.x * A_TL;
   for (int idx = threadIdx.x; idx < A_TL * S; idx += A_THREADS) {
     const int c = idx / S, v = idx % S;
     const int l = l0 + c, i = a0 + t.shift + v;
-    Xs[idx] = (l < n && i >= 0 && i < n && v < A_TA + t.taps - 1) ? X[size_t(l) * n + i] : 0.0;
+    Xs[idx] = (l < n && i >= 0 && i < n && v < A_TA + (TAPS > 0 ? TAPS : t.taps) - 1) ? X[size_t(l) * n + i] : 0.0;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t nn = size_t(n) * n;
   const int l = l0 + lane;
   const bool vec = (n & 1) == 0;
+#if KP_BAND_A_STAGED
+  // Each thread's 8 outputs are 8 rows of one column (lanes = 32 columns), so
+  // storing them straight from registers touches 32 lines per instruction.
+  // Instead the Y_k tile goes through shared memory ([A_TL][A_SO]) and each
+  // warp stores whole 512-byte column runs.
+  double* Ys = Xs + A_TL * S;
+#endif
   for (int k = 0; k < r; ++k) {
-    double* Yk = Y + k * nn + size_t(l) * n;
 #pragma unroll
     for (int h = 0; h < A_TA / 8 / (A_THREADS / 32); ++h) {
       const int b = warp + h * (A_THREADS / 32);  // 8-row block
       double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       const double* base = Xs + lane * S + 8 * b;
-      corr8(acc, t.w[k], t.taps, [&](int i) { return base[i]; });
-      // straight from registers: 8 consecutive rows of column l (64 contiguous bytes)
+      if constexpr (TAPS > 0)
+        corr8_blocks<TAPS>(acc, t.w[k], [&](int i) { return base[i]; });
+      else
+        corr8(acc, t.w[k], t.taps, [&](int i) { return base[i]; });
+#if KP_BAND_A_STAGED
+#pragma unroll
+      for (int q = 0; q < 8; q += 2)
+        *reinterpret_cast<double2*>(Ys + lane * A_SO + 8 * b + q) = make_double2(acc[q], acc[q + 1]);
+#else
+      double* Yk = Y + k * nn + size_t(l) * n;
       const int a = a0 + 8 * b;
       if (l < n) {
         if (vec && a + 8 <= n) {
@@ -121,7 +209,30 @@ __global__ void __launch_bounds__(A_THREADS) band_cols_kernel(const double* __re
             if (a + q < n) Yk[a + q] = acc[q];
         }
       }
+#endif
     }
+#if KP_BAND_A_STAGED
+    __syncthreads();
+    double* Yk = Y + k * nn;
+    if (vec) {  // a warp stores one column: 32 lanes x 2 rows
+#pragma unroll
+      for (int it = 0; it < A_TL * A_TA / 2 / A_THREADS; ++it) {
+        const int idx = threadIdx.x + it * A_THREADS;
+        const int c = idx / (A_TA / 2), pr = 2 * (idx % (A_TA / 2));
+        const int lc = l0 + c, a = a0 + pr;
+        if (lc < n && a < n)
+          *reinterpret_cast<double2*>(Yk + size_t(lc) * n + a) =
+              *reinterpret_cast<const double2*>(Ys + c * A_SO + pr);
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < A_TL * A_TA; idx += A_THREADS) {
+        const int c = idx / A_TA, rr = idx % A_TA;
+        const int lc = l0 + c, a = a0 + rr;
+        if (lc < n && a < n) Yk[size_t(lc) * n + a] = Ys[c * A_SO + rr];
+      }
+    }
+    __syncthreads();  // Ys is rewritten by the next term
+#endif
   }
 }
 
@@ -137,6 +248,7 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool v
 // Pass B. The Y_k tiles (B_TJ + taps - 1 columns of B_TA rows) are
 // double-buffered with cp.async so term k+1 streams in while term k's
 // correlation runs.
+template <int TAPS>
 __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __restrict__ Y, int n,
                                                               int r, const __grid_constant__ BandTaps t,
                                                               const F64Epilogue e,
@@ -144,8 +256,8 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
   pdl_wait();
   if (stopped(status)) return;
   extern __shared__ double sm[];
-  const int rows = B_TJ + t.taps - 1;
-  const int buf_doubles = (rows + 1) * B_TA;  // +1 row: corr8 prefetch slack
+  const int rows = (TAPS > 0 ? TAPS : t.taps) + B_TJ - 1;  // rows loaded
+  const int buf_doubles = rows_halo<TAPS>(t.taps) * B_TA;
   const int a0 = blockIdx.y * B_TA, j0 = blockIdx.x * B_TJ;
   const int a = threadIdx.x % B_TA, jq = threadIdx.x / B_TA;  // jq in [0, 8): 8-column block
   const size_t nn = size_t(n) * n;
@@ -185,7 +297,10 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
     __syncthreads();
     const double* Ys = sm + (k & 1) * buf_doubles;
     const double* base = Ys + (8 * jq) * B_TA + a;
-    corr8_tail(acc, t.w[k], t.real, [&](int i) { return base[i * B_TA]; });
+    if constexpr (TAPS > 0)
+      corr8_fixed<TAPS>(acc, t.w[k], [&](int i) { return base[i * B_TA]; });
+    else
+      corr8_tail(acc, t.w[k], t.real, [&](int i) { return base[i * B_TA]; });
     __syncthreads();  // buffer (k & 1) is refilled at iteration k + 1
   }
   // epilogue (same contract as the GEMM epilogue)
@@ -226,15 +341,54 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
   }
 }
 
+// Tap counts with specialised kernels (the BASELINE PSFs: 41 (C5), 31
+// (C2/C3), 19 (C1), 17 (C4)); any other count runs the generic kernels.
+template <template <int> class F, typename... Args>
+void by_taps(int real, Args&&... args) {
+  switch (real) {
+    case 17: F<17>::run(args...); break;
+    case 19: F<19>::run(args...); break;
+    case 31: F<31>::run(args...); break;
+    case 41: F<41>::run(args...); break;
+    default: F<0>::run(args...); break;
+  }
+}
+
+template <int TAPS>
+struct ColsLaunch {
+  static void run(const double* X, double* Y, int n, int r, const BandTaps& t, const int* status) {
+    const size_t smem = size_t(A_TL) * (cols_stride<TAPS>(t.taps) + (KP_BAND_A_STAGED ? A_SO : 0)) * sizeof(double);
+    auto k = band_cols_kernel<TAPS>;
+    set_smem_limit(reinterpret_cast<const void*>(k), smem);
+    dim3 grid(cdiv(n, A_TL), cdiv(n, A_TA));
+    launch_pdl(k, grid, dim3(A_THREADS), smem, X, Y, n, r, t, status);
+  }
+};
+template <int TAPS>
+struct RowsLaunch {
+  static void run(const double* Y, int n, int r, const BandTaps& t, const F64Epilogue& e,
+                  const int* status) {
+    const size_t smem = 2 * size_t(rows_halo<TAPS>(t.taps)) * B_TA * sizeof(double);  // two buffers
+    auto k = band_rows_kernel<TAPS>;
+    set_smem_limit(reinterpret_cast<const void*>(k), smem);
+    dim3 grid(cdiv(n, B_TJ), cdiv(n, B_TA));
+    launch_pdl(k, grid, dim3(B_THREADS), smem, Y, n, r, t, e, status);
+  }
+};
+
+bool generic_only() {
+  static const bool g = [] {
+    const char* e = getenv("KP_BAND_GENERIC");
+    return e && atoi(e) != 0;
+  }();
+  return g;
+}
+
 }  // namespace
 
 void band_cols(const double* X, double* Y, int n, int r, const BandTaps& t, const int* status) {
-  const int S = (A_TA + t.taps) | 1;
-  const size_t smem = size_t(A_TL) * S * sizeof(double);
-  set_smem_limit(reinterpret_cast<const void*>(band_cols_kernel), smem);
   LaunchScope scope(KC_OPERATOR);
-  dim3 grid(cdiv(n, A_TL), cdiv(n, A_TA));
-  launch_pdl(band_cols_kernel, grid, dim3(A_THREADS), smem, X, Y, n, r, t, status);
+  by_taps<ColsLaunch>(generic_only() ? 0 : t.real, X, Y, n, r, t, status);
   check_launch("band_cols");
 }
 
@@ -242,12 +396,8 @@ int band_rows_num_ctas(int n) { return int(cdiv(n, B_TJ) * cdiv(n, B_TA)); }
 
 void band_rows(const double* Y, int n, int r, const BandTaps& t, const F64Epilogue& e,
                const int* status) {
-  // two buffers; +1 row each: corr8 prefetches one value past the taps
-  const size_t smem = 2 * size_t(B_TJ + t.taps) * B_TA * sizeof(double);
-  set_smem_limit(reinterpret_cast<const void*>(band_rows_kernel), smem);
   LaunchScope scope(KC_OPERATOR);
-  dim3 grid(cdiv(n, B_TJ), cdiv(n, B_TA));
-  launch_pdl(band_rows_kernel, grid, dim3(B_THREADS), smem, Y, n, r, t, e, status);
+  by_taps<RowsLaunch>(generic_only() ? 0 : t.real, Y, n, r, t, e, status);
   check_launch("band_rows");
 }
 
