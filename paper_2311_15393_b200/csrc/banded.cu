@@ -82,6 +82,15 @@ __device__ __forceinline__ void corr8_tail(double (&acc)[8], const double* w, in
   }
 }
 
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0));
+}
+
 // Compile-time tap count: fully unrolled, exact taps (no zero padding), the
 // 8-value window kept as a register ring (src(i) in slot i % 8, refilled
 // right after its last use), weights as constant-bank DFMA operands.
@@ -164,10 +173,21 @@ __global__ void __launch_bounds__(A_THREADS, KP_BAND_A_MINB) band_cols_kernel(co
   const int S = cols_stride<TAPS>(t.taps);  // odd column stride (no bank sharing across lanes)
   double* Xs = sm;                          // [A_TL][S]
   const int a0 = blockIdx.y * A_TA, l0 = blockIdx.x * A_TL;
-  for (int idx = threadIdx.x; idx < A_TL * S; idx += A_THREADS) {
-    const int c = idx / S, v = idx % S;
-    const int l = l0 + c, i = a0 + t.shift + v;
-    Xs[idx] = (l < n && i >= 0 && i < n && v < A_TA + (TAPS > 0 ? TAPS : t.taps) - 1) ? X[size_t(l) * n + i] : 0.0;
+  {  // halo tile: warp w copies columns w, w + 8, ..; lanes walk the rows (coalesced)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int vmax = A_TA + (TAPS > 0 ? TAPS : t.taps) - 1;  // rows with data, zeros beyond
+    const uint32_t xs = static_cast<uint32_t>(__cvta_generic_to_shared(Xs));
+    for (int c = warp; c < A_TL; c += A_THREADS / 32) {
+      const int l = l0 + c;
+      const double* col = X + size_t(l) * n;  // dereferenced only when l < n
+      for (int v = lane; v < S; v += 32) {
+        const int i = a0 + t.shift + v;
+        const bool ok = l < n && v < vmax && i >= 0 && i < n;
+        cp_async8(xs + uint32_t(c * S + v) * 8u, ok ? col + i : X, ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -236,15 +256,6 @@ __global__ void __launch_bounds__(A_THREADS, KP_BAND_A_MINB) band_cols_kernel(co
   }
 }
 
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src),
-               "r"(valid ? 8 : 0));
-}
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
-               "r"(valid ? 16 : 0));
-}
-
 // Pass B. The Y_k tiles (B_TJ + taps - 1 columns of B_TA rows) are
 // double-buffered with cp.async so term k+1 streams in while term k's
 // correlation runs.
@@ -263,15 +274,35 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
   const size_t nn = size_t(n) * n;
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
   const bool vec = (n & 1) == 0;  // 16-byte copies (pairs of rows) when n is even
+  // Copy plan of the 16-byte path, computed once: thread -> row pair aa,
+  // tile columns jw0 + 16 it (it < PLAN); per term only the base moves.
+  constexpr int PAIRS = B_TA / 2, STEP = B_THREADS / PAIRS;
+  constexpr int PLAN = (B_TJ + (TAPS > 0 ? TAPS - 1 : BAND_MAX_TAPS) + STEP - 1) / STEP;
+  static_assert(B_THREADS % PAIRS == 0, "copy plan");
+  const int aa = 2 * (threadIdx.x % PAIRS), jw0 = threadIdx.x / PAIRS;
+  uint32_t in_tile = 0, in_range = 0;
+#pragma unroll
+  for (int it = 0; it < PLAN; ++it) {
+    const int jw = jw0 + STEP * it, j = j0 + t.shift + jw;
+    if (jw < rows) in_tile |= 1u << it;
+    if (jw < rows && j >= 0 && j < n && a0 + aa < n) in_range |= 1u << it;
+  }
+  const long goff0 = (long(j0 + t.shift + jw0) * n + a0 + aa) * long(sizeof(double));
+  const long gstep = long(STEP) * n * long(sizeof(double));
+  const uint32_t soff0 = uint32_t(jw0 * B_TA + aa) * 8u;
   auto load = [&](int k, int buf) {
     const double* Yk = Y + k * nn;
     const uint32_t dst0 = sbase + uint32_t(buf * buf_doubles) * 8u;
     if (vec) {
-      for (int idx = threadIdx.x; idx < rows * (B_TA / 2); idx += B_THREADS) {
-        const int jw = idx / (B_TA / 2), aa = 2 * (idx % (B_TA / 2));
-        const int j = j0 + t.shift + jw, ai = a0 + aa;
-        const bool v = j >= 0 && j < n && ai < n;
-        cp_async16(dst0 + uint32_t(jw * B_TA + aa) * 8u, v ? Yk + size_t(j) * n + ai : Y, v);
+      const char* g = reinterpret_cast<const char*>(Yk) + goff0;  // tile column jw0 (may be outside Y)
+      const uint32_t d = dst0 + soff0;
+#pragma unroll
+      for (int it = 0; it < PLAN; ++it) {
+        if (in_tile & (1u << it)) {
+          const bool v = in_range & (1u << it);
+          const char* src = g + it * gstep;
+          cp_async16(d + uint32_t(it * STEP * B_TA * 8), v ? src : reinterpret_cast<const char*>(Y), v);
+        }
       }
     } else {
       for (int idx = threadIdx.x; idx < rows * B_TA; idx += B_THREADS) {

@@ -494,6 +494,22 @@ def test_banded_operator_matches_dense_and_oracle(kind, n, rank):
     assert np.linalg.norm(K.kronsum_apply(a, y) - dense) <= 1e-13 * np.linalg.norm(dense)
 
 
+@pytest.mark.parametrize("n_p", [17, 19, 23, 31, 41])
+@pytest.mark.parametrize("n", [97, 130])
+def test_banded_tap_specialisations_match_oracle(n_p, n):
+    """The BASELINE tap counts (17/19/31/41) run kernels specialised for that
+    count, 23 the generic ones; odd n takes the scalar load/store paths."""
+    psf = P.make_psf("gaussian", n_p, sigma=n_p / 6.0)
+    a, _ = P.psf_to_kronsum(psf, n, truncation_tol=0.0, max_rank=3)
+    mode, tc, tr = a.mode()
+    assert mode == "banded" and tc == n_p and tr == n_p
+    y = np.random.default_rng(n_p).standard_normal(n * n)
+    for g, o in ((K.kronsum_apply, O.kronsum_apply),
+                 (K.kronsum_apply_transpose, O.kronsum_apply_transpose)):
+        want = o(a, y)
+        assert np.linalg.norm(g(a, y) - want) <= 1e-13 * np.linalg.norm(want)
+
+
 def test_config_psfs_are_banded():
     for name, taps in (("C1", 19), ("C2", 31), ("C4", 17), ("C5", 41)):
         cfg = configs_small(name)
