@@ -41,10 +41,10 @@ BF16_PEAK_TFLOPS = 1653.4  # MEASURED_PEAKS.json bf16_tflops (burst; fp16 kind::
 # DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the
 # committed ncu --set full captures (profiles/r01_ncu_key_metrics.txt)
 TRAFFIC = {
-    ("gemm_f16ref_kernel", 4096): 68.37e6 + 22.35e6,   # r01_gemm_f16ref_u64_n4096.ncu-rep
-    ("gemm_f16tc_kernel", 4096): (74.24e6 + 13.7e6 + 118.3e6 + 17.75e6 + 72.9e6 + 14.26e6
-                                  + 440.1e6 + 109.1e6) / 4,  # mean of the 4 products of a solve
-    ("band", 4096): (134.6e6 + 619.9e6 + 671.2e6 + 123.5e6) / 2,  # per pass, r01_band_vec
+    ("gemm_f16ref_kernel", 4096): 68.29e6 + 21.03e6,   # r01_gemm_f16ref_u64_n4096.ncu-rep
+    ("gemm_f16tc_kernel", 4096): (73.37e6 + 13.91e6 + 118.5e6 + 18.64e6 + 72.79e6 + 13.88e6
+                                  + 71.8e6 + 15.19e6) / 4,  # mean of the 4 products of a solve
+    ("band", 4096): (134.2e6 + 613.1e6 + 671.1e6 + 121.8e6) / 2,  # per pass, r01_band_vec
 }
 
 
@@ -58,14 +58,46 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks and throttle reasons during the timed region.
+
+    NVML (pynvml) polled every 2 ms from a thread, plus one sample on entry
+    and one on exit, so even a millisecond-long region (C1) has samples;
+    nvidia-smi -lms 200 when NVML is unavailable."""
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
 
     def __init__(self, index: int):
-        self.index = index
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        self.index = int(ids[index]) if index < len(ids) and ids[index].isdigit() else index
         self.proc = None
+        self.nvml = None
         self.lines: list[str] = []
+        self.samples: list[tuple[float, float, int]] = []
+        self.stop = threading.Event()
+
+    def _nvml_sample(self):
+        n, h = self.nvml, self.handle
+        self.samples.append((float(n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)),
+                             float(n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)),
+                             int(n.nvmlDeviceGetCurrentClocksEventReasons(h))))
+
+    def _poll(self):
+        while not self.stop.wait(0.002):
+            self._nvml_sample()
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml, self.handle = pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._nvml_sample()
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -84,6 +116,11 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        if self.nvml:
+            self.stop.set()
+            self.t.join(timeout=1)
+            self._nvml_sample()
+            return
         if self.proc:
             self.proc.terminate()
             try:
@@ -93,7 +130,12 @@ class ClockSampler:
 
     def summary(self) -> dict:
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if self.nvml:
+            for clk, cmax, bits in self.samples:
+                sm.append(clk)
+                mx = max(mx, cmax)
+                reasons.update(nm for nm, b in self.REASONS if bits & b)
+        names = [nm for nm, _ in self.REASONS]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
@@ -107,7 +149,8 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def dist_env():
