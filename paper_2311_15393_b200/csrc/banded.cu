@@ -155,9 +155,6 @@ __host__ __device__ constexpr int rows_halo(int padded_taps) {
   return TAPS > 0 ? B_TJ + TAPS - 1 : B_TJ + padded_taps;  // generic: +1 row corr8 slack
 }
 
-#ifndef KP_BAND_A_STAGED
-#define KP_BAND_A_STAGED 1
-#endif
 constexpr int A_SO = A_TA + 2;  // staged output tile stride: 16-byte aligned, conflict-free 128-bit accesses
 #ifndef KP_BAND_A_MINB
 #define KP_BAND_A_MINB 4
@@ -192,15 +189,12 @@ __global__ void __launch_bounds__(A_THREADS, KP_BAND_A_MINB) band_cols_kernel(co
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t nn = size_t(n) * n;
-  const int l = l0 + lane;
   const bool vec = (n & 1) == 0;
-#if KP_BAND_A_STAGED
   // Each thread's 8 outputs are 8 rows of one column (lanes = 32 columns), so
   // storing them straight from registers touches 32 lines per instruction.
   // Instead the Y_k tile goes through shared memory ([A_TL][A_SO]) and each
   // warp stores whole 512-byte column runs.
   double* Ys = Xs + A_TL * S;
-#endif
   for (int k = 0; k < r; ++k) {
 #pragma unroll
     for (int h = 0; h < A_TA / 8 / (A_THREADS / 32); ++h) {
@@ -211,27 +205,10 @@ __global__ void __launch_bounds__(A_THREADS, KP_BAND_A_MINB) band_cols_kernel(co
         corr8_blocks<TAPS>(acc, t.w[k], [&](int i) { return base[i]; });
       else
         corr8(acc, t.w[k], t.taps, [&](int i) { return base[i]; });
-#if KP_BAND_A_STAGED
 #pragma unroll
       for (int q = 0; q < 8; q += 2)
         *reinterpret_cast<double2*>(Ys + lane * A_SO + 8 * b + q) = make_double2(acc[q], acc[q + 1]);
-#else
-      double* Yk = Y + k * nn + size_t(l) * n;
-      const int a = a0 + 8 * b;
-      if (l < n) {
-        if (vec && a + 8 <= n) {
-#pragma unroll
-          for (int q = 0; q < 8; q += 2)
-            *reinterpret_cast<double2*>(Yk + a + q) = make_double2(acc[q], acc[q + 1]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (a + q < n) Yk[a + q] = acc[q];
-        }
-      }
-#endif
     }
-#if KP_BAND_A_STAGED
     __syncthreads();
     double* Yk = Y + k * nn;
     if (vec) {  // a warp stores one column: 32 lanes x 2 rows
@@ -252,7 +229,6 @@ __global__ void __launch_bounds__(A_THREADS, KP_BAND_A_MINB) band_cols_kernel(co
       }
     }
     __syncthreads();  // Ys is rewritten by the next term
-#endif
   }
 }
 
@@ -388,7 +364,7 @@ void by_taps(int real, Args&&... args) {
 template <int TAPS>
 struct ColsLaunch {
   static void run(const double* X, double* Y, int n, int r, const BandTaps& t, const int* status) {
-    const size_t smem = size_t(A_TL) * (cols_stride<TAPS>(t.taps) + (KP_BAND_A_STAGED ? A_SO : 0)) * sizeof(double);
+    const size_t smem = size_t(A_TL) * (cols_stride<TAPS>(t.taps) + A_SO) * sizeof(double);
     auto k = band_cols_kernel<TAPS>;
     set_smem_limit(reinterpret_cast<const void*>(k), smem);
     dim3 grid(cdiv(n, A_TL), cdiv(n, A_TA));
