@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   pdl_wait();
   constexpr int TILE_B_BYTES = BN * BKH * 2;
   constexpr int STAGE_BYTES = TILE_A_BYTES + TILE_B_BYTES;
-  constexpr int TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulators
+  // double-buffered fp32 accumulators; the allocation is a power of two >= 32 columns
+  constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
   if (args.status && *args.status != 0) return;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -359,13 +360,13 @@ void launch_tc(const F16GemmArgs& a) {
 // (lp_matmul's FP64 result), whose epilogue is memory bound and needs the
 // finer tiles to overlap it with the MMAs. The M-solve's last product stores
 // binary16 z and leaves widening + dots to msolve_finish_f16 (vec.cu).
-// KP_F16TC_BN = 128 | 256 forces one width for all products.
+// KP_F16TC_BN = 128 | 192 | 256 forces one width for all products.
 int tc_bn(int mode) {
   static int forced = [] {
     const char* e = getenv("KP_F16TC_BN");
     return e ? atoi(e) : 0;
   }();
-  if (forced == 128 || forced == 256) return forced;
+  if (forced == 128 || forced == 192 || forced == 256) return forced;
   return mode == F16OUT_F64 ? 128 : 256;
 }
 
@@ -380,10 +381,11 @@ void gemm_f16tc(const F16GemmArgs& a, int kernel_class) {
   if (a.A.ld % BKH || a.B.ld % BKH || a.A.ld < a.K || a.B.ld < a.K)
     throw InvalidArgument("gemm_f16tc: operand leading dimension must be a multiple of 64 >= K");
   LaunchScope scope(kernel_class);
-  if (tc_bn(a.epi.mode) == 256)
-    launch_tc<256>(a);
-  else
-    launch_tc<128>(a);
+  switch (tc_bn(a.epi.mode)) {
+    case 256: launch_tc<256>(a); break;
+    case 192: launch_tc<192>(a); break;
+    default: launch_tc<128>(a); break;
+  }
   check_launch("gemm_f16tc");
 }
 

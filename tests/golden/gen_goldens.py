@@ -10,7 +10,8 @@ lambda choices, solution checksums). Usage:
     python tests/golden/gen_goldens.py C1 C2 C3 C4 C5 [C5fpcg] [--threads 8]
 
 C5fpcg writes C5_fpcg_full.json: the headline FPCG run to its end;
-C5cgls writes C5_cgls_full.json: the CGLS run to convergence.
+C5cgls writes C5_cgls_full.json: the CGLS run to convergence;
+C5pcg64 writes C5_pcg64_full.json: PCG with the FP64 preconditioner.
 """
 from __future__ import annotations
 
@@ -110,5 +111,7 @@ if __name__ == "__main__":
             gen("C5", only="fpcg", tag="C5_fpcg_full")
         elif name == "C5cgls":  # CGLS to convergence (about 45 min on 8 threads)
             gen("C5", only="cgls", tag="C5_cgls_full")
+        elif name == "C5pcg64":  # PCG with the FP64 preconditioner to convergence
+            gen("C5", only="pcg", tag="C5_pcg64_full")
         else:
             gen(name)

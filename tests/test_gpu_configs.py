@@ -222,3 +222,18 @@ def test_c5_cgls_full_solve_vs_golden():
     cfg = configs.build("C5")
     (run,) = device_runs(cfg, cfg.lambda_, [("cgls", None, 2000)])
     check_against(run, ref, prefix_rows=20)
+
+
+def test_c5_pcg_fp64_full_solve_vs_golden():
+    """C5's third run: PCG with the FP64 Kronecker-SVD preconditioner to
+    convergence, against the oracle's complete run
+    (tests/golden/C5_pcg64_full.json): iteration count, convergence, final
+    relative error, residual / error history over a 20-row prefix at 1e-8."""
+    path = os.path.join(os.path.dirname(__file__), "golden", "C5_pcg64_full.json")
+    if not os.path.exists(path):
+        pytest.skip("C5_pcg64_full.json not generated")
+    ref = json.load(open(path))["images"][0]["runs"][0]
+    assert ref["solver"] == "pcg" and ref["fmt"] == "fp64"
+    cfg = configs.build("C5")
+    (run,) = device_runs(cfg, cfg.lambda_, [("pcg", "fp64", 100)])
+    check_against(run, ref, prefix_rows=20)
