@@ -384,10 +384,10 @@ __global__ void pcg_p_update_kernel(DevState* st, double* p, const double* z, si
          i += size_t(gridDim.x) * blockDim.x)
       p[i] = z[i] + beta * p[i];
   }
-}
-__global__ void pcg_rho_scalar_kernel(DevState* st) {
-  pdl_wait();
-  if (stopped(st) || threadIdx.x) return;
+  // rho = rz and the positivity check, by one thread once its share of p is
+  // done (no other CTA reads rho or k; a CTA that starts after an abort skips
+  // its share of p, which the stopped solve never reads again)
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
   st->rho = st->rz;
   if (st->rho <= 0.0) {
     st->status = ST_ABORTED, st->abort_code = AB_POSITIVITY, st->abort_iter = st->k;
@@ -744,7 +744,6 @@ void pcg_beta_scalar(DevState* st, const double* part_z, int n) {
 void pcg_p_update(DevState* st, double* p, const double* z, size_t nn) {
   const bool vec2 = nn % 2 == 0 && al16(p) && al16(z);
   KP_LAUNCH(KC_VECTOR, pcg_p_update_kernel, vec_grid(nn), VEC_THREADS, st, p, z, nn, vec2);
-  KP_LAUNCH(KC_VECTOR, pcg_rho_scalar_kernel, 1, 32, st);
 }
 
 void cgls_init_scalar(DevState* st, DevHistory h, const double* part_s, int ns,
