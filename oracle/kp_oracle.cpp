@@ -303,8 +303,72 @@ static void lp_matmul_fp16_fast(const double* a, long m, long K,
   }
 }
 
-// lp_matmul (lpblas.cpp:59-70). mode: 0 auto (fast fp16 when applicable),
-// 1 literal, 2 streamed generic.
+// Double-covering formats (fp64): the same stage tree with no rounding,
+// eight consecutive output rows at a time. All eight share the counter state
+// (it depends only on the leaf index), so every sum is the one TreeAcc forms;
+// A is read through a row-major copy so each row streams contiguously.
+static void lp_matmul_tree_f64(const double* a, long m, long K, const double* b, long n,
+                               double* out) {
+  std::vector<double> at(size_t(m) * K);
+#pragma omp parallel for schedule(static) num_threads(g_threads)
+  for (long r = 0; r < m; ++r)
+    for (long i = 0; i < K; ++i) at[size_t(r) * K + i] = a[size_t(i) * m + r];
+#pragma omp parallel for schedule(dynamic, 1) num_threads(g_threads)
+  for (long j = 0; j < n; ++j) {
+    const double* bj = b + size_t(j) * K;
+    for (long r0 = 0; r0 < m; r0 += 8) {
+      const int R = int(std::min<long>(8, m - r0));
+      const double* ar[8];
+      for (int q = 0; q < 8; ++q) ar[q] = at.data() + size_t(r0 + (q < R ? q : 0)) * K;
+      double lvl[64][8];
+      uint64_t occ = 0;
+      // aligned 8-leaf blocks: their subtree is fixed ((01)(23))((45)(67)) and
+      // the block value enters the counter at level 3 (bits 0-2 are clear)
+      const long K8 = K & ~7L;
+      for (long i0 = 0; i0 < K8; i0 += 8) {
+        double v[8];
+        for (int q = 0; q < 8; ++q) {
+          const double* x = ar[q] + i0;
+          const double* y = bj + i0;
+          const double s01 = x[0] * y[0] + x[1] * y[1], s23 = x[2] * y[2] + x[3] * y[3];
+          const double s45 = x[4] * y[4] + x[5] * y[5], s67 = x[6] * y[6] + x[7] * y[7];
+          v[q] = (s01 + s23) + (s45 + s67);
+        }
+        int L = 3;
+        while (occ & (uint64_t(1) << L)) {
+          for (int q = 0; q < 8; ++q) v[q] = lvl[L][q] + v[q];
+          occ &= ~(uint64_t(1) << L);
+          ++L;
+        }
+        for (int q = 0; q < 8; ++q) lvl[L][q] = v[q];
+        occ |= uint64_t(1) << L;
+      }
+      for (long i = K8; i < K; ++i) {
+        double v[8];
+        for (int q = 0; q < 8; ++q) v[q] = ar[q][i] * bj[i];
+        int L = 0;
+        while (occ & (uint64_t(1) << L)) {
+          for (int q = 0; q < 8; ++q) v[q] = lvl[L][q] + v[q];
+          occ &= ~(uint64_t(1) << L);
+          ++L;
+        }
+        for (int q = 0; q < 8; ++q) lvl[L][q] = v[q];
+        occ |= uint64_t(1) << L;
+      }
+      double acc[8];
+      bool have = false;
+      for (int L = 0; L < 64; ++L) {
+        if (!(occ & (uint64_t(1) << L))) continue;
+        for (int q = 0; q < 8; ++q) acc[q] = have ? lvl[L][q] + acc[q] : lvl[L][q];
+        have = true;
+      }
+      for (int q = 0; q < R; ++q) out[size_t(j) * m + r0 + q] = acc[q];
+    }
+  }
+}
+
+// lp_matmul (lpblas.cpp:59-70). mode: 0 auto (fast fp16 / fp64 tree when
+// applicable), 1 literal, 2 streamed generic.
 static void lp_matmul(const double* a, long m, long K, const double* b, long n,
                       const Fmt& fmt, double* out, int mode = 0) {
   if (K == 0) throw std::invalid_argument("lp_matmul: empty input");
@@ -316,6 +380,8 @@ static void lp_matmul(const double* a, long m, long K, const double* b, long n,
   if (mode == 0 && fmt.is_fp16() && all_fp16(a, size_t(m) * K) &&
       all_fp16(b, size_t(K) * n))
     lp_matmul_fp16_fast(a, m, K, b, n, out);
+  else if (mode == 0 && fmt.covers_double())
+    lp_matmul_tree_f64(a, m, K, b, n, out);
   else
     lp_matmul_streamed_generic(a, m, K, b, n, fmt, out);
 }

@@ -246,6 +246,13 @@ def test_streamed_tree_equals_literal(K):
         x = rng.uniform(-2, 2, (4, K))
         y = rng.uniform(-2, 2, (K, 3))
         assert np.array_equal(O.lp_matmul(x, y, fmt, 2), O.lp_matmul(x, y, fmt, 1))
+    # fp64: the eight-row tree path (mode 0) == generic streamed == literal;
+    # 13 rows exercise a partial group of eight, wide magnitudes the order
+    x = rng.uniform(-2, 2, (13, K)) * 10.0 ** rng.integers(-8, 8, (13, K))
+    y = rng.uniform(-2, 2, (K, 3)) * 10.0 ** rng.integers(-8, 8, (K, 3))
+    lit = O.lp_matmul(x, y, PF.fp64(), 1)
+    assert np.array_equal(O.lp_matmul(x, y, PF.fp64(), 0), lit)
+    assert np.array_equal(O.lp_matmul(x, y, PF.fp64(), 2), lit)
 
 
 def test_fast_fp16_path_exhaustive_pairs():
