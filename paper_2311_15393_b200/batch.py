@@ -98,12 +98,15 @@ class C4Shard:
     """Shared operator / preconditioner factors for the C4 batch on one GPU
     (all 64 images share the PSF, hence A and the Kronecker factors).
 
-    solve_many() runs `workers` host threads; each has its own library
+    accum="tensor" builds the tcgen05 tensor-mode preconditioner (not
+    bit-exact; the bench's secondary C4 run). solve_many() runs `workers`
+    host threads; each has its own library
     context (stream) and its own operator handle, so independent images
     overlap on the device (the kernels of one image at n = 1024 do not fill
     the 148 SMs on their own)."""
 
-    def __init__(self, n: int | None = None, svd: str = "host", device: int = 0):
+    def __init__(self, n: int | None = None, svd: str = "host", device: int = 0,
+                 accum: str = "reference"):
         import numpy as np
 
         from . import configs
@@ -126,10 +129,11 @@ class C4Shard:
                 u, s, vh = torch.linalg.svd(torch.from_numpy(np.ascontiguousarray(f)).cuda())
                 pair.append(SvdTriple(np.asfortranarray(u.cpu().numpy()), s.cpu().numpy().copy(),
                                       np.asfortranarray(vh.T.cpu().numpy())))
-            self.m0 = K.build_preconditioner_from_svd(pair[0], pair[1], 1.0, K.PrecisionFormat.fp16())
+            self.m0 = K.build_preconditioner_from_svd(pair[0], pair[1], 1.0, K.PrecisionFormat.fp16(),
+                                                      accum=accum)
         else:
             self.m0 = K.build_preconditioner(base.term.row_factor, base.term.col_factor, 1.0,
-                                             K.PrecisionFormat.fp16())
+                                             K.PrecisionFormat.fp16(), accum=accum)
 
     def problem(self, image: int):
         P, np = self.P, self.np
