@@ -386,7 +386,7 @@ def main():
     ap.add_argument("--no-other-runs", action="store_true",
                     help="skip the config's other solver runs (C5: PCG fp64-precond, CGLS)")
     ap.add_argument("--operator", default="auto", choices=["auto", "dense", "banded"])
-    ap.add_argument("--workers", type=int, default=8,
+    ap.add_argument("--workers", type=int, default=6,
                     help="C4: concurrent host threads / streams per GPU")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="collective backend for timing reduction / result gather")
