@@ -785,8 +785,13 @@ void spectral_filter(const double* s_r, const double* s_c, int n, double l2, dou
 template <int KIND>
 void launch_sums(const double* s_r, const double* s_c, const double* bhat, const double* xhat,
                  int n, const double* lambdas, int m, double omega, double* part) {
+  // lambdas per pass: 1, 4 (the discrepancy look-ahead's 3) or LCHUNK; every
+  // value is summed in the same element order whatever the width
   if (m == 1)
     KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<1, KIND>), VEC_CTAS, VEC_THREADS, s_r, s_c, bhat,
+              xhat, n, lambdas, m, omega, part);
+  else if (m <= 4)
+    KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<4, KIND>), VEC_CTAS, VEC_THREADS, s_r, s_c, bhat,
               xhat, n, lambdas, m, omega, part);
   else
     KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<LCHUNK, KIND>), VEC_CTAS, VEC_THREADS, s_r, s_c,

@@ -557,3 +557,23 @@ def test_concurrent_streams_match_sequential():
     for a, b in zip(seq, con):
         assert (a.image, a.lam, a.iterations, a.converged, a.rel_err, a.abort_reason) == \
                (b.image, b.lam, b.iterations, b.converged, b.rel_err, b.abort_reason)
+
+
+@pytest.mark.parametrize("noise", [0.001, 0.01, 0.05])
+def test_discrepancy_lookahead_equals_sequential_bisection(noise):
+    """kp_discrepancy evaluates six bisection levels per batched launch; its
+    lambda must be bit-identical to find_root (regparam.cpp:184-214) driven
+    one single-value discrepancy_gap at a time."""
+    import math
+    n = 96
+    psf = P.make_psf("gaussian", 13, sigma=2.5)
+    tp = P.make_test_problem(P.blob_image(n, 41), psf, noise, 42)
+    term = P.nearest_kron(psf, n)
+    m0 = K.build_preconditioner(term.row_factor, term.col_factor, 1.0, K.PrecisionFormat.fp16())
+    sd = K.make_spectral_data(m0, tp.b)
+    nn = float(np.linalg.norm(tp.noise))
+    got = K.discrepancy(sd, nn, 1.01)
+    eps = 1.01 * nn
+    u = K.find_root(lambda v: K.discrepancy_gap(sd, eps, math.exp(v)),
+                    math.log(got.bracket_lo), math.log(got.bracket_hi), 1e-12)
+    assert got.lambda_ == math.exp(u)
