@@ -249,7 +249,10 @@ int kp_wgcv(const kp_spectral* sd, double omega, kp_param_choice* choice);
  * the Kronecker approximation, FP64 on the device; x is n*n (host). */
 int kp_filtered_solution(const kp_precond* p, const double* b, double lambda,
                          double* x);
-/* discrepancy (regparam.cpp:288-327); KP_ERR_NO_ROOT when no root. */
+/* discrepancy (regparam.cpp:288-327); KP_ERR_NO_ROOT when no root. The
+ * bisection (find_root, regparam.cpp:184-214) evaluates two levels of
+ * candidate midpoints per device launch; lambda is bit-identical to the
+ * one-point-at-a-time bisection. */
 int kp_discrepancy(const kp_spectral* sd, double noise_norm, double eta,
                    kp_param_choice* choice);
 
