@@ -872,7 +872,7 @@ void run_pcg(kp_operator* op, const double* b_in, kp_precond* m, const kp_solver
     pcg_alpha_scalar(s.st, part_op.p, nop);
     pcg_update(s.st, s.dh, x, r.p, flexible ? rprev.p : nullptr, p.p, q.p, z.p, xt,
                fp16 ? m->r16.p : nullptr, n, fp16 ? m->sh->ldh : 0, part_vec.p);
-    pcg_resid_scalar(s.st, s.dh, part_vec.p, VEC_CTAS);
+    pcg_resid_scalar(s.st, s.dh, part_vec.p, pcg_update_ctas(n));
     msolve(m, r.p, z.p, r.p, flexible ? r.p : nullptr, flexible ? rprev.p : nullptr, status);
     pcg_beta_scalar(s.st, m->part.p, nms);
     pcg_p_update(s.st, p.p, z.p, nn);

@@ -723,16 +723,21 @@ void pcg_alpha_scalar(DevState* st, const double* part_pq, int n) {
   KP_LAUNCH(KC_VECTOR, pcg_alpha_scalar_kernel, 1, SCALAR_THREADS, st, part_pq, n);
 }
 
+int pcg_update_ctas(int n) {
+  // one pair (or element) per thread at most; the fixed VEC_CTAS from n ~ 1560 up
+  const size_t units = (n % 2 == 0) ? size_t(n) * n / 2 : size_t(n) * n;
+  return int(vec_grid(units));
+}
 void pcg_update(DevState* st, DevHistory h, double* x, double* r, double* r_prev, const double* p,
                 const double* q, const double* z, const double* xt, __half* r16, int n, long ldh,
                 double* partials) {
   const bool vec2 = n % 2 == 0 && al16(x) && al16(r) && al16(r_prev) && al16(p) && al16(q) &&
                     al16(z) && al16(xt) && al16(h.iterates) && ldh % 2 == 0;
   if (vec2)
-    KP_LAUNCH(KC_VECTOR, pcg_update_kernel<true>, VEC_CTAS, VEC_THREADS, st, h, x, r, r_prev, p, q,
+    KP_LAUNCH(KC_VECTOR, pcg_update_kernel<true>, pcg_update_ctas(n), VEC_THREADS, st, h, x, r, r_prev, p, q,
               z, xt, r16, n, ldh, partials);
   else
-    KP_LAUNCH(KC_VECTOR, pcg_update_kernel<false>, VEC_CTAS, VEC_THREADS, st, h, x, r, r_prev, p,
+    KP_LAUNCH(KC_VECTOR, pcg_update_kernel<false>, pcg_update_ctas(n), VEC_THREADS, st, h, x, r, r_prev, p,
               q, z, xt, r16, n, ldh, partials);
 }
 void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n) {

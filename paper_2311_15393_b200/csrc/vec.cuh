@@ -81,6 +81,8 @@ void pcg_init_scalar(DevState* st, DevHistory h, const double* part_r, int nr,
 // after first M-solve (partials: [0]=r.z, [2]=#nonfinite)
 void pcg_init_msolve_scalar(DevState* st, const double* part_z, int nz);
 void pcg_alpha_scalar(DevState* st, const double* part_pq, int n);
+// CTAs (= partials) pcg_update uses at size n (fixed for a given n)
+int pcg_update_ctas(int n);
 // x += a p; r -= a q; [r_prev = r]; R16 = round16(r); partials:
 // [0] ||r||^2, [1] ||x - xt||^2, [2] r.z, [3] ||z||^2
 void pcg_update(DevState* st, DevHistory h, double* x, double* r, double* r_prev,
