@@ -238,7 +238,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64+f16(emulated)", "data": "synthetic",
-        "config": workload_config(cfg),
+        "config": workload_config(cfg, device=False),
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": threads, "kind": "port",
                          "sample": f"one {solver_name.upper()} iteration's normal_matvec + "
                                    "precond_solve (fp16 reference-exact emulation) per step"},
@@ -357,14 +357,15 @@ def run_c4(args):
     return 0
 
 
-def workload_config(cfg) -> dict:
+def workload_config(cfg, device: bool = True) -> dict:
     solver, _, maxit = cfg.solvers[0]
     lam = cfg.lambda_ if cfg.select == "fixed" else f"{cfg.select} ({cfg.lambda_:.6g})"
     return {"workload": f"{cfg.name}: n={cfg.n} r={len(cfg.problem.a.terms)} {solver.upper()}, fp16 "
                         f"Kronecker-SVD preconditioner (reference-exact rounding), "
                         f"lambda={lam}, tol={cfg.tol}, maxit {maxit}",
             "unknowns": cfg.n * cfg.n,
-            "l2": ("working set (~4 GB) far larger than the 126 MB L2; no flush needed" if cfg.n >= 4096
+            "l2": ("host CPU run (no GPU L2 involved)" if not device
+                   else "working set (~4 GB) far larger than the 126 MB L2; no flush needed" if cfg.n >= 4096
                    else "L2 flushed before every timed step (256 MB zero-fill), steps timed separately")}
 
 
