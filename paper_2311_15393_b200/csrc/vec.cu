@@ -5,7 +5,8 @@
 // Every kernel first reads DevState::status and returns when the solve has
 // stopped, so the host can enqueue iterations without synchronising; the
 // scalar kernels reproduce the reference's check order and abort messages.
-// All reductions use a fixed grid (VEC_CTAS) and fixed-order combination, so
+// All reductions use a grid fixed for a given n (VEC_CTAS, or fewer CTAs
+// for pcg_update at small n) and fixed-order combination, so
 // results are run-to-run deterministic.
 #include "vec.cuh"
 
@@ -669,8 +670,9 @@ unsigned vec_grid(size_t nn) {
 
 }  // namespace
 
-// Host wrappers. The vector kernels always use VEC_CTAS CTAs (fixed
-// reduction order); the CTAs beyond the data simply contribute zero.
+// Host wrappers. The reducing vector kernels use VEC_CTAS CTAs (pcg_update:
+// pcg_update_ctas(n), fewer at small n) so the reduction order is fixed for a
+// given n; CTAs beyond the data simply contribute zero.
 #define KP_LAUNCH(cls, kernel, grid, block, ...)                   \
   do {                                                             \
     LaunchScope scope_(cls);                                       \
