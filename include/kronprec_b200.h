@@ -60,6 +60,20 @@ typedef struct kp_format {
 #define KP_ACCUM_REFERENCE 0
 #define KP_ACCUM_TENSOR 1
 
+/* Engine of the reference-exact binary16 products (KP_ACCUM_REFERENCE).
+ * Both give bit-identical results (lp_matmul, lpblas.cpp:59-70):
+ *   KP_FP16_PRODUCTS_CUDA_CORES  rounded products and tree adds on the f16x2
+ *                                pipe (gemm_f16ref)
+ *   KP_FP16_PRODUCTS_TENSOR      rounded products from tcgen05 MMAs with an
+ *                                f16 accumulator and a diagonal-expanded B
+ *                                operand, tree adds on the f16x2 pipe
+ *                                (gemm_f16x)
+ *   KP_FP16_PRODUCTS_AUTO        tensor from n >= 512 (default; environment
+ *                                KP_FP16_PRODUCTS=cuda|tensor|auto) */
+#define KP_FP16_PRODUCTS_AUTO 0
+#define KP_FP16_PRODUCTS_CUDA_CORES 1
+#define KP_FP16_PRODUCTS_TENSOR 2
+
 /* SolverOptions (krylov.hpp:14-22). When device_pointers != 0, b, x and
  * x_true passed to the solvers are device pointers (kp_device_alloc). */
 typedef struct kp_solver_options {
@@ -127,6 +141,10 @@ int kp_profile_enable(int on);
 int kp_profile_read(int kernel_class, double* total_ms, long long* launches);
 int kp_profile_reset(void);
 long long kp_launch_count(void);   /* kernels launched by this library (all threads) */
+/* Process-wide engine for reference-exact binary16 products (see above);
+ * kp_get_fp16_products reports whether size n would use the tensor engine. */
+int kp_set_fp16_products(int mode);
+int kp_get_fp16_products(int n, int* uses_tensor);
 /* Device timestamps on the library stream (slots 0..15), for callers that
  * time whole solves on the device. */
 int kp_event_record(int slot);

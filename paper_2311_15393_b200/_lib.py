@@ -24,6 +24,10 @@ KP_ERR_UNSUPPORTED = 5
 KP_ACCUM_REFERENCE = 0
 KP_ACCUM_TENSOR = 1
 
+KP_FP16_PRODUCTS_AUTO = 0
+KP_FP16_PRODUCTS_CUDA_CORES = 1
+KP_FP16_PRODUCTS_TENSOR = 2
+
 KP_OP_AUTO = 0
 KP_OP_DENSE = 1
 KP_OP_BANDED = 2
@@ -71,7 +75,7 @@ EXPORTS = [
     "kp_discrepancy", "kp_operator_set_mode", "kp_operator_get_mode", "kp_event_record", "kp_event_elapsed", "kp_host_alloc", "kp_host_free",
     "kp_spectral_create_x", "kp_spectral_export_xhat", "kp_opt_objective", "kp_wgcv_objective",
     "kp_lambda_opt", "kp_wgcv", "kp_filtered_solution", "kp_round_array", "kp_lp_matmul",
-    "kp_lp_matmul_ex",
+    "kp_lp_matmul_ex", "kp_set_fp16_products", "kp_get_fp16_products",
 ]
 
 _lib = None
@@ -133,6 +137,8 @@ def lib() -> C.CDLL:
             "kp_event_elapsed": ([I, I, C.POINTER(C.c_float)], I),
             "kp_host_alloc": ([C.c_size_t, C.POINTER(C.c_void_p)], I),
             "kp_host_free": ([P], I),
+            "kp_set_fp16_products": ([I], I),
+            "kp_get_fp16_products": ([I, C.POINTER(I)], I),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

@@ -29,6 +29,7 @@
 #include "common.cuh"
 #include "gemm_f16ref.cuh"
 #include "gemm_f16tc.cuh"
+#include "gemm_f16x.cuh"
 #include "lp_generic.cuh"
 #include "gemm_f64.cuh"
 #include "host_la.h"
@@ -272,6 +273,7 @@ struct kp_precond {
   DBuf<double> t1d, wd, t3d;
   DBuf<double> rlp;  // generic formats: round_array(unvec(r), fmt)
   DBuf<double> part;
+  DBuf<unsigned> zfix;  // gemm_f16x zero-sign fix-up workspace (zeroed)
 };
 
 struct kp_spectral {
@@ -398,10 +400,49 @@ void detect_banded(kp_operator* op, const double* rows, const double* cols) {
   op->is_banded = true;
 }
 
+// Reference-exact binary16 products: KP_FP16_PRODUCTS_CUDA_CORES runs
+// gemm_f16ref (HMUL2 + HADD2 on the f16x2 pipe), KP_FP16_PRODUCTS_TENSOR
+// gemm_f16x (rounded leaves from tcgen05 MMAs, HADD2 trees); both are
+// bit-identical to lp_matmul. AUTO picks gemm_f16x from n >= 512, where its
+// 128 x 32 tiles fill the SMs (env KP_FP16_PRODUCTS=cuda|tensor|auto sets the
+// process default).
+std::atomic<int> g_fp16_products{-1};
+int fp16_products_setting() {
+  int v = g_fp16_products.load();
+  if (v < 0) {
+    v = KP_FP16_PRODUCTS_AUTO;
+    if (const char* e = getenv("KP_FP16_PRODUCTS")) {
+      const std::string s(e);
+      if (s == "cuda") v = KP_FP16_PRODUCTS_CUDA_CORES;
+      else if (s == "tensor") v = KP_FP16_PRODUCTS_TENSOR;
+    }
+    g_fp16_products.store(v);
+  }
+  return v;
+}
+bool use_f16x(int n) {
+  const int v = fp16_products_setting();
+  if (v == KP_FP16_PRODUCTS_CUDA_CORES) return false;
+  if (v == KP_FP16_PRODUCTS_TENSOR) return true;
+  return n >= 512;
+}
+bool msolve_f16x(const kp_precond* p) {
+  return is_fp16(p->fmt) && p->accum == KP_ACCUM_REFERENCE && use_f16x(p->n);
+}
+
 int msolve_partials_ctas(const kp_precond* p) {
   if (is_generic(p->fmt)) return LP_PART_CTAS;
   if (covers_double(p->fmt)) return gemm_f64_num_ctas(p->n, p->n);
-  return p->accum == KP_ACCUM_TENSOR ? VEC_CTAS : gemm_f16ref_num_ctas(p->n, p->n);
+  if (p->accum == KP_ACCUM_TENSOR) return VEC_CTAS;
+  return msolve_f16x(p) ? gemm_f16x_num_ctas(p->n, p->n) : gemm_f16ref_num_ctas(p->n, p->n);
+}
+
+// zero-initialised gemm_f16x fix-up workspace for M x N products
+void ensure_zfix(DBuf<unsigned>& z, int M, int N) {
+  const size_t words = size_t(f16x_zfix_words(M, N)) + 2;
+  if (z.n >= words) return;
+  z.alloc(words);
+  KP_CUDA(cudaMemsetAsync(z.p, 0, words * sizeof(unsigned), ctx().stream));
 }
 
 void ensure_ws(kp_precond* p) {
@@ -423,7 +464,9 @@ void ensure_ws(kp_precond* p) {
       fill_u16(p->t1h.p, p->t1h.n, 0x8000);  // A operands: -0 padding
       fill_u16(p->t3h.p, p->t3h.n, 0x8000);
     }
-    if (!p->part.p) p->part.alloc(size_t(msolve_partials_ctas(p)) * 4);
+    if (!p->part.p || p->part.n < size_t(msolve_partials_ctas(p)) * 4)
+      p->part.alloc(size_t(msolve_partials_ctas(p)) * 4);
+    if (msolve_f16x(p)) ensure_zfix(p->zfix, n, n);
   }
 }
 
@@ -479,6 +522,30 @@ void msolve(kp_precond* p, const double* r, double* z, const double* d0, const d
   }
   if (!is_fp16(p->fmt)) throw Unsupported("precond_solve: only fp16 and double-covering formats run on the B200 path");
   const long ldh = sh->ldh;
+  if (msolve_f16x(p)) {
+    // gemm_f16x needs a finite A operand (the expanded-B filler zeros multiply
+    // it): A is always a singular-vector factor, B the data. The second and
+    // fourth products are therefore formed transposed (out^T = B'^T A'^T),
+    // which also makes every epilogue store row-contiguous.
+    F16GemmArgs g;
+    g.M = n, g.N = n, g.K = n, g.status = status, g.zfix = p->zfix.p;
+    g.A = {sh->vc_a.p, ldh}, g.B = {p->r16.p, ldh};  // t1(a,j) = lp(V_c^T R)
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = ldh, g.epi.cn = 1;
+    gemm_f16x(g, KC_PRECOND);
+    g.A = {sh->vr_b.p, ldh}, g.B = {p->t1h.p, ldh};  // w(a,b) = round(S .* lp(t1 V_r)), as (b, a)
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF_SCALED, g.epi.Ch = p->wh.p, g.epi.cm = ldh,
+    g.epi.cn = 1, g.epi.scale = p->s16.p, g.epi.sm = n, g.epi.sn = 1;
+    gemm_f16x(g, KC_PRECOND);
+    g.A = {sh->vct_a.p, ldh}, g.B = {p->wh.p, ldh};  // t3(i,b) = lp(V_c w)
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t3h.p, g.epi.cm = ldh, g.epi.cn = 1;
+    gemm_f16x(g, KC_PRECOND);
+    g.A = {sh->vrt_b.p, ldh}, g.B = {p->t3h.p, ldh};  // z(i,j) = lp(t3 V_r^T), as (j, i)
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z, g.epi.cm = n, g.epi.cn = 1;
+    g.epi.vm = n, g.epi.vn = 1, g.epi.d0 = d0, g.epi.d1a = d1a, g.epi.d1b = d1b;
+    g.epi.partials = p->part.p;
+    gemm_f16x(g, KC_PRECOND);
+    return;
+  }
   auto gemm = p->accum == KP_ACCUM_TENSOR ? gemm_f16tc : gemm_f16ref;
   F16GemmArgs g;
   g.M = n, g.N = n, g.K = n, g.status = status;
@@ -1234,6 +1301,20 @@ int kp_profile_read(int cls, double* total_ms, long long* launches) {
   })
 }
 long long kp_launch_count(void) { return kp::g_launches.load(); }
+int kp_set_fp16_products(int mode) {
+  KP_API({
+    if (mode < KP_FP16_PRODUCTS_AUTO || mode > KP_FP16_PRODUCTS_TENSOR)
+      throw InvalidArgument("fp16 products: mode must be KP_FP16_PRODUCTS_AUTO, _CUDA_CORES or _TENSOR");
+    fp16_products_setting();
+    g_fp16_products.store(mode);
+  })
+}
+int kp_get_fp16_products(int n, int* uses_tensor) {
+  KP_API({
+    if (!uses_tensor) throw InvalidArgument("fp16 products: null output");
+    *uses_tensor = use_f16x(n) ? 1 : 0;
+  })
+}
 int kp_event_record(int slot) {
   KP_API({
     static cudaEvent_t ev[16] = {};
@@ -1479,7 +1560,16 @@ int kp_lp_matmul_ex(int m, int k, int n, const double* a, const double* b, kp_fo
       g.M = m, g.N = n, g.K = k;
       g.A = {ha.p, ldh}, g.B = {hb.p, ldh};
       g.epi.mode = F16OUT_F64, g.epi.Cd = dc.p, g.epi.cm = 1, g.epi.cn = m;
-      gemm_f16ref(g, KC_PRECOND);
+      bool a_finite = true;  // gemm_f16x: A must be finite (see gemm_f16x.cu)
+      for (size_t q = 0; q < na && a_finite; ++q) a_finite = std::isfinite(a[q]);
+      if (a_finite && use_f16x(std::min(m, n))) {
+        DBuf<unsigned> zf;
+        ensure_zfix(zf, m, n);
+        g.zfix = zf.p;
+        gemm_f16x(g, KC_PRECOND);
+      } else {
+        gemm_f16ref(g, KC_PRECOND);
+      }
     } else {
       LpGemmArgs g;
       g.M = m, g.N = n, g.K = k, g.f = lp_format(fmt), g.round_leaves = round_leaves != 0;

@@ -38,6 +38,10 @@ struct F16GemmArgs {
   F16Operand A, B;  // C(m,n) = tree_k round16(A(m,k) * B(n,k))
   F16Epilogue epi;
   const int* status = nullptr;
+  // gemm_f16x only: zero-sign fix-up workspace, f16x_zfix_words(M, N) + 2
+  // unsigned words with [0] = [1] = 0 ([0] listed outputs, [1] fix-up
+  // completion counter, [2..] the list); every launch leaves [0] = [1] = 0.
+  unsigned* zfix = nullptr;
 };
 
 int gemm_f16ref_num_ctas(int M, int N);

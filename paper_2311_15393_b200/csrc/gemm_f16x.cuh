@@ -1,0 +1,13 @@
+// Reference-exact binary16 GEMM with tcgen05-generated rounded products
+// (gemm_f16x.cu). Same operand / epilogue contract as gemm_f16ref
+// (gemm_f16ref.cuh), bit-identical results; additionally A must be finite and
+// args.zfix must point at f16x_zfix_words(M, N) + 2 zeroed words.
+#pragma once
+
+#include "gemm_f16ref.cuh"
+
+namespace kp {
+long f16x_zfix_words(int M, int N);
+int gemm_f16x_num_ctas(int M, int N);  // = output tiles (one partial slot each)
+void gemm_f16x(const F16GemmArgs& a, int kernel_class);
+}  // namespace kp

@@ -29,7 +29,8 @@ __all__ = [
     "plateau_iteration", "WorkReport", "work_report", "SpectralData", "make_spectral_data",
     "ParamChoice", "gcv_objective", "opt_objective", "wgcv_objective", "discrepancy_gap", "gcv",
     "gcv_grid", "lambda_opt", "wgcv", "discrepancy", "filtered_solution", "NoRootError",
-    "MinimizeResult", "minimize_1d", "find_root", "param_method_name",
+    "MinimizeResult", "minimize_1d", "find_root", "param_method_name", "set_fp16_products",
+    "fp16_products_engine",
 ]
 
 
@@ -117,6 +118,25 @@ def _lp(a, b, fmt: PrecisionFormat, round_leaves: bool) -> np.ndarray:
     c = np.empty((m, n), dtype=np.float64, order="F")
     check(lib().kp_lp_matmul_ex(m, k, n, ptr(af), ptr(bf), fmt.c(), int(round_leaves), ptr(c)))
     return np.ascontiguousarray(c)
+
+
+_FP16_PRODUCTS = {"auto": 0, "cuda": 1, "tensor": 2}
+
+
+def set_fp16_products(engine: str) -> None:
+    """Engine of the reference-exact binary16 products (bit-identical either
+    way): "cuda" (f16x2 HMUL2 + HADD2), "tensor" (tcgen05 rounded leaves +
+    HADD2 trees) or "auto" (tensor from n >= 512). Process-wide."""
+    if engine not in _FP16_PRODUCTS:
+        raise ValueError(f"unknown fp16 product engine: {engine}")
+    check(lib().kp_set_fp16_products(_FP16_PRODUCTS[engine]))
+
+
+def fp16_products_engine(n: int) -> str:
+    """Engine "auto" picks for an n x n preconditioner solve."""
+    t = C.c_int()
+    check(lib().kp_get_fp16_products(int(n), C.byref(t)))
+    return "tensor" if t.value else "cuda"
 
 
 def lp_matmul(a, b, fmt: PrecisionFormat) -> np.ndarray:
