@@ -136,7 +136,8 @@ int kp_memcpy_h2d(void* dst, const void* src, size_t bytes);
 int kp_memcpy_d2h(void* dst, const void* src, size_t bytes);
 /* Per-kernel-class device timing (CUDA events on the library stream).
  * class ids: 0 fp64 operator GEMM, 1 preconditioner GEMM, 2 vector kernels,
- * 3 spectral / lambda kernels. */
+ * 3 spectral / lambda kernels, 4 preconditioner auxiliaries (row sign
+ * hashes and zero-sign fix-ups of the tensor fp16 product engine). */
 int kp_profile_enable(int on);
 int kp_profile_read(int kernel_class, double* total_ms, long long* launches);
 int kp_profile_reset(void);

@@ -257,6 +257,8 @@ struct PrecondShared {
   // extremes of s_r(j) s_c(i) over all (i, j), computed once (spectral data)
   bool have_range = false;
   double smin = 0.0, smax = 0.0;
+  // gemm_f16x row sign hashes of the four binary16 factor operands (lazy)
+  DBuf<unsigned long long> hash_vc_a, hash_vr_b, hash_vct_a, hash_vrt_b;
   std::mutex lazy_mu;  // guards the lazily created members above (shared across handles)
 };
 
@@ -274,6 +276,7 @@ struct kp_precond {
   DBuf<double> rlp;  // generic formats: round_array(unvec(r), fmt)
   DBuf<double> part;
   DBuf<unsigned> zfix;  // gemm_f16x zero-sign fix-up workspace (zeroed)
+  DBuf<unsigned long long> hash_b;  // gemm_f16x B-operand row sign hashes
 };
 
 struct kp_spectral {
@@ -466,7 +469,20 @@ void ensure_ws(kp_precond* p) {
     }
     if (!p->part.p || p->part.n < size_t(msolve_partials_ctas(p)) * 4)
       p->part.alloc(size_t(msolve_partials_ctas(p)) * 4);
-    if (msolve_f16x(p)) ensure_zfix(p->zfix, n, n);
+    if (msolve_f16x(p)) {
+      ensure_zfix(p->zfix, n, n);
+      if (!p->hash_b.p) p->hash_b.alloc(size_t(n));
+      auto* sh = p->sh.get();
+      std::lock_guard<std::mutex> lk(sh->lazy_mu);
+      if (!sh->hash_vc_a.p) {  // the factor operands never change: hash them once
+        sh->hash_vc_a.alloc(n), sh->hash_vr_b.alloc(n), sh->hash_vct_a.alloc(n), sh->hash_vrt_b.alloc(n);
+        f16x_row_hash({sh->vc_a.p, ldh}, n, n, sh->hash_vc_a.p);
+        f16x_row_hash({sh->vr_b.p, ldh}, n, n, sh->hash_vr_b.p);
+        f16x_row_hash({sh->vct_a.p, ldh}, n, n, sh->hash_vct_a.p);
+        f16x_row_hash({sh->vrt_b.p, ldh}, n, n, sh->hash_vrt_b.p);
+        sync();  // shared across handles / threads
+      }
+    }
   }
 }
 
@@ -529,16 +545,21 @@ void msolve(kp_precond* p, const double* r, double* z, const double* d0, const d
     // which also makes every epilogue store row-contiguous.
     F16GemmArgs g;
     g.M = n, g.N = n, g.K = n, g.status = status, g.zfix = p->zfix.p;
+    g.hash_a_ready = true, g.hash_b = p->hash_b.p;
+    g.hash_a = sh->hash_vc_a.p;
     g.A = {sh->vc_a.p, ldh}, g.B = {p->r16.p, ldh};  // t1(a,j) = lp(V_c^T R)
     g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = ldh, g.epi.cn = 1;
     gemm_f16x(g, KC_PRECOND);
+    g.hash_a = sh->hash_vr_b.p;
     g.A = {sh->vr_b.p, ldh}, g.B = {p->t1h.p, ldh};  // w(a,b) = round(S .* lp(t1 V_r)), as (b, a)
     g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF_SCALED, g.epi.Ch = p->wh.p, g.epi.cm = ldh,
     g.epi.cn = 1, g.epi.scale = p->s16.p, g.epi.sm = n, g.epi.sn = 1;
     gemm_f16x(g, KC_PRECOND);
+    g.hash_a = sh->hash_vct_a.p;
     g.A = {sh->vct_a.p, ldh}, g.B = {p->wh.p, ldh};  // t3(i,b) = lp(V_c w)
     g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t3h.p, g.epi.cm = ldh, g.epi.cn = 1;
     gemm_f16x(g, KC_PRECOND);
+    g.hash_a = sh->hash_vrt_b.p;
     g.A = {sh->vrt_b.p, ldh}, g.B = {p->t3h.p, ldh};  // z(i,j) = lp(t3 V_r^T), as (j, i)
     g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z, g.epi.cm = n, g.epi.cn = 1;
     g.epi.vm = n, g.epi.vn = 1, g.epi.d0 = d0, g.epi.d1a = d1a, g.epi.d1b = d1b;
@@ -1565,7 +1586,8 @@ int kp_lp_matmul_ex(int m, int k, int n, const double* a, const double* b, kp_fo
       if (a_finite && use_f16x(std::min(m, n))) {
         DBuf<unsigned> zf;
         ensure_zfix(zf, m, n);
-        g.zfix = zf.p;
+        DBuf<unsigned long long> hsa(m), hsb(n);
+        g.zfix = zf.p, g.hash_a = hsa.p, g.hash_b = hsb.p;
         gemm_f16x(g, KC_PRECOND);
       } else {
         gemm_f16ref(g, KC_PRECOND);

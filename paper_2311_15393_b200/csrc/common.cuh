@@ -35,7 +35,15 @@ struct Unsupported : std::runtime_error {
       throw ::kp::CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-enum KernelClass { KC_OPERATOR = 0, KC_PRECOND = 1, KC_VECTOR = 2, KC_SPECTRAL = 3, KC_COUNT = 4 };
+// KC_PRECOND_AUX: gemm_f16x's row sign hashes and zero-sign fix-up launches
+enum KernelClass {
+  KC_OPERATOR = 0,
+  KC_PRECOND = 1,
+  KC_VECTOR = 2,
+  KC_SPECTRAL = 3,
+  KC_PRECOND_AUX = 4,
+  KC_COUNT = 5
+};
 
 struct Ctx {
   int device = -1;
@@ -46,8 +54,8 @@ struct Ctx {
   // timing: event pairs recorded around launches, per kernel class
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending[KC_COUNT];
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
-  double total_ms[KC_COUNT] = {0, 0, 0, 0};
-  long long count[KC_COUNT] = {0, 0, 0, 0};
+  double total_ms[KC_COUNT] = {};
+  long long count[KC_COUNT] = {};
   cudaEvent_t events[16] = {};
   // dynamic shared-memory limit already set per kernel on this thread's device
   std::unordered_map<const void*, size_t> smem_attr;

@@ -42,6 +42,12 @@ struct F16GemmArgs {
   // unsigned words with [0] = [1] = 0 ([0] listed outputs, [1] fix-up
   // completion counter, [2..] the list); every launch leaves [0] = [1] = 0.
   unsigned* zfix = nullptr;
+  // gemm_f16x only: row sign hashes of A (M words; computed by the call unless
+  // hash_a_ready) and B (N words, computed by the call), and their target sum.
+  unsigned long long* hash_a = nullptr;
+  bool hash_a_ready = false;
+  unsigned long long* hash_b = nullptr;
+  unsigned long long hsum = 0;
 };
 
 int gemm_f16ref_num_ctas(int M, int N);

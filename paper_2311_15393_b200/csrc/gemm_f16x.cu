@@ -51,6 +51,8 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "gemm_f16ref.cuh"
@@ -389,13 +391,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int m = mb + quad * 32 + lane;
       const int n0 = nb + g * 8;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      uint32_t zbits = 0;  // outputs whose tree value is +-0 (sign fixed up later)
+      uint32_t zbits = 0;  // outputs whose tree value is +-0
       if (m < M) {
 #pragma unroll
         for (int p = 0; p < 4; ++p)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
             if (((acc[p] >> (16 * h)) & 0x7fffu) == 0 && n0 + 2 * p + h < N) zbits |= 1u << (2 * p + h);
+        if (zbits) {
+          // Zero outputs: the reference value is -0 iff sign(A(m,k)) != sign(B(n,k))
+          // for all k < K. Necessary condition on the row sign hashes:
+          // hash_a[m] + hash_b[n] == hsum. Otherwise the value is +0 (set here);
+          // candidates keep their bits and go to the exact fix-up.
+          const unsigned long long ha = args.hash_a[m];
+          uint32_t cand = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (((zbits >> q) & 1) && ha + args.hash_b[n0 + q] == args.hsum) cand |= 1u << q;
+          const uint32_t plus = zbits & ~cand;
+#pragma unroll
+          for (int p = 0; p < 4; ++p)
+            acc[p] &= ~((((plus >> (2 * p)) & 1) ? 0x8000u : 0u) | (((plus >> (2 * p + 1)) & 1) ? 0x80000000u : 0u));
+          zbits = cand;
+        }
         const bool full = n0 + 8 <= N;
         if (e.mode == F16OUT_HALF) {
           if (full && e.cn == 1 && ((e.cm * m + n0) & 7) == 0) {
@@ -450,7 +468,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
-      if (zbits) {  // rare: record the output for the sign fix-up
+      if (zbits) {  // rare (hash match): record the output for the exact sign fix-up
         const unsigned base = atomicAdd(args.zfix, unsigned(__popc(zbits)));
         unsigned* list = args.zfix + 2;
         int q = 0;
@@ -481,6 +499,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+// Row sign hashes: out[r] = sum over k < K with sign(X(r,k)) = 1 of R(k)
+// (mod 2^64), R(k) = splitmix64(k) from a table. If row a of A and row b of
+// B have opposite signs at every k then hash_a + hash_b = sum_k R(k); the
+// converse fails only on a 64-bit collision, which the fix-up re-checks.
+__global__ void row_sign_hash_kernel(const __half* X, long ld, int rows, int K,
+                                     const unsigned long long* R, unsigned long long* out) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const long warp0 = (long(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const long nwarps = (long(gridDim.x) * blockDim.x) >> 5;
+  const int KV = K / 8;
+  for (long r = warp0; r < rows; r += nwarps) {
+    const uint4* row = reinterpret_cast<const uint4*>(X + r * ld);
+    unsigned long long h = 0;
+    for (int c = lane; c < KV; c += 32) {
+      const uint4 v = row[c];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if ((w[e >> 1] >> (16 * (e & 1) + 15)) & 1u) h += R[8 * c + e];
+    }
+    const unsigned short* rs = reinterpret_cast<const unsigned short*>(X + r * ld);
+    for (int k = KV * 8 + lane; k < K; k += 32)
+      if (rs[k] & 0x8000u) h += R[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) h += __shfl_xor_sync(0xffffffffu, h, off);
+    if (lane == 0) out[r] = h;
+  }
+}
+
+__global__ void hash_table_kernel(unsigned long long* R, int K) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) {
+    unsigned long long z = (unsigned long long)k + 0x9E3779B97F4A7C15ull;  // splitmix64
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    R[k] = z ^ (z >> 31);
+  }
 }
 
 // Sign fix-up of outputs whose tree value was +-0 (see the header): the
@@ -570,18 +627,66 @@ int counter_levels(int K) {
   return levels;
 }
 
+
+unsigned long long splitmix64(unsigned long long k) {
+  unsigned long long z = k + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// R(k) table for k < K on the calling thread's device (grown on demand; kept
+// for the process lifetime, shared by all threads of the device).
+const unsigned long long* sign_hash_table(int K) {
+  static std::mutex mu;
+  static std::map<int, std::pair<unsigned long long*, int>> tables;
+  std::lock_guard<std::mutex> lk(mu);
+  auto& t = tables[ctx().device];
+  if (t.second < K) {
+    const int cap = std::max(K, 4096);
+    unsigned long long* p = nullptr;
+    KP_CUDA(cudaMalloc(&p, size_t(cap) * sizeof(unsigned long long)));
+    hash_table_kernel<<<cdiv(cap, 256), 256, 0, ctx().stream>>>(p, cap);
+    check_launch("sign hash table");
+    KP_CUDA(cudaStreamSynchronize(ctx().stream));  // usable from every stream
+    t = {p, cap};  // the previous (smaller) table stays allocated: graphs may reference it
+  }
+  return t.first;
+}
+
+void row_hash_launch(const F16Operand& X, int rows, int K, unsigned long long* out) {
+  LaunchScope scope(KC_PRECOND_AUX);
+  const unsigned long long* R = sign_hash_table(K);
+  const int grid = std::max(1, std::min<int>(2 * ctx().num_sms, int(cdiv(rows, 8))));
+  launch_pdl(row_sign_hash_kernel, dim3(grid), dim3(256), 0, X.p, X.ld, rows, K, R, out);
+  check_launch("row sign hash");
+}
+
 }  // namespace
 
 long f16x_zfix_words(int M, int N) { return long(M) * N; }
-
 int gemm_f16x_num_ctas(int M, int N) { return int(cdiv(M, BM) * cdiv(N, BN)); }
 
-void gemm_f16x(const F16GemmArgs& a, int kernel_class) {
-  if (a.M <= 0 || a.N <= 0) return;
-  if (a.K <= 0) throw InvalidArgument("lp_matmul: empty input");
-  if (a.A.ld % BK || a.B.ld % BK || a.A.ld < a.K || a.B.ld < a.K)
+unsigned long long f16x_hash_sum(int K) {
+  unsigned long long s = 0;
+  for (int k = 0; k < K; ++k) s += splitmix64((unsigned long long)k);
+  return s;
+}
+
+void f16x_row_hash(const F16Operand& X, int rows, int K, unsigned long long* out) {
+  row_hash_launch(X, rows, K, out);
+}
+
+void gemm_f16x(const F16GemmArgs& a_in, int kernel_class) {
+  if (a_in.M <= 0 || a_in.N <= 0) return;
+  if (a_in.K <= 0) throw InvalidArgument("lp_matmul: empty input");
+  if (a_in.A.ld % BK || a_in.B.ld % BK || a_in.A.ld < a_in.K || a_in.B.ld < a_in.K)
     throw InvalidArgument("gemm_f16x: operand leading dimension must be a multiple of 64 >= K");
-  if (!a.zfix) throw InvalidArgument("gemm_f16x: zero-sign workspace missing");
+  if (!a_in.zfix || !a_in.hash_a || !a_in.hash_b) throw InvalidArgument("gemm_f16x: zero-sign workspace missing");
+  F16GemmArgs a = a_in;
+  a.hsum = f16x_hash_sum(a.K);
+  if (!a.hash_a_ready) row_hash_launch(a.A, a.M, a.K, a.hash_a);
+  row_hash_launch(a.B, a.N, a.K, a.hash_b);
   const int levels = counter_levels(a.K);
   const int smem_levels = levels > REG_LEVELS ? levels - REG_LEVELS : 0;
   const size_t smem = 1024 + size_t(NSTAGE) * STAGE_BYTES + 2 * size_t(BEXP_BYTES) +
@@ -598,7 +703,7 @@ void gemm_f16x(const F16GemmArgs& a, int kernel_class) {
     check_launch("gemm_f16x");
   }
   {
-    LaunchScope scope(kernel_class);
+    LaunchScope scope(KC_PRECOND_AUX);
     launch_pdl(f16x_zero_fix_kernel, dim3(ctx().num_sms), dim3(256), 0, a);
     check_launch("gemm_f16x zero fix-up");
   }
