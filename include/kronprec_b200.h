@@ -154,6 +154,25 @@ int kp_event_elapsed(int slot_start, int slot_end, float* ms);
 int kp_host_alloc(size_t bytes, void** hptr);
 int kp_host_free(void* hptr);
 
+/* ---- operator setup from a PSF: deblur.hpp / factor.hpp --------------- */
+/* psf_to_kronsum (deblur.hpp:69-70, deblur.cpp:167-199): SVD of the n_p x n_p
+ * PSF array (column-major, center (center_row, center_col)); every term with
+ * s_k > truncation_tol * s_0 becomes a pair of n x n banded Toeplitz factors
+ * (sign-fixed so the largest |u| entry is positive). max_rank > 0 keeps only
+ * the first max_rank terms (the BASELINE configs' rank cap; 0 = none).
+ * row_factors / col_factors receive `capacity` n*n blocks; *rank the number of
+ * terms written. Pass them to kp_operator_create. */
+int kp_psf_to_kronsum(const double* psf, int np, int center_row, int center_col, int n,
+                      double truncation_tol, int max_rank, int capacity, double* row_factors,
+                      double* col_factors, int* rank);
+/* nearest_kron (factor.hpp:34-35, factor.cpp:25-58): one Kronecker pair
+ * (A_r, A_c) for the preconditioner; weighting KronWeighting::Uniform or
+ * ::Toeplitz (the reference default). */
+#define KP_KRON_UNIFORM 0
+#define KP_KRON_TOEPLITZ 1
+int kp_nearest_kron(const double* psf, int np, int center_row, int center_col, int n, int weighting,
+                    double* row_factor, double* col_factor);
+
 /* ---- operator: kron.hpp / kron.cpp ------------------------------------ */
 /* row_factors / col_factors: r consecutive n-by-n column-major matrices,
  * term k = (row_factor_k, col_factor_k) as in KronTerm (kron.hpp:12-15). */

@@ -5,6 +5,7 @@
 // an Eigen caller passes .data() pointers.
 #pragma once
 
+#include <algorithm>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -61,6 +62,18 @@ struct KronTerm {
   Vec row_factor, col_factor;
 };
 
+// SvdTriple (factor.hpp:14-18): column-major n x n u, v; s nonincreasing.
+struct SvdTriple {
+  Vec u, s, v;
+};
+
+// Psf (deblur.hpp:47-54): n_p x n_p column-major values and the center.
+struct Psf {
+  Vec values;
+  int np = 0;
+  int center_row = 0, center_col = 0;
+};
+
 class KroneckerSum {
  public:
   KroneckerSum(std::vector<KronTerm> terms, int n) : terms_(std::move(terms)), n_(n) {
@@ -85,6 +98,36 @@ class KroneckerSum {
   int n_;
   std::shared_ptr<kp_operator> op_;
 };
+
+// psf_to_kronsum (deblur.hpp:69-70); max_rank > 0 caps the number of terms.
+inline KroneckerSum psf_to_kronsum(const Psf& psf, int n, double truncation_tol = 1e-12,
+                                   int max_rank = 0) {
+  if (psf.np < 1 || psf.values.size() != size_t(psf.np) * psf.np)
+    throw std::invalid_argument("psf_to_kronsum: psf values must be np x np");
+  const int cap = max_rank > 0 ? std::min(max_rank, psf.np) : psf.np;
+  const size_t nn = size_t(n) * n;
+  Vec rows(size_t(cap) * nn), cols(size_t(cap) * nn);
+  int r = 0;
+  check(kp_psf_to_kronsum(psf.values.data(), psf.np, psf.center_row, psf.center_col, n, truncation_tol,
+                          max_rank, cap, rows.data(), cols.data(), &r));
+  std::vector<KronTerm> terms(r);
+  for (int k = 0; k < r; ++k) {
+    terms[k].row_factor.assign(rows.begin() + k * nn, rows.begin() + (k + 1) * nn);
+    terms[k].col_factor.assign(cols.begin() + k * nn, cols.begin() + (k + 1) * nn);
+  }
+  return KroneckerSum(std::move(terms), n);
+}
+// nearest_kron (factor.hpp:34-35)
+inline KronTerm nearest_kron(const Psf& psf, int n, int weighting = KP_KRON_TOEPLITZ) {
+  if (psf.np < 1 || psf.values.size() != size_t(psf.np) * psf.np)
+    throw std::invalid_argument("nearest_kron: psf values must be np x np");
+  KronTerm t;
+  t.row_factor.resize(size_t(n) * n);
+  t.col_factor.resize(size_t(n) * n);
+  check(kp_nearest_kron(psf.values.data(), psf.np, psf.center_row, psf.center_col, n, weighting,
+                        t.row_factor.data(), t.col_factor.data()));
+  return t;
+}
 
 inline Vec kronsum_apply(const KroneckerSum& k, const Vec& y) {  // kron.cpp:73-79
   Vec out(y.size());
@@ -126,8 +169,24 @@ class KronSvdPreconditioner {
 inline KronSvdPreconditioner build_preconditioner(const Vec& a_r, const Vec& a_c, int n,
                                                   double lambda, kp_format fmt,
                                                   int accum = KP_ACCUM_REFERENCE) {
+  if (n < 1 || a_r.size() != size_t(n) * n || a_c.size() != size_t(n) * n)  // factor.cpp:84-87
+    throw std::invalid_argument("build_preconditioner: factors must be square and equally sized");
   kp_precond* p = nullptr;  // factor.cpp:80-104
   check(kp_precond_build(a_r.data(), a_c.data(), n, lambda, fmt, accum, &p));
+  return KronSvdPreconditioner(p);
+}
+// The same preconditioner from SVDs the caller already holds (the
+// reference's KronSvdPreconditioner::svd_r / svd_c): no SVD is recomputed.
+inline KronSvdPreconditioner build_preconditioner_from_svd(const SvdTriple& r, const SvdTriple& c, int n,
+                                                           double lambda, kp_format fmt,
+                                                           int accum = KP_ACCUM_REFERENCE) {
+  const size_t nn = size_t(n) * n;
+  if (n < 1 || r.u.size() != nn || r.v.size() != nn || c.u.size() != nn || c.v.size() != nn ||
+      r.s.size() != size_t(n) || c.s.size() != size_t(n))
+    throw std::invalid_argument("build_preconditioner: factors must be square and equally sized");
+  kp_precond* p = nullptr;
+  check(kp_precond_build_from_svd(n, r.u.data(), r.s.data(), r.v.data(), c.u.data(), c.s.data(),
+                                  c.v.data(), lambda, fmt, accum, &p));
   return KronSvdPreconditioner(p);
 }
 inline KronSvdPreconditioner with_lambda(const KronSvdPreconditioner& p, double lambda) {
@@ -136,6 +195,8 @@ inline KronSvdPreconditioner with_lambda(const KronSvdPreconditioner& p, double 
   return KronSvdPreconditioner(q);
 }
 inline Vec precond_solve(const KronSvdPreconditioner& p, const Vec& r) {  // factor.cpp:117-132
+  const int n = p.n();
+  if (r.size() != size_t(n) * n) throw std::invalid_argument("precond_solve: vector length is not n^2");
   Vec z(r.size());
   check(kp_precond_solve(p.handle(), r.data(), z.data()));
   return z;
@@ -164,8 +225,16 @@ struct SolveResult {
 namespace detail {
 template <typename F>
 SolveResult solve(const KroneckerSum& a, const Vec& b, const SolverOptions& o, F&& call) {
-  const size_t nn = size_t(a.n()) * a.n();
+  const size_t nn = size_t(a.n()) * a.n();  // check_common, krylov.cpp:12-27
   if (b.size() != nn) throw std::invalid_argument("solver: right-hand side length mismatch");
+  if (o.max_iterations < 1) throw std::invalid_argument("solver: max_iterations must be at least 1");
+  if (!(o.rel_residual_tol > 0.0)) throw std::invalid_argument("solver: tolerance must be positive");
+  if (o.x_true) {
+    if (o.x_true->size() != nn) throw std::invalid_argument("solver: x_true length mismatch");
+    bool nonzero = false;
+    for (double v : *o.x_true) nonzero = nonzero || v != 0.0;
+    if (!nonzero) throw std::invalid_argument("solver: x_true must be nonzero");
+  }
   const int cap = o.max_iterations + 1;
   SolveResult r;
   r.x.resize(nn);

@@ -75,7 +75,8 @@ EXPORTS = [
     "kp_discrepancy", "kp_operator_set_mode", "kp_operator_get_mode", "kp_event_record", "kp_event_elapsed", "kp_host_alloc", "kp_host_free",
     "kp_spectral_create_x", "kp_spectral_export_xhat", "kp_opt_objective", "kp_wgcv_objective",
     "kp_lambda_opt", "kp_wgcv", "kp_filtered_solution", "kp_round_array", "kp_lp_matmul",
-    "kp_lp_matmul_ex", "kp_set_fp16_products", "kp_get_fp16_products",
+    "kp_lp_matmul_ex", "kp_set_fp16_products", "kp_get_fp16_products", "kp_psf_to_kronsum",
+    "kp_nearest_kron",
 ]
 
 _lib = None
@@ -138,6 +139,8 @@ def lib() -> C.CDLL:
             "kp_host_alloc": ([C.c_size_t, C.POINTER(C.c_void_p)], I),
             "kp_host_free": ([P], I),
             "kp_set_fp16_products": ([I], I),
+            "kp_psf_to_kronsum": ([P, I, I, I, I, D, I, I, P, P, C.POINTER(I)], I),
+            "kp_nearest_kron": ([P, I, I, I, I, I, P, P], I),
             "kp_get_fp16_products": ([I, C.POINTER(I)], I),
         }
         for name, (args, res) in sig.items():

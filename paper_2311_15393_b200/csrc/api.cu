@@ -752,6 +752,14 @@ void check_common(const kp_operator* op, const kp_solver_options* o, kp_history*
   if (!(o->rel_residual_tol > 0.0)) throw InvalidArgument("solver: tolerance must be positive");
   if (h->capacity < 1 || !h->residual_norm || !h->work_units)
     throw InvalidArgument("solver: history arrays missing");
+  if (o->record_iterates) {  // the iterate buffer is sized for max_iterations + 1 rows up front
+    if (!h->iterates) throw InvalidArgument("solver: record_iterates needs kp_history.iterates");
+    size_t free_b = 0, total_b = 0;
+    KP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const double need = double(o->max_iterations + 1) * double(op->n) * op->n * sizeof(double);
+    if (need > 0.5 * double(free_b))
+      throw InvalidArgument("solver: record_iterates needs (max_iterations + 1) n^2 doubles of device memory");
+  }
 }
 
 std::string abort_message(int code, int k) {
@@ -892,6 +900,7 @@ void finish(Solve& s, const kp_solver_options* o, kp_history* h, double work) {
   d2h(pst, s.st, sizeof(DevState));
   sync();
   const DevState st = *pst;
+  if (st.status == ST_INVALID) throw InvalidArgument("solver: x_true must be nonzero");
   const int rows = std::min(st.rows, h->capacity);
   const int ncos = std::min(st.ncos, h->capacity);
   d2h(h->residual_norm, s.resid, rows * sizeof(double));
@@ -1281,6 +1290,37 @@ void project_dev(int n, const double* ul, const double* ur, const double* x, dou
   }
 
 extern "C" {
+// host setup routines of problem.cpp (same library)
+const char* kpg_last_error(void);
+int kpg_psf_to_kronsum(const double* psf, int np, int crow, int ccol, int n, double tol, int max_rank,
+                       int capacity, double* row_factors, double* col_factors, int* r_out,
+                       double* truncated_psf);
+int kpg_nearest_kron(const double* psf, int np, int crow, int ccol, int n, int weighting,
+                     double* row_factor, double* col_factor);
+}
+
+namespace {
+void check_gen(int status) {  // problem.cpp status (1 invalid_argument, 2 runtime)
+  if (status == 0) return;
+  if (status == 1) throw InvalidArgument(kpg_last_error());
+  throw std::runtime_error(kpg_last_error());
+}
+}  // namespace
+
+// Host-only entry points (setup on the CPU, no device needed).
+#define KP_API_HOST(...)                                \
+  try {                                                 \
+    __VA_ARGS__;                                        \
+    return KP_OK;                                       \
+  } catch (const std::invalid_argument& e) {            \
+    kp::g_last_error = e.what();                        \
+    return KP_ERR_INVALID_ARGUMENT;                     \
+  } catch (const std::exception& e) {                   \
+    kp::g_last_error = e.what();                        \
+    return KP_ERR_RUNTIME;                              \
+  }
+
+extern "C" {
 
 const char* kp_last_error(void) { return kp::g_last_error.c_str(); }
 
@@ -1288,9 +1328,13 @@ int kp_init(int device) {
   KP_API({
     Ctx& c = ctx();
     if (device != c.device) {
+      // Handles created on the previous device keep the stream they were
+      // allocated on (DBuf frees on it), so the old stream is not destroyed;
+      // the per-kernel smem limits and events belong to the old device.
       KP_CUDA(cudaSetDevice(device));
-      if (c.stream) cudaStreamDestroy(c.stream);
       KP_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      c.smem_attr.clear();
+      for (auto& e : c.events) e = nullptr;
       KP_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
       init_pool(device);
       c.device = device;
@@ -1338,11 +1382,10 @@ int kp_get_fp16_products(int n, int* uses_tensor) {
 }
 int kp_event_record(int slot) {
   KP_API({
-    static cudaEvent_t ev[16] = {};
     if (slot < 0 || slot >= 16) throw InvalidArgument("event slot out of range");
-    if (!ev[slot]) KP_CUDA(cudaEventCreate(&ev[slot]));
-    KP_CUDA(cudaEventRecord(ev[slot], ctx().stream));
-    ctx().events[slot] = ev[slot];
+    Ctx& c = ctx();  // the calling thread's events, created on its device
+    if (!c.events[slot]) KP_CUDA(cudaEventCreate(&c.events[slot]));
+    KP_CUDA(cudaEventRecord(c.events[slot], c.stream));
   })
 }
 int kp_event_elapsed(int a, int b, float* ms) {
@@ -1439,6 +1482,32 @@ int kp_normal_matvec(const kp_operator* opc, double lambda, const double* p, dou
     op_apply(op, da.p, dz.p, true, &e, nullptr);
     dz.download(out, nn);
     sync();
+  })
+}
+
+// psf_to_kronsum (deblur.cpp:167-199) and nearest_kron (factor.cpp:25-58):
+// host setup, FP64 SVD of the n_p x n_p PSF array.
+int kp_psf_to_kronsum(const double* psf, int np, int center_row, int center_col, int n,
+                      double truncation_tol, int max_rank, int capacity, double* row_factors,
+                      double* col_factors, int* rank) {
+  KP_API_HOST({
+    if (!psf || np < 1 || !row_factors || !col_factors || !rank || capacity < 1)
+      throw InvalidArgument("psf_to_kronsum: bad arguments");
+    if (center_row < 0 || center_row >= np || center_col < 0 || center_col >= np)
+      throw InvalidArgument("psf_to_kronsum: center outside the psf");
+    check_gen(kpg_psf_to_kronsum(psf, np, center_row, center_col, n, truncation_tol, max_rank, capacity,
+                                 row_factors, col_factors, rank, nullptr));
+  })
+}
+int kp_nearest_kron(const double* psf, int np, int center_row, int center_col, int n, int weighting,
+                    double* row_factor, double* col_factor) {
+  KP_API_HOST({
+    if (!psf || np < 1 || !row_factor || !col_factor) throw InvalidArgument("nearest_kron: bad arguments");
+    if (weighting != KP_KRON_UNIFORM && weighting != KP_KRON_TOEPLITZ)
+      throw InvalidArgument("nearest_kron: unknown weighting");
+    if (center_row < 0 || center_row >= np || center_col < 0 || center_col >= np)
+      throw InvalidArgument("nearest_kron: center outside the psf");
+    check_gen(kpg_nearest_kron(psf, np, center_row, center_col, n, weighting, row_factor, col_factor));
   })
 }
 
@@ -1826,6 +1895,8 @@ int kp_wgcv_objective(const kp_spectral* sd, double omega, double lambda, double
 // discrepancy (regparam.cpp:288-327)
 int kp_discrepancy(const kp_spectral* sd, double noise_norm, double eta, kp_param_choice* choice) {
   KP_API({
+    check_spectral(sd, false);  // regparam.cpp: validation order of discrepancy()
+    if (!choice) throw InvalidArgument("discrepancy: null output");
     if (!(noise_norm > 0.0)) throw InvalidArgument("discrepancy: noise_norm must be positive");
     if (!(eta > 0.0)) throw InvalidArgument("discrepancy: eta must be positive");
     const double eps = eta * noise_norm;

@@ -183,6 +183,10 @@ __global__ void pcg_init_scalar_kernel(DevState* st, DevHistory h, const double*
   const double rr = sum_partials(part_r, nr, 0);
   const double xx = st->has_xt ? sum_partials(part_xt, nxt, 0) : 0.0;
   if (threadIdx.x) return;
+  if (st->has_xt && xx == 0.0) {  // solver: x_true must be nonzero
+    st->status = ST_INVALID;
+    return;
+  }
   st->r0 = sqrt(rr);
   st->xnorm = sqrt(xx);
   h.resid[0] = st->r0;  // rec.row(0, x = 0, r0)
@@ -406,6 +410,10 @@ __global__ void cgls_init_scalar_kernel(DevState* st, DevHistory h, const double
   const double ss = sum_partials(part_s, ns, 0);
   const double xx = st->has_xt ? sum_partials(part_xt, nxt, 0) : 0.0;
   if (threadIdx.x) return;
+  if (st->has_xt && xx == 0.0) {  // solver: x_true must be nonzero
+    st->status = ST_INVALID;
+    return;
+  }
   st->r0 = sqrt(ss);
   st->xnorm = sqrt(xx);
   h.resid[0] = st->r0;

@@ -7,7 +7,8 @@
 namespace kp {
 
 // Solver status values (DevState::status).
-enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_ABORTED = 2, ST_MAXIT = 3 };
+// ST_INVALID: x_true is all zero (krylov.cpp:21-25 throws invalid_argument)
+enum { ST_RUNNING = 0, ST_CONVERGED = 1, ST_ABORTED = 2, ST_MAXIT = 3, ST_INVALID = 4 };
 // Abort codes -> reference messages (krylov.cpp:75-139, 175-194).
 enum {
   AB_NONE = 0,

@@ -60,6 +60,55 @@ int main() {
   const Vec xf = filtered_solution(mx, b, 0.05);
   CHECK(xf.size() == b.size() && std::isfinite(xf[0]));
 
+  // operator setup from a PSF (deblur.hpp:69-70, factor.hpp:34-35): a
+  // separable 5 x 5 PSF is one Kronecker term, and nearest_kron returns it
+  Psf psf;
+  psf.np = 5;
+  psf.center_row = psf.center_col = 2;
+  const double g[5] = {0.1, 0.2, 0.4, 0.2, 0.1};
+  for (int j = 0; j < 5; ++j)
+    for (int i = 0; i < 5; ++i) psf.values.push_back(g[i] * g[j]);
+  KroneckerSum ap = psf_to_kronsum(psf, 16);
+  const Vec ones(256, 1.0);
+  const Vec ay = kronsum_apply(ap, ones);
+  CHECK(std::fabs(ay[8 * 16 + 8] - 1.0) <= 1e-12);  // interior pixel: the PSF sums to 1
+  const KronTerm nk = nearest_kron(psf, 16);
+  CHECK(nk.row_factor.size() == 256 && std::fabs(nk.row_factor[8 * 16 + 8] * nk.col_factor[8 * 16 + 8] - 0.16) <= 1e-12);
+  KroneckerSum ap2 = psf_to_kronsum(psf, 16, 1e-12, 1);  // rank cap
+  CHECK(std::fabs(kronsum_apply(ap2, ones)[8 * 16 + 8] - 1.0) <= 1e-12);
+
+  // the preconditioner from caller-held SVDs (KronSvdPreconditioner::svd_r /
+  // svd_c) equals the one the library builds: diagonal factors, u = v = I
+  Vec d(size_t(n) * n, 0.0);
+  const double dv[4] = {2.0, 1.5, 1.0, 0.5};
+  for (int i = 0; i < n; ++i) d[size_t(i) * n + i] = dv[i];
+  SvdTriple sv{eye(n), Vec(dv, dv + 4), eye(n)};
+  KronSvdPreconditioner ms = build_preconditioner_from_svd(sv, sv, n, 0.1, fp16());
+  KronSvdPreconditioner mb = build_preconditioner(d, d, n, 0.1, fp16());
+  const Vec zs = precond_solve(ms, b), zb = precond_solve(mb, b);
+  bool same = true;
+  for (int i = 0; i < 16; ++i) same = same && zs[i] == zb[i];
+  CHECK(same);
+
+  // the reference's argument checks (krylov.cpp:12-27, factor.cpp:84-87, :119-120)
+  bool threw_len = false;
+  try { precond_solve(ms, Vec(15, 1.0)); } catch (const std::invalid_argument&) { threw_len = true; }
+  CHECK(threw_len);
+  bool threw_fac = false;
+  try { build_preconditioner(eye(n), Vec(15, 1.0), n, 0.1, fp16()); } catch (const std::invalid_argument&) { threw_fac = true; }
+  CHECK(threw_fac);
+  const Vec zero(16, 0.0);
+  SolverOptions oz;
+  oz.x_true = &zero;
+  bool threw_x = false;
+  try { cgls(I, b, oz); } catch (const std::invalid_argument&) { threw_x = true; }
+  CHECK(threw_x);
+  SolverOptions o0;
+  o0.max_iterations = 0;
+  bool threw_it = false;
+  try { cgls(I, b, o0); } catch (const std::invalid_argument&) { threw_it = true; }
+  CHECK(threw_it);
+
   // errors surface as the reference's exception types
   bool threw = false;
   try { build_preconditioner(eye(2), eye(2), 2, -1.0, fp64()); } catch (const std::invalid_argument&) { threw = true; }

@@ -109,3 +109,38 @@ def test_config_shapes_reduced():
     c4 = [configs.build("C4", image=i, n=64).problem.noise_level for i in range(3)]
     assert c4 == [0.001, 0.01, 0.05]
     assert configs.GCV_GRID[0] == 1e-4 and configs.GCV_GRID[-1] == 1.0 and configs.GCV_GRID.size == 64
+
+
+def test_c_abi_psf_to_kronsum_and_nearest_kron():
+    """kp_psf_to_kronsum / kp_nearest_kron (the boundary's operator setup,
+    deblur.hpp:69-70, factor.hpp:34-35) are host-only: they run here without a
+    GPU and agree with the package wrappers and the oracle."""
+    import ctypes as C
+    from paper_2311_15393_b200._lib import check, lib, ptr
+    from oracle import pyoracle as O
+    L = lib()
+    psf = P.make_psf("gaussian", 9, sigma=1.5)
+    n = 24
+    v = np.asfortranarray(psf.values)
+    rows = np.zeros((n, n * 9), order="F")
+    cols = np.zeros((n, n * 9), order="F")
+    r = C.c_int()
+    check(L.kp_psf_to_kronsum(ptr(v), 9, psf.center_row, psf.center_col, n, 1e-12, 0, 9, ptr(rows),
+                              ptr(cols), C.byref(r)))
+    a, _ = P.psf_to_kronsum(psf, n)
+    assert r.value == len(a.terms)
+    for k, t in enumerate(a.terms):
+        assert np.array_equal(rows[:, k * n:(k + 1) * n], t.row_factor)
+        assert np.array_equal(cols[:, k * n:(k + 1) * n], t.col_factor)
+    for weighting, code in (("uniform", 0), ("toeplitz", 1)):
+        rf = np.zeros((n, n), order="F")
+        cf = np.zeros((n, n), order="F")
+        check(L.kp_nearest_kron(ptr(v), 9, psf.center_row, psf.center_col, n, code, ptr(rf), ptr(cf)))
+        t = P.nearest_kron(psf, n, weighting)
+        assert np.array_equal(rf, t.row_factor) and np.array_equal(cf, t.col_factor)
+        if weighting == "toeplitz":  # the oracle restates the reference default
+            orf, ocf = O.nearest_kron(psf, n)
+            assert np.allclose(rf, orf, rtol=0, atol=1e-12) and np.allclose(cf, ocf, rtol=0, atol=1e-12)
+    # argument errors are KP_ERR_INVALID_ARGUMENT with the reference's message
+    assert L.kp_nearest_kron(ptr(v), 9, 4, 4, 5, 1, ptr(rf), ptr(cf)) == 1
+    assert b"image smaller than psf" in L.kp_last_error()
