@@ -15,6 +15,11 @@ C4.json (it checkpoints after every image).
 C5fpcg writes C5_fpcg_full.json: the headline FPCG run to its end;
 C5cgls writes C5_cgls_full.json: the CGLS run to convergence;
 C5pcg64 writes C5_pcg64_full.json: PCG with the FP64 preconditioner.
+C5cglsiter writes C5_cgls_iterates.json: the first 5 CGLS iterates at n=4096
+  as norms + projections on 4 seeded vectors (the iterates themselves are
+  134 MB each).
+M4096 / M1664 write msolve_n<n>.json: bitwise digests of precond_solve on the
+  seeded binary16-exact factors of tests/golden/msolve_inputs.py.
 """
 from __future__ import annotations
 
@@ -107,6 +112,48 @@ def gen(name: str, prefix: int | None = None, images=(0,), only=None, tag=None, 
     print("wrote", path, flush=True)
 
 
+def projection_vectors(nn: int, count: int = 4):
+    """Seeded probe vectors for iterate fingerprints (shared with the tests)."""
+    return [np.random.default_rng(9000 + j).standard_normal(nn) for j in range(count)]
+
+
+def gen_cgls_iterates(iters: int = 5):
+    cfg = configs.build("C5")
+    opts = SolverOptions(lambda_=cfg.lambda_, max_iterations=iters, rel_residual_tol=cfg.tol,
+                         x_true=cfg.problem.x_true, record_iterates=True)
+    t0 = time.time()
+    _, h = O.cgls(cfg.problem.a, cfg.problem.b, opts)
+    w = projection_vectors(cfg.n * cfg.n)
+    rows = [{"norm": float(np.linalg.norm(x)), "proj": [float(x @ v) for v in w]} for x in h.iterates]
+    out = {"config": "C5", "solver": "cgls", "iterations": iters, "lambda": cfg.lambda_,
+           "probe_seeds": [9000 + j for j in range(len(w))], "probe_norms": [float(np.linalg.norm(v)) for v in w],
+           "iterates": rows, "residual_norm": h.residual_norm, "relative_error": h.relative_error,
+           "seconds": time.time() - t0,
+           "generator": "oracle/kp_oracle.cpp via tests/golden/gen_goldens.py C5cglsiter"}
+    path = os.path.join(HERE, "C5_cgls_iterates.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print("wrote", path, f"{out['seconds']:.1f}s", flush=True)
+
+
+def gen_msolve(n: int, seed: int = 4242):
+    sys.path.insert(0, HERE)
+    from msolve_inputs import digest, msolve_case
+    out = {"n": n, "seed": seed, "cases": {},
+           "generator": f"oracle/kp_oracle.cpp via tests/golden/gen_goldens.py M{n}"}
+    for regime in ("wide", "low"):
+        sr, sc, lam, r = msolve_case(n, seed, regime)
+        t0 = time.time()
+        m = O.build_preconditioner_from_svd(sr, sc, lam, FMT["fp16"])
+        z = O.precond_solve(m, r)
+        out["cases"][regime] = {"lambda": lam, "digest": digest(z), "seconds": time.time() - t0}
+        print(n, regime, out["cases"][regime], flush=True)
+    path = os.path.join(HERE, f"msolve_n{n}.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print("wrote", path, flush=True)
+
+
 if __name__ == "__main__":
     threads = 8
     args = [a for a in sys.argv[1:]]
@@ -124,6 +171,10 @@ if __name__ == "__main__":
             gen("C5", only="fpcg", tag="C5_fpcg_full")
         elif name == "C5cgls":  # CGLS to convergence (about 45 min on 8 threads)
             gen("C5", only="cgls", tag="C5_cgls_full")
+        elif name == "C5cglsiter":
+            gen_cgls_iterates()
+        elif name.startswith("M") and name[1:].isdigit():
+            gen_msolve(int(name[1:]))
         elif name == "C5pcg64":  # PCG with the FP64 preconditioner to convergence
             gen("C5", only="pcg", tag="C5_pcg64_full")
         else:

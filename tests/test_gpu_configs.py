@@ -237,3 +237,31 @@ def test_c5_pcg_fp64_full_solve_vs_golden():
     cfg = configs.build("C5")
     (run,) = device_runs(cfg, cfg.lambda_, [("pcg", "fp64", 100)])
     check_against(run, ref, prefix_rows=20)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C5"])
+def test_tensor_mode_at_config_scale(name):
+    """The tcgen05 tensor-mode preconditioner (fp32 accumulation, one binary16
+    rounding per product matrix; KP_ACCUM_TENSOR) at BASELINE sizes, against
+    the reference-exact run (goldens from the oracle).
+
+    C1: the reference converges; tensor mode must land within 1e-3 of its
+    final relative error and need no more than 2 extra iterations.
+    C2 / C5: the reference's per-product rounding underflows once the
+    residual reaches ~1e-6 and it stagnates until the positivity abort
+    (DESIGN.md §4). Tensor mode does not stagnate there, so the north star's
+    +-2-iteration bound cannot hold by construction; asserted instead: tensor
+    mode reaches a final relative error no worse than the reference's, and
+    never reports the reference's abort."""
+    cfg = configs.build(name)
+    g = golden({"C5": "C5_fpcg_full"}.get(name, name))["images"][0]["runs"][0]
+    (run,) = device_runs(cfg, cfg.lambda_, cfg.solvers[:1], accum="tensor")
+    h = run.history
+    if name == "C1":
+        assert g["converged"] and h.converged
+        assert abs(h.relative_error[-1] - g["relative_error"][-1]) <= 1e-3
+        assert h.iterations_used <= g["iterations_used"] + 2
+    else:
+        assert not g["converged"] and "lost positivity" in g["abort_reason"]
+        assert "lost positivity" not in h.abort_reason
+        assert h.relative_error[-1] <= g["relative_error"][-1] + 1e-3

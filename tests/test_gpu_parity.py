@@ -468,9 +468,10 @@ def test_tensor_mode_solver_within_north_star_bounds(solver):
     _, ho = getattr(O, solver)(tp.a, tp.b, o, opts)
     assert rg.history.converged
     assert abs(rg.history.relative_error[-1] - ho.relative_error[-1]) <= 1e-3
-    # iteration-count parity is reported (SURVEY §0.5 expects fp32 accumulation
-    # to change the count); the bound is checked at config scale in
-    # tests/test_gpu_configs.py
+    # fp32 accumulation changes the count: tensor mode never
+    # needs more than 2 iterations beyond the reference; the config-scale
+    # behaviour (C1 within the bounds, C2 / C5 where the reference stagnates)
+    # is asserted in tests/test_gpu_configs.py::test_tensor_mode_at_config_scale
     assert rg.history.iterations_used <= ho.iterations_used + 2
 
 
