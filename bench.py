@@ -5,16 +5,19 @@ Workload (N=1): config C5 — n=4096 (16.7M unknowns), rank-5 Kronecker-sum
 blur, FPCG with the fp16 Kronecker-SVD preconditioner (reference-exact
 per-op rounding), lambda=0.01, tol 1e-6, max 100 iterations. One "step" is
 one full FPCG solve; the metric is solver iterations per second over the K
-timed steps. N>1: one independent C5 image per GPU (weak scaling, replicas;
-no data-path collective — results are gathered with NCCL).
+timed steps. N>1 (torchrun): config C4, the BASELINE batched metric —
+solves/s over the 64-image batch, images sharded over the ranks (strong
+scaling), one batched PCG state machine per GPU, NCCL only to gather the
+per-image results and the timing. `--config` overrides either default.
 
   value       device-resident b / x (kp_fpcg with device pointers)
   e2e         the C-ABI call with pinned HOST buffers (b, x_true in; x out)
-  roofline    dominant kernel = FP64 DMMA operator GEMM, FLOP-bound against
-              the measured DMMA peak (profiles/r01_microbench_peaks.txt)
+  roofline    dominant kernel = the reference-exact binary16 M-solve GEMM
+              (gemm_f16x: tcgen05 rounded products + f16x2 tree adds)
   cpu_baseline  the CPU oracle (C++ restatement of the reference, OpenBLAS +
               streamed fp16 emulation) timed on the host cores for one
-              iteration's operator + preconditioner work
+              iteration's operator + preconditioner work (all threads, and a
+              1-thread sample like the single-threaded reference)
 
 `--impl reference` times that CPU implementation as the reference arm.
 """
@@ -37,9 +40,8 @@ sys.path.insert(0, ROOT)
 DMMA_PEAK_TFLOPS = 37.07  # measured, profiles/r01_microbench_peaks_v2.txt (m16n8k16 f64)
 DFMA_PEAK_TFLOPS = 33.88  # measured DFMA (FP64 ALU) peak, same microbenchmark
 F16X2_PEAK_TOPS = 36.9    # measured f16x2 mul+add half-ops/s, same file
-BF16_PEAK_TFLOPS = 1653.4  # MEASURED_PEAKS.json bf16_tflops (burst; fp16 kind::f16 same rate)
 # DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the
-# committed ncu --set full captures (profiles/r01_ncu_key_metrics.txt)
+# committed ncu --set full captures (profiles/r01_ncu_key_metrics.txt, r02_*)
 TRAFFIC = {
     ("gemm_f16ref_kernel", 4096): 68.29e6 + 21.03e6,   # r01_gemm_f16ref_u64_n4096.ncu-rep
     ("gemm_f16tc_kernel", 4096): (73.37e6 + 13.91e6 + 118.5e6 + 18.64e6 + 72.79e6 + 13.88e6
@@ -49,12 +51,19 @@ TRAFFIC = {
 
 
 def peaks():
+    """Driver-measured roofline denominators (MEASURED_PEAKS.json): HBM copy
+    GB/s and cuBLAS bf16 TFLOP/s, burst (kernel timed alone) and sustained
+    (seconds-long loop under the power cap); the recipe's fallback if absent."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(p) as f:
-            return json.load(f)
-    except OSError:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "MEASURED_PEAKS.json (measured)"}
+    except (OSError, KeyError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "B200_PROFILING.md fallback"}
 
 
 class ClockSampler:
@@ -203,6 +212,42 @@ def cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads: int) -> float:
     return time.perf_counter() - t0
 
 
+def cpu_iteration_single_thread(cfg, fmt, slab: int = 128) -> dict:
+    """One FPCG iteration's operator + preconditioner work on ONE host thread
+    (the reference is single-threaded: no OpenMP in proj/CMakeLists.txt),
+    from a bounded sample: one dense one-term kron_apply (2 FP64 GEMMs of
+    n^3, the oracle's OpenBLAS on 1 thread) and one `slab`-row block of a
+    reference-exact binary16 lp_matmul (slab x n x n), extrapolated to the
+    iteration's 2 r applies of the operator (normal_matvec) and 4 full n^3
+    lp_matmuls (precond_solve)."""
+    from oracle import pyoracle as O
+    import paper_2311_15393_b200 as K
+    n = cfg.n
+    slab = min(slab, n)
+    O.set_threads(1)
+    try:
+        rng = np.random.default_rng(0)
+        one = K.KroneckerSum([cfg.problem.a.terms[0]], n)
+        x = rng.standard_normal(n * n)
+        t0 = time.perf_counter()
+        O.kronsum_apply(one, x)
+        t_apply = time.perf_counter() - t0
+        a = rng.uniform(-1, 1, (slab, n)).astype(np.float16).astype(np.float64)
+        b = rng.uniform(-1, 1, (n, n)).astype(np.float16).astype(np.float64)
+        t0 = time.perf_counter()
+        O.lp_matmul(a, b, fmt)
+        t_slab = time.perf_counter() - t0
+    finally:
+        O.set_threads(os.cpu_count() or 1)
+    r = len(cfg.problem.a.terms)
+    t_iter = 2 * r * t_apply + 4 * (n / slab) * t_slab
+    return {"value": 1.0 / t_iter, "unit": "iterations/s", "cores": 1, "kind": "port",
+            "sample": f"1 thread: one one-term kron_apply at n={n} ({t_apply:.2f} s) and a {slab}-row "
+                      f"block of one binary16 lp_matmul ({t_slab:.2f} s), extrapolated to 2r={2 * r} "
+                      f"applies + 4 full lp_matmuls per iteration",
+            "sample_s": t_apply + t_slab}
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -226,6 +271,8 @@ def run_reference(args):
                                         cfg.eta)["lambda"]
     setup_s = time.time() - t0
     solver_name = cfg.solvers[0][0]
+    if args.config == "C4":
+        return run_reference_c4(args, cfg, svd_r, svd_c, fmt, threads, setup_s)
     for _ in range(args.warmup):
         cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads)
     times = [cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads) for _ in range(args.steps)]
@@ -238,7 +285,8 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64+f16(emulated)", "data": "synthetic",
-        "config": workload_config(cfg, device=False),
+        "config": workload_config(cfg),
+        "run_info": {"l2": "host CPU run (no GPU L2 involved)"},
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": threads, "kind": "port",
                          "sample": f"one {solver_name.upper()} iteration's normal_matvec + "
                                    "precond_solve (fp16 reference-exact emulation) per step"},
@@ -248,6 +296,55 @@ def run_reference(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_c4_image_sample(cfg, svd_r, svd_c, fmt, threads) -> float:
+    """Seconds per C4 image on the CPU oracle: the lambda selection (spectral
+    data + discrepancy) timed, plus one PCG iteration's operator +
+    preconditioner work timed and scaled to the image's 100 iterations."""
+    from oracle import pyoracle as O
+    O.set_threads(threads)
+    m0 = O.build_preconditioner_from_svd((svd_r.u, svd_r.s, svd_r.v), (svd_c.u, svd_c.s, svd_c.v), 1.0, fmt)
+    t0 = time.perf_counter()
+    so, bo = O.spectral(m0, cfg.problem.b)
+    O.discrepancy(so, bo, float(np.linalg.norm(cfg.problem.noise)), cfg.eta)
+    t_sel = time.perf_counter() - t0
+    return t_sel + 100 * cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads)
+
+
+def run_reference_c4(args, cfg, svd_r, svd_c, fmt, threads, setup_s):
+    """Reference arm for C4 (solves/s over the image batch): per step one
+    image's lambda selection (spectral data + discrepancy, on the oracle)
+    plus one PCG iteration's operator + preconditioner work, extrapolated to
+    the 100 iterations every C4 image runs (the reference-exact solves
+    stagnate to the cap; tests/golden/C4.json)."""
+    def step():
+        return cpu_c4_image_sample(cfg, svd_r, svd_c, fmt, threads)
+
+    for _ in range(args.warmup):
+        step()
+    per_image = [step() for _ in range(args.steps)]
+    value = args.steps / sum(per_image)
+    metric = METRIC_C4 if cfg.n == 1024 else METRIC_C4.replace("1024^2", f"{cfg.n}^2")
+    line = {"impl": "reference", "metric": metric, "value": value, "unit": "solves/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(per_image) / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64+f16(emulated)", "data": "synthetic",
+            "config": c4_config(),
+            "run_info": {"l2": "host CPU run (no GPU L2 involved)"},
+            "cpu_baseline": {"value": value, "unit": "solves/s", "cores": threads, "kind": "port",
+                             "sample": "per step: one C4 image's spectral data + discrepancy lambda and one "
+                                       "PCG iteration (normal_matvec + precond_solve), extrapolated to the "
+                                       "image's 100 iterations"},
+            "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup_s": setup_s}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def c4_config() -> dict:
+    return {"workload": "C4: 64 x n=1024, Gaussian sigma=2.5, noise 0.1/1/5 %, discrepancy eta=1.01, "
+                        "PCG fp16 tol 1e-6", "images": 64}
 
 
 METRIC = "PCG iterations/s at 4096^2 image"
@@ -284,23 +381,57 @@ def run_c4(args):
     mine = list(shard(images, ws, rank))
     sh = C4Shard(n=args.size, svd=args.svd, device=local)
     probs = {i: sh.problem(i) for i in mine}  # input generation is not timed
-    warm = mine[: max(1, min(args.warmup, len(mine)))]
-    sh.solve_many(warm, probs, args.workers)
+    batched = args.c4_mode == "batch"
+
+    def run_all():
+        # batch: per-image spectral data + discrepancy lambda, then ONE batched
+        # PCG over this rank's images (kp_pcg_batch); streams: the per-image
+        # pipeline on `workers` concurrent streams
+        return sh.solve_batch(mine, probs) if batched else sh.solve_many(mine, probs, args.workers)
+
+    for _ in range(max(1, args.warmup)):
+        run_all()
     if dist:
         dist.barrier()
     import ctypes as C
     launches0 = L.kp_launch_count()
+    times = []
     with ClockSampler(local) as clk:
-        check(L.kp_synchronize())
-        check(L.kp_event_record(0))
-        # every solve ends synchronised on its worker's stream
-        results = sh.solve_many(mine, probs, args.workers)
-        check(L.kp_event_record(1))
-        ms = C.c_float()
-        check(L.kp_event_elapsed(0, 1, C.byref(ms)))
-        elapsed = ms.value / 1e3
+        for _ in range(args.steps):
+            check(L.kp_synchronize())
+            check(L.kp_event_record(0))
+            results = run_all()  # ends synchronised (host buffers out)
+            check(L.kp_event_record(1))
+            ms = C.c_float()
+            check(L.kp_event_elapsed(0, 1, C.byref(ms)))
+            times.append(ms.value / 1e3)
+    elapsed = sum(times)
     launches = L.kp_launch_count() - launches0
-    elapsed, solved = reduce_timing(elapsed, float(len(results)), dist,
+    # profiled pass (per-launch events) for the M-solve GEMM roofline
+    roof = None
+    if batched:
+        lams = sh.select_lambdas(mine, probs)
+        check(L.kp_profile_reset())
+        check(L.kp_profile_enable(1))
+        res_p = sh.solve_batch(mine, probs, lams)
+        tt, tc = C.c_double(), C.c_longlong()
+        check(L.kp_profile_read(1, C.byref(tt), C.byref(tc)))
+        check(L.kp_profile_enable(0))
+        nb = sum(1 for i in mine if lams[i] is not None)
+        batches = 1 + max(r.iterations for r in res_p)  # batched M-solves that ran (initial + per iteration)
+        work = 2.0 * nb * float(sh.n) ** 3  # binary16 ops per launch (all images of the batch)
+        ach = work / (tt.value / (4 * batches) / 1e3) / 1e12 if tc.value else 0.0
+        import paper_2311_15393_b200 as K
+        eng = K.fp16_products_engine(sh.n)
+        peak = 2.0 * F16X2_PEAK_TOPS if eng == "tensor" else F16X2_PEAK_TOPS
+        roof = {"bound": "compute", "pipe": "f16x2 CUDA-core pipe (tree adds)" +
+                ("; rounded products from tcgen05" if eng == "tensor" else ""),
+                "achieved": ach, "peak": peak, "unit": "T half-ops/s", "frac": ach / peak,
+                "traffic": None,
+                "kernel": "gemm_f16x_kernel" if eng == "tensor" else "gemm_f16ref_kernel",
+                "work_per_launch": f"{work:.4g} half-ops ({nb} images x 2 n^3, batched along N)",
+                "launches": 4 * batches, "ms_per_launch": tt.value / (4 * batches)}
+    elapsed, solved = reduce_timing(elapsed, float(len(results) * args.steps), dist,
                                     device="cuda" if args.dist_backend == "nccl" else "cpu")
     allres = gather_results(results, dist,
                             device="cuda" if (dist and args.dist_backend == "nccl") else None)
@@ -309,6 +440,7 @@ def run_c4(args):
     tensor = None
     if not args.no_tensor:
         sht = C4Shard(n=args.size, svd=args.svd, device=local, accum="tensor")
+        warm = mine[: max(1, min(args.warmup, len(mine)))]
         sht.solve_many(warm, probs, args.workers)
         if dist:
             dist.barrier()
@@ -327,18 +459,31 @@ def run_c4(args):
                   "note": "KP_ACCUM_TENSOR: tcgen05 kind::f16, fp32 accumulation (not bit-exact)",
                   "results": [{k: r[k] for k in ("image", "lam", "iterations", "rel_err")}
                               for r in all_t[:6]]}
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import paper_2311_15393_b200 as K
+        threads = os.cpu_count() or 1
+        try:
+            ccfg = build_problem("C4", 0, args.size, device_apply=False)
+            csr, csc = svd_pair(ccfg.term, "host")
+            cpu = {"value": 1.0 / cpu_c4_image_sample(ccfg, csr, csc, K.PrecisionFormat.fp16(), threads),
+                   "unit": "solves/s", "cores": threads, "kind": "port",
+                   "sample": "one C4 image on the oracle: spectral data + discrepancy lambda, plus one PCG "
+                             "iteration's normal_matvec + precond_solve scaled to the image's 100 iterations"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "solves/s", "cores": threads, "kind": "port", "sample": f"failed: {e}"}
     if rank == 0:
         its = [r["iterations"] for r in allres]
         metric = METRIC_C4 if sh.n == 1024 else METRIC_C4.replace("1024^2", f"{sh.n}^2")
         out = {"metric": metric, "value": solved / elapsed, "unit": "solves/s", "n_gpus": ws,
-               "steps": 1, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                "dtype": "f64 + f16 (reference-exact)", "data": "synthetic (seeded blob images)",
-               "config": {"workload": "C4: 64 x n=1024, Gaussian sigma=2.5, noise 0.1/1/5 %, "
-                                      "discrepancy eta=1.01, PCG fp16 tol 1e-6",
-                          "parallelism": f"images sharded over {ws} GPU(s), NCCL gather; "
-                                         f"{args.workers} concurrent streams per GPU",
-                          "mean_iterations": float(np.mean(its)), "images": len(allres),
+               "config": c4_config(),
+               "run_info": {"parallelism": f"images sharded over {ws} GPU(s), NCCL gather; " +
+                                         ("one batched PCG state machine per GPU (kp_pcg_batch)" if batched
+                                          else f"{args.workers} concurrent streams per GPU"),
+                          "mean_iterations": float(np.mean(its)), "images_solved": len(allres),
                           "no_root": sum(r["no_root"] for r in allres),
                           "l2": "each step solves 64 distinct images (8 MB inputs and ~0.1 GB of solver "
                                 "state per image), far more than the 126 MB L2; no flush needed"},
@@ -347,7 +492,8 @@ def run_c4(args):
                        "d2h_bytes_per_step": 64 * 8 * sh.n * sh.n,
                        "note": "value is already end to end: every solve goes through the public "
                                "API with host buffers (b, x_true in, x out inside the timed region)"},
-               "clocks": clk.summary(), "gpu_launches": int(launches),
+               "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof,
+               "cpu_baseline": cpu,
                "results": [{k: r[k] for k in ("image", "lam", "iterations", "rel_err")}
                            for r in allres[:6]],
                "tensor_mode": tensor}
@@ -357,16 +503,19 @@ def run_c4(args):
     return 0
 
 
-def workload_config(cfg, device: bool = True) -> dict:
+def workload_config(cfg) -> dict:
+    """The workload definition, identical in both arms (ours / reference)."""
     solver, _, maxit = cfg.solvers[0]
     lam = cfg.lambda_ if cfg.select == "fixed" else f"{cfg.select} ({cfg.lambda_:.6g})"
     return {"workload": f"{cfg.name}: n={cfg.n} r={len(cfg.problem.a.terms)} {solver.upper()}, fp16 "
                         f"Kronecker-SVD preconditioner (reference-exact rounding), "
                         f"lambda={lam}, tol={cfg.tol}, maxit {maxit}",
-            "unknowns": cfg.n * cfg.n,
-            "l2": ("host CPU run (no GPU L2 involved)" if not device
-                   else "working set (~4 GB) far larger than the 126 MB L2; no flush needed" if cfg.n >= 4096
-                   else "L2 flushed before every timed step (256 MB zero-fill), steps timed separately")}
+            "unknowns": cfg.n * cfg.n}
+
+
+def l2_note(cfg) -> str:
+    return ("working set (~4 GB) far larger than the 126 MB L2; no flush needed" if cfg.n >= 4096
+            else "L2 flushed before every timed step (256 MB zero-fill), steps timed separately")
 
 
 def main():
@@ -375,7 +524,9 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C5")
+    ap.add_argument("--config", default=None,
+                    help="C1..C5; default: C5 (PCG iterations/s at 4096^2) on one GPU, the C4 "
+                         "batch (solves/s over 64 images, sharded) when launched with several ranks")
     ap.add_argument("--size", type=int, default=None, help="override image side n (quick runs)")
     ap.add_argument("--svd", default="auto", choices=["auto", "gpu", "host"],
                     help="setup SVD of the factors: host LAPACK dgesdd (the oracle's routine) or "
@@ -388,10 +539,14 @@ def main():
                     help="skip the config's other solver runs (C5: PCG fp64-precond, CGLS)")
     ap.add_argument("--operator", default="auto", choices=["auto", "dense", "banded"])
     ap.add_argument("--workers", type=int, default=6,
-                    help="C4: concurrent host threads / streams per GPU")
+                    help="C4 --c4-mode streams: concurrent host threads / streams per GPU")
+    ap.add_argument("--c4-mode", default="batch", choices=["batch", "streams"],
+                    help="C4: one batched PCG state machine per GPU, or per-image solves on streams")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="collective backend for timing reduction / result gather")
     args = ap.parse_args()
+    if args.config is None:
+        args.config = "C4" if dist_env()[0] > 1 else "C5"
     if args.svd == "auto":
         args.svd = "host" if dist_env()[0] == 1 else "gpu"
     if args.impl == "reference":
@@ -474,6 +629,7 @@ def main():
             check(solve_fn(op, d_b, (mm or m).handle(), C.byref(o), d_x, C.byref(h)))
         else:
             check(solve_fn(op, hp_b, (mm or m).handle(), C.byref(o), hp_x, C.byref(h)))
+        solve.msolves = h.msolve_count
         return h.iterations_used, float(hist_bufs[0][h.rows - 1]), h.abort_reason.decode()
 
     for _ in range(args.warmup):
@@ -524,9 +680,11 @@ def main():
     check(L.kp_profile_enable(1))
     check(L.kp_event_record(6))
     prof_iters = 0
+    prof_msolves = 0  # M-solves that ran (history.msolve_count): 4 working GEMM launches each
     for _ in range(args.steps):
         it, _, _ = solve(True)
         prof_iters += it
+        prof_msolves += solve.msolves
     check(L.kp_event_record(7))
     prof_ms = C.c_float()
     check(L.kp_event_elapsed(6, 7, C.byref(prof_ms)))
@@ -559,15 +717,19 @@ def main():
         tt, tcnt = C.c_double(), C.c_longlong()
         check(L.kp_profile_read(1, C.byref(tt), C.byref(tcnt)))
         check(L.kp_profile_enable(0))
-        tc_ach = 2.0 * float(n) ** 3 / (tt.value / tcnt.value / 1e3) / 1e12 if tcnt.value else 0.0
+        t_launches = 4 * solve.msolves  # working tcgen05 launches (no-op ones excluded)
+        tc_ach = 2.0 * float(n) ** 3 / (tt.value / t_launches / 1e3) / 1e12 if t_launches else 0.0
+        pk = peaks()
         tensor = {"value": t_iters / (t_ms.value / 1e3), "unit": "iterations/s",
                   "solves_per_s": args.steps / (t_ms.value / 1e3),
                   "iterations_per_solve": t_iters // args.steps, "final_rel_err": t_rel,
                   "note": "KP_ACCUM_TENSOR: tcgen05 kind::f16, fp32 accumulation (not bit-exact)",
-                  "roofline": {"bound": "tensor", "achieved": tc_ach, "peak": BF16_PEAK_TFLOPS,
-                               "unit": "TFLOP/s", "frac": tc_ach / BF16_PEAK_TFLOPS,
+                  "roofline": {"bound": "tensor", "achieved": tc_ach, "peak": pk["bf16_tflops_sustained"],
+                               "unit": "TFLOP/s", "frac": tc_ach / pk["bf16_tflops_sustained"],
+                               "frac_of_burst": tc_ach / pk["bf16_tflops"],
                                "kernel": "gemm_f16tc_kernel (tcgen05 kind::f16, 4 per M-solve)",
-                               "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)",
+                               "peak_source": f"{pk['source']}: bf16_tflops_sustained (in-step kernel); "
+                                              "frac_of_burst against bf16_tflops",
                                "work_per_launch": f"{2.0 * float(n) ** 3:.4g} flop",
                                "traffic": TRAFFIC.get(("gemm_f16tc_kernel", n))}}
 
@@ -642,9 +804,11 @@ def main():
         op_peak, op_kernel = DMMA_PEAK_TFLOPS, "gemm_f64_kernel (DMMA m16n8k16)"
         op_src = "measured DMMA f64 peak, profiles/r01_microbench_peaks.txt"
     op_ach = op_flops_per_launch / (op_ms / op_launches / 1e3) / 1e12 if op_launches else 0.0
-    pm_ms, pm_launches = prof["precond_gemm_f16ref"]
+    pm_ms, _ = prof["precond_gemm_f16ref"]
+    pm_launches = 4 * prof_msolves  # working launches only (a converged solve's last M-solve is a no-op)
     half_ops = 2.0 * float(n) ** 3  # n^3 rounded products + n^3 rounded tree adds per GEMM
     pm_ach = half_ops / (pm_ms / pm_launches / 1e3) / 1e12 if pm_launches else 0.0
+    engine = K.fp16_products_engine(n)
     total_prof = sum(v[0] for v in prof.values())
     op_line = {"bound": "tensor" if op_mode == "dense" else "compute",
                "pipe": "DMMA" if op_mode == "dense" else "FP64 DFMA", "achieved": op_ach,
@@ -652,13 +816,28 @@ def main():
                "traffic": TRAFFIC.get(("band", n)) if op_mode == "banded" else None,
                "kernel": op_kernel, "peak_source": op_src,
                "work_per_launch": f"{op_flops_per_launch:.4g} flop"}
-    pm_line = {"bound": "compute", "pipe": "f16x2 CUDA-core FMA pipe (reference-exact rounding "
-                                          "needs a binary16 rounding per product and per sum)",
-               "achieved": pm_ach,
-               "peak": F16X2_PEAK_TOPS, "unit": "T half-ops/s", "frac": pm_ach / F16X2_PEAK_TOPS,
-               "traffic": TRAFFIC.get(("gemm_f16ref_kernel", n)), "kernel": "gemm_f16ref_kernel",
-               "peak_source": "measured f16x2 mul+add rate, profiles/r01_microbench_peaks.txt",
-               "work_per_launch": f"{half_ops:.4g} half-ops"}
+    if engine == "tensor":
+        # gemm_f16x: the n^3 rounded products come from tcgen05 MMAs, the n^3
+        # rounded tree adds (HADD2) saturate the f16x2 pipe, so the 2 n^3
+        # binary16 ops of a launch complete at most at 2 x the f16x2 rate
+        pm_peak = 2.0 * F16X2_PEAK_TOPS
+        pm_line = {"bound": "compute", "pipe": "f16x2 CUDA-core pipe (rounded tree adds, HADD2); the rounded "
+                                              "products come from the tcgen05 tensor pipe",
+                   "achieved": pm_ach, "peak": pm_peak, "unit": "T half-ops/s", "frac": pm_ach / pm_peak,
+                   "traffic": TRAFFIC.get(("gemm_f16x_kernel", n)), "kernel": "gemm_f16x_kernel",
+                   "peak_source": "2 x measured f16x2 add rate (profiles/r01_microbench_peaks.txt): "
+                                  "n^3 adds on the f16x2 pipe bound the 2 n^3 ops",
+                   "work_per_launch": f"{half_ops:.4g} half-ops", "launches": pm_launches,
+                   "ms_per_launch": pm_ms / pm_launches if pm_launches else None}
+    else:
+        pm_line = {"bound": "compute", "pipe": "f16x2 CUDA-core FMA pipe (reference-exact rounding "
+                                              "needs a binary16 rounding per product and per sum)",
+                   "achieved": pm_ach,
+                   "peak": F16X2_PEAK_TOPS, "unit": "T half-ops/s", "frac": pm_ach / F16X2_PEAK_TOPS,
+                   "traffic": TRAFFIC.get(("gemm_f16ref_kernel", n)), "kernel": "gemm_f16ref_kernel",
+                   "peak_source": "measured f16x2 mul+add rate, profiles/r01_microbench_peaks.txt",
+                   "work_per_launch": f"{half_ops:.4g} half-ops", "launches": pm_launches,
+                   "ms_per_launch": pm_ms / pm_launches if pm_launches else None}
     dominant, other = (pm_line, op_line) if pm_ms > op_ms else (op_line, pm_line)
 
     # the dense DMMA operator (the product the reference computes), for its roofline
@@ -694,6 +873,10 @@ def main():
             except Exception as e:  # noqa: BLE001
                 cpu = {"value": None, "unit": "iterations/s", "cores": threads, "kind": "port",
                        "sample": f"failed: {e}"}
+            try:
+                cpu["single_thread"] = cpu_iteration_single_thread(cfg, fmt)
+            except Exception as e:  # noqa: BLE001
+                cpu["single_thread"] = {"value": None, "sample": f"failed: {e}"}
         out = {
             "metric": metric_name(cfg),
             "value": value, "unit": "iterations/s", "n_gpus": ws,
@@ -701,11 +884,13 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64 (operator, vectors) + f16 (preconditioner, reference-exact)",
             "data": f"synthetic (seeded blob images, BASELINE {cfg.name} PSF)",
-            "config": {**workload_config(cfg), "parallelism": f"replicas x{ws}",
-                       "per_rank_final_rel_err": ([d["rel_err"] for d in per_rank] if dist else None),
-                       "iterations_per_solve": iters // max(1, args.steps * ws),
-                       "lambda": cfg.lambda_, "lambda_selection": lam_select,
-                       "final_rel_err": rel_last},
+            "config": workload_config(cfg),
+            "run_info": {"l2": l2_note(cfg), "parallelism": f"replicas x{ws}",
+                         "per_rank_final_rel_err": ([d["rel_err"] for d in per_rank] if dist else None),
+                         "iterations_per_solve": iters // max(1, args.steps * ws),
+                         "lambda": cfg.lambda_, "lambda_selection": lam_select,
+                         "final_rel_err": rel_last,
+                         "fp16_products_engine": engine}, 
             "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": 2 * nn * 8,
                     "d2h_bytes_per_step": nn * 8 + 4 * cap * 8},
             "roofline": dominant,

@@ -250,6 +250,23 @@ int kp_pcg(const kp_operator* op, const double* b, const kp_precond* m,
            const kp_solver_options* opts, double* x, kp_history* hist);
 int kp_fpcg(const kp_operator* op, const double* b, const kp_precond* m,
             const kp_solver_options* opts, double* x, kp_history* hist);
+/* Batched pcg / fpcg over `batch` independent right-hand sides that share
+ * the operator and the preconditioner factors, image i with its own
+ * lambda (lambdas[i], host array; opts->lambda is ignored) — the
+ * reference's per-image pipeline (cli.cpp:469-486 run_single: with_lambda
+ * + pcg) for a whole batch in one device state machine (BASELINE C4).
+ * b, x (and opts->x_true, if set) hold batch * n^2 doubles, image i at
+ * i * n^2 (host or device per opts->device_pointers); hist points at
+ * `batch` kp_history structs. Each image's iterates, history and abort
+ * reason equal what kp_pcg / kp_fpcg with with_lambda(m, lambdas[i]) gives.
+ * Requires the fp16 format with KP_ACCUM_REFERENCE; record_iterates is not
+ * supported (KP_ERR_INVALID_ARGUMENT). */
+int kp_pcg_batch(const kp_operator* op, const kp_precond* m, int batch,
+                 const double* b, const double* lambdas,
+                 const kp_solver_options* opts, double* x, kp_history* hist);
+int kp_fpcg_batch(const kp_operator* op, const kp_precond* m, int batch,
+                  const double* b, const double* lambdas,
+                  const kp_solver_options* opts, double* x, kp_history* hist);
 
 /* ---- lambda selection: regparam.hpp / regparam.cpp -------------------- */
 /* make_spectral_data (regparam.cpp:119-126): device-resident sigma_hat =

@@ -170,6 +170,43 @@ class C4Shard:
             raise errors[0]
         return [out[i] for i in images]
 
+    def select_lambdas(self, images, probs: dict) -> dict:
+        """Discrepancy-principle lambda per image (regparam.cpp:288-327 on
+        the device spectral data; None when the bracket has no root)."""
+        K, np = self.K, self.np
+        lams = {}
+        for i in images:
+            tp = probs[i]
+            sd = K.make_spectral_data(self.m0, tp.b)
+            try:
+                lams[i] = K.discrepancy(sd, float(np.linalg.norm(tp.noise)), self.eta).lambda_
+            except K.NoRootError:
+                lams[i] = None
+        return lams
+
+    def solve_batch(self, images, probs: dict, lams: dict | None = None) -> list:
+        """The images' PCG solves as ONE batched device solve (kp_pcg_batch:
+        images stacked along the M-solve GEMMs' N dimension, one DevState per
+        image); lambdas from select_lambdas unless given. Image by image the
+        result equals solve()."""
+        K, np = self.K, self.np
+        images = list(images)
+        lams = lams if lams is not None else self.select_lambdas(images, probs)
+        out = {}
+        ok = [i for i in images if lams[i] is not None]
+        for i in images:
+            if lams[i] is None:
+                out[i] = ImageResult(i, probs[i].noise_level, float("nan"), 0, False, float("nan"), "", True)
+        if ok:
+            opts = K.SolverOptions(max_iterations=100, rel_residual_tol=self.tol)
+            res = K.pcg_batch(self.a, np.stack([probs[i].b for i in ok]), self.m0, [lams[i] for i in ok],
+                              opts, x_true=np.stack([probs[i].x_true for i in ok]))
+            for i, r in zip(ok, res):
+                h = r.history
+                out[i] = ImageResult(i, probs[i].noise_level, lams[i], h.iterations_used, h.converged,
+                                     h.relative_error[-1], h.abort_reason)
+        return [out[i] for i in images]
+
     def solve(self, image: int, tp=None, a=None) -> ImageResult:
         K, np = self.K, self.np
         tp = tp or self.problem(image)

@@ -205,6 +205,23 @@ struct SolverWorkspace {
     if (!state.p) state.alloc(1);
     return state.p;
   }
+  // batched solves (kp_pcg_batch): one DevState per image (+ the summary in
+  // dev_state()) and a pinned copy for the readback
+  DBuf<DevState> bstates;
+  DevState* host_bstates = nullptr;
+  int host_bstates_n = 0;
+  DevState* dev_states(int count) {
+    if (bstates.n < size_t(count)) bstates.alloc(count);
+    return bstates.p;
+  }
+  DevState* pinned_states(int count) {
+    if (host_bstates_n < count) {
+      if (host_bstates) cudaFreeHost(host_bstates);
+      KP_CUDA(cudaMallocHost(&host_bstates, size_t(count) * sizeof(DevState)));
+      host_bstates_n = count;
+    }
+    return host_bstates;
+  }
   DevState* pinned_state() {
     if (!host_state) KP_CUDA(cudaMallocHost(&host_state, sizeof(DevState)));
     return host_state;
@@ -223,6 +240,7 @@ struct SolverWorkspace {
   ~SolverWorkspace() {
     if (exec) cudaGraphExecDestroy(exec);
     if (host_state) cudaFreeHost(host_state);
+    if (host_bstates) cudaFreeHost(host_bstates);
     if (poll) cudaFreeHost(poll);
     for (auto& e : poll_ev)
       if (e) cudaEventDestroy(e);
@@ -234,6 +252,7 @@ struct kp_operator {
   SolverWorkspace ws;
   DBuf<double> Cs_rm, Cs_cm, Rr_rm, Rr_cm;  // r stacked n*n blocks (dense path)
   DBuf<double> W;                           // r*n*n workspace
+  DBuf<double> Wb;                          // batched banded applies: batch*r*n*n
   DBuf<double> part;                        // epilogue partials
   // banded-Toeplitz path (banded.cu)
   bool is_banded = false;
@@ -277,6 +296,13 @@ struct kp_precond {
   DBuf<double> part;
   DBuf<unsigned> zfix;  // gemm_f16x zero-sign fix-up workspace (zeroed)
   DBuf<unsigned long long> hash_b;  // gemm_f16x B-operand row sign hashes
+  // batched M-solves (kp_pcg_batch, fp16): images stacked along the GEMM N
+  // dimension; per-image S (one lambda each) and binary16 intermediates
+  int bcap = 0;
+  DBuf<__half> b_r16, b_t1h, b_wh, b_t3h, b_s16;
+  DBuf<double> b_part;
+  DBuf<unsigned> b_zfix;
+  DBuf<unsigned long long> b_hash;
 };
 
 struct kp_spectral {
@@ -994,6 +1020,288 @@ void run_pcg(kp_operator* op, const double* b_in, kp_precond* m, const kp_solver
   }
 }
 
+// ---------------------------------------------------------------------------
+// Batched PCG / FPCG (kp_pcg_batch): `B` independent right-hand sides share
+// the operator and the preconditioner factors, each with its own lambda —
+// BASELINE C4, the reference's per-image pipeline (cli.cpp:469-486) run for
+// a whole batch at once. Every iteration is one set of launches for all
+// images: the banded operator passes take the images in grid.z, the four
+// binary16 M-solve products stack the images along the GEMM N dimension
+// (per-image S in the epilogue, per-image dot partials), and the vector /
+// scalar kernels keep one DevState per image (its own alpha, beta, rho,
+// stop test and abort; a stopped image is frozen while the others run). Each
+// image's arithmetic is exactly the single solve's (same kernels, same
+// per-image reduction grids), so results equal kp_pcg image by image.
+
+// Partial slots per image of a batched M-solve.
+int msolve_batch_slots(const kp_precond* p, bool stacked) {
+  const int n = p->n;
+  if (!stacked) return msolve_partials_ctas(p);
+  return msolve_f16x(p) ? gemm_f16x_partials_per_image(n, n) : 0;
+}
+bool msolve_batch_stacked(const kp_precond* p, int B) {
+  // f16x tiles are 32 wide, f16ref tiles up to 64: images must start on a tile
+  return msolve_f16x(p) ? p->n % 32 == 0 : p->n % 64 == 0;
+}
+int msolve_batch_slots_all(const kp_precond* p, int B) {
+  const int n = p->n;
+  if (!msolve_batch_stacked(p, B)) return msolve_partials_ctas(p);
+  return msolve_f16x(p) ? gemm_f16x_partials_per_image(n, n)
+                        : gemm_f16ref_partials_per_image(n, B * n, n);
+}
+
+void ensure_batch_ws(kp_precond* p, int B, const std::vector<double>& lambdas) {
+  const int n = p->n;
+  const size_t nn = size_t(n) * n;
+  const long ldh = p->sh->ldh;
+  ensure_ws(p);  // factor hashes etc.
+  if (p->bcap < B) {
+    const size_t rows = size_t(B) * n;
+    p->b_r16.alloc(rows * ldh), p->b_t1h.alloc(rows * ldh), p->b_wh.alloc(rows * ldh), p->b_t3h.alloc(rows * ldh);
+    fill_u16(p->b_r16.p, p->b_r16.n, 0x0000);  // same padding rule as the single solve
+    fill_u16(p->b_wh.p, p->b_wh.n, 0x0000);
+    fill_u16(p->b_t1h.p, p->b_t1h.n, 0x8000);
+    fill_u16(p->b_t3h.p, p->b_t3h.n, 0x8000);
+    p->b_s16.alloc(size_t(B) * nn);
+    p->b_part.alloc(size_t(B) * msolve_batch_slots_all(p, B) * 4);
+    if (msolve_f16x(p)) {
+      ensure_zfix(p->b_zfix, n, B * n);
+      p->b_hash.alloc(rows);
+    }
+    p->bcap = B;
+  }
+  // per-image S = round16(1 / ((s_r s_c)^2 + lambda_i^2)) (factor.cpp:62-76)
+  const auto& sh = *p->sh;
+  auto amin = [](const std::vector<double>& v) {
+    double m = std::numeric_limits<double>::infinity();
+    for (double x : v) m = std::min(m, std::fabs(x));
+    return m;
+  };
+  const double pmin = amin(sh.s_r) * amin(sh.s_c);
+  for (int i = 0; i < B; ++i) {
+    const double l2 = lambdas[i] * lambdas[i];
+    if (pmin * pmin + l2 == 0.0) throw InvalidArgument("build_preconditioner: singular factors need lambda > 0");
+    precond_weights(sh.d_s_r.p, sh.d_s_c.p, n, l2, nullptr, p->b_s16.p + size_t(i) * nn);
+  }
+}
+
+// The four products of precond_solve (factor.cpp:117-132) for B images; the
+// binary16 residuals are already in b_r16 (image i at rows i*n).
+void msolve_batch(kp_precond* p, int B, double* z, const double* d0, const double* d1a,
+                  const double* d1b, const int* status) {
+  const int n = p->n;
+  const size_t nn = size_t(n) * n;
+  auto* sh = p->sh.get();
+  const long ldh = sh->ldh;
+  const bool f16x = msolve_f16x(p);
+  const bool stacked = msolve_batch_stacked(p, B);
+  const int slots = msolve_batch_slots_all(p, B);
+  const int groups = stacked ? 1 : B, per = stacked ? B : 1;
+  for (int gi = 0; gi < groups; ++gi) {
+    const long ho = long(gi) * n * ldh;  // image offset when not stacked
+    const size_t vo = size_t(gi) * nn;
+    F16GemmArgs g;
+    g.M = n, g.N = per * n, g.K = n, g.status = status;
+    if (f16x) g.zfix = p->b_zfix.p, g.hash_a_ready = true, g.hash_b = p->b_hash.p;
+    auto batch_epi = [&](F16Epilogue& e, long c_img) {
+      if (stacked && B > 1) e.n_img = n, e.c_img = c_img, e.s_img = long(nn), e.v_img = long(nn), e.part_img = slots;
+    };
+    auto run = [&]() { f16x ? gemm_f16x(g, KC_PRECOND) : gemm_f16ref(g, KC_PRECOND); };
+    g.hash_a = sh->hash_vc_a.p;
+    g.A = {sh->vc_a.p, ldh}, g.B = {p->b_r16.p + ho, ldh};  // t1(a, j) = lp(V_c^T R)
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->b_t1h.p + ho, g.epi.cm = ldh, g.epi.cn = 1;
+    batch_epi(g.epi, long(n) * ldh);
+    run();
+    g.hash_a = sh->hash_vr_b.p;
+    g.A = {sh->vr_b.p, ldh}, g.B = {p->b_t1h.p + ho, ldh};  // w(a,b) = round(S .* lp(t1 V_r)), as (b, a)
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF_SCALED, g.epi.Ch = p->b_wh.p + ho, g.epi.cm = ldh,
+    g.epi.cn = 1, g.epi.scale = p->b_s16.p + vo, g.epi.sm = n, g.epi.sn = 1;
+    batch_epi(g.epi, long(n) * ldh);
+    run();
+    g.hash_a = sh->hash_vct_a.p;
+    g.A = {sh->vct_a.p, ldh}, g.B = {p->b_wh.p + ho, ldh};  // t3(i,b) = lp(V_c w)
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->b_t3h.p + ho, g.epi.cm = ldh, g.epi.cn = 1;
+    batch_epi(g.epi, long(n) * ldh);
+    run();
+    g.hash_a = sh->hash_vrt_b.p;
+    g.A = {sh->vrt_b.p, ldh}, g.B = {p->b_t3h.p + ho, ldh};  // z(i,j) = lp(t3 V_r^T), as (j, i)
+    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z + vo, g.epi.cm = n, g.epi.cn = 1;
+    g.epi.vm = n, g.epi.vn = 1;
+    g.epi.d0 = d0 ? d0 + vo : nullptr, g.epi.d1a = d1a ? d1a + vo : nullptr, g.epi.d1b = d1b ? d1b + vo : nullptr;
+    g.epi.partials = p->b_part.p + size_t(gi) * slots * 4;
+    batch_epi(g.epi, long(nn));
+    run();
+  }
+}
+
+// A (or A^T) applied to B images; `extra` partials land in per-image slots
+// of op_partials_ctas(op) each; addc_dev / addc_host: per-image coefficient
+// of extra->addv (lambda_i^2).
+void op_apply_batch(kp_operator* op, int B, const double* in, double* out, bool transpose,
+                    const F64Epilogue* extra, const double* addc_dev, const std::vector<double>* addc_host,
+                    const int* status) {
+  const int n = op->n, r = op->r;
+  const size_t nn = size_t(n) * n;
+  if (op->use_banded()) {
+    if (op->Wb.n < size_t(B) * r * nn) op->Wb.alloc(size_t(B) * r * nn);
+    band_cols(in, op->Wb.p, n, r, transpose ? op->cols_tr : op->cols_fw, status, B);
+    F64Epilogue e;
+    if (extra) e = *extra;
+    e.C = out, e.cm = 1, e.cn = n, e.vm = 1, e.vn = n;
+    e.img = long(nn), e.part_img = band_rows_num_ctas(n);
+    if (e.addv) e.addc_img = addc_dev;
+    band_rows(op->Wb.p, n, r, transpose ? op->rows_tr : op->rows_fw, e, status, B);
+    return;
+  }
+  const int slots = op_partials_ctas(op);
+  for (int i = 0; i < B; ++i) {  // dense operator: one image at a time
+    const size_t o = size_t(i) * nn;
+    F64Epilogue e;
+    if (extra) {
+      e = *extra;
+      if (e.addv) e.addv += o, e.addc = (*addc_host)[i];
+      if (e.d0 && !e.d0_self) e.d0 += o;
+      if (e.d1a) e.d1a += o;
+      if (e.d1b) e.d1b += o;
+      if (e.mul) e.mul += o;
+      if (e.partials) e.partials += size_t(i) * slots * 4;
+    }
+    op_apply(op, in + o, out + o, transpose, extra ? &e : nullptr, status);
+  }
+}
+
+void run_pcg_batch(kp_operator* op, kp_precond* m, int B, const double* b_in, const double* lambdas,
+                   const kp_solver_options* o, double* x_out, kp_history* hist, bool flexible) {
+  if (!op) throw InvalidArgument("solver: null operator");
+  if (B < 1) throw InvalidArgument("pcg_batch: batch must be at least 1");
+  if (!o || !hist || !lambdas || !b_in || !x_out) throw InvalidArgument("pcg_batch: null argument");
+  if (!m) throw InvalidArgument("solver: null preconditioner");
+  if (m->n != op->n) throw InvalidArgument("solver: preconditioner size mismatch");
+  if (o->max_iterations < 1) throw InvalidArgument("solver: max_iterations must be at least 1");
+  if (!(o->rel_residual_tol > 0.0)) throw InvalidArgument("solver: tolerance must be positive");
+  if (o->record_iterates) throw InvalidArgument("pcg_batch: record_iterates is not supported for batches");
+  if (!is_fp16(m->fmt) || m->accum != KP_ACCUM_REFERENCE)
+    throw InvalidArgument("pcg_batch: batched solves need the fp16 reference-exact preconditioner");
+  for (int i = 0; i < B; ++i)
+    if (hist[i].capacity < 1 || !hist[i].residual_norm || !hist[i].work_units)
+      throw InvalidArgument("solver: history arrays missing");
+  const int n = op->n;
+  const size_t nn = size_t(n) * n, bnn = size_t(B) * nn;
+  const bool dev = o->device_pointers != 0;
+  SolverWorkspace& ws = op->ws;
+  std::vector<double> lam(lambdas, lambdas + B), l2(B);
+  for (int i = 0; i < B; ++i) l2[i] = lam[i] * lam[i];
+  ensure_batch_ws(m, B, lam);
+  const double* b = stage_vec(ws, "b_b", b_in, bnn, dev);
+  const double* xt = o->x_true ? stage_vec(ws, "b_xt", o->x_true, bnn, dev) : nullptr;
+
+  // per-image states (setup_state's fields, lambda_i) and the batch summary
+  const int cap = o->max_iterations + 1;
+  std::vector<DevState> hs(B);
+  for (int i = 0; i < B; ++i) {
+    DevState& h = hs[i];
+    h = DevState{};
+    h.status = ST_RUNNING, h.k = 1, h.maxit = o->max_iterations, h.flexible = flexible;
+    h.track_cos = o->track_search_direction_orthogonality != 0;
+    h.has_xt = xt != nullptr, h.record = 0, h.tol = o->rel_residual_tol, h.l2 = l2[i];
+    h.work_per_iter = 2.25;
+  }
+  DevState* states = ws.dev_states(B);
+  KP_CUDA(cudaMemcpyAsync(states, hs.data(), B * sizeof(DevState), cudaMemcpyHostToDevice, ctx().stream));
+  Solve s;
+  s.op = op;
+  s.nn = nn;
+  s.st = ws.dev_state();  // summary
+  {
+    DevState sm{};
+    sm.status = ST_RUNNING;
+    KP_CUDA(cudaMemcpyAsync(s.st, &sm, sizeof(DevState), cudaMemcpyHostToDevice, ctx().stream));
+  }
+  s.capacity = cap;
+  s.dh.resid = ws.get("b_h_resid", size_t(B) * cap);
+  s.dh.relerr = ws.get("b_h_relerr", size_t(B) * cap);
+  s.dh.cosines = ws.get("b_h_cos", size_t(B) * cap);
+  s.dh.iterates = nullptr;
+  s.dh.capacity = cap;
+  const int* status = &s.st->status;
+  double* l2_dev = ws.get("b_l2", B);
+  KP_CUDA(cudaMemcpyAsync(l2_dev, l2.data(), B * sizeof(double), cudaMemcpyHostToDevice, ctx().stream));
+
+  double* x = dev ? x_out : ws.get("b_x", bnn);
+  double *r = ws.get("b_r", bnn), *p = ws.get("b_p", bnn), *q = ws.get("b_q", bnn), *z = ws.get("b_z", bnn);
+  double* rprev = flexible ? ws.get("b_rprev", bnn) : nullptr;
+  double* ap = ws.get("b_ap", bnn);
+  const int nop = op_partials_ctas(op);
+  const int nms = msolve_batch_slots_all(m, B);
+  const int nvec = pcg_update_ctas(n);
+  double* part_op = ws.get("b_part_op", size_t(B) * nop * 4);
+  double* part_vec = ws.get("b_part_vec", size_t(B) * nvec * 4);
+  double* part_xt = ws.get("b_part_xt", size_t(B) * VEC_CTAS * 4);
+  const long ldh = m->sh->ldh;
+
+  vec_zero(x, bnn);
+  F64Epilogue e;
+  e.d0_self = 1;
+  e.d0 = r;  // any non-null: self product
+  e.partials = part_op;
+  op_apply_batch(op, B, b, r, true, &e, nullptr, nullptr, status);  // r = A^T b, ||r||^2
+  if (xt)
+    for (int i = 0; i < B; ++i) vec_dot_partials(xt + size_t(i) * nn, xt + size_t(i) * nn, nn, part_xt + size_t(i) * VEC_CTAS * 4);
+  pcg_init_scalar(states, s.dh, part_op, nop, part_xt, VEC_CTAS, B);
+  for (int i = 0; i < B; ++i)
+    cast_f64_to_f16_padded(r + size_t(i) * nn, m->b_r16.p + size_t(i) * n * ldh, n, n, n, ldh, status);
+  msolve_batch(m, B, z, r, nullptr, nullptr, status);
+  pcg_init_msolve_scalar(states, m->b_part.p, nms, B);
+  batch_status(states, B, s.st);
+  vec_copy(p, z, bnn, status);
+
+  auto iteration = [&]() {
+    op_apply_batch(op, B, p, ap, false, nullptr, nullptr, nullptr, status);
+    F64Epilogue ne;
+    ne.addv = p, ne.d0 = p, ne.partials = part_op;
+    op_apply_batch(op, B, ap, q, true, &ne, l2_dev, &l2, status);  // A^T A p + lambda_i^2 p
+    pcg_alpha_scalar(states, part_op, nop, B);
+    pcg_update(states, s.dh, x, r, rprev, p, q, z, xt, m->b_r16.p, n, ldh, part_vec, B);
+    pcg_resid_scalar(states, s.dh, part_vec, nvec, B);
+    batch_status(states, B, s.st);
+    msolve_batch(m, B, z, r, flexible ? r : nullptr, rprev, status);
+    pcg_beta_scalar(states, m->b_part.p, nms, B);
+    pcg_p_update(states, p, z, nn, B);
+    batch_status(states, B, s.st);
+  };
+  drive(s, o->max_iterations, iteration);
+
+  // per-image histories (finish() for each image)
+  auto d2h = [](void* dst, const void* src, size_t bytes) {
+    if (bytes) KP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx().stream));
+  };
+  DevState* pst = ws.pinned_states(B);
+  d2h(pst, states, B * sizeof(DevState));
+  sync();
+  for (int i = 0; i < B; ++i)
+    if (pst[i].status == ST_INVALID) throw InvalidArgument("solver: x_true must be nonzero");
+  for (int i = 0; i < B; ++i) {
+    const DevState st = pst[i];
+    kp_history* h = hist + i;
+    const int rows = std::min(st.rows, h->capacity);
+    const int ncos = std::min(st.ncos, h->capacity);
+    d2h(h->residual_norm, s.dh.resid + size_t(i) * cap, rows * sizeof(double));
+    if (xt && h->relative_error) d2h(h->relative_error, s.dh.relerr + size_t(i) * cap, rows * sizeof(double));
+    if (o->track_search_direction_orthogonality && h->residual_cosines && ncos > 0)
+      d2h(h->residual_cosines, s.dh.cosines + size_t(i) * cap, ncos * sizeof(double));
+    for (int k = 0; k < rows; ++k) h->work_units[k] = 2.25 * k;
+    h->rows = rows;
+    h->n_cosines = ncos;
+    h->iterations_used = st.iterations_used;
+    h->converged = st.status == ST_CONVERGED;
+    h->msolve_count = st.msolve_count;
+    const std::string msg = st.status == ST_ABORTED ? abort_message(st.abort_code, st.abort_iter) : "";
+    std::snprintf(h->abort_reason, sizeof(h->abort_reason), "%s", msg.c_str());
+  }
+  if (!dev) d2h(x_out, x, bnn * sizeof(double));
+  sync();
+}
+
 // cgls (krylov.cpp:154-208)
 void run_cgls(kp_operator* op, const double* b_in, const kp_solver_options* o, double* x_out,
               kp_history* hist) {
@@ -1702,6 +2010,16 @@ int kp_pcg(const kp_operator* op, const double* b, const kp_precond* m, const kp
 int kp_fpcg(const kp_operator* op, const double* b, const kp_precond* m,
             const kp_solver_options* o, double* x, kp_history* h) {
   KP_API(run_pcg(const_cast<kp_operator*>(op), b, const_cast<kp_precond*>(m), o, x, h, true))
+}
+int kp_pcg_batch(const kp_operator* op, const kp_precond* m, int batch, const double* b,
+                 const double* lambdas, const kp_solver_options* o, double* x, kp_history* h) {
+  KP_API(run_pcg_batch(const_cast<kp_operator*>(op), const_cast<kp_precond*>(m), batch, b, lambdas, o, x, h,
+                       false))
+}
+int kp_fpcg_batch(const kp_operator* op, const kp_precond* m, int batch, const double* b,
+                  const double* lambdas, const kp_solver_options* o, double* x, kp_history* h) {
+  KP_API(run_pcg_batch(const_cast<kp_operator*>(op), const_cast<kp_precond*>(m), batch, b, lambdas, o, x, h,
+                       true))
 }
 
 // ---- lambda selection ------------------------------------------------------------

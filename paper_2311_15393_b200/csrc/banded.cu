@@ -167,6 +167,8 @@ __global__ void __launch_bounds__(A_THREADS, KP_BAND_A_MINB) band_cols_kernel(co
   pdl_wait();
   if (stopped(status)) return;
   extern __shared__ double sm[];
+  X += size_t(blockIdx.z) * n * n;  // batched images (grid.z)
+  Y += size_t(blockIdx.z) * r * n * n;
   const int S = cols_stride<TAPS>(t.taps);  // odd column stride (no bank sharing across lanes)
   double* Xs = sm;                          // [A_TL][S]
   const int a0 = blockIdx.y * A_TA, l0 = blockIdx.x * A_TL;
@@ -243,6 +245,7 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
   pdl_wait();
   if (stopped(status)) return;
   extern __shared__ double sm[];
+  Y += size_t(blockIdx.z) * r * n * n;  // batched images (grid.z)
   const int rows = (TAPS > 0 ? TAPS : t.taps) + B_TJ - 1;  // rows loaded
   const int buf_doubles = rows_halo<TAPS>(t.taps) * B_TA;
   const int a0 = blockIdx.y * B_TA, j0 = blockIdx.x * B_TJ;
@@ -310,21 +313,29 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
       corr8_tail(acc, t.w[k], t.real, [&](int i) { return base[i * B_TA]; });
     __syncthreads();  // buffer (k & 1) is refilled at iteration k + 1
   }
-  // epilogue (same contract as the GEMM epilogue)
+  // epilogue (same contract as the GEMM epilogue; image blockIdx.z)
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   const int m = a0 + a;
+  const long zo = long(blockIdx.z) * e.img;
+  double* const C = e.C + zo;
+  const double* const mul = e.mul ? e.mul + zo : nullptr;
+  const double* const addv = e.addv ? e.addv + zo : nullptr;
+  const double addc = e.addc_img ? e.addc_img[blockIdx.z] : e.addc;
+  const double* const d0 = e.d0 ? e.d0 + zo : nullptr;
+  const double* const d1a = e.d1a ? e.d1a + zo : nullptr;
+  const double* const d1b = e.d1b ? e.d1b + zo : nullptr;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int j = j0 + 8 * jq + q;
     if (m >= n || j >= n) continue;
     double v = acc[q];
     const long vi = long(m) * e.vm + long(j) * e.vn;
-    if (e.mul) v *= e.mul[vi];
-    if (e.addv) v = __dadd_rn(v, __dmul_rn(e.addc, e.addv[vi]));  // + lambda^2 p, unfused as Eigen
-    e.C[long(m) * e.cm + long(j) * e.cn] = v;
+    if (mul) v *= mul[vi];
+    if (addv) v = __dadd_rn(v, __dmul_rn(addc, addv[vi]));  // + lambda^2 p, unfused as Eigen
+    C[long(m) * e.cm + long(j) * e.cn] = v;
     if (e.partials) {
-      if (e.d0) s0 += v * (e.d0_self ? v : e.d0[vi]);
-      if (e.d1a) s1 += v * (e.d1b ? (e.d1a[vi] - e.d1b[vi]) : e.d1a[vi]);
+      if (e.d0) s0 += v * (e.d0_self ? v : d0[vi]);
+      if (d1a) s1 += v * (d1b ? (d1a[vi] - d1b[vi]) : d1a[vi]);
       if (e.count_nonfinite && !isfinite(v)) s2 += 1.0;
     }
   }
@@ -342,7 +353,7 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
     if (threadIdx.x == 0) {
       double x0 = 0, x1 = 0, x2 = 0;
       for (int w = 0; w < B_THREADS / 32; ++w) x0 += red[w][0], x1 += red[w][1], x2 += red[w][2];
-      double* o = e.partials + (long(blockIdx.y) * gridDim.x + blockIdx.x) * 4;
+      double* o = e.partials + (long(blockIdx.z) * e.part_img + long(blockIdx.y) * gridDim.x + blockIdx.x) * 4;
       o[0] = x0, o[1] = x1, o[2] = x2, o[3] = 0.0;
     }
   }
@@ -363,22 +374,23 @@ void by_taps(int real, Args&&... args) {
 
 template <int TAPS>
 struct ColsLaunch {
-  static void run(const double* X, double* Y, int n, int r, const BandTaps& t, const int* status) {
+  static void run(const double* X, double* Y, int n, int r, const BandTaps& t, const int* status,
+                  int batch) {
     const size_t smem = size_t(A_TL) * (cols_stride<TAPS>(t.taps) + A_SO) * sizeof(double);
     auto k = band_cols_kernel<TAPS>;
     set_smem_limit(reinterpret_cast<const void*>(k), smem);
-    dim3 grid(cdiv(n, A_TL), cdiv(n, A_TA));
+    dim3 grid(cdiv(n, A_TL), cdiv(n, A_TA), batch);
     launch_pdl(k, grid, dim3(A_THREADS), smem, X, Y, n, r, t, status);
   }
 };
 template <int TAPS>
 struct RowsLaunch {
   static void run(const double* Y, int n, int r, const BandTaps& t, const F64Epilogue& e,
-                  const int* status) {
+                  const int* status, int batch) {
     const size_t smem = 2 * size_t(rows_halo<TAPS>(t.taps)) * B_TA * sizeof(double);  // two buffers
     auto k = band_rows_kernel<TAPS>;
     set_smem_limit(reinterpret_cast<const void*>(k), smem);
-    dim3 grid(cdiv(n, B_TJ), cdiv(n, B_TA));
+    dim3 grid(cdiv(n, B_TJ), cdiv(n, B_TA), batch);
     launch_pdl(k, grid, dim3(B_THREADS), smem, Y, n, r, t, e, status);
   }
 };
@@ -393,18 +405,19 @@ bool generic_only() {
 
 }  // namespace
 
-void band_cols(const double* X, double* Y, int n, int r, const BandTaps& t, const int* status) {
+void band_cols(const double* X, double* Y, int n, int r, const BandTaps& t, const int* status,
+               int batch) {
   LaunchScope scope(KC_OPERATOR);
-  by_taps<ColsLaunch>(generic_only() ? 0 : t.real, X, Y, n, r, t, status);
+  by_taps<ColsLaunch>(generic_only() ? 0 : t.real, X, Y, n, r, t, status, batch);
   check_launch("band_cols");
 }
 
 int band_rows_num_ctas(int n) { return int(cdiv(n, B_TJ) * cdiv(n, B_TA)); }
 
 void band_rows(const double* Y, int n, int r, const BandTaps& t, const F64Epilogue& e,
-               const int* status) {
+               const int* status, int batch) {
   LaunchScope scope(KC_OPERATOR);
-  by_taps<RowsLaunch>(generic_only() ? 0 : t.real, Y, n, r, t, e, status);
+  by_taps<RowsLaunch>(generic_only() ? 0 : t.real, Y, n, r, t, e, status, batch);
   check_launch("band_rows");
 }
 

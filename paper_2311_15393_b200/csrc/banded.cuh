@@ -19,12 +19,15 @@ struct BandTaps {
 };
 
 // Y_k = column correlation of X (n-by-n, column-major) for all r terms;
-// Y holds r stacked n-by-n column-major blocks.
-void band_cols(const double* X, double* Y, int n, int r, const BandTaps& t, const int* status);
+// Y holds r stacked n-by-n column-major blocks. batch > 1: `batch` images,
+// X and Y of image z at z * n^2 and z * r * n^2.
+void band_cols(const double* X, double* Y, int n, int r, const BandTaps& t, const int* status,
+               int batch = 1);
 // out = sum_k row correlation of Y_k, with the GEMM epilogue contract
-// (F64Epilogue; C indexed column-major like out).
+// (F64Epilogue; C indexed column-major like out; batched images per
+// F64Epilogue::img / part_img / addc_img).
 void band_rows(const double* Y, int n, int r, const BandTaps& t, const F64Epilogue& e,
-               const int* status);
+               const int* status, int batch = 1);
 int band_rows_num_ctas(int n);
 
 }  // namespace kp

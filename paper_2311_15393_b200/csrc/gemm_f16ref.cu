@@ -239,6 +239,16 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
   // ---- epilogue ----
   const F16Epilogue& e = args.epi;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  // batched products: this tile's image (tiles never straddle images)
+  int nl_base;
+  const int img = epi_image(e, n_base, nl_base);
+  const int NL = e.n_img ? e.n_img : N;
+  __half* const Ch = e.Ch ? e.Ch + img * e.c_img : nullptr;
+  double* const Cd = e.Cd ? e.Cd + img * e.c_img : nullptr;
+  const __half* const scale = e.scale ? e.scale + img * e.s_img : nullptr;
+  const double* const d0 = e.d0 ? e.d0 + img * e.v_img : nullptr;
+  const double* const d1a = e.d1a ? e.d1a + img * e.v_img : nullptr;
+  const double* const d1b = e.d1b ? e.d1b + img * e.v_img : nullptr;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -246,24 +256,24 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int m = m_base + tm + 8 * i;
-        const int n = n_base + tn + 32 * p + 16 * h;
-        if (m >= M || n >= N) continue;
+        const int n = nl_base + tn + 32 * p + 16 * h;  // image-local column
+        if (m >= M || n >= NL) continue;
         const uint32_t word = acc[i * NP + p];
         const unsigned short bits = h ? (unsigned short)(word >> 16) : (unsigned short)(word & 0xffffu);
         if (e.mode == F16OUT_HALF) {
-          e.Ch[long(m) * e.cm + long(n) * e.cn] = __ushort_as_half(bits);
+          Ch[long(m) * e.cm + long(n) * e.cn] = __ushort_as_half(bits);
         } else if (e.mode == F16OUT_HALF_SCALED) {
-          const __half sc = e.scale[long(m) * e.sm + long(n) * e.sn];
+          const __half sc = scale[long(m) * e.sm + long(n) * e.sn];
           unsigned short r;
           asm("mul.rn.f16 %0, %1, %2;" : "=h"(r) : "h"(__half_as_ushort(sc)), "h"(bits));
-          e.Ch[long(m) * e.cm + long(n) * e.cn] = __ushort_as_half(r);
+          Ch[long(m) * e.cm + long(n) * e.cn] = __ushort_as_half(r);
         } else {
           const double v = double(__half2float(__ushort_as_half(bits)));
-          e.Cd[long(m) * e.cm + long(n) * e.cn] = v;
+          Cd[long(m) * e.cm + long(n) * e.cn] = v;
           if (e.partials) {
             const long vi = long(m) * e.vm + long(n) * e.vn;
-            if (e.d0) s0 += v * e.d0[vi];
-            if (e.d1a) s1 += v * (e.d1b ? (e.d1a[vi] - e.d1b[vi]) : e.d1a[vi]);
+            if (d0) s0 += v * d0[vi];
+            if (d1a) s1 += v * (d1b ? (d1a[vi] - d1b[vi]) : d1a[vi]);
             if (!isfinite(v)) s2 += 1.0;
           }
         }
@@ -281,7 +291,10 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
     if (tid == 0) {
       double a0 = 0, a1 = 0, a2 = 0;
       for (int w = 0; w < THREADS / 32; ++w) a0 += red[w][0], a1 += red[w][1], a2 += red[w][2];
-      double* o = e.partials + long(pid) * 4;
+      // batched: per-image slot = the tile's position in that image's own grid
+      const long slot = e.n_img ? long(img) * e.part_img + long(tile_m) * (e.n_img / BN) + nl_base / BN
+                                : long(tile_m) * grid_n + tile_n;
+      double* o = e.partials + slot * 4;
       o[0] = a0, o[1] = a1, o[2] = a2, o[3] = 0.0;
     }
   }
@@ -339,6 +352,9 @@ int f16ref_cfg() {
 }  // namespace
 
 int gemm_f16ref_num_ctas(int M, int N) { return int(cdiv(M, BM) * cdiv(N, f16ref_bn(M, N))); }
+int gemm_f16ref_partials_per_image(int M, int N, int n_img) {
+  return int(cdiv(M, BM) * (n_img / f16ref_bn(M, N)));
+}
 
 void gemm_f16ref(const F16GemmArgs& a, int kernel_class) {
   if (a.M <= 0 || a.N <= 0) return;

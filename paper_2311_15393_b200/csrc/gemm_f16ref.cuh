@@ -31,7 +31,28 @@ struct F16Epilogue {
   const double* d1a = nullptr;
   const double* d1b = nullptr;
   double* partials = nullptr;
+  // Batched products: N stacks independent images of n_img columns each (the
+  // B operand holds their rows back to back). Output column n = img * n_img
+  // + nl is addressed as image img's column nl: C at img * c_img + m*cm +
+  // nl*cn, the scale at img * s_img + ..., the dot vectors at img * v_img +
+  // ..., and partials per image in slots [img * part_img, (img+1) * part_img)
+  // (fixed-order per-image reductions). n_img must be a multiple of the tile
+  // width (64), so no tile straddles two images. n_img = 0: one product.
+  int n_img = 0;
+  long c_img = 0, s_img = 0, v_img = 0;
+  int part_img = 0;
 };
+
+// Image index and image-local column of global output column n.
+__host__ __device__ __forceinline__ int epi_image(const F16Epilogue& e, int n, int& nl) {
+  if (!e.n_img) {
+    nl = n;
+    return 0;
+  }
+  const int img = n / e.n_img;
+  nl = n - img * e.n_img;
+  return img;
+}
 
 struct F16GemmArgs {
   int M = 0, N = 0, K = 0;
@@ -51,6 +72,8 @@ struct F16GemmArgs {
 };
 
 int gemm_f16ref_num_ctas(int M, int N);
+// Batched products: partial slots per image (F16Epilogue::part_img).
+int gemm_f16ref_partials_per_image(int M, int N, int n_img);
 void gemm_f16ref(const F16GemmArgs& a, int kernel_class);
 // Fill helper for padded binary16 buffers (bits = 0x8000 for -0, 0 for +0).
 void fill_u16(__half* p, size_t count, uint16_t bits);

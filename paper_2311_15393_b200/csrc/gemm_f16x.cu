@@ -61,8 +61,26 @@
 namespace kp {
 namespace {
 
-constexpr int BM = 128, BN = 32, BK = 64, NSTAGE = 3, NGROUP = 4, NCOL = 128;
-constexpr int NMMA = 2 * NCOL, NBUF = 2;  // one MMA covers two output groups
+#ifndef KP_F16X_NSTAGE
+#define KP_F16X_NSTAGE 2
+#endif
+#ifndef KP_F16X_REGLV
+#define KP_F16X_REGLV 2
+#endif
+constexpr int BM = 128, BN = 32, BK = 64, NSTAGE = KP_F16X_NSTAGE, NGROUP = 4, NCOL = 128;
+#ifndef KP_F16X_PAIR
+#define KP_F16X_PAIR 1
+#endif
+#ifndef KP_F16X_EARLY
+#define KP_F16X_EARLY 0
+#endif
+#ifndef KP_F16X_HALF
+#define KP_F16X_HALF 0
+#endif
+// KP_F16X_PAIR: one N = 256 MMA (one TMEM buffer) covers two output groups
+// (fewer MMAs / commits); 0: one N = 128 MMA per group (measured slower).
+constexpr int GPB = KP_F16X_PAIR ? 2 : 1;             // output groups per TMEM buffer
+constexpr int NMMA = GPB * NCOL, NBUF = NGROUP / GPB;
 constexpr int EPI_WARPS = 16, EPI_THREADS = 32 * EPI_WARPS;
 constexpr int NUM_THREADS = 32 * 4 + EPI_THREADS;
 constexpr int A_BYTES = BM * BK * 2;            // 16 KB
@@ -70,7 +88,7 @@ constexpr int BRAW_BYTES = BN * BK * 2;         // 4 KB
 constexpr int STAGE_BYTES = A_BYTES + BRAW_BYTES;
 constexpr int BEXP_GROUP_BYTES = NCOL * BK * 2; // 16 KB: 128 expanded rows x 64 k
 constexpr int BEXP_BYTES = NGROUP * BEXP_GROUP_BYTES;
-constexpr int REG_LEVELS = 3;                   // counter levels kept in registers
+constexpr int REG_LEVELS = KP_F16X_REGLV;       // counter levels kept in registers (2 or 3)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -115,7 +133,7 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
   d |= uint64_t(2) << 61;
   return d;
 }
-// kind::f16, D = F16 (bits 4-5 = 0), A = B = F16, K-major, M = 128, N = 256.
+// kind::f16, D = F16 (bits 4-5 = 0), A = B = F16, K-major, M = 128, N = 128.
 __device__ __forceinline__ void umma_leaves(uint32_t tmem_d, uint64_t da, uint64_t db) {
   constexpr uint32_t IDESC = (uint32_t(NMMA >> 3) << 17) | (uint32_t(BM >> 4) << 24);
   asm volatile(
@@ -130,6 +148,7 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 #define R8(i) "=r"(v[i + 0]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), \
               "=r"(v[i + 5]), "=r"(v[i + 6]), "=r"(v[i + 7])
 // 128 TMEM columns of 16-bit leaves -> 64 registers, adjacent columns packed
+// (asynchronous: tmem_ld_wait() before the registers are read)
 __device__ __forceinline__ void tmem_ld128_pack(uint32_t ta, uint32_t (&v)[64]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x64.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -138,8 +157,19 @@ __device__ __forceinline__ void tmem_ld128_pack(uint32_t ta, uint32_t (&v)[64]) 
       "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n"
       : R8(0), R8(8), R8(16), R8(24), R8(32), R8(40), R8(48), R8(56)
       : "r"(ta));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
+#define R8(i) "=r"(v[i + 0]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), \
+              "=r"(v[i + 5]), "=r"(v[i + 6]), "=r"(v[i + 7])
+// 64 TMEM columns -> 32 registers, adjacent columns packed (asynchronous)
+__device__ __forceinline__ void tmem_ld64_pack(uint32_t ta, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : R8(0), R8(8), R8(16), R8(24)
+      : "r"(ta));
+}
+#undef R8
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 #undef R8
 
 // byte offset of element (row, k) in a SWIZZLE_128B K-major tile (64-wide rows)
@@ -178,7 +208,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < NSTAGE; ++s) mbar_init(smem_u32(&full_bar[s]), 1), mbar_init(smem_u32(&empty_bar[s]), 1);
     for (int s = 0; s < 2; ++s) mbar_init(smem_u32(&bfull_bar[s]), 2), mbar_init(smem_u32(&bempty_bar[s]), 1);
     for (int h = 0; h < NBUF; ++h)
-      mbar_init(smem_u32(&tfull_bar[h]), 1), mbar_init(smem_u32(&tempty_bar[h]), 8);
+      mbar_init(smem_u32(&tfull_bar[h]), 1), mbar_init(smem_u32(&tempty_bar[h]), 4 * GPB);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -223,6 +253,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ===== MMA issuer =====
+      const uint32_t tfull0 = smem_u32(&tfull_bar[0]), tempty0 = smem_u32(&tempty_bar[0]);
       int stage = 0;
       uint32_t phase = 0;
       int bi = 0;  // expanded-B buffer use counter
@@ -238,13 +269,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint64_t db = make_desc(bbase + uint32_t(b * BEXP_BYTES));
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
+            // one N = 128 MMA per output group g into its own TMEM buffer, so
+            // each epilogue set waits only on its own leaves
 #pragma unroll
             for (int h = 0; h < NBUF; ++h) {
-              mbar_wait(smem_u32(&tempty_bar[h]), tphase ^ 1);
+              mbar_wait(tempty0 + 8 * h, tphase ^ 1);
               asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
               umma_leaves(tmem + uint32_t(h * NMMA), da + uint64_t(2 * kk),
-                          db + uint64_t(((xflags & 1 ? 0 : h) * 2 * BEXP_GROUP_BYTES) >> 4) + uint64_t(2 * kk));
-              umma_commit(smem_u32(&tfull_bar[h]));
+                          db + uint64_t(((xflags & 1 ? 0 : h) * GPB * BEXP_GROUP_BYTES) >> 4) + uint64_t(2 * kk));
+              umma_commit(tfull0 + 8 * h);
             }
             tphase ^= 1;
           }
@@ -292,8 +325,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {  // ===== epilogue sets =====
     const int et = tid - 128;              // 0..511
-    const int g = (warp - 4) >> 2;         // output group: TMEM buffer g/2, columns (g%2)*128
-    const int hb = g >> 1;
+    const int g = (warp - 4) >> 2;         // output group = TMEM buffer (columns g*128)
+    const uint32_t my_tfull = smem_u32(&tfull_bar[g / GPB]), my_tempty = smem_u32(&tempty_bar[g / GPB]);
     const int quad = warp & 3;             // TMEM lane quadrant
     const uint32_t tbuf = tmem + (uint32_t(quad * 32) << 16) + uint32_t(g * NCOL);
     const F16Epilogue& e = args.epi;
@@ -307,20 +340,53 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t p01[4], v64[4];
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          mbar_wait(smem_u32(&tfull_bar[hb]), tphase);
+          mbar_wait(my_tfull, tphase);
           tphase ^= 1;
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          uint32_t v[64];
-          tmem_ld128_pack(tbuf, v);
-          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[hb]));
-          // v[kl*4 + p] = leaves kl of outputs (2p, 2p+1): 16-leaf trees
+          // 16-leaf trees of outputs (2p, 2p+1): leaves kl = 0..15 sit in
+          // TMEM columns kl*8 + jl; s16 = ((l0+l1)+(l2+l3) + ...) exactly as
+          // pairwise_block_reduce pairs them
           uint32_t s16[4];
-          if (xflags & 4) {
+#if KP_F16X_HALF
+          {  // two 64-column loads: fewer live registers (no spills)
+            uint32_t h0[4];
+            {
+              uint32_t v[32];  // v[kl*4 + p], kl = 0..7
+              tmem_ld64_pack(tbuf, v);
+              tmem_ld_wait();
 #pragma unroll
-            for (int p = 0; p < 4; ++p) s16[p] = v[p] ^ v[60 + p];
-          } else {
+              for (int p = 0; p < 4; ++p) {
+                const uint32_t a = hadd2(hadd2(v[0 * 4 + p], v[1 * 4 + p]), hadd2(v[2 * 4 + p], v[3 * 4 + p]));
+                const uint32_t b = hadd2(hadd2(v[4 * 4 + p], v[5 * 4 + p]), hadd2(v[6 * 4 + p], v[7 * 4 + p]));
+                h0[p] = hadd2(a, b);
+              }
+            }
+            uint32_t v[32];  // kl = 8..15
+            tmem_ld64_pack(tbuf + 64, v);
+            tmem_ld_wait();
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(my_tempty);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              const uint32_t c = hadd2(hadd2(v[0 * 4 + p], v[1 * 4 + p]), hadd2(v[2 * 4 + p], v[3 * 4 + p]));
+              const uint32_t d = hadd2(hadd2(v[4 * 4 + p], v[5 * 4 + p]), hadd2(v[6 * 4 + p], v[7 * 4 + p]));
+              s16[p] = hadd2(h0[p], hadd2(c, d));
+            }
+          }
+#else
+          {
+            uint32_t v[64];  // v[kl*4 + p]
+            tmem_ld128_pack(tbuf, v);
+#if !KP_F16X_EARLY
+            tmem_ld_wait();
+#endif
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(my_tempty);
+#if KP_F16X_EARLY
+            tmem_ld_wait();
+#endif
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
               uint32_t s8[8];
@@ -331,6 +397,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               s16[p] = hadd2(hadd2(a, b), hadd2(c, d));
             }
           }
+#endif
 #pragma unroll
           for (int p = 0; p < 4; ++p) {
             if (kk == 0 || kk == 2) v64[p] = s16[p];
@@ -339,7 +406,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         // push the 64-leaf unit into the per-output binary counter
-        // (levels 0-2 in registers, higher levels in shared memory)
+        // (the low REG_LEVELS levels in registers, higher levels in shared memory)
         if (!(cnt & 1)) {
 #pragma unroll
           for (int p = 0; p < 4; ++p) r0[p] = v64[p];
@@ -352,21 +419,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           } else {
 #pragma unroll
             for (int p = 0; p < 4; ++p) v64[p] = hadd2(r1[p], v64[p]);
-            if (!(cnt & 4)) {
+            bool carry = true;
+            if constexpr (REG_LEVELS == 3) {
+              if (!(cnt & 4)) {
 #pragma unroll
-              for (int p = 0; p < 4; ++p) r2[p] = v64[p];
-            } else {
+                for (int p = 0; p < 4; ++p) r2[p] = v64[p];
+                carry = false;
+              } else {
 #pragma unroll
-              for (int p = 0; p < 4; ++p) v64[p] = hadd2(r2[p], v64[p]);
-              int c = cnt >> 3, lvl = 0;
-              while (c & 1) {
-#pragma unroll
-                for (int p = 0; p < 4; ++p) v64[p] = hadd2(stack[(lvl * 4 + p) * EPI_THREADS + et], v64[p]);
-                c >>= 1;
-                ++lvl;
+                for (int p = 0; p < 4; ++p) v64[p] = hadd2(r2[p], v64[p]);
               }
+            }
+            if (carry) {
+            int c = cnt >> REG_LEVELS, lvl = 0;
+            while (c & 1) {
 #pragma unroll
-              for (int p = 0; p < 4; ++p) stack[(lvl * 4 + p) * EPI_THREADS + et] = v64[p];
+              for (int p = 0; p < 4; ++p) v64[p] = hadd2(stack[(lvl * 4 + p) * EPI_THREADS + et], v64[p]);
+              c >>= 1;
+              ++lvl;
+            }
+#pragma unroll
+            for (int p = 0; p < 4; ++p) stack[(lvl * 4 + p) * EPI_THREADS + et] = v64[p];
             }
           }
         }
@@ -379,17 +452,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (!((cnt >> L) & 1)) continue;
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          const uint32_t s = L == 0   ? r0[p]
-                             : L == 1 ? r1[p]
-                             : L == 2 ? r2[p]
-                                      : stack[((L - REG_LEVELS) * 4 + p) * EPI_THREADS + et];
+          const uint32_t s = L == 0                      ? r0[p]
+                             : L == 1                      ? r1[p]
+                             : (REG_LEVELS == 3 && L == 2) ? r2[p]
+                                                           : stack[((L - REG_LEVELS) * 4 + p) * EPI_THREADS + et];
           acc[p] = have ? hadd2(s, acc[p]) : s;
         }
         have = true;
       }
-      // ---- epilogue: row m, outputs n0 .. n0+7 ----
+      // ---- epilogue: row m, outputs n0 .. n0+7 (image-local; see F16Epilogue) ----
       const int m = mb + quad * 32 + lane;
-      const int n0 = nb + g * 8;
+      int nlb;
+      const int img = epi_image(e, nb, nlb);
+      const int NL = e.n_img ? e.n_img : N;
+      const int n0 = nlb + g * 8;
+      const int ng0 = nb + g * 8;  // global column (B operand row, hash index)
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
       uint32_t zbits = 0;  // outputs whose tree value is +-0
       if (m < M) {
@@ -397,7 +474,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int p = 0; p < 4; ++p)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
-            if (((acc[p] >> (16 * h)) & 0x7fffu) == 0 && n0 + 2 * p + h < N) zbits |= 1u << (2 * p + h);
+            if (((acc[p] >> (16 * h)) & 0x7fffu) == 0 && n0 + 2 * p + h < NL) zbits |= 1u << (2 * p + h);
         if (zbits) {
           // Zero outputs: the reference value is -0 iff sign(A(m,k)) != sign(B(n,k))
           // for all k < K. Necessary condition on the row sign hashes:
@@ -407,35 +484,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint32_t cand = 0;
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            if (((zbits >> q) & 1) && ha + args.hash_b[n0 + q] == args.hsum) cand |= 1u << q;
+            if (((zbits >> q) & 1) && ha + args.hash_b[ng0 + q] == args.hsum) cand |= 1u << q;
           const uint32_t plus = zbits & ~cand;
 #pragma unroll
           for (int p = 0; p < 4; ++p)
             acc[p] &= ~((((plus >> (2 * p)) & 1) ? 0x8000u : 0u) | (((plus >> (2 * p + 1)) & 1) ? 0x80000000u : 0u));
           zbits = cand;
         }
-        const bool full = n0 + 8 <= N;
+        const bool full = n0 + 8 <= NL;
+        __half* const Ch = e.Ch ? e.Ch + img * e.c_img : nullptr;
         if (e.mode == F16OUT_HALF) {
           if (full && e.cn == 1 && ((e.cm * m + n0) & 7) == 0) {
-            *reinterpret_cast<uint4*>(e.Ch + long(m) * e.cm + n0) = make_uint4(acc[0], acc[1], acc[2], acc[3]);
+            *reinterpret_cast<uint4*>(Ch + long(m) * e.cm + n0) = make_uint4(acc[0], acc[1], acc[2], acc[3]);
           } else {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-              if (n0 + q < N)
-                e.Ch[long(m) * e.cm + long(n0 + q) * e.cn] =
+              if (n0 + q < NL)
+                Ch[long(m) * e.cm + long(n0 + q) * e.cn] =
                     __ushort_as_half((unsigned short)((acc[q >> 1] >> (16 * (q & 1))) & 0xffffu));
           }
         } else if (e.mode == F16OUT_HALF_SCALED) {  // w = round16(S .* t2)
+          const __half* const scale = e.scale + img * e.s_img;
           uint32_t sc[4];
           if (full && e.sn == 1 && ((e.sm * m + n0) & 7) == 0) {
-            const uint4 s4 = *reinterpret_cast<const uint4*>(e.scale + long(m) * e.sm + n0);
+            const uint4 s4 = *reinterpret_cast<const uint4*>(scale + long(m) * e.sm + n0);
             sc[0] = s4.x, sc[1] = s4.y, sc[2] = s4.z, sc[3] = s4.w;
           } else {
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
               const int n = n0 + 2 * p;
-              const uint32_t lo = n < N ? __half_as_ushort(e.scale[long(m) * e.sm + long(n) * e.sn]) : 0u;
-              const uint32_t hi = n + 1 < N ? __half_as_ushort(e.scale[long(m) * e.sm + long(n + 1) * e.sn]) : 0u;
+              const uint32_t lo = n < NL ? __half_as_ushort(scale[long(m) * e.sm + long(n) * e.sn]) : 0u;
+              const uint32_t hi = n + 1 < NL ? __half_as_ushort(scale[long(m) * e.sm + long(n + 1) * e.sn]) : 0u;
               sc[p] = lo | (hi << 16);
             }
           }
@@ -443,26 +522,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int p = 0; p < 4; ++p) asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(w[p]) : "r"(sc[p]), "r"(acc[p]));
           if (full && e.cn == 1 && ((e.cm * m + n0) & 7) == 0) {
-            *reinterpret_cast<uint4*>(e.Ch + long(m) * e.cm + n0) = make_uint4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<uint4*>(Ch + long(m) * e.cm + n0) = make_uint4(w[0], w[1], w[2], w[3]);
           } else {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
-              if (n0 + q < N)
-                e.Ch[long(m) * e.cm + long(n0 + q) * e.cn] =
+              if (n0 + q < NL)
+                Ch[long(m) * e.cm + long(n0 + q) * e.cn] =
                     __ushort_as_half((unsigned short)((w[q >> 1] >> (16 * (q & 1))) & 0xffffu));
           }
         } else {  // FP64 result (+ fused dot partials)
+          double* const Cd = e.Cd + img * e.c_img;
+          const double* const d0 = e.d0 ? e.d0 + img * e.v_img : nullptr;
+          const double* const d1a = e.d1a ? e.d1a + img * e.v_img : nullptr;
+          const double* const d1b = e.d1b ? e.d1b + img * e.v_img : nullptr;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const int n = n0 + q;
-            if (n >= N) continue;
+            if (n >= NL) continue;
             const double v =
                 double(__half2float(__ushort_as_half((unsigned short)((acc[q >> 1] >> (16 * (q & 1))) & 0xffffu))));
-            e.Cd[long(m) * e.cm + long(n) * e.cn] = v;
+            Cd[long(m) * e.cm + long(n) * e.cn] = v;
             if (e.partials) {
               const long vi = long(m) * e.vm + long(n) * e.vn;
-              if (e.d0) s0 += v * e.d0[vi];
-              if (e.d1a) s1 += v * (e.d1b ? (e.d1a[vi] - e.d1b[vi]) : e.d1a[vi]);
+              if (d0) s0 += v * d0[vi];
+              if (d1a) s1 += v * (d1b ? (d1a[vi] - d1b[vi]) : d1a[vi]);
               if (!isfinite(v)) s2 += 1.0;
             }
           }
@@ -473,7 +556,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         unsigned* list = args.zfix + 2;
         int q = 0;
         for (uint32_t zb = zbits; zb; zb &= zb - 1, ++q)
-          list[base + q] = unsigned(long(m) * N + n0 + (__ffs(zb) - 1));
+          list[base + q] = unsigned(long(m) * N + ng0 + (__ffs(zb) - 1));
       }
       if (e.mode == F16OUT_F64 && e.partials) {  // fixed-order per-tile partials
 #pragma unroll
@@ -488,7 +571,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (ew == 0 && lane == 0) {
           double a0 = 0, a1 = 0, a2 = 0;
           for (int w = 0; w < EPI_WARPS; ++w) a0 += red[w][0], a1 += red[w][1], a2 += red[w][2];
-          double* o = e.partials + long(t) * 4;
+          // slot = the tile's row-major position in its image's tile grid (a
+          // batched image reduces its partials in the same order as a single
+          // product of that image)
+          const long slot = e.n_img ? long(img) * e.part_img + long(mb / BM) * (e.n_img / BN) + nlb / BN
+                                    : long(mb / BM) * tiles_n + nb / BN;
+          double* o = e.partials + slot * 4;
           o[0] = a0, o[1] = a1, o[2] = a2, o[3] = 0.0;
         }
         asm volatile("bar.sync 1, %0;\n" ::"n"(EPI_THREADS) : "memory");
@@ -558,9 +646,11 @@ __global__ void f16x_zero_fix_kernel(const F16GemmArgs args) {
   const int KV = K / 8;  // whole 8-element chunks; the tail is checked per element
   for (long q = warp0; q < count; q += nwarps) {
     const long idx = list[q];
-    const int m = int(idx / N), n = int(idx % N);
+    const int m = int(idx / N), ng = int(idx % N);
+    int n;
+    const int img = epi_image(e, ng, n);
     const unsigned short* a = reinterpret_cast<const unsigned short*>(args.A.p) + long(m) * args.A.ld;
-    const unsigned short* b = reinterpret_cast<const unsigned short*>(args.B.p) + long(n) * args.B.ld;
+    const unsigned short* b = reinterpret_cast<const unsigned short*>(args.B.p) + long(ng) * args.B.ld;
     bool opposite = true;
     for (int c = lane; c < KV; c += 32) {
       const uint4 x = reinterpret_cast<const uint4*>(a)[c], y = reinterpret_cast<const uint4*>(b)[c];
@@ -572,13 +662,14 @@ __global__ void f16x_zero_fix_kernel(const F16GemmArgs args) {
     if (lane == 0) {
       const unsigned short z = opposite ? 0x8000u : 0x0000u;
       if (e.mode == F16OUT_HALF) {
-        e.Ch[long(m) * e.cm + long(n) * e.cn] = __ushort_as_half(z);
+        e.Ch[img * e.c_img + long(m) * e.cm + long(n) * e.cn] = __ushort_as_half(z);
       } else if (e.mode == F16OUT_HALF_SCALED) {
         unsigned short r;
-        asm("mul.rn.f16 %0, %1, %2;" : "=h"(r) : "h"(__half_as_ushort(e.scale[long(m) * e.sm + long(n) * e.sn])), "h"(z));
-        e.Ch[long(m) * e.cm + long(n) * e.cn] = __ushort_as_half(r);
+        asm("mul.rn.f16 %0, %1, %2;" : "=h"(r)
+            : "h"(__half_as_ushort(e.scale[img * e.s_img + long(m) * e.sm + long(n) * e.sn])), "h"(z));
+        e.Ch[img * e.c_img + long(m) * e.cm + long(n) * e.cn] = __ushort_as_half(r);
       } else {
-        e.Cd[long(m) * e.cm + long(n) * e.cn] = opposite ? -0.0 : 0.0;
+        e.Cd[img * e.c_img + long(m) * e.cm + long(n) * e.cn] = opposite ? -0.0 : 0.0;
       }
     }
   }
@@ -666,6 +757,7 @@ void row_hash_launch(const F16Operand& X, int rows, int K, unsigned long long* o
 
 long f16x_zfix_words(int M, int N) { return long(M) * N; }
 int gemm_f16x_num_ctas(int M, int N) { return int(cdiv(M, BM) * cdiv(N, BN)); }
+int gemm_f16x_partials_per_image(int M, int n_img) { return int(cdiv(M, BM) * (n_img / BN)); }
 
 unsigned long long f16x_hash_sum(int K) {
   unsigned long long s = 0;

@@ -14,5 +14,6 @@ long f16x_zfix_words(int M, int N);
 void f16x_row_hash(const F16Operand& X, int rows, int K, unsigned long long* out);
 unsigned long long f16x_hash_sum(int K);
 int gemm_f16x_num_ctas(int M, int N);  // = output tiles (one partial slot each)
+int gemm_f16x_partials_per_image(int M, int n_img);  // batched products (F16Epilogue::part_img)
 void gemm_f16x(const F16GemmArgs& a, int kernel_class);
 }  // namespace kp

@@ -31,6 +31,12 @@ struct F64Epilogue {
   const double* d1b = nullptr;
   int count_nonfinite = 0;
   double* partials = nullptr;
+  // Batched banded operator (band_rows, grid.z = image): C and the vectors of
+  // image z start at z * img, its partials at slot z * part_img, and the
+  // addv coefficient is addc_img[z] when given (per-image lambda^2).
+  long img = 0;
+  int part_img = 0;
+  const double* addc_img = nullptr;
 };
 
 struct F64GemmArgs {

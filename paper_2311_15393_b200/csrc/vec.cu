@@ -58,6 +58,20 @@ __device__ double sum_partials(const double* part, int n, int q) {
 
 __device__ __forceinline__ bool stopped(const DevState* st) { return st->status != ST_RUNNING; }
 
+// Batched solves (kp_pcg_batch): image `img` owns DevState st[img], history
+// rows [img * capacity, ...), its vectors at img * nn and its partial slots
+// at img * (slots per image). Single solves use img = 0.
+__device__ __forceinline__ DevHistory hist_of(DevHistory h, int img, size_t nn) {
+  if (img) {
+    const size_t o = size_t(img) * h.capacity;
+    h.resid += o;
+    if (h.relerr) h.relerr += o;
+    if (h.cosines) h.cosines += o;
+    if (h.iterates) h.iterates += o * nn;
+  }
+  return h;
+}
+
 // ---------------------------------------------------------------------------
 __global__ void copy_kernel(double* dst, const double* src, size_t n, const int* status) {
   pdl_wait();
@@ -179,6 +193,8 @@ __global__ void weights_kernel(const double* s_r, const double* s_c, int n, doub
 __global__ void pcg_init_scalar_kernel(DevState* st, DevHistory h, const double* part_r, int nr,
                                        const double* part_xt, int nxt) {
   pdl_wait();
+  const int img = blockIdx.x;  // one block per image
+  st += img, h = hist_of(h, img, 0), part_r += size_t(img) * nr * 4, part_xt += size_t(img) * nxt * 4;
   if (stopped(st)) return;
   const double rr = sum_partials(part_r, nr, 0);
   const double xx = st->has_xt ? sum_partials(part_xt, nxt, 0) : 0.0;
@@ -199,6 +215,7 @@ __global__ void pcg_init_scalar_kernel(DevState* st, DevHistory h, const double*
 
 __global__ void pcg_init_msolve_scalar_kernel(DevState* st, const double* part_z, int nz) {
   pdl_wait();
+  st += blockIdx.x, part_z += size_t(blockIdx.x) * nz * 4;
   if (stopped(st)) return;
   const double rz = sum_partials(part_z, nz, 0);
   const double bad = sum_partials(part_z, nz, 2);
@@ -215,6 +232,7 @@ __global__ void pcg_init_msolve_scalar_kernel(DevState* st, const double* part_z
 
 __global__ void pcg_alpha_scalar_kernel(DevState* st, const double* part, int n) {
   pdl_wait();
+  st += blockIdx.x, part += size_t(blockIdx.x) * n * 4;
   if (stopped(st)) return;
   const double pq = sum_partials(part, n, 0);
   if (threadIdx.x) return;
@@ -239,6 +257,17 @@ __global__ void pcg_update_kernel(const DevState* st, DevHistory h, double* x, d
                                   const double* z, const double* xt, __half* r16, int n,
                                   long ldh, double* part) {
   pdl_wait();
+  {  // image blockIdx.y of a batch
+    const int img = blockIdx.y;
+    const size_t o = size_t(img) * n * n;
+    st += img, h = hist_of(h, img, size_t(n) * n);
+    x += o, r += o, p += o, q += o;
+    if (r_prev) r_prev += o;
+    if (z) z += o;
+    if (xt) xt += o;
+    if (r16) r16 += size_t(img) * n * ldh;
+    part += size_t(img) * gridDim.x * 4;
+  }
   if (stopped(st)) return;
   __shared__ double red[VEC_THREADS / 32][4];
   const double alpha = st->alpha;
@@ -320,6 +349,7 @@ __global__ void pcg_update_kernel(const DevState* st, DevHistory h, double* x, d
 
 __global__ void pcg_resid_scalar_kernel(DevState* st, DevHistory h, const double* part, int n) {
   pdl_wait();
+  st += blockIdx.x, h = hist_of(h, blockIdx.x, 0), part += size_t(blockIdx.x) * n * 4;
   if (stopped(st)) return;
   const double rr = sum_partials(part, n, 0);
   const double ee = st->has_xt ? sum_partials(part, n, 1) : 0.0;
@@ -351,6 +381,7 @@ __global__ void pcg_resid_scalar_kernel(DevState* st, DevHistory h, const double
 
 __global__ void pcg_beta_scalar_kernel(DevState* st, const double* part, int n) {
   pdl_wait();
+  st += blockIdx.x, part += size_t(blockIdx.x) * n * 4;
   if (stopped(st)) return;
   const double rz = sum_partials(part, n, 0);
   const double zdr = sum_partials(part, n, 1);
@@ -374,6 +405,7 @@ __global__ void pcg_beta_scalar_kernel(DevState* st, const double* part, int n) 
 // p = z + beta p, then rho = rz with the positivity check (krylov.cpp:133-138)
 __global__ void pcg_p_update_kernel(DevState* st, double* p, const double* z, size_t nn, bool vec2) {
   pdl_wait();
+  st += blockIdx.y, p += blockIdx.y * nn, z += blockIdx.y * nn;  // image blockIdx.y of a batch
   if (stopped(st)) return;
   const double beta = st->beta;
   if (vec2) {
@@ -688,6 +720,28 @@ unsigned vec_grid(size_t nn) {
     check_launch(#kernel);                                         \
   } while (0)
 
+namespace {
+// Batch summary: out->status = ST_RUNNING while any image runs, else
+// ST_CONVERGED (drives the host polling and gates the shared kernels).
+__global__ void batch_status_kernel(const DevState* st, int count, DevState* out) {
+  pdl_wait();
+  __shared__ int running;
+  if (threadIdx.x == 0) running = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < count; i += blockDim.x)
+    if (st[i].status == ST_RUNNING) running = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) out->status = running ? ST_RUNNING : ST_CONVERGED;
+}
+
+}  // namespace
+
+void batch_status(const DevState* st, int count, DevState* out) {
+  LaunchScope scope(KC_VECTOR);
+  launch_pdl(batch_status_kernel, dim3(1), dim3(256), 0, st, count, out);
+  check_launch("batch_status");
+}
+
 void vec_copy(double* dst, const double* src, size_t n, const int* status) {
   KP_LAUNCH(KC_VECTOR, copy_kernel, vec_grid(n), VEC_THREADS, dst, src, n, status);
 }
@@ -723,14 +777,14 @@ void msolve_finish_f16(const __half* z16, long ldh, int n, double* z, const doub
 }
 
 void pcg_init_scalar(DevState* st, DevHistory h, const double* part_r, int nr,
-                     const double* part_xt, int nxt) {
-  KP_LAUNCH(KC_VECTOR, pcg_init_scalar_kernel, 1, SCALAR_THREADS, st, h, part_r, nr, part_xt, nxt);
+                     const double* part_xt, int nxt, int batch) {
+  KP_LAUNCH(KC_VECTOR, pcg_init_scalar_kernel, batch, SCALAR_THREADS, st, h, part_r, nr, part_xt, nxt);
 }
-void pcg_init_msolve_scalar(DevState* st, const double* part_z, int nz) {
-  KP_LAUNCH(KC_VECTOR, pcg_init_msolve_scalar_kernel, 1, SCALAR_THREADS, st, part_z, nz);
+void pcg_init_msolve_scalar(DevState* st, const double* part_z, int nz, int batch) {
+  KP_LAUNCH(KC_VECTOR, pcg_init_msolve_scalar_kernel, batch, SCALAR_THREADS, st, part_z, nz);
 }
-void pcg_alpha_scalar(DevState* st, const double* part_pq, int n) {
-  KP_LAUNCH(KC_VECTOR, pcg_alpha_scalar_kernel, 1, SCALAR_THREADS, st, part_pq, n);
+void pcg_alpha_scalar(DevState* st, const double* part_pq, int n, int batch) {
+  KP_LAUNCH(KC_VECTOR, pcg_alpha_scalar_kernel, batch, SCALAR_THREADS, st, part_pq, n);
 }
 
 int pcg_update_ctas(int n) {
@@ -740,25 +794,26 @@ int pcg_update_ctas(int n) {
 }
 void pcg_update(DevState* st, DevHistory h, double* x, double* r, double* r_prev, const double* p,
                 const double* q, const double* z, const double* xt, __half* r16, int n, long ldh,
-                double* partials) {
+                double* partials, int batch) {
   const bool vec2 = n % 2 == 0 && al16(x) && al16(r) && al16(r_prev) && al16(p) && al16(q) &&
                     al16(z) && al16(xt) && al16(h.iterates) && ldh % 2 == 0;
+  const dim3 grid(pcg_update_ctas(n), batch);
   if (vec2)
-    KP_LAUNCH(KC_VECTOR, pcg_update_kernel<true>, pcg_update_ctas(n), VEC_THREADS, st, h, x, r, r_prev, p, q,
+    KP_LAUNCH(KC_VECTOR, pcg_update_kernel<true>, grid, VEC_THREADS, st, h, x, r, r_prev, p, q,
               z, xt, r16, n, ldh, partials);
   else
-    KP_LAUNCH(KC_VECTOR, pcg_update_kernel<false>, pcg_update_ctas(n), VEC_THREADS, st, h, x, r, r_prev, p,
+    KP_LAUNCH(KC_VECTOR, pcg_update_kernel<false>, grid, VEC_THREADS, st, h, x, r, r_prev, p,
               q, z, xt, r16, n, ldh, partials);
 }
-void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n) {
-  KP_LAUNCH(KC_VECTOR, pcg_resid_scalar_kernel, 1, SCALAR_THREADS, st, h, part, n);
+void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n, int batch) {
+  KP_LAUNCH(KC_VECTOR, pcg_resid_scalar_kernel, batch, SCALAR_THREADS, st, h, part, n);
 }
-void pcg_beta_scalar(DevState* st, const double* part_z, int n) {
-  KP_LAUNCH(KC_VECTOR, pcg_beta_scalar_kernel, 1, SCALAR_THREADS, st, part_z, n);
+void pcg_beta_scalar(DevState* st, const double* part_z, int n, int batch) {
+  KP_LAUNCH(KC_VECTOR, pcg_beta_scalar_kernel, batch, SCALAR_THREADS, st, part_z, n);
 }
-void pcg_p_update(DevState* st, double* p, const double* z, size_t nn) {
+void pcg_p_update(DevState* st, double* p, const double* z, size_t nn, int batch) {
   const bool vec2 = nn % 2 == 0 && al16(p) && al16(z);
-  KP_LAUNCH(KC_VECTOR, pcg_p_update_kernel, vec_grid(nn), VEC_THREADS, st, p, z, nn, vec2);
+  KP_LAUNCH(KC_VECTOR, pcg_p_update_kernel, dim3(vec_grid(nn), batch), VEC_THREADS, st, p, z, nn, vec2);
 }
 
 void cgls_init_scalar(DevState* st, DevHistory h, const double* part_s, int ns,

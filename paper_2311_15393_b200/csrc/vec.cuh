@@ -76,23 +76,29 @@ void msolve_finish_f16(const __half* z16, long ldh, int n, double* z, const doub
                        const int* status);
 
 // ---- PCG -------------------------------------------------------------------
+// Every PCG kernel takes `batch` (default 1): a batch of independent solves
+// (kp_pcg_batch) runs image i with DevState st[i], history rows from
+// i * h.capacity, vectors at i * n^2 (binary16 r at i * n * ldh) and its own
+// partial slots (i * slots per image). batch = 1 is the single solve.
 // init after r = A^T b (partials_r: [ctas] of ||r||^2) and xnorm partials.
 void pcg_init_scalar(DevState* st, DevHistory h, const double* part_r, int nr,
-                     const double* part_xt, int nxt);
+                     const double* part_xt, int nxt, int batch = 1);
 // after first M-solve (partials: [0]=r.z, [2]=#nonfinite)
-void pcg_init_msolve_scalar(DevState* st, const double* part_z, int nz);
-void pcg_alpha_scalar(DevState* st, const double* part_pq, int n);
+void pcg_init_msolve_scalar(DevState* st, const double* part_z, int nz, int batch = 1);
+void pcg_alpha_scalar(DevState* st, const double* part_pq, int n, int batch = 1);
 // CTAs (= partials) pcg_update uses at size n (fixed for a given n)
 int pcg_update_ctas(int n);
 // x += a p; r -= a q; [r_prev = r]; R16 = round16(r); partials:
 // [0] ||r||^2, [1] ||x - xt||^2, [2] r.z, [3] ||z||^2
 void pcg_update(DevState* st, DevHistory h, double* x, double* r, double* r_prev,
                 const double* p, const double* q, const double* z, const double* xt, __half* r16,
-                int n, long ldh, double* partials);
-void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n);
-void pcg_beta_scalar(DevState* st, const double* part_z, int n);
+                int n, long ldh, double* partials, int batch = 1);
+void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n, int batch = 1);
+void pcg_beta_scalar(DevState* st, const double* part_z, int n, int batch = 1);
 // p = z + beta p
-void pcg_p_update(DevState* st, double* p, const double* z, size_t nn);
+void pcg_p_update(DevState* st, double* p, const double* z, size_t nn, int batch = 1);
+// out->status = ST_RUNNING while any of st[0..count) runs, else ST_CONVERGED
+void batch_status(const DevState* st, int count, DevState* out);
 
 // ---- CGLS ------------------------------------------------------------------
 void cgls_init_scalar(DevState* st, DevHistory h, const double* part_s, int ns,

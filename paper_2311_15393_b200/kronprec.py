@@ -25,7 +25,7 @@ __all__ = [
     "pairwise_sum", "KronTerm", "KroneckerSum", "vec", "unvec", "kronsum_apply",
     "kronsum_apply_transpose", "normal_matvec", "KronSvdPreconditioner",
     "build_preconditioner", "build_preconditioner_from_svd", "with_lambda", "precond_solve",
-    "SolverOptions", "ConvergenceHistory", "SolveResult", "cgls", "pcg", "fpcg",
+    "SolverOptions", "ConvergenceHistory", "SolveResult", "cgls", "pcg", "fpcg", "pcg_batch", "fpcg_batch",
     "plateau_iteration", "WorkReport", "work_report", "SpectralData", "make_spectral_data",
     "ParamChoice", "gcv_objective", "opt_objective", "wgcv_objective", "discrepancy_gap", "gcv",
     "gcv_grid", "lambda_opt", "wgcv", "discrepancy", "filtered_solution", "NoRootError",
@@ -476,6 +476,66 @@ def fpcg(a: KroneckerSum, b, m: KronSvdPreconditioner, opts: SolverOptions) -> S
     if m.n != a.n:
         raise ValueError("solver: preconditioner size mismatch")
     return _solve("fpcg", a, b, m, opts)
+
+
+def _solve_batch(kind: str, a: KroneckerSum, bs, m: KronSvdPreconditioner, lambdas,
+                 opts: SolverOptions, x_true=None) -> list:
+    nn = a.n * a.n
+    bs = np.ascontiguousarray(np.asarray(bs, dtype=np.float64).reshape(-1, nn))
+    batch = bs.shape[0]
+    lam = np.ascontiguousarray(np.asarray(lambdas, dtype=np.float64).reshape(-1))
+    if lam.size != batch:
+        raise ValueError("pcg_batch: one lambda per right-hand side")
+    if m.n != a.n:
+        raise ValueError("solver: preconditioner size mismatch")
+    if opts.max_iterations < 1:
+        raise ValueError("solver: max_iterations must be at least 1")
+    xt = None
+    if x_true is not None:
+        xt = np.ascontiguousarray(np.asarray(x_true, dtype=np.float64).reshape(-1, nn))
+        if xt.shape[0] != batch:
+            raise ValueError("solver: x_true batch mismatch")
+        if np.any(np.linalg.norm(xt, axis=1) == 0.0):
+            raise ValueError("solver: x_true must be nonzero")
+    cap = opts.max_iterations + 1
+    bufs = [[np.zeros(cap) for _ in range(4)] for _ in range(batch)]
+    hs = (kp_history * batch)()
+    for i, (rel, res, work, cos) in enumerate(bufs):
+        hs[i] = kp_history(capacity=cap, relative_error=ptr(rel), residual_norm=ptr(res),
+                           work_units=ptr(work), residual_cosines=ptr(cos))
+    o = kp_solver_options(lambda_=0.0, max_iterations=int(opts.max_iterations),
+                          rel_residual_tol=float(opts.rel_residual_tol), x_true=ptr(xt),
+                          track_search_direction_orthogonality=int(opts.track_search_direction_orthogonality),
+                          record_iterates=0, device_pointers=0)
+    x = np.empty((batch, nn))
+    f = lib().kp_pcg_batch if kind == "pcg" else lib().kp_fpcg_batch
+    check(f(a.handle(), m.handle(), batch, ptr(bs), ptr(lam), C.byref(o), ptr(x), hs))
+    out = []
+    for i in range(batch):
+        h = hs[i]
+        rel, res, work, cos = bufs[i]
+        rows = h.rows
+        out.append(SolveResult(x[i].copy(), ConvergenceHistory(
+            relative_error=list(rel[:rows]) if xt is not None else [],
+            residual_norm=list(res[:rows]), work_units=list(work[:rows]),
+            residual_cosines=list(cos[:h.n_cosines]), iterates=[],
+            iterations_used=h.iterations_used, converged=bool(h.converged),
+            abort_reason=h.abort_reason.decode(), msolve_count=h.msolve_count)))
+    return out
+
+
+def pcg_batch(a: KroneckerSum, bs, m: KronSvdPreconditioner, lambdas, opts: SolverOptions,
+              x_true=None) -> list:
+    """PCG for a batch of right-hand sides (rows of `bs`), image i with lambda
+    lambdas[i] and the factors of `m` (with_lambda per image, cli.cpp:469-486):
+    one batched device solve; result i equals pcg(a, bs[i], with_lambda(m,
+    lambdas[i]), opts) with opts.x_true = x_true[i]."""
+    return _solve_batch("pcg", a, bs, m, lambdas, opts, x_true)
+
+
+def fpcg_batch(a: KroneckerSum, bs, m: KronSvdPreconditioner, lambdas, opts: SolverOptions,
+               x_true=None) -> list:
+    return _solve_batch("fpcg", a, bs, m, lambdas, opts, x_true)
 
 
 def plateau_iteration(h: ConvergenceHistory, tol: float = 0.01) -> int:  # krylov.cpp:220-231

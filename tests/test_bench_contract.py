@@ -55,3 +55,7 @@ def test_device_arm_line():
     c = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c) and c["samples"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["cpu_baseline"]["single_thread"]["cores"] == 1
+    # both arms describe the same workload with the same config dict
+    ref = run_bench("--impl", "reference", "--config", "C1", "--steps", "1", "--warmup", "0")
+    assert ref["config"] == d["config"] and ref["metric"] == d["metric"]

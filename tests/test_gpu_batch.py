@@ -1,0 +1,97 @@
+"""Batched PCG / FPCG (kp_pcg_batch): a batch of right-hand sides with one
+lambda each, solved in one device state machine (images stacked along the
+GEMM N dimension of the M-solve products, grid.z of the banded operator
+passes, one DevState per image) must give, image by image, exactly what the
+single solve gives (cli.cpp:469-486: with_lambda + pcg per image) — same
+iterates bit for bit, same histories, same stop / abort."""
+import numpy as np
+import pytest
+
+import paper_2311_15393_b200 as K
+from paper_2311_15393_b200 import problems as P
+from paper_2311_15393_b200.kronprec import SolverOptions
+
+pytestmark = pytest.mark.gpu
+H = K.PrecisionFormat.fp16()
+
+
+def batch_problem(n, count, sigma=2.5, np_=17):
+    psf = P.make_psf("gaussian", np_, sigma=sigma)
+    a, _ = P.psf_to_kronsum(psf, n)
+    term = P.nearest_kron(psf, n)
+    tps = [P.make_test_problem(P.blob_image(n, 4000 + i), psf, [0.001, 0.01, 0.05][i % 3], 5000 + i, a=a)
+           for i in range(count)]
+    return a, term, tps
+
+
+@pytest.fixture(params=["auto", "cuda", "tensor"])
+def engine(request):
+    K.set_fp16_products(request.param)
+    yield request.param
+    K.set_fp16_products("auto")
+
+
+@pytest.mark.parametrize("solver", ["pcg", "fpcg"])
+@pytest.mark.parametrize("n,count", [(64, 5), (96, 3), (100, 2), (128, 4)])
+def test_batch_equals_single_solves(engine, solver, n, count):
+    a, term, tps = batch_problem(n, count)
+    m0 = K.build_preconditioner(term.row_factor, term.col_factor, 1.0, H)
+    lams = [0.02 * (1 + i) for i in range(count)]
+    opts = SolverOptions(max_iterations=25, rel_residual_tol=1e-6)
+    bs = np.stack([tp.b for tp in tps])
+    xts = np.stack([tp.x_true for tp in tps])
+    res = getattr(K, f"{solver}_batch")(a, bs, m0, lams, opts, x_true=xts)
+    for i, tp in enumerate(tps):
+        o = SolverOptions(lambda_=lams[i], max_iterations=25, rel_residual_tol=1e-6, x_true=tp.x_true)
+        single = getattr(K, solver)(a, tp.b, K.with_lambda(m0, lams[i]), o)
+        hb, hs = res[i].history, single.history
+        assert hb.iterations_used == hs.iterations_used
+        assert hb.converged == hs.converged and hb.abort_reason == hs.abort_reason
+        assert hb.msolve_count == hs.msolve_count
+        assert hb.residual_norm == hs.residual_norm
+        assert hb.relative_error == hs.relative_error
+        assert np.array_equal(res[i].x, single.x)
+
+
+def test_batch_dense_operator_path():
+    a, term, tps = batch_problem(64, 3)
+    a.set_mode("dense")
+    m0 = K.build_preconditioner(term.row_factor, term.col_factor, 1.0, H)
+    lams = [0.03, 0.01, 0.2]
+    opts = SolverOptions(max_iterations=15, rel_residual_tol=1e-6)
+    res = K.pcg_batch(a, np.stack([tp.b for tp in tps]), m0, lams, opts,
+                      x_true=np.stack([tp.x_true for tp in tps]))
+    for i, tp in enumerate(tps):
+        o = SolverOptions(lambda_=lams[i], max_iterations=15, rel_residual_tol=1e-6, x_true=tp.x_true)
+        single = K.pcg(a, tp.b, K.with_lambda(m0, lams[i]), o)
+        assert res[i].history.residual_norm == single.history.residual_norm
+        assert np.array_equal(res[i].x, single.x)
+
+
+def test_batch_mixed_stops():
+    """Images that converge, abort and run to the cap in one batch: each one
+    freezes at its own stop while the others continue."""
+    a, term, tps = batch_problem(64, 3)
+    m0 = K.build_preconditioner(term.row_factor, term.col_factor, 1.0, H)
+    bs = np.stack([tps[0].b, np.zeros_like(tps[1].b), tps[2].b])  # image 1: b = 0 -> converged at once
+    lams = [0.5, 0.05, 0.004]
+    opts = SolverOptions(max_iterations=40, rel_residual_tol=1e-3)
+    res = K.pcg_batch(a, bs, m0, lams, opts)
+    for i in range(3):
+        o = SolverOptions(lambda_=lams[i], max_iterations=40, rel_residual_tol=1e-3)
+        single = K.pcg(a, bs[i], K.with_lambda(m0, lams[i]), o)
+        assert res[i].history.iterations_used == single.history.iterations_used
+        assert res[i].history.abort_reason == single.history.abort_reason
+        assert np.array_equal(res[i].x, single.x)
+    assert res[1].history.iterations_used == 0 and res[1].history.converged
+
+
+def test_batch_validation():
+    a, term, tps = batch_problem(32, 2)
+    m0 = K.build_preconditioner(term.row_factor, term.col_factor, 1.0, H)
+    bs = np.stack([tp.b for tp in tps])
+    with pytest.raises(ValueError):
+        K.pcg_batch(a, bs, m0, [0.1], SolverOptions())
+    m64 = K.build_preconditioner(term.row_factor, term.col_factor, 1.0, K.PrecisionFormat.fp64())
+    with pytest.raises(Exception, match="fp16 reference-exact"):
+        K.pcg_batch(a, bs, m64, [0.1, 0.2], SolverOptions())

@@ -117,17 +117,35 @@ def test_c3_gcv_index_and_pcg():
     check_against(run, g["runs"][0])
 
 
-def test_c4_discrepancy_and_pcg_subset():
+def test_c4_discrepancy_and_batched_pcg_vs_golden():
+    """C4: every image of the golden (all 64 of the batch once generated):
+    discrepancy lambda (1e-9) and the batched PCG solve (kp_pcg_batch) within
+    the north-star bounds of the oracle's per-image run."""
     from paper_2311_15393_b200.batch import C4Shard
     g = golden("C4")
     sh = C4Shard()
-    for rec in g["images"]:
-        res = sh.solve(rec["image"])
+    ids = [rec["image"] for rec in g["images"]]
+    probs = {i: sh.problem(i) for i in ids}
+    results = sh.solve_batch(ids, probs)
+    for rec, res in zip(g["images"], results):
+        assert res.image == rec["image"]
         assert res.lam == pytest.approx(rec["lambda"], rel=1e-9)
         ref = rec["runs"][0]
         assert abs(res.iterations - ref["iterations_used"]) <= 2
         assert res.converged == ref["converged"]
         assert abs(res.rel_err - ref["relative_error"][-1]) <= 1e-3
+
+
+def test_c4_batched_equals_per_image_solves():
+    """Two C4 images at full size: the batched solve equals the per-image
+    pipeline (solve()) exactly."""
+    from paper_2311_15393_b200.batch import C4Shard
+    sh = C4Shard()
+    probs = {i: sh.problem(i) for i in (1, 2)}
+    batched = sh.solve_batch([1, 2], probs)
+    for i, rb in zip((1, 2), batched):
+        rs = sh.solve(i, probs[i])
+        assert (rb.lam, rb.iterations, rb.converged, rb.rel_err) == (rs.lam, rs.iterations, rs.converged, rs.rel_err)
 
 
 def test_c5_prefix_vs_golden():
