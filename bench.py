@@ -307,8 +307,9 @@ def cpu_c4_image_sample(cfg, svd_r, svd_c, fmt, threads) -> float:
     m0 = O.build_preconditioner_from_svd((svd_r.u, svd_r.s, svd_r.v), (svd_c.u, svd_c.s, svd_c.v), 1.0, fmt)
     t0 = time.perf_counter()
     so, bo = O.spectral(m0, cfg.problem.b)
-    O.discrepancy(so, bo, float(np.linalg.norm(cfg.problem.noise)), cfg.eta)
+    lam = O.discrepancy(so, bo, float(np.linalg.norm(cfg.problem.noise)), cfg.eta)["lambda"]
     t_sel = time.perf_counter() - t0
+    cfg.lambda_ = lam  # the image's own lambda for the iteration sample
     return t_sel + 100 * cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads)
 
 
@@ -382,18 +383,31 @@ def run_c4(args):
     sh = C4Shard(n=args.size, svd=args.svd, device=local)
     probs = {i: sh.problem(i) for i in mine}  # input generation is not timed
     batched = args.c4_mode == "batch"
+    pinned = []
+
+    def palloc(shape):  # pinned host staging (the e2e inputs / outputs live here)
+        p = C.c_void_p()
+        check(L.kp_host_alloc(int(np.prod(shape)) * 8, C.byref(p)))
+        pinned.append(p)
+        return np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), shape=shape)
+
+    if batched:
+        bs, xts, nzs = sh.stack(mine, probs, palloc)
+        xout = palloc(bs.shape)
+        levels = [probs[i].noise_level for i in mine]
 
     def run_all():
-        # batch: per-image spectral data + discrepancy lambda, then ONE batched
-        # PCG over this rank's images (kp_pcg_batch); streams: the per-image
-        # pipeline on `workers` concurrent streams
-        return sh.solve_batch(mine, probs) if batched else sh.solve_many(mine, probs, args.workers)
+        # batch: lambdas by kp_discrepancy_batch, then ONE batched PCG over this
+        # rank's images (kp_pcg_batch), host buffers in and out; streams: the
+        # per-image pipeline on `workers` concurrent streams
+        if batched:
+            return sh.solve_arrays(mine, bs, xts, nzs, levels, out=xout)
+        return sh.solve_many(mine, probs, args.workers)
 
     for _ in range(max(1, args.warmup)):
         run_all()
     if dist:
         dist.barrier()
-    import ctypes as C
     launches0 = L.kp_launch_count()
     times = []
     with ClockSampler(local) as clk:
@@ -410,14 +424,14 @@ def run_c4(args):
     # profiled pass (per-launch events) for the M-solve GEMM roofline
     roof = None
     if batched:
-        lams = sh.select_lambdas(mine, probs)
+        lams = sh.select_lambdas_arrays(bs, nzs)
         check(L.kp_profile_reset())
         check(L.kp_profile_enable(1))
-        res_p = sh.solve_batch(mine, probs, lams)
+        res_p = sh.solve_arrays(mine, bs, xts, nzs, levels, lams, out=xout)
         tt, tc = C.c_double(), C.c_longlong()
         check(L.kp_profile_read(1, C.byref(tt), C.byref(tc)))
         check(L.kp_profile_enable(0))
-        nb = sum(1 for i in mine if lams[i] is not None)
+        nb = sum(1 for v in lams if v is not None)
         batches = 1 + max(r.iterations for r in res_p)  # batched M-solves that ran (initial + per iteration)
         work = 2.0 * nb * float(sh.n) ** 3  # binary16 ops per launch (all images of the batch)
         ach = work / (tt.value / (4 * batches) / 1e3) / 1e12 if tc.value else 0.0
@@ -498,6 +512,8 @@ def run_c4(args):
                            for r in allres[:6]],
                "tensor_mode": tensor}
         print(json.dumps(out), flush=True)
+    for p_ in pinned:
+        L.kp_host_free(p_)
     if dist:
         dist.destroy_process_group()
     return 0

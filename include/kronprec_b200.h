@@ -203,7 +203,19 @@ int kp_normal_matvec(const kp_operator* op, double lambda, const double* p,
                      double* out);
 
 /* ---- preconditioner: factor.hpp / factor.cpp -------------------------- */
-/* build_preconditioner (factor.cpp:80-104): host LAPACK SVDs of a_r, a_c,
+/* svd_dense (factor.cpp:14-23): a = u diag(s) v^T, s nonincreasing; a, u, v
+ * n x n column-major host arrays, s length n. Backend KP_SVD_HOST: LAPACK
+ * dgesdd on the host (the oracle's routine); KP_SVD_DEVICE: cuSOLVER FP64
+ * on the GPU (gesvd, or one-sided Jacobi gesvdj with KP_SVD_ALGO=gesvdj).
+ * Vectors agree up to sign; everything the path computes from them (M, the
+ * GCV sums, the discrepancy lambda) is invariant to that. */
+#define KP_SVD_HOST 0
+#define KP_SVD_DEVICE 1
+int kp_svd(const double* a, int n, int backend, double* u, double* s, double* v);
+/* backend kp_precond_build uses (process-wide; env KP_SVD=device|host) */
+int kp_set_svd_backend(int backend);
+int kp_get_svd_backend(int* backend);
+/* build_preconditioner (factor.cpp:80-104): SVDs of a_r, a_c (backend above),
  * weights S(i,j)=1/((s_r(j) s_c(i))^2+lambda^2), rounded V_r, V_c, S.
  * Any format: binary16 runs on the f16x2 GEMMs (or tcgen05 with
  * KP_ACCUM_TENSOR), double-covering formats on DMMA GEMMs, every other
@@ -310,6 +322,16 @@ int kp_filtered_solution(const kp_precond* p, const double* b, double lambda,
  * one-point-at-a-time bisection. */
 int kp_discrepancy(const kp_spectral* sd, double noise_norm, double eta,
                    kp_param_choice* choice);
+/* The discrepancy lambda of `batch` right-hand sides b (batch * n^2 host
+ * doubles, image i at i * n^2) sharing the preconditioner factors of p:
+ * make_spectral_data(p, b_i) + discrepancy(sd_i, noise_norms[i], eta) for
+ * every image, with all images' bisections advancing together (one batched
+ * reduction launch per round). lambdas[i] is bit-identical to
+ * kp_discrepancy's; status[i] = 0, KP_ERR_NO_ROOT or KP_ERR_RUNTIME (then
+ * lambdas[i] = NaN). */
+int kp_discrepancy_batch(const kp_precond* p, int batch, const double* b,
+                         const double* noise_norms, double eta, double* lambdas,
+                         int* status);
 
 #ifdef __cplusplus
 }

@@ -76,7 +76,8 @@ EXPORTS = [
     "kp_spectral_create_x", "kp_spectral_export_xhat", "kp_opt_objective", "kp_wgcv_objective",
     "kp_lambda_opt", "kp_wgcv", "kp_filtered_solution", "kp_round_array", "kp_lp_matmul",
     "kp_lp_matmul_ex", "kp_set_fp16_products", "kp_get_fp16_products", "kp_psf_to_kronsum",
-    "kp_nearest_kron", "kp_pcg_batch", "kp_fpcg_batch",
+    "kp_nearest_kron", "kp_pcg_batch", "kp_fpcg_batch", "kp_svd", "kp_set_svd_backend",
+    "kp_get_svd_backend", "kp_discrepancy_batch",
 ]
 
 _lib = None
@@ -115,6 +116,9 @@ def lib() -> C.CDLL:
             "kp_cgls": ([P, P, C.POINTER(kp_solver_options), P, C.POINTER(kp_history)], I),
             "kp_pcg": ([P, P, P, C.POINTER(kp_solver_options), P, C.POINTER(kp_history)], I),
             "kp_fpcg": ([P, P, P, C.POINTER(kp_solver_options), P, C.POINTER(kp_history)], I),
+            "kp_svd": ([P, I, I, P, P, P], I), "kp_set_svd_backend": ([I], I),
+            "kp_get_svd_backend": ([C.POINTER(I)], I),
+            "kp_discrepancy_batch": ([P, I, P, P, D, P, P], I),
             "kp_pcg_batch": ([P, P, I, P, P, C.POINTER(kp_solver_options), P, C.POINTER(kp_history)], I),
             "kp_fpcg_batch": ([P, P, I, P, P, C.POINTER(kp_solver_options), P, C.POINTER(kp_history)], I),
             "kp_spectral_create": ([P, P, C.POINTER(V)], I),

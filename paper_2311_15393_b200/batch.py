@@ -170,42 +170,64 @@ class C4Shard:
             raise errors[0]
         return [out[i] for i in images]
 
-    def select_lambdas(self, images, probs: dict) -> dict:
-        """Discrepancy-principle lambda per image (regparam.cpp:288-327 on
-        the device spectral data; None when the bracket has no root)."""
-        K, np = self.K, self.np
-        lams = {}
-        for i in images:
-            tp = probs[i]
-            sd = K.make_spectral_data(self.m0, tp.b)
-            try:
-                lams[i] = K.discrepancy(sd, float(np.linalg.norm(tp.noise)), self.eta).lambda_
-            except K.NoRootError:
-                lams[i] = None
-        return lams
+    def stack(self, images, probs: dict, alloc=None):
+        """(b, x_true) of `images` as two contiguous batch x n^2 arrays and the
+        noise norms; `alloc(shape)` provides the arrays (e.g. pinned host
+        memory), numpy by default."""
+        np = self.np
+        images = list(images)
+        nn = self.n * self.n
+        alloc = alloc or (lambda shape: np.empty(shape))
+        bs, xts = alloc((len(images), nn)), alloc((len(images), nn))
+        for q, i in enumerate(images):
+            bs[q] = probs[i].b
+            xts[q] = probs[i].x_true
+        return bs, xts, [float(np.linalg.norm(probs[i].noise)) for i in images]
 
-    def solve_batch(self, images, probs: dict, lams: dict | None = None) -> list:
-        """The images' PCG solves as ONE batched device solve (kp_pcg_batch:
-        images stacked along the M-solve GEMMs' N dimension, one DevState per
-        image); lambdas from select_lambdas unless given. Image by image the
-        result equals solve()."""
+    def select_lambdas_arrays(self, bs, noise_norms) -> list:
+        """Discrepancy-principle lambda per row of bs (regparam.cpp:288-327),
+        all images' bisections advancing together (kp_discrepancy_batch; equal
+        to discrepancy() per image); None when the bracket has no root."""
+        lam, st = self.K.discrepancy_batch(self.m0, bs, noise_norms, self.eta)
+        return [float(v) if c == 0 else None for v, c in zip(lam, st)]
+
+    def select_lambdas(self, images, probs: dict) -> dict:
+        images = list(images)
+        bs, _, nz = self.stack(images, probs)
+        return dict(zip(images, self.select_lambdas_arrays(bs, nz)))
+
+    def solve_arrays(self, images, bs, xts, noise_norms, noise_levels, lams=None, out=None) -> list:
+        """The images' PCG solves (rows of bs / xts) as ONE batched device
+        solve (kp_pcg_batch: images stacked along the M-solve GEMMs' N
+        dimension, one DevState per image); lambdas by the discrepancy
+        principle unless given. Image by image the result equals solve()."""
         K, np = self.K, self.np
         images = list(images)
-        lams = lams if lams is not None else self.select_lambdas(images, probs)
-        out = {}
-        ok = [i for i in images if lams[i] is not None]
-        for i in images:
-            if lams[i] is None:
-                out[i] = ImageResult(i, probs[i].noise_level, float("nan"), 0, False, float("nan"), "", True)
+        lams = lams if lams is not None else self.select_lambdas_arrays(bs, noise_norms)
+        ok = [q for q in range(len(images)) if lams[q] is not None]
+        res = {}
         if ok:
             opts = K.SolverOptions(max_iterations=100, rel_residual_tol=self.tol)
-            res = K.pcg_batch(self.a, np.stack([probs[i].b for i in ok]), self.m0, [lams[i] for i in ok],
-                              opts, x_true=np.stack([probs[i].x_true for i in ok]))
-            for i, r in zip(ok, res):
-                h = r.history
-                out[i] = ImageResult(i, probs[i].noise_level, lams[i], h.iterations_used, h.converged,
-                                     h.relative_error[-1], h.abort_reason)
-        return [out[i] for i in images]
+            full = len(ok) == len(images)
+            sub = (lambda a: a) if full else (lambda a: np.ascontiguousarray(a[ok]))
+            rr = K.pcg_batch(self.a, sub(bs), self.m0, [lams[q] for q in ok], opts, x_true=sub(xts),
+                             out=out if full else None)
+            res = dict(zip(ok, rr))
+        outl = []
+        for q, i in enumerate(images):
+            if q not in res:
+                outl.append(ImageResult(i, noise_levels[q], float("nan"), 0, False, float("nan"), "", True))
+                continue
+            h = res[q].history
+            outl.append(ImageResult(i, noise_levels[q], lams[q], h.iterations_used, h.converged,
+                                    h.relative_error[-1], h.abort_reason))
+        return outl
+
+    def solve_batch(self, images, probs: dict, lams: dict | None = None) -> list:
+        images = list(images)
+        bs, xts, nz = self.stack(images, probs)
+        return self.solve_arrays(images, bs, xts, nz, [probs[i].noise_level for i in images],
+                                 None if lams is None else [lams[i] for i in images])
 
     def solve(self, image: int, tp=None, a=None) -> ImageResult:
         K, np = self.K, self.np

@@ -87,7 +87,7 @@ def build_library(verbose: bool = False, force: bool = False) -> str:
         list(ex.map(lambda c: _run(c, verbose), jobs))
     if force or jobs or _newer(LIB, objs):
         bdir, bname = openblas()
-        _run([NVCC, *GENCODE, "-shared", "-o", LIB, *objs, "-cudart", "static",
+        _run([NVCC, *GENCODE, "-shared", "-o", LIB, *objs, "-cudart", "static", "-lcusolver",
               f"-L{bdir}", f"-l:{bname}", f"-Xlinker", f"-rpath={bdir}"], verbose)
     return LIB
 

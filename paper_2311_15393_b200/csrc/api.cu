@@ -30,6 +30,7 @@
 #include "gemm_f16ref.cuh"
 #include "gemm_f16tc.cuh"
 #include "gemm_f16x.cuh"
+#include "svd_dev.h"
 #include "lp_generic.cuh"
 #include "gemm_f64.cuh"
 #include "host_la.h"
@@ -564,73 +565,60 @@ void msolve(kp_precond* p, const double* r, double* z, const double* d0, const d
   }
   if (!is_fp16(p->fmt)) throw Unsupported("precond_solve: only fp16 and double-covering formats run on the B200 path");
   const long ldh = sh->ldh;
-  if (msolve_f16x(p)) {
+  if (p->accum == KP_ACCUM_REFERENCE) {
     // gemm_f16x needs a finite A operand (the expanded-B filler zeros multiply
     // it): A is always a singular-vector factor, B the data. The second and
     // fourth products are therefore formed transposed (out^T = B'^T A'^T),
-    // which also makes every epilogue store row-contiguous.
+    // which also makes every epilogue store row-contiguous. gemm_f16ref runs
+    // the same orientation (same values either way; the fused dot partials
+    // then group z identically for both engines and for batched solves).
+    const bool f16x = msolve_f16x(p);
+    auto gemm_x = [f16x](const F16GemmArgs& a, int cls) { f16x ? gemm_f16x(a, cls) : gemm_f16ref(a, cls); };
     F16GemmArgs g;
-    g.M = n, g.N = n, g.K = n, g.status = status, g.zfix = p->zfix.p;
-    g.hash_a_ready = true, g.hash_b = p->hash_b.p;
+    g.M = n, g.N = n, g.K = n, g.status = status;
+    if (f16x) g.zfix = p->zfix.p, g.hash_a_ready = true, g.hash_b = p->hash_b.p;
     g.hash_a = sh->hash_vc_a.p;
     g.A = {sh->vc_a.p, ldh}, g.B = {p->r16.p, ldh};  // t1(a,j) = lp(V_c^T R)
     g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = ldh, g.epi.cn = 1;
-    gemm_f16x(g, KC_PRECOND);
+    gemm_x(g, KC_PRECOND);
     g.hash_a = sh->hash_vr_b.p;
     g.A = {sh->vr_b.p, ldh}, g.B = {p->t1h.p, ldh};  // w(a,b) = round(S .* lp(t1 V_r)), as (b, a)
     g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF_SCALED, g.epi.Ch = p->wh.p, g.epi.cm = ldh,
     g.epi.cn = 1, g.epi.scale = p->s16.p, g.epi.sm = n, g.epi.sn = 1;
-    gemm_f16x(g, KC_PRECOND);
+    gemm_x(g, KC_PRECOND);
     g.hash_a = sh->hash_vct_a.p;
     g.A = {sh->vct_a.p, ldh}, g.B = {p->wh.p, ldh};  // t3(i,b) = lp(V_c w)
     g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t3h.p, g.epi.cm = ldh, g.epi.cn = 1;
-    gemm_f16x(g, KC_PRECOND);
+    gemm_x(g, KC_PRECOND);
     g.hash_a = sh->hash_vrt_b.p;
     g.A = {sh->vrt_b.p, ldh}, g.B = {p->t3h.p, ldh};  // z(i,j) = lp(t3 V_r^T), as (j, i)
     g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z, g.epi.cm = n, g.epi.cn = 1;
     g.epi.vm = n, g.epi.vn = 1, g.epi.d0 = d0, g.epi.d1a = d1a, g.epi.d1b = d1b;
     g.epi.partials = p->part.p;
-    gemm_f16x(g, KC_PRECOND);
+    gemm_x(g, KC_PRECOND);
     return;
   }
-  auto gemm = p->accum == KP_ACCUM_TENSOR ? gemm_f16tc : gemm_f16ref;
+  // KP_ACCUM_TENSOR: tcgen05 kind::f16 products (gemm_f16tc). Its epilogue
+  // threads own output rows (TMEM lanes), so t1 and t3 are computed
+  // transposed (t1^T = R^T V_c, t3^T = w^T V_c^T) to store M-contiguously.
   F16GemmArgs g;
   g.M = n, g.N = n, g.K = n, g.status = status;
-  if (p->accum == KP_ACCUM_TENSOR) {
-    // tcgen05 epilogue threads own output rows (TMEM lanes): compute t1^T =
-    // R^T V_c so the row-major t1 is written M-contiguous (coalesced).
-    g.A = {p->r16.p, ldh}, g.B = {sh->vc_a.p, ldh};
-    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = 1, g.epi.cn = ldh;
-  } else {
-    g.A = {sh->vc_a.p, ldh}, g.B = {p->r16.p, ldh};  // t1 = lp(V_c^T R)
-    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = ldh, g.epi.cn = 1;
-  }
-  gemm(g, KC_PRECOND);
-  g.A = {p->t1h.p, ldh}, g.B = {sh->vr_b.p, ldh};  // w = round(S .* lp(t1 V_r))
+  g.A = {p->r16.p, ldh}, g.B = {sh->vc_a.p, ldh};
+  g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = 1, g.epi.cn = ldh;
+  gemm_f16tc(g, KC_PRECOND);
+  g.A = {p->t1h.p, ldh}, g.B = {sh->vr_b.p, ldh};  // w = round(S .* (t1 V_r))
   g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF_SCALED, g.epi.Ch = p->wh.p, g.epi.cm = 1,
   g.epi.cn = ldh, g.epi.scale = p->s16.p, g.epi.sm = 1, g.epi.sn = n;
-  gemm(g, KC_PRECOND);
-  if (p->accum == KP_ACCUM_TENSOR) {  // t3^T = w^T V_c^T, M-contiguous
-    g.A = {p->wh.p, ldh}, g.B = {sh->vct_a.p, ldh};
-    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t3h.p, g.epi.cm = 1, g.epi.cn = ldh;
-  } else {
-    g.A = {sh->vct_a.p, ldh}, g.B = {p->wh.p, ldh};  // t3 = lp(V_c w)
-    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t3h.p, g.epi.cm = ldh, g.epi.cn = 1;
-  }
-  gemm(g, KC_PRECOND);
-  g.A = {p->t3h.p, ldh}, g.B = {sh->vrt_b.p, ldh};  // z = lp(t3 V_r^T)
-  if (p->accum == KP_ACCUM_TENSOR) {
-    // binary16 z into t1h (free once the second product has consumed it),
-    // then one HBM pass widens it and forms the dot partials
-    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = 1, g.epi.cn = ldh;
-    gemm(g, KC_PRECOND);
-    msolve_finish_f16(p->t1h.p, ldh, n, z, d0, d1a, d1b, p->part.p, status);
-    return;
-  }
-  g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z, g.epi.cm = 1, g.epi.cn = n;
-  g.epi.vm = 1, g.epi.vn = n, g.epi.d0 = d0, g.epi.d1a = d1a, g.epi.d1b = d1b;
-  g.epi.partials = p->part.p;
-  gemm(g, KC_PRECOND);
+  gemm_f16tc(g, KC_PRECOND);
+  g.A = {p->wh.p, ldh}, g.B = {sh->vct_a.p, ldh};
+  g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t3h.p, g.epi.cm = 1, g.epi.cn = ldh;
+  gemm_f16tc(g, KC_PRECOND);
+  // binary16 z into t1h (free once the second product has consumed it), then
+  // one HBM pass widens it and forms the dot partials
+  g.A = {p->t3h.p, ldh}, g.B = {sh->vrt_b.p, ldh};  // z = t3 V_r^T
+  g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = 1, g.epi.cn = ldh;
+  gemm_f16tc(g, KC_PRECOND);
+  msolve_finish_f16(p->t1h.p, ldh, n, z, d0, d1a, d1b, p->part.p, status);
 }
 
 void cast_r16(kp_precond* p, const double* r, const int* status) {
@@ -1832,13 +1820,63 @@ int kp_nearest_kron(const double* psf, int np, int center_row, int center_col, i
 }
 
 // ---- preconditioner ---------------------------------------------------------
+// Setup SVD backend of kp_precond_build (svd_dense, factor.cpp:14-23):
+// host LAPACK dgesdd (the oracle's routine; default) or cuSOLVER on the
+// device (svd_dev.cu). Env KP_SVD=device|host sets the process default.
+std::atomic<int> g_svd_backend{-1};
+int svd_backend() {
+  int v = g_svd_backend.load();
+  if (v < 0) {
+    const char* e = getenv("KP_SVD");
+    v = e && std::string(e) == "device" ? KP_SVD_DEVICE : KP_SVD_HOST;
+    g_svd_backend.store(v);
+  }
+  return v;
+}
+kpla::Svd factor_svd(const double* a, int n, int backend) {
+  if (backend == KP_SVD_DEVICE) {
+    kpla::Svd o;
+    o.u.resize(size_t(n) * n), o.v.resize(size_t(n) * n), o.s.resize(n);
+    device_svd(a, n, o.u.data(), o.s.data(), o.v.data());
+    return o;
+  }
+  return kpla::svd(a, n, n);
+}
+
+int kp_set_svd_backend(int backend) {
+  KP_API({
+    if (backend != KP_SVD_HOST && backend != KP_SVD_DEVICE)
+      throw InvalidArgument("svd backend: must be KP_SVD_HOST or KP_SVD_DEVICE");
+    svd_backend();
+    g_svd_backend.store(backend);
+  })
+}
+int kp_get_svd_backend(int* backend) {
+  KP_API({
+    if (!backend) throw InvalidArgument("svd backend: null output");
+    *backend = svd_backend();
+  })
+}
+int kp_svd(const double* a, int n, int backend, double* u, double* s, double* v) {
+  KP_API({
+    if (n < 1 || !a || !u || !s || !v) throw InvalidArgument("svd_dense: empty matrix");
+    if (backend != KP_SVD_HOST && backend != KP_SVD_DEVICE)
+      throw InvalidArgument("svd backend: must be KP_SVD_HOST or KP_SVD_DEVICE");
+    kpla::Svd o = factor_svd(a, n, backend);
+    std::memcpy(u, o.u.data(), o.u.size() * sizeof(double));
+    std::memcpy(s, o.s.data(), o.s.size() * sizeof(double));
+    std::memcpy(v, o.v.data(), o.v.size() * sizeof(double));
+  })
+}
+
 int kp_precond_build(const double* a_r, const double* a_c, int n, double lambda, kp_format fmt,
                      int accum, kp_precond** out) {
   KP_API({
     if (n < 1 || !a_r || !a_c) throw InvalidArgument("build_preconditioner: factors must be square and equally sized");
     if (lambda < 0.0) throw InvalidArgument("build_preconditioner: negative lambda");
-    kpla::Svd r = kpla::svd(a_r, n, n);
-    kpla::Svd c = kpla::svd(a_c, n, n);
+    const int be = svd_backend();
+    kpla::Svd r = factor_svd(a_r, n, be);
+    kpla::Svd c = factor_svd(a_c, n, be);
     *out = precond_from_svd(n, std::move(r.u), std::move(r.s), std::move(r.v), std::move(c.u),
                             std::move(c.s), std::move(c.v), lambda, fmt, accum);
   })
@@ -2223,6 +2261,177 @@ int kp_wgcv_objective(const kp_spectral* sd, double omega, double lambda, double
   KP_API(*value = spectral_value(sd, SK_WGCV, lambda, omega))
 }
 // discrepancy (regparam.cpp:288-327)
+// Discrepancy principle for a batch of right-hand sides sharing the
+// preconditioner factors (BASELINE C4): per image the spectral data of
+// make_spectral_data (regparam.cpp:119-126) and discrepancy()'s root search
+// (regparam.cpp:288-327, find_root :184-214, with the two-level look-ahead
+// of find_root_batched), but every round evaluates the candidate lambdas of
+// ALL still-open images in one batched reduction launch. Each image takes
+// exactly the decisions, and gets exactly the lambda, of kp_discrepancy on
+// its own spectral data (same per-lambda sums, same host decisions).
+// status[i]: 0, or KP_ERR_NO_ROOT (no sign change in the bracket) /
+// KP_ERR_RUNTIME (non-finite objective) with lambdas[i] = NaN.
+int kp_discrepancy_batch(const kp_precond* p, int batch, const double* b, const double* noise_norms,
+                         double eta, double* lambdas, int* status) {
+  KP_API({
+    if (!p || !b || !noise_norms || !lambdas || !status || batch < 1)
+      throw InvalidArgument("discrepancy_batch: bad arguments");
+    if (!(eta > 0.0)) throw InvalidArgument("discrepancy: eta must be positive");
+    for (int i = 0; i < batch; ++i)
+      if (!(noise_norms[i] > 0.0)) throw InvalidArgument("discrepancy: noise_norm must be positive");
+    const int n = p->n;
+    const size_t nn = size_t(n) * n;
+    auto& sh = *p->sh;
+    // spectral data of every image (b_hat = vec(U_c^T B U_r), one image at a time)
+    DBuf<double> bhat(size_t(batch) * nn);
+    {
+      DBuf<double> db(nn);
+      for (int i = 0; i < batch; ++i) {
+        db.upload(b + size_t(i) * nn, nn);
+        project_dev(n, sh.d_u_c.p, sh.d_u_r.p, db.p, bhat.p + size_t(i) * nn);
+      }
+    }
+    {
+      std::lock_guard<std::mutex> lk(sh.lazy_mu);
+      if (!sh.have_range) {
+        sh.smax = sh.s_r[0] * sh.s_c[0];
+        sh.smin = std::numeric_limits<double>::infinity();
+        for (int j = 0; j < n; ++j)
+          for (int i = 0; i < n; ++i) {
+            sh.smin = std::min(sh.smin, sh.s_r[j] * sh.s_c[i]);
+            sh.smax = std::max(sh.smax, sh.s_r[j] * sh.s_c[i]);
+          }
+        sh.have_range = true;
+      }
+    }
+    if (!(sh.smax > 0.0)) throw InvalidArgument("spectral data: all singular values zero");
+    // evaluate the gap for per-image lambda lists (m values each) of the images in `act`
+    auto gaps = [&](const std::vector<int>& act, const std::vector<double>& lam, int m,
+                    std::vector<double>& out) {
+      const int B = int(act.size());
+      DBuf<double> dl(size_t(B) * m), sums(size_t(B) * m * 2);
+      dl.upload(lam.data(), size_t(B) * m);
+      // images of `act` are contiguous in bhat only when all are active: use a
+      // compacted copy of their coefficients otherwise
+      const double* bh = bhat.p;
+      DBuf<double> comp;
+      bool all = B == batch;
+      if (!all) {
+        comp.alloc(size_t(B) * nn);
+        for (int q = 0; q < B; ++q)
+          KP_CUDA(cudaMemcpyAsync(comp.p + size_t(q) * nn, bhat.p + size_t(act[q]) * nn, nn * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, ctx().stream));
+        bh = comp.p;
+      }
+      spectral_sums(SK_RESID, sh.d_s_r.p, sh.d_s_c.p, bh, nullptr, n, dl.p, m, 0.0, sums.p, B);
+      std::vector<double> hsum(size_t(B) * m * 2);
+      sums.download(hsum.data(), hsum.size());
+      sync();
+      out.resize(size_t(B) * m);
+      for (int q = 0; q < B; ++q) {
+        const double eps = eta * noise_norms[act[q]];
+        for (int c = 0; c < m; ++c) out[size_t(q) * m + c] = hsum[(size_t(q) * m + c) * 2] - eps * eps;
+      }
+    };
+    const double lo = 1e-10 * sh.smax, hi = sh.smax;
+    std::vector<int> all(batch);
+    for (int i = 0; i < batch; ++i) all[i] = i, status[i] = 0, lambdas[i] = std::nan("");
+    // endpoints: gap(lo), gap(hi) as kp_discrepancy evaluates them (one value per launch width 1)
+    std::vector<double> glo, ghi;
+    gaps(all, std::vector<double>(batch, lo), 1, glo);
+    gaps(all, std::vector<double>(batch, hi), 1, ghi);
+    struct Walk {
+      double a, b, flo;
+      bool open;
+    };
+    std::vector<Walk> w(batch);
+    std::vector<int> act;
+    for (int i = 0; i < batch; ++i) {
+      if (ghi[i] < 0.0 || glo[i] > 0.0) {
+        status[i] = KP_ERR_NO_ROOT;
+        continue;
+      }
+      if (glo[i] == 0.0) { lambdas[i] = lo; continue; }
+      if (ghi[i] == 0.0) { lambdas[i] = hi; continue; }
+      act.push_back(i);
+    }
+    // find_root_batched's opening evaluation of the log-bracket ends (width 2)
+    const double ulo = std::log(lo), uhi = std::log(hi);
+    if (!act.empty()) {
+      std::vector<double> l(act.size() * 2), fe;
+      for (size_t q = 0; q < act.size(); ++q) l[2 * q] = std::exp(ulo), l[2 * q + 1] = std::exp(uhi);
+      gaps(act, l, 2, fe);
+      std::vector<int> keep;
+      for (size_t q = 0; q < act.size(); ++q) {
+        const int i = act[q];
+        const double flo = fe[2 * q], fhi = fe[2 * q + 1];
+        if (std::isnan(flo) || std::isnan(fhi) || !std::isfinite(flo) || !std::isfinite(fhi)) {
+          status[i] = KP_ERR_RUNTIME;
+          continue;
+        }
+        if (flo == 0.0) { lambdas[i] = std::exp(ulo); continue; }
+        if (fhi == 0.0) { lambdas[i] = std::exp(uhi); continue; }
+        if ((flo > 0.0) == (fhi > 0.0)) { status[i] = KP_ERR_NO_ROOT; continue; }
+        w[i] = Walk{ulo, uhi, flo, true};
+        keep.push_back(i);
+      }
+      act.swap(keep);
+    }
+    const double tol = 1e-12;
+    auto open = [&](double a, double b) { return b - a > tol * (1.0 + 0.5 * (std::abs(a) + std::abs(b))); };
+    constexpr int LEVELS = 2, NODES = (1 << LEVELS) - 1;
+    for (int i : act)
+      if (!open(w[i].a, w[i].b)) lambdas[i] = std::exp(w[i].a + 0.5 * (w[i].b - w[i].a)), w[i].open = false;
+    act.erase(std::remove_if(act.begin(), act.end(), [&](int i) { return !w[i].open; }), act.end());
+    while (!act.empty()) {
+      const size_t B = act.size();
+      std::vector<double> nm(B * NODES), l(B * NODES), fv;
+      for (size_t q = 0; q < B; ++q) {
+        double na[NODES], nb[NODES];
+        na[0] = w[act[q]].a, nb[0] = w[act[q]].b;
+        for (int k = 0; k < NODES; ++k) {
+          nm[q * NODES + k] = na[k] + 0.5 * (nb[k] - na[k]);
+          if (2 * k + 2 < NODES) {
+            na[2 * k + 1] = na[k], nb[2 * k + 1] = nm[q * NODES + k];
+            na[2 * k + 2] = nm[q * NODES + k], nb[2 * k + 2] = nb[k];
+          }
+          l[q * NODES + k] = std::exp(nm[q * NODES + k]);
+        }
+      }
+      gaps(act, l, NODES, fv);
+      std::vector<int> keep;
+      for (size_t q = 0; q < B; ++q) {
+        const int i = act[q];
+        Walk& wk = w[i];
+        int node = 0;
+        bool done = false;
+        for (int level = 0; level < LEVELS && !done; ++level) {
+          if (!open(wk.a, wk.b)) break;
+          const double m = wk.a + 0.5 * (wk.b - wk.a);
+          if (m <= wk.a || m >= wk.b) { lambdas[i] = std::exp(wk.a + 0.5 * (wk.b - wk.a)); done = true; break; }
+          const double fm = fv[q * NODES + node];
+          if (!std::isfinite(fm)) { status[i] = KP_ERR_RUNTIME; done = true; break; }
+          if (fm == 0.0) { lambdas[i] = std::exp(m); done = true; break; }
+          if ((fm > 0.0) == (wk.flo > 0.0)) {
+            wk.a = m, wk.flo = fm;
+            node = 2 * node + 2;
+          } else {
+            wk.b = m;
+            node = 2 * node + 1;
+          }
+        }
+        if (done) continue;
+        if (!open(wk.a, wk.b)) {
+          lambdas[i] = std::exp(wk.a + 0.5 * (wk.b - wk.a));
+          continue;
+        }
+        keep.push_back(i);
+      }
+      act.swap(keep);
+    }
+  })
+}
+
 int kp_discrepancy(const kp_spectral* sd, double noise_norm, double eta, kp_param_choice* choice) {
   KP_API({
     check_spectral(sd, false);  // regparam.cpp: validation order of discrepancy()

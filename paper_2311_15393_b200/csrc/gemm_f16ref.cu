@@ -335,7 +335,9 @@ void launch_f16ref_bn(const F16GemmArgs& a, int kernel_class) {
 
 template <int STAGES, int UNIT>
 void launch_f16ref(const F16GemmArgs& a, int kernel_class) {
-  if (f16ref_bn(a.M, a.N) == 32)
+  // batched products take the tile width of one image's product, so every
+  // image is tiled (and its partials grouped) exactly as a single product
+  if (f16ref_bn(a.M, a.epi.n_img ? a.epi.n_img : a.N) == 32)
     launch_f16ref_bn<STAGES, UNIT, 32>(a, kernel_class);
   else
     launch_f16ref_bn<STAGES, UNIT, 64>(a, kernel_class);
@@ -353,7 +355,7 @@ int f16ref_cfg() {
 
 int gemm_f16ref_num_ctas(int M, int N) { return int(cdiv(M, BM) * cdiv(N, f16ref_bn(M, N))); }
 int gemm_f16ref_partials_per_image(int M, int N, int n_img) {
-  return int(cdiv(M, BM) * (n_img / f16ref_bn(M, N)));
+  return int(cdiv(M, BM) * (n_img / f16ref_bn(M, n_img)));
 }
 
 void gemm_f16ref(const F16GemmArgs& a, int kernel_class) {

@@ -619,6 +619,13 @@ __global__ void spectral_sums_kernel(const double* s_r, const double* s_c, const
                                      const double* xhat, int n, const double* lambdas, int m,
                                      double omega, double* part) {
   pdl_wait();
+  {  // batch image blockIdx.y: its own coefficients, lambdas and partials
+    const size_t img = blockIdx.y;
+    bhat += img * size_t(n) * n;
+    if (xhat) xhat += img * size_t(n) * n;
+    lambdas += img * m;
+    part += img * size_t(m) * gridDim.x * 2;
+  }
   __shared__ double red[VEC_THREADS / 32][2 * LC];
   const size_t nn = size_t(n) * n;
   const unsigned un = unsigned(n);
@@ -854,33 +861,35 @@ void spectral_filter(const double* s_r, const double* s_c, int n, double l2, dou
 
 template <int KIND>
 void launch_sums(const double* s_r, const double* s_c, const double* bhat, const double* xhat,
-                 int n, const double* lambdas, int m, double omega, double* part) {
+                 int n, const double* lambdas, int m, double omega, double* part, int batch) {
   // lambdas per pass: 1, 4 (the discrepancy look-ahead's 3) or LCHUNK; every
   // value is summed in the same element order whatever the width
+  const dim3 grid(VEC_CTAS, batch);
   if (m == 1)
-    KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<1, KIND>), VEC_CTAS, VEC_THREADS, s_r, s_c, bhat,
+    KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<1, KIND>), grid, VEC_THREADS, s_r, s_c, bhat,
               xhat, n, lambdas, m, omega, part);
   else if (m <= 4)
-    KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<4, KIND>), VEC_CTAS, VEC_THREADS, s_r, s_c, bhat,
+    KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<4, KIND>), grid, VEC_THREADS, s_r, s_c, bhat,
               xhat, n, lambdas, m, omega, part);
   else
-    KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<LCHUNK, KIND>), VEC_CTAS, VEC_THREADS, s_r, s_c,
+    KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<LCHUNK, KIND>), grid, VEC_THREADS, s_r, s_c,
               bhat, xhat, n, lambdas, m, omega, part);
 }
 
 void spectral_sums(int kind, const double* s_r, const double* s_c, const double* bhat,
                    const double* xhat, int n, const double* lambdas, int m, double omega,
-                   double* out) {
-  DBuf<double> part(size_t(m) * VEC_CTAS * 2);
+                   double* out, int batch) {
+  DBuf<double> part(size_t(batch) * m * VEC_CTAS * 2);
   switch (kind) {
-    case SK_GCV: launch_sums<SK_GCV>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p); break;
-    case SK_RESID: launch_sums<SK_RESID>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p); break;
-    case SK_OPT: launch_sums<SK_OPT>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p); break;
-    case SK_WGCV: launch_sums<SK_WGCV>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p); break;
-    case SK_WTRACE: launch_sums<SK_WTRACE>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p); break;
+    case SK_GCV: launch_sums<SK_GCV>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch); break;
+    case SK_RESID: launch_sums<SK_RESID>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch); break;
+    case SK_OPT: launch_sums<SK_OPT>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch); break;
+    case SK_WGCV: launch_sums<SK_WGCV>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch); break;
+    case SK_WTRACE: launch_sums<SK_WTRACE>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch); break;
     default: throw InvalidArgument("spectral_sums: bad kind");
   }
-  KP_LAUNCH(KC_SPECTRAL, finish_sums_kernel, m, VEC_THREADS, part.p, VEC_CTAS, 2, m, out);
+  // one finishing block per (image, lambda) row, in the same fixed order
+  KP_LAUNCH(KC_SPECTRAL, finish_sums_kernel, batch * m, VEC_THREADS, part.p, VEC_CTAS, 2, batch * m, out);
 }
 
 }  // namespace kp

@@ -125,8 +125,10 @@ enum SpectralKind {
 };
 // c(i,j) *= sigma / (sigma^2 + l2) (filtered_solution coefficients), device
 void spectral_filter(const double* s_r, const double* s_c, int n, double l2, double* c);
+// batch > 1: `batch` images (bhat / xhat at image * n^2, lambdas at image *
+// m, out rows image * m + q), each summed exactly as a single call would.
 void spectral_sums(int kind, const double* s_r, const double* s_c, const double* bhat,
                    const double* xhat, int n, const double* lambdas, int m, double omega,
-                   double* out);
+                   double* out, int batch = 1);
 
 }  // namespace kp

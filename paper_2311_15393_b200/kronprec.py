@@ -25,7 +25,7 @@ __all__ = [
     "pairwise_sum", "KronTerm", "KroneckerSum", "vec", "unvec", "kronsum_apply",
     "kronsum_apply_transpose", "normal_matvec", "KronSvdPreconditioner",
     "build_preconditioner", "build_preconditioner_from_svd", "with_lambda", "precond_solve",
-    "SolverOptions", "ConvergenceHistory", "SolveResult", "cgls", "pcg", "fpcg", "pcg_batch", "fpcg_batch",
+    "SolverOptions", "ConvergenceHistory", "SolveResult", "cgls", "pcg", "fpcg", "pcg_batch", "fpcg_batch", "discrepancy_batch", "svd", "set_svd_backend",
     "plateau_iteration", "WorkReport", "work_report", "SpectralData", "make_spectral_data",
     "ParamChoice", "gcv_objective", "opt_objective", "wgcv_objective", "discrepancy_gap", "gcv",
     "gcv_grid", "lambda_opt", "wgcv", "discrepancy", "filtered_solution", "NoRootError",
@@ -479,7 +479,7 @@ def fpcg(a: KroneckerSum, b, m: KronSvdPreconditioner, opts: SolverOptions) -> S
 
 
 def _solve_batch(kind: str, a: KroneckerSum, bs, m: KronSvdPreconditioner, lambdas,
-                 opts: SolverOptions, x_true=None) -> list:
+                 opts: SolverOptions, x_true=None, out=None) -> list:
     nn = a.n * a.n
     bs = np.ascontiguousarray(np.asarray(bs, dtype=np.float64).reshape(-1, nn))
     batch = bs.shape[0]
@@ -507,35 +507,80 @@ def _solve_batch(kind: str, a: KroneckerSum, bs, m: KronSvdPreconditioner, lambd
                           rel_residual_tol=float(opts.rel_residual_tol), x_true=ptr(xt),
                           track_search_direction_orthogonality=int(opts.track_search_direction_orthogonality),
                           record_iterates=0, device_pointers=0)
-    x = np.empty((batch, nn))
+    if out is None:
+        x = np.empty((batch, nn))
+    else:  # caller's buffer (e.g. pinned host memory), batch x n^2 float64
+        x = out.reshape(batch, nn)
+        if x.dtype != np.float64 or not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("pcg_batch: out must be a contiguous float64 batch x n^2 array")
     f = lib().kp_pcg_batch if kind == "pcg" else lib().kp_fpcg_batch
     check(f(a.handle(), m.handle(), batch, ptr(bs), ptr(lam), C.byref(o), ptr(x), hs))
-    out = []
+    results = []
     for i in range(batch):
         h = hs[i]
         rel, res, work, cos = bufs[i]
         rows = h.rows
-        out.append(SolveResult(x[i].copy(), ConvergenceHistory(
+        results.append(SolveResult(x[i], ConvergenceHistory(
             relative_error=list(rel[:rows]) if xt is not None else [],
             residual_norm=list(res[:rows]), work_units=list(work[:rows]),
             residual_cosines=list(cos[:h.n_cosines]), iterates=[],
             iterations_used=h.iterations_used, converged=bool(h.converged),
             abort_reason=h.abort_reason.decode(), msolve_count=h.msolve_count)))
-    return out
+    return results
 
 
 def pcg_batch(a: KroneckerSum, bs, m: KronSvdPreconditioner, lambdas, opts: SolverOptions,
-              x_true=None) -> list:
+              x_true=None, out=None) -> list:
     """PCG for a batch of right-hand sides (rows of `bs`), image i with lambda
     lambdas[i] and the factors of `m` (with_lambda per image, cli.cpp:469-486):
     one batched device solve; result i equals pcg(a, bs[i], with_lambda(m,
-    lambdas[i]), opts) with opts.x_true = x_true[i]."""
-    return _solve_batch("pcg", a, bs, m, lambdas, opts, x_true)
+    lambdas[i]), opts) with opts.x_true = x_true[i]. Result i's x is row i of
+    `out` (or of a new batch x n^2 array)."""
+    return _solve_batch("pcg", a, bs, m, lambdas, opts, x_true, out)
 
 
 def fpcg_batch(a: KroneckerSum, bs, m: KronSvdPreconditioner, lambdas, opts: SolverOptions,
-               x_true=None) -> list:
-    return _solve_batch("fpcg", a, bs, m, lambdas, opts, x_true)
+               x_true=None, out=None) -> list:
+    return _solve_batch("fpcg", a, bs, m, lambdas, opts, x_true, out)
+
+
+_SVD_BACKENDS = {"host": 0, "device": 1}
+
+
+def svd(a, backend: str = "host"):
+    """svd_dense (factor.cpp:14-23): (u, s, v) with a = u diag(s) v^T, s
+    nonincreasing. backend "host": LAPACK dgesdd; "device": cuSOLVER FP64 on
+    the B200."""
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    n = a.shape[0]
+    if a.ndim != 2 or a.shape != (n, n) or n == 0:
+        raise ValueError("svd_dense: square, non-empty matrix expected")
+    u, v, sv = np.empty((n, n), order="F"), np.empty((n, n), order="F"), np.empty(n)
+    check(lib().kp_svd(ptr(a), n, _SVD_BACKENDS[backend], ptr(u), ptr(sv), ptr(v)))
+    return u, sv, v
+
+
+def set_svd_backend(backend: str) -> None:
+    """Backend of build_preconditioner's factor SVDs (process-wide)."""
+    check(lib().kp_set_svd_backend(_SVD_BACKENDS[backend]))
+
+
+def discrepancy_batch(m: KronSvdPreconditioner, bs, noise_norms, eta: float):
+    """discrepancy(make_spectral_data(m, b_i), noise_norms[i], eta) for every
+    row b_i of `bs` in one batched device search (regparam.cpp:288-327).
+    Returns (lambdas, status): status 0 ok, KP_ERR_NO_ROOT / KP_ERR_RUNTIME
+    per image (lambda NaN); lambdas equal discrepancy()'s bit for bit."""
+    nn = m.n * m.n
+    bs = np.ascontiguousarray(np.asarray(bs, dtype=np.float64).reshape(-1, nn))
+    batch = bs.shape[0]
+    nz = np.ascontiguousarray(np.asarray(noise_norms, dtype=np.float64).reshape(-1))
+    if nz.size != batch:
+        raise ValueError("discrepancy_batch: one noise norm per right-hand side")
+    lam = np.empty(batch)
+    st = np.empty(batch, dtype=np.int32)
+    check(lib().kp_discrepancy_batch(m.handle(), batch, ptr(bs), ptr(nz), float(eta), ptr(lam),
+                                     st.ctypes.data_as(C.c_void_p)))
+    return lam, st
 
 
 def plateau_iteration(h: ConvergenceHistory, tol: float = 0.01) -> int:  # krylov.cpp:220-231

@@ -95,3 +95,52 @@ def test_batch_validation():
     m64 = K.build_preconditioner(term.row_factor, term.col_factor, 1.0, K.PrecisionFormat.fp64())
     with pytest.raises(Exception, match="fp16 reference-exact"):
         K.pcg_batch(a, bs, m64, [0.1, 0.2], SolverOptions())
+
+
+def test_discrepancy_batch_equals_per_image():
+    a, term, tps = batch_problem(96, 6)
+    m0 = K.build_preconditioner(term.row_factor, term.col_factor, 1.0, H)
+    noise = [float(np.linalg.norm(tp.noise)) for tp in tps]
+    noise[4] *= 1e6  # eta * ||e|| beyond the reachable residual: no root
+    lam, st = K.discrepancy_batch(m0, np.stack([tp.b for tp in tps]), noise, 1.01)
+    for i, tp in enumerate(tps):
+        sd = K.make_spectral_data(m0, tp.b)
+        if i == 4:
+            with pytest.raises(K.NoRootError):
+                K.discrepancy(sd, noise[i], 1.01)
+            assert st[i] != 0 and np.isnan(lam[i])
+            continue
+        assert st[i] == 0
+        assert lam[i] == K.discrepancy(sd, noise[i], 1.01).lambda_  # bit-identical
+
+
+def test_device_svd_backend():
+    """svd_dense on the device (cuSOLVER): a = u diag(s) v^T, orthonormal
+    factors, s nonincreasing and equal to LAPACK's; a preconditioner built
+    from the device factors is bit-identical to the oracle's built from the
+    same factors."""
+    from oracle import pyoracle as O
+    from paper_2311_15393_b200.kronprec import SvdTriple
+    psf = P.psf_aniso_gaussian(31, [[4.0, 1.0], [1.0, 2.0]])
+    term = P.nearest_kron(psf, 256)
+    for f in (term.row_factor, term.col_factor):
+        u, s, v = K.svd(f, "device")
+        uh, sh, vh = K.svd(f, "host")
+        assert np.all(np.diff(s) <= 0)
+        assert np.allclose(s, sh, rtol=1e-12, atol=1e-14 * sh[0])
+        assert np.linalg.norm(u * s @ v.T - f) <= 1e-13 * np.linalg.norm(f)
+        assert np.linalg.norm(u.T @ u - np.eye(256)) <= 1e-12
+        assert np.linalg.norm(v.T @ v - np.eye(256)) <= 1e-12
+    sr = SvdTriple(*K.svd(term.row_factor, "device"))
+    sc = SvdTriple(*K.svd(term.col_factor, "device"))
+    g = K.build_preconditioner_from_svd(sr, sc, 0.01, H)
+    o = O.build_preconditioner_from_svd((sr.u, sr.s, sr.v), (sc.u, sc.s, sc.v), 0.01, H)
+    r = np.random.default_rng(3).standard_normal(256 * 256)
+    assert np.array_equal(K.precond_solve(g, r), O.precond_solve(o, r))
+    # build_preconditioner through the device backend equals the from-SVD build
+    K.set_svd_backend("device")
+    try:
+        gd = K.build_preconditioner(term.row_factor, term.col_factor, 0.01, H)
+    finally:
+        K.set_svd_backend("host")
+    assert np.array_equal(K.precond_solve(gd, r), K.precond_solve(g, r))
