@@ -184,18 +184,14 @@ def build_problem(name: str, image: int, n: int | None, device_apply: bool):
 
 
 def svd_pair(term, how: str):
+    """Setup SVDs of the two factors: host LAPACK dgesdd (the oracle's
+    routine) or the library's device SVD (cuSOLVER FP64, kp_svd)."""
+    import paper_2311_15393_b200 as K
     from paper_2311_15393_b200 import problems as P
     from paper_2311_15393_b200.kronprec import SvdTriple
-    if how == "host":
+    if how == "host":  # host-only entry point (also used by the CPU reference arm)
         return SvdTriple(*P.host_svd(term.row_factor)), SvdTriple(*P.host_svd(term.col_factor))
-    import torch
-    out = []
-    for a in (term.row_factor, term.col_factor):
-        t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
-        u, s, vh = torch.linalg.svd(t)
-        out.append(SvdTriple(np.asfortranarray(u.cpu().numpy()), s.cpu().numpy().copy(),
-                             np.asfortranarray(vh.T.cpu().numpy())))
-    return out[0], out[1]
+    return SvdTriple(*K.svd(term.row_factor, "device")), SvdTriple(*K.svd(term.col_factor, "device"))
 
 
 def cpu_iteration_sample(cfg, svd_r, svd_c, fmt, threads: int) -> float:
@@ -546,7 +542,7 @@ def main():
     ap.add_argument("--size", type=int, default=None, help="override image side n (quick runs)")
     ap.add_argument("--svd", default="auto", choices=["auto", "gpu", "host"],
                     help="setup SVD of the factors: host LAPACK dgesdd (the oracle's routine) or "
-                         "cuSOLVER via torch; auto = host on one GPU, cuSOLVER when several "
+                         "the library's cuSOLVER SVD; auto = host on one GPU, device when several "
                          "ranks would contend for the host cores")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tensor", action="store_true", help="skip the tensor-mode secondary run")

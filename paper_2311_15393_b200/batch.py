@@ -122,13 +122,8 @@ class C4Shard:
         self.psf = base.problem.psf
         self.eta = base.eta
         self.tol = base.tol
-        if svd == "gpu":
-            import torch
-            pair = []
-            for f in (base.term.row_factor, base.term.col_factor):
-                u, s, vh = torch.linalg.svd(torch.from_numpy(np.ascontiguousarray(f)).cuda())
-                pair.append(SvdTriple(np.asfortranarray(u.cpu().numpy()), s.cpu().numpy().copy(),
-                                      np.asfortranarray(vh.T.cpu().numpy())))
+        if svd == "gpu":  # the library's device SVD (cuSOLVER, svd_dev.cu)
+            pair = [SvdTriple(*K.svd(f, "device")) for f in (base.term.row_factor, base.term.col_factor)]
             self.m0 = K.build_preconditioner_from_svd(pair[0], pair[1], 1.0, K.PrecisionFormat.fp16(),
                                                       accum=accum)
         else:

@@ -177,18 +177,13 @@ def test_c5_operator_full_size_properties():
 
 
 def test_setup_svd_backend_invariance():
-    """The factor SVDs may come from host LAPACK or cuSOLVER (bench / C4 setup);
+    """The factor SVDs may come from host LAPACK or the library's cuSOLVER SVD (kp_svd);
     their vectors differ in sign and last bits. M, the GCV sums and the
     discrepancy lambda are invariant (SURVEY §7 'setup cost')."""
-    import torch
     cfg = configs.build("C1")
     term = cfg.term
     host = [SvdTriple(*P.host_svd(f)) for f in (term.row_factor, term.col_factor)]
-    dev = []
-    for f in (term.row_factor, term.col_factor):
-        u, s, vh = torch.linalg.svd(torch.from_numpy(np.ascontiguousarray(f)).cuda())
-        dev.append(SvdTriple(np.asfortranarray(u.cpu().numpy()), s.cpu().numpy().copy(),
-                             np.asfortranarray(vh.T.cpu().numpy())))
+    dev = [SvdTriple(*K.svd(f, "device")) for f in (term.row_factor, term.col_factor)]  # cuSOLVER
     r = np.random.default_rng(8).standard_normal(cfg.n * cfg.n)
     for fmt, tol in ((K.PrecisionFormat.fp64(), 1e-10), (K.PrecisionFormat.fp16(), 2e-3)):
         mh = K.build_preconditioner_from_svd(host[0], host[1], 0.01, fmt)

@@ -71,3 +71,26 @@ def test_single_process_fallbacks():
     res = [ImageResult(3, 0.01, 0.1, 5, True, 0.2), ImageResult(1, 0.001, 0.1, 4, True, 0.2)]
     assert [d["image"] for d in gather_results(res)] == [1, 3]
     assert reduce_timing(2.5, 7.0) == (2.5, 7.0)
+
+
+@pytest.mark.gpu
+def test_sharded_c4_bench_two_ranks_on_one_gpu():
+    """The N > 1 bench path end to end (torchrun, 2 ranks, C4 images sharded,
+    one batched solve per rank, results gathered to rank 0) at n = 256. Both
+    ranks share cuda:0 and gather over gloo: no rank waits on another's
+    kernels, so this checks the sharding / gather logic, not scaling."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--size", "256", "--dist-backend", "gloo", "--steps", "1", "--warmup", "1", "--no-tensor"]
+    out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["unit"] == "solves/s" and d["scaling"] == "strong"
+    assert d["run_info"]["images_solved"] == 64
+    assert [r["image"] for r in d["results"]] == list(range(6))
