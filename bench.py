@@ -697,6 +697,9 @@ def main():
         it, _, _ = solve(True)
         prof_iters += it
         prof_msolves += solve.msolves
+    # operator launches that did work: A^T b at setup + 2 applies per iteration
+    # (an overshoot iteration's launches return at once and are not counted)
+    prof_op_applies = args.steps + 2 * prof_iters
     check(L.kp_event_record(7))
     prof_ms = C.c_float()
     check(L.kp_event_elapsed(6, 7, C.byref(prof_ms)))
@@ -806,7 +809,8 @@ def main():
     e2e_value = e2e_iters / e2e_elapsed
     r = len(cfg.problem.a.terms)
     op_mode, tc, tr = cfg.problem.a.mode()
-    op_ms, op_launches = prof["operator_gemm_f64"]
+    op_ms, _ = prof["operator_gemm_f64"]
+    op_launches = 2 * prof_op_applies  # two launches (passes / GEMMs) per apply
     if op_mode == "banded":  # two correlation passes per apply: 2 r (Lc + Lr) n^2 flop
         op_flops_per_launch = 2.0 * r * (tc + tr) * float(n) ** 2 / 2.0
         op_peak, op_kernel = DFMA_PEAK_TFLOPS, "band_cols/band_rows (FP64 DFMA, banded Toeplitz)"

@@ -872,18 +872,10 @@ void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
   // else it doubles up to 16.
   int* slot = s.op->ws.poll_slots();
   cudaEvent_t* ev = s.op->ws.poll_ev;
-  if (c.profile) {
-    // Profiled runs (per-launch events for the roofline) read the status
-    // after every iteration and enqueue nothing past the stop, so every
-    // timed launch did work (no early-exit launches in the per-launch mean).
-    for (int k = 0; k < maxit; ++k) {
-      iteration();
-      KP_CUDA(cudaMemcpyAsync(&slot[0], &s.st->status, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-      KP_CUDA(cudaStreamSynchronize(c.stream));
-      if (slot[0] != ST_RUNNING) break;
-    }
-    return;
-  }
+  // (Profiled runs use the same pipelined loop; the no-op launches of an
+  // overshoot iteration are excluded by the caller's working-launch counts —
+  // history.msolve_count and iterations_used — not by serialising the loop,
+  // which would expose host launch latency in the per-launch events.)
   int done = 0, chunk = 1, cur = 0;
   bool pending = false;
   auto t_prev = std::chrono::steady_clock::now();
