@@ -44,6 +44,7 @@ F16X2_PEAK_TOPS = 36.9    # measured f16x2 mul+add half-ops/s, same file
 # committed ncu --set full captures (profiles/r01_ncu_key_metrics.txt, r02_*)
 TRAFFIC = {
     ("gemm_f16ref_kernel", 4096): 68.29e6 + 21.03e6,   # r01_gemm_f16ref_u64_n4096.ncu-rep
+    ("gemm_f16x_kernel", 4096): 73.48e6 + 18.53e6,     # r02_gemm_f16x_c5.ncu-rep
     ("gemm_f16tc_kernel", 4096): (73.37e6 + 13.91e6 + 118.5e6 + 18.64e6 + 72.79e6 + 13.88e6
                                   + 71.8e6 + 15.19e6) / 4,  # mean of the 4 products of a solve
     ("band", 4096): (134.2e6 + 613.1e6 + 671.1e6 + 121.8e6) / 2,  # per pass, r01_band_vec
