@@ -812,7 +812,12 @@ def main():
     op_mode, tc, tr = cfg.problem.a.mode()
     op_ms, _ = prof["operator_gemm_f64"]
     op_launches = 2 * prof_op_applies  # two launches (passes / GEMMs) per apply
-    if op_mode == "banded":  # two correlation passes per apply: 2 r (Lc + Lr) n^2 flop
+    if op_mode == "banded_fused":  # passes A + B in one launch per apply: 2 r (Lc + Lr) n^2 flop
+        op_launches = prof_op_applies
+        op_flops_per_launch = 2.0 * r * (tc + tr) * float(n) ** 2
+        op_peak, op_kernel = DFMA_PEAK_TFLOPS, "band_fused (FP64 DFMA, banded Toeplitz, both passes)"
+        op_src = "measured DFMA peak, profiles/r01_microbench_peaks.txt"
+    elif op_mode == "banded":  # two correlation passes per apply: 2 r (Lc + Lr) n^2 flop
         op_flops_per_launch = 2.0 * r * (tc + tr) * float(n) ** 2 / 2.0
         op_peak, op_kernel = DFMA_PEAK_TFLOPS, "band_cols/band_rows (FP64 DFMA, banded Toeplitz)"
         op_src = "measured DFMA peak, profiles/r01_microbench_peaks.txt"
@@ -859,7 +864,7 @@ def main():
 
     # the dense DMMA operator (the product the reference computes), for its roofline
     dense = None
-    if op_mode == "banded" and not args.no_dense:
+    if op_mode.startswith("banded") and not args.no_dense:
         cfg.problem.a.set_mode("dense")
         check(L.kp_profile_reset())
         check(L.kp_profile_enable(1))

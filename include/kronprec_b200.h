@@ -190,9 +190,15 @@ int kp_operator_info(const kp_operator* op, int* n, int* r);
 #define KP_OP_AUTO 0
 #define KP_OP_DENSE 1
 #define KP_OP_BANDED 2
+/* banded with both correlation passes in ONE kernel (shared-memory halo
+ * tiles, no r n^2 intermediate in HBM); short bands only (17 or 19
+ * diagonals in both directions), KP_ERR_INVALID_ARGUMENT otherwise. Opt-in:
+ * measured no faster than the two passes on B200. */
+#define KP_OP_BANDED_FUSED 3
 int kp_operator_set_mode(kp_operator* op, int mode);
-/* mode in use (KP_OP_DENSE / KP_OP_BANDED) and the number of diagonals of
- * the column and row factors when banded (0 otherwise). */
+/* mode in use (KP_OP_DENSE / KP_OP_BANDED / KP_OP_BANDED_FUSED) and the
+ * number of diagonals of the column and row factors when banded (0
+ * otherwise). */
 int kp_operator_get_mode(const kp_operator* op, int* mode, int* col_taps, int* row_taps);
 /* kronsum_apply (kron.cpp:73-79) / kronsum_apply_transpose (kron.cpp:81-88) */
 int kp_kronsum_apply(const kp_operator* op, const double* y, double* out);

@@ -261,6 +261,8 @@ struct kp_operator {
   int col_taps = 0, row_taps = 0;
   BandTaps cols_fw, cols_tr, rows_fw, rows_tr;
   bool use_banded() const { return is_banded && mode != KP_OP_DENSE; }
+  // short bands: both passes in one kernel (no r n^2 intermediate in HBM)
+  bool use_fused() const { return use_banded() && mode == KP_OP_BANDED_FUSED; }
 };
 
 struct PrecondShared {
@@ -343,6 +345,13 @@ long round_up(long v, long m) { return (v + m - 1) / m * m; }
 void op_apply(kp_operator* op, const double* in, double* out, bool transpose,
               const F64Epilogue* extra, const int* status) {
   const int n = op->n, r = op->r;
+  if (op->use_fused()) {
+    F64Epilogue e;
+    if (extra) e = *extra;
+    e.C = out, e.cm = 1, e.cn = n, e.vm = 1, e.vn = n;
+    band_fused(in, n, r, transpose ? op->cols_tr : op->cols_fw, transpose ? op->rows_tr : op->rows_fw, e, status);
+    return;
+  }
   if (op->use_banded()) {
     band_cols(in, op->W.p, n, r, transpose ? op->cols_tr : op->cols_fw, status);
     F64Epilogue e;
@@ -370,6 +379,7 @@ void op_apply(kp_operator* op, const double* in, double* out, bool transpose,
 }
 
 int op_partials_ctas(const kp_operator* op) {
+  if (op->use_fused()) return band_fused_num_ctas(op->n);
   return op->use_banded() ? band_rows_num_ctas(op->n) : gemm_f64_num_ctas(op->n, op->n);
 }
 
@@ -1122,6 +1132,15 @@ void op_apply_batch(kp_operator* op, int B, const double* in, double* out, bool 
                     const int* status) {
   const int n = op->n, r = op->r;
   const size_t nn = size_t(n) * n;
+  if (op->use_fused()) {
+    F64Epilogue e;
+    if (extra) e = *extra;
+    e.C = out, e.cm = 1, e.cn = n, e.vm = 1, e.vn = n;
+    e.img = long(nn), e.part_img = band_fused_num_ctas(n);
+    if (e.addv) e.addc_img = addc_dev;
+    band_fused(in, n, r, transpose ? op->cols_tr : op->cols_fw, transpose ? op->rows_tr : op->rows_fw, e, status, B);
+    return;
+  }
   if (op->use_banded()) {
     if (op->Wb.n < size_t(B) * r * nn) op->Wb.alloc(size_t(B) * r * nn);
     band_cols(in, op->Wb.p, n, r, transpose ? op->cols_tr : op->cols_fw, status, B);
@@ -1734,8 +1753,10 @@ int kp_operator_info(const kp_operator* op, int* n, int* r) {
 }
 int kp_operator_set_mode(kp_operator* op, int mode) {
   KP_API({
-    if (!op || mode < KP_OP_AUTO || mode > KP_OP_BANDED) throw InvalidArgument("operator mode");
-    if (mode == KP_OP_BANDED && !op->is_banded)
+    if (!op || mode < KP_OP_AUTO || mode > KP_OP_BANDED_FUSED) throw InvalidArgument("operator mode");
+    if (mode == KP_OP_BANDED_FUSED && !(op->is_banded && band_fused_supported(op->col_taps, op->row_taps)))
+      throw InvalidArgument("KroneckerSum: the fused banded kernel needs 17 or 19 diagonals per factor");
+    if ((mode == KP_OP_BANDED || mode == KP_OP_BANDED_FUSED) && !op->is_banded)
       throw InvalidArgument("KroneckerSum: factors are not banded Toeplitz");
     op->mode = mode;
   })
@@ -1743,7 +1764,7 @@ int kp_operator_set_mode(kp_operator* op, int mode) {
 int kp_operator_get_mode(const kp_operator* op, int* mode, int* col_taps, int* row_taps) {
   KP_API({
     if (!op) throw InvalidArgument("null operator");
-    *mode = op->use_banded() ? KP_OP_BANDED : KP_OP_DENSE;
+    *mode = op->use_fused() ? KP_OP_BANDED_FUSED : op->use_banded() ? KP_OP_BANDED : KP_OP_DENSE;
     *col_taps = op->use_banded() ? op->col_taps : 0;
     *row_taps = op->use_banded() ? op->row_taps : 0;
   })

@@ -359,6 +359,144 @@ __global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __re
   }
 }
 
+// Fused passes (A + B in one kernel) for short bands, where the two-pass
+// form is bound by its r n^2 HBM intermediate rather than by DFMA (C4: 17
+// taps, 2 * 17 flop per 16 B moved per pass): each CTA loads the X halo of
+// its 64 x 64 output tile (64 + Lc - 1 rows, 64 + Lr - 1 columns) once,
+// computes Y_k on those columns in shared memory (pass A's correlation on
+// (64 + Lr - 1) / 64 of the columns) and correlates Y_k's rows into the
+// output registers (pass B), term by term. HBM traffic is x in + out (+ the
+// epilogue's vectors); the result equals the two-pass kernels' up to FP64
+// summation order (same taps, same per-element accumulation order: pass A's
+// sum over u of the column taps, then pass B's over the row taps, terms in
+// order). TC / TR: compile-time tap counts.
+constexpr int F_TA = 64, F_TJ = 64, F_THREADS = 256;
+template <int TC, int TR>
+struct FusedDims {
+  static constexpr int XR = F_TA + TC - 1;          // X halo rows
+  static constexpr int NC = F_TJ + TR - 1;          // X halo / Y columns
+  static constexpr int SX = XR | 1;                 // odd column stride of X (doubles)
+  static constexpr int SY = F_TA + 1;               // column stride of Y
+  static constexpr size_t SMEM = (size_t(NC) * SX + size_t(NC) * SY) * sizeof(double);
+};
+
+template <int TC, int TR>
+__global__ void __launch_bounds__(F_THREADS) band_fused_kernel(const double* __restrict__ X, int n, int r,
+                                                               const __grid_constant__ BandTaps tc,
+                                                               const __grid_constant__ BandTaps tr,
+                                                               const F64Epilogue e, const int* status) {
+  using D = FusedDims<TC, TR>;
+  pdl_wait();
+  if (stopped(status)) return;
+  extern __shared__ double sm[];
+  double* Xs = sm;                 // [NC][SX]: Xs[c * SX + i] = X(a0 + sc + i, j0 + sr + c)
+  double* Ys = sm + D::NC * D::SX;  // [NC][SY]: Ys[c * SY + a] = Y_k(a0 + a, j0 + sr + c)
+  X += size_t(blockIdx.z) * n * n;
+  const int a0 = blockIdx.y * F_TA, j0 = blockIdx.x * F_TJ;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  {  // X halo: warp per column, lanes down the rows (coalesced), zeros outside [0, n)
+    const uint32_t xs = static_cast<uint32_t>(__cvta_generic_to_shared(Xs));
+    for (int c = warp; c < D::NC; c += F_THREADS / 32) {
+      const int l = j0 + tr.shift + c;
+      const double* col = X + size_t(l) * n;
+      for (int v = lane; v < D::XR; v += 32) {
+        const int i = a0 + tc.shift + v;
+        const bool ok = l >= 0 && l < n && i >= 0 && i < n;
+        cp_async8(xs + uint32_t(c * D::SX + v) * 8u, ok ? col + i : X, ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  }
+  __syncthreads();
+  // output tasks: (row a, 8-column block jb), two per thread
+  constexpr int OUT_TASKS = F_TA * (F_TJ / 8) / F_THREADS;
+  double acc[OUT_TASKS][8];
+#pragma unroll
+  for (int h = 0; h < OUT_TASKS; ++h)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[h][q] = 0.0;
+  constexpr int Y_TASKS = D::NC * (F_TA / 8);  // (column c, 8-row block b)
+  for (int k = 0; k < r; ++k) {
+    // pass A on the halo columns: Y_k(a, c) = sum_u wc_k[u] X(a + sc + u, c)
+    for (int id = threadIdx.x; id < Y_TASKS; id += F_THREADS) {
+      const int c = id % D::NC, b = id / D::NC;
+      double y[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      const double* base = Xs + c * D::SX + 8 * b;
+      corr8_fixed<TC>(y, tc.w[k], [&](int i) { return base[i]; });
+#pragma unroll
+      for (int q = 0; q < 8; ++q) Ys[c * D::SY + 8 * b + q] = y[q];
+    }
+    __syncthreads();
+    // pass B: out(a, j) += sum_u wr_k[u] Y_k(a, j + sr + u)
+#pragma unroll
+    for (int h = 0; h < OUT_TASKS; ++h) {
+      const int id = threadIdx.x + h * F_THREADS;
+      const int a = id % F_TA, jb = id / F_TA;
+      const double* base = Ys + (8 * jb) * D::SY + a;
+      corr8_fixed<TR>(acc[h], tr.w[k], [&](int i) { return base[i * D::SY]; });
+    }
+    __syncthreads();  // Ys is rewritten by the next term
+  }
+  // epilogue (band_rows' contract; image blockIdx.z)
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  const long zo = long(blockIdx.z) * e.img;
+  double* const C = e.C + zo;
+  const double* const mul = e.mul ? e.mul + zo : nullptr;
+  const double* const addv = e.addv ? e.addv + zo : nullptr;
+  const double addc = e.addc_img ? e.addc_img[blockIdx.z] : e.addc;
+  const double* const d0 = e.d0 ? e.d0 + zo : nullptr;
+  const double* const d1a = e.d1a ? e.d1a + zo : nullptr;
+  const double* const d1b = e.d1b ? e.d1b + zo : nullptr;
+#pragma unroll
+  for (int h = 0; h < OUT_TASKS; ++h) {
+    const int id = threadIdx.x + h * F_THREADS;
+    const int m = a0 + id % F_TA, jb = id / F_TA;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = j0 + 8 * jb + q;
+      if (m >= n || j >= n) continue;
+      double v = acc[h][q];
+      const long vi = long(m) * e.vm + long(j) * e.vn;
+      if (mul) v *= mul[vi];
+      if (addv) v = __dadd_rn(v, __dmul_rn(addc, addv[vi]));  // + lambda^2 p, unfused as Eigen
+      C[long(m) * e.cm + long(j) * e.cn] = v;
+      if (e.partials) {
+        if (e.d0) s0 += v * (e.d0_self ? v : d0[vi]);
+        if (d1a) s1 += v * (d1b ? (d1a[vi] - d1b[vi]) : d1a[vi]);
+        if (e.count_nonfinite && !isfinite(v)) s2 += 1.0;
+      }
+    }
+  }
+  if (e.partials) {
+    __shared__ double red[F_THREADS / 32][3];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, off);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+    }
+    if (lane == 0) red[warp][0] = s0, red[warp][1] = s1, red[warp][2] = s2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double x0 = 0, x1 = 0, x2 = 0;
+      for (int w = 0; w < F_THREADS / 32; ++w) x0 += red[w][0], x1 += red[w][1], x2 += red[w][2];
+      double* o = e.partials + (long(blockIdx.z) * e.part_img + long(blockIdx.y) * gridDim.x + blockIdx.x) * 4;
+      o[0] = x0, o[1] = x1, o[2] = x2, o[3] = 0.0;
+    }
+  }
+}
+
+template <int TC, int TR>
+void launch_fused(const double* X, int n, int r, const BandTaps& tc, const BandTaps& tr, const F64Epilogue& e,
+                  const int* status, int batch) {
+  using D = FusedDims<TC, TR>;
+  auto k = band_fused_kernel<TC, TR>;
+  set_smem_limit(reinterpret_cast<const void*>(k), D::SMEM);
+  dim3 grid(cdiv(n, F_TJ), cdiv(n, F_TA), batch);
+  launch_pdl(k, grid, dim3(F_THREADS), D::SMEM, X, n, r, tc, tr, e, status);
+}
+
 // Tap counts with specialised kernels (the BASELINE PSFs: 41 (C5), 31
 // (C2/C3), 19 (C1), 17 (C4)); any other count runs the generic kernels.
 template <template <int> class F, typename... Args>
@@ -413,6 +551,23 @@ void band_cols(const double* X, double* Y, int n, int r, const BandTaps& t, cons
 }
 
 int band_rows_num_ctas(int n) { return int(cdiv(n, B_TJ) * cdiv(n, B_TA)); }
+
+bool band_fused_supported(int col_taps, int row_taps) {
+  return col_taps == row_taps && (col_taps == 17 || col_taps == 19);
+}
+int band_fused_num_ctas(int n) { return int(cdiv(n, F_TJ) * cdiv(n, F_TA)); }
+
+void band_fused(const double* X, int n, int r, const BandTaps& tc, const BandTaps& tr, const F64Epilogue& e,
+                const int* status, int batch) {
+  LaunchScope scope(KC_OPERATOR);
+  if (tc.real == 17 && tr.real == 17)
+    launch_fused<17, 17>(X, n, r, tc, tr, e, status, batch);
+  else if (tc.real == 19 && tr.real == 19)
+    launch_fused<19, 19>(X, n, r, tc, tr, e, status, batch);
+  else
+    throw InvalidArgument("band_fused: unsupported tap counts");
+  check_launch("band_fused");
+}
 
 void band_rows(const double* Y, int n, int r, const BandTaps& t, const F64Epilogue& e,
                const int* status, int batch) {

@@ -29,5 +29,13 @@ void band_cols(const double* X, double* Y, int n, int r, const BandTaps& t, cons
 void band_rows(const double* Y, int n, int r, const BandTaps& t, const F64Epilogue& e,
                const int* status, int batch = 1);
 int band_rows_num_ctas(int n);
+// Both passes in one kernel (short bands, where the two-pass form is HBM-
+// bound): out = sum_k row-correlation(column-correlation(X)), epilogue as
+// band_rows. Supported tap counts: band_fused_supported(); partial slots per
+// image: band_fused_num_ctas(n).
+bool band_fused_supported(int col_taps, int row_taps);
+int band_fused_num_ctas(int n);
+void band_fused(const double* X, int n, int r, const BandTaps& tc, const BandTaps& tr, const F64Epilogue& e,
+                const int* status, int batch = 1);
 
 }  // namespace kp

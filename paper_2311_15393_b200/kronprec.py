@@ -220,18 +220,19 @@ class KroneckerSum:
             self._h = h
         return self._h
 
-    _MODES = {"auto": 0, "dense": 1, "banded": 2}
+    _MODES = {"auto": 0, "dense": 1, "banded": 2, "banded_fused": 3}
 
     def set_mode(self, mode: str) -> None:
         """Operator algorithm: "auto" (banded-Toeplitz kernels when the
         factors have that structure), "dense" (DMMA GEMMs, the product the
-        reference computes) or "banded"."""
+        reference computes), "banded", or "banded_fused" (both passes in one
+        kernel; 17 / 19 diagonals only)."""
         check(lib().kp_operator_set_mode(self.handle(), KroneckerSum._MODES[mode]))
 
     def mode(self) -> tuple[str, int, int]:
         m, tc, tr = C.c_int(), C.c_int(), C.c_int()
         check(lib().kp_operator_get_mode(self.handle(), C.byref(m), C.byref(tc), C.byref(tr)))
-        return ("banded" if m.value == 2 else "dense"), tc.value, tr.value
+        return {1: "dense", 2: "banded", 3: "banded_fused"}[m.value], tc.value, tr.value
 
     def release(self) -> None:
         if self._h is not None:

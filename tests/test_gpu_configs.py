@@ -162,7 +162,7 @@ def test_c5_operator_full_size_properties():
     operator equals the dense DMMA product, is linear, and A^T is its adjoint."""
     psf, cap = configs._psf("C5")
     a, _ = P.psf_to_kronsum(psf, 4096, max_rank=cap)
-    assert a.mode()[0] == "banded"
+    assert a.mode()[0].startswith("banded")
     rng = np.random.default_rng(55)
     x, y = rng.standard_normal(4096 * 4096), rng.standard_normal(4096 * 4096)
     ax = K.kronsum_apply(a, x)

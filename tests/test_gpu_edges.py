@@ -143,7 +143,7 @@ def test_banded_detection_limit(n_p, expect_banded):
     psf = P.make_psf("gaussian", n_p, sigma=n_p / 6.0)
     a, _ = P.psf_to_kronsum(psf, n, max_rank=1)
     mode, ct, rt = a.mode()
-    assert (mode == "banded") == expect_banded
+    assert mode.startswith("banded") == expect_banded
     x = np.random.default_rng(1).standard_normal(n * n)
     want = O.kronsum_apply(a, x)
     assert np.linalg.norm(K.kronsum_apply(a, x) - want) <= 1e-13 * np.linalg.norm(want)
@@ -158,7 +158,7 @@ def test_banded_term_limit(r, expect_banded):
         cols = [banded_toeplitz(rng.standard_normal(5), 2, n) for _ in range(2)]
         terms.append(KronTerm(cols[0], cols[1]))
     a = KroneckerSum(terms, n)
-    assert (a.mode()[0] == "banded") == expect_banded
+    assert (a.mode()[0].startswith("banded")) == expect_banded
     x = rng.standard_normal(n * n)
     for f, fo in ((K.kronsum_apply, O.kronsum_apply), (K.kronsum_apply_transpose, O.kronsum_apply_transpose)):
         want = fo(a, x)

@@ -481,7 +481,7 @@ def test_tensor_mode_solver_within_north_star_bounds(solver):
 def test_banded_operator_matches_dense_and_oracle(kind, n, rank):
     psf = P.make_psf(kind, 7, sigma=1.3, length=5, steps=20, blob_count=4, seed=5)
     a, _ = P.psf_to_kronsum(psf, n, truncation_tol=0.0, max_rank=rank)
-    assert a.mode()[0] == "banded"
+    assert a.mode()[0].startswith("banded")
     y = np.random.default_rng(n).standard_normal(n * n)
     for g, o in ((K.kronsum_apply, O.kronsum_apply),
                  (K.kronsum_apply_transpose, O.kronsum_apply_transpose)):
@@ -508,14 +508,44 @@ def test_banded_tap_specialisations_match_oracle(n_p, n):
     for g, o in ((K.kronsum_apply, O.kronsum_apply),
                  (K.kronsum_apply_transpose, O.kronsum_apply_transpose)):
         want = o(a, y)
-        assert np.linalg.norm(g(a, y) - want) <= 1e-13 * np.linalg.norm(want)
+        got = g(a, y)
+        assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
+        if n_p in (17, 19):  # the fused single-kernel form against the two passes
+            a.set_mode("banded_fused")
+            assert np.linalg.norm(g(a, y) - got) <= 1e-14 * np.linalg.norm(got)
+            a.set_mode("auto")
+
+
+def test_fused_banded_solvers_match_two_pass():
+    """Short bands (C1 / C4 tap counts) can run passes A + B fused in one
+    kernel (opt-in); solves agree with the two-pass kernels to FP64
+    summation order."""
+    psf = P.make_psf("gaussian", 17, sigma=2.5)
+    n = 128
+    a, _ = P.psf_to_kronsum(psf, n)
+    a.set_mode("banded_fused")
+    assert a.mode()[0] == "banded_fused"
+    term = P.nearest_kron(psf, n)
+    tp = P.make_test_problem(P.blob_image(n, 9), psf, 0.01, 19, a=a)
+    m = K.build_preconditioner(term.row_factor, term.col_factor, 0.03, H)
+    opts = SolverOptions(lambda_=0.03, max_iterations=30, rel_residual_tol=1e-6, x_true=tp.x_true)
+    fused = K.pcg(a, tp.b, m, opts)
+    p = np.random.default_rng(2).standard_normal(n * n)
+    nf = K.normal_matvec(a, 0.03, p)
+    a.set_mode("banded")
+    assert a.mode()[0] == "banded"
+    two = K.pcg(a, tp.b, m, opts)
+    assert np.linalg.norm(K.normal_matvec(a, 0.03, p) - nf) <= 1e-14 * np.linalg.norm(nf)
+    a.set_mode("auto")
+    assert abs(fused.history.iterations_used - two.history.iterations_used) <= 2
+    assert abs(fused.history.relative_error[-1] - two.history.relative_error[-1]) <= 1e-6
 
 
 def test_config_psfs_are_banded():
     for name, taps in (("C1", 19), ("C2", 31), ("C4", 17), ("C5", 41)):
         cfg = configs_small(name)
         mode, tc, tr = cfg.problem.a.mode()
-        assert mode == "banded" and tc == taps and tr == taps
+        assert mode.startswith("banded") and tc == taps and tr == taps
 
 
 def configs_small(name):
@@ -532,7 +562,7 @@ def test_random_factors_stay_dense():
 
 def test_banded_normal_matvec_and_solvers():
     tp, term = blob_problem(96)
-    assert tp.a.mode()[0] == "banded"
+    assert tp.a.mode()[0].startswith("banded")
     p = np.random.default_rng(1).standard_normal(96 * 96)
     want = O.normal_matvec(tp.a, 0.01, p)
     assert np.linalg.norm(K.normal_matvec(tp.a, 0.01, p) - want) <= 1e-13 * np.linalg.norm(want)
