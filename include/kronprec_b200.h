@@ -277,8 +277,8 @@ int kp_fpcg(const kp_operator* op, const double* b, const kp_precond* m,
  * i * n^2 (host or device per opts->device_pointers); hist points at
  * `batch` kp_history structs. Each image's iterates, history and abort
  * reason equal what kp_pcg / kp_fpcg with with_lambda(m, lambdas[i]) gives.
- * Requires the fp16 format with KP_ACCUM_REFERENCE; record_iterates is not
- * supported (KP_ERR_INVALID_ARGUMENT). */
+ * Requires the fp16 format (KP_ACCUM_REFERENCE or KP_ACCUM_TENSOR);
+ * record_iterates is not supported (KP_ERR_INVALID_ARGUMENT). */
 int kp_pcg_batch(const kp_operator* op, const kp_precond* m, int batch,
                  const double* b, const double* lambdas,
                  const kp_solver_options* opts, double* x, kp_history* hist);

@@ -1030,11 +1030,14 @@ int msolve_batch_slots(const kp_precond* p, bool stacked) {
   return msolve_f16x(p) ? gemm_f16x_partials_per_image(n, n) : 0;
 }
 bool msolve_batch_stacked(const kp_precond* p, int B) {
-  // f16x tiles are 32 wide, f16ref tiles up to 64: images must start on a tile
+  // f16x tiles are 32 wide, f16ref tiles up to 64, tcgen05 (tensor mode)
+  // tiles 128 tall: images must start on a tile
+  if (p->accum == KP_ACCUM_TENSOR) return p->n % 128 == 0;
   return msolve_f16x(p) ? p->n % 32 == 0 : p->n % 64 == 0;
 }
 int msolve_batch_slots_all(const kp_precond* p, int B) {
   const int n = p->n;
+  if (p->accum == KP_ACCUM_TENSOR) return VEC_CTAS;  // msolve_finish partials per image
   if (!msolve_batch_stacked(p, B)) return msolve_partials_ctas(p);
   return msolve_f16x(p) ? gemm_f16x_partials_per_image(n, n)
                         : gemm_f16ref_partials_per_image(n, B * n, n);
@@ -1087,6 +1090,39 @@ void msolve_batch(kp_precond* p, int B, double* z, const double* d0, const doubl
   const bool stacked = msolve_batch_stacked(p, B);
   const int slots = msolve_batch_slots_all(p, B);
   const int groups = stacked ? 1 : B, per = stacked ? B : 1;
+  if (p->accum == KP_ACCUM_TENSOR) {
+    // tcgen05 products (msolve's tensor orientation: the data is the A
+    // operand), images stacked along M; binary16 z, then one widening pass
+    for (int gi = 0; gi < groups; ++gi) {
+      const long ho = long(gi) * n * ldh;
+      const size_t vo = size_t(gi) * nn;
+      F16GemmArgs g;
+      g.M = per * n, g.N = n, g.K = n, g.status = status;
+      auto batch_epi = [&](F16Epilogue& e) {
+        if (stacked && B > 1) e.m_img = n, e.c_img = long(n) * ldh, e.s_img = long(nn);
+      };
+      g.A = {p->b_r16.p + ho, ldh}, g.B = {sh->vc_a.p, ldh};  // t1^T = R^T V_c
+      g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->b_t1h.p + ho, g.epi.cm = 1, g.epi.cn = ldh;
+      batch_epi(g.epi);
+      gemm_f16tc(g, KC_PRECOND);
+      g.A = {p->b_t1h.p + ho, ldh}, g.B = {sh->vr_b.p, ldh};  // w = round(S .* (t1 V_r))
+      g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF_SCALED, g.epi.Ch = p->b_wh.p + ho, g.epi.cm = 1,
+      g.epi.cn = ldh, g.epi.scale = p->b_s16.p + vo, g.epi.sm = 1, g.epi.sn = n;
+      batch_epi(g.epi);
+      gemm_f16tc(g, KC_PRECOND);
+      g.A = {p->b_wh.p + ho, ldh}, g.B = {sh->vct_a.p, ldh};  // t3^T = w^T V_c^T
+      g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->b_t3h.p + ho, g.epi.cm = 1, g.epi.cn = ldh;
+      batch_epi(g.epi);
+      gemm_f16tc(g, KC_PRECOND);
+      g.A = {p->b_t3h.p + ho, ldh}, g.B = {sh->vrt_b.p, ldh};  // z = t3 V_r^T, binary16 into t1h
+      g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->b_t1h.p + ho, g.epi.cm = 1, g.epi.cn = ldh;
+      batch_epi(g.epi);
+      gemm_f16tc(g, KC_PRECOND);
+      msolve_finish_f16(p->b_t1h.p + ho, ldh, n, z + vo, d0 ? d0 + vo : nullptr, d1a ? d1a + vo : nullptr,
+                        d1b ? d1b + vo : nullptr, p->b_part.p + size_t(gi) * slots * 4, status, per);
+    }
+    return;
+  }
   for (int gi = 0; gi < groups; ++gi) {
     const long ho = long(gi) * n * ldh;  // image offset when not stacked
     const size_t vo = size_t(gi) * nn;
@@ -1179,8 +1215,8 @@ void run_pcg_batch(kp_operator* op, kp_precond* m, int B, const double* b_in, co
   if (o->max_iterations < 1) throw InvalidArgument("solver: max_iterations must be at least 1");
   if (!(o->rel_residual_tol > 0.0)) throw InvalidArgument("solver: tolerance must be positive");
   if (o->record_iterates) throw InvalidArgument("pcg_batch: record_iterates is not supported for batches");
-  if (!is_fp16(m->fmt) || m->accum != KP_ACCUM_REFERENCE)
-    throw InvalidArgument("pcg_batch: batched solves need the fp16 reference-exact preconditioner");
+  if (!is_fp16(m->fmt))
+    throw InvalidArgument("pcg_batch: batched solves need the fp16 preconditioner (reference-exact or tensor mode)");
   for (int i = 0; i < B; ++i)
     if (hist[i].capacity < 1 || !hist[i].residual_norm || !hist[i].work_units)
       throw InvalidArgument("solver: history arrays missing");

@@ -41,6 +41,10 @@ struct F16Epilogue {
   int n_img = 0;
   long c_img = 0, s_img = 0, v_img = 0;
   int part_img = 0;
+  // gemm_f16tc only: the images stacked along M instead (the A operand holds
+  // their rows back to back; m_img rows each, a multiple of 128); same
+  // per-image offsets c_img / s_img. Binary16 outputs only.
+  int m_img = 0;
 };
 
 // Image index and image-local column of global output column n.

@@ -263,26 +263,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           continue;
         }
-        __half* __restrict__ Ch = e.Ch;
+        // batched products stacked along M: this tile's image and local row
+        const int img = e.m_img ? mb / e.m_img : 0;
+        const int ml = m - img * e.m_img;
+        __half* __restrict__ Ch = e.Ch + img * e.c_img;
         if (e.mode == F16OUT_HALF_SCALED) {  // w = round16(S .* t2), as the reference
-          const __half* __restrict__ sc = e.scale;
+          const __half* __restrict__ sc = e.scale + img * e.s_img;
           __half sv[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) {  // all scale loads first
             const int n = nb + c0 + j;
-            sv[j] = n < N ? sc[long(m) * e.sm + long(n) * e.sn] : __ushort_as_half(0);
+            sv[j] = n < N ? sc[long(ml) * e.sm + long(n) * e.sn] : __ushort_as_half(0);
           }
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int n = nb + c0 + j;
             if (n < N)
-              Ch[long(m) * e.cm + long(n) * e.cn] = __hmul_rn(sv[j], __float2half_rn(__uint_as_float(v[j])));
+              Ch[long(ml) * e.cm + long(n) * e.cn] = __hmul_rn(sv[j], __float2half_rn(__uint_as_float(v[j])));
           }
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int n = nb + c0 + j;
-            if (n < N) Ch[long(m) * e.cm + long(n) * e.cn] = __float2half_rn(__uint_as_float(v[j]));
+            if (n < N) Ch[long(ml) * e.cm + long(n) * e.cn] = __float2half_rn(__uint_as_float(v[j]));
           }
         }
       }

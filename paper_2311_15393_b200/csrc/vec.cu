@@ -122,9 +122,17 @@ __global__ void msolve_finish_f16_kernel(const __half* z16, long ldh, int n, dou
                                          double* part, const int* status) {
   pdl_wait();
   if (status && *status) return;
+  const size_t nn = size_t(n) * n;
+  {  // batch image blockIdx.y
+    const size_t img = blockIdx.y;
+    z16 += img * n * ldh, z += img * nn;
+    if (d0) d0 += img * nn;
+    if (d1a) d1a += img * nn;
+    if (d1b) d1b += img * nn;
+    part += img * gridDim.x * 4;
+  }
   __shared__ double red[VEC_THREADS / 32][3];
   const unsigned un = unsigned(n);
-  const size_t nn = size_t(n) * n;
   const bool same = d0 && d1a == d0;
   double v[3] = {0.0, 0.0, 0.0};
   if (VEC2) {
@@ -773,13 +781,14 @@ static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) =
 
 void msolve_finish_f16(const __half* z16, long ldh, int n, double* z, const double* d0,
                        const double* d1a, const double* d1b, double* partials,
-                       const int* status) {
+                       const int* status, int batch) {
   const bool vec2 = n % 2 == 0 && ldh % 2 == 0 && al16(z) && al16(d0) && al16(d1a) && al16(d1b);
+  const dim3 grid(VEC_CTAS, batch);
   if (vec2)
-    KP_LAUNCH(KC_VECTOR, msolve_finish_f16_kernel<true>, VEC_CTAS, VEC_THREADS, z16, ldh, n, z, d0,
+    KP_LAUNCH(KC_VECTOR, msolve_finish_f16_kernel<true>, grid, VEC_THREADS, z16, ldh, n, z, d0,
               d1a, d1b, partials, status);
   else
-    KP_LAUNCH(KC_VECTOR, msolve_finish_f16_kernel<false>, VEC_CTAS, VEC_THREADS, z16, ldh, n, z,
+    KP_LAUNCH(KC_VECTOR, msolve_finish_f16_kernel<false>, grid, VEC_THREADS, z16, ldh, n, z,
               d0, d1a, d1b, partials, status);
 }
 

@@ -71,9 +71,11 @@ void precond_weights(const double* s_r, const double* s_c, int n, double l2, dou
 // Last step of the tensor-mode M-solve: z[l*n + i] = double(z16[l*ldh + i])
 // (exact) with the M-solve dot partials over the fixed VEC_CTAS grid:
 // [0] z.d0, [1] z.(d1a - d1b) (d1b optional), [2] #non-finite z.
+// batch > 1: image i's z16 at i * n * ldh, vectors at i * n^2, partials at
+// i * VEC_CTAS slots.
 void msolve_finish_f16(const __half* z16, long ldh, int n, double* z, const double* d0,
                        const double* d1a, const double* d1b, double* partials,
-                       const int* status);
+                       const int* status, int batch = 1);
 
 // ---- PCG -------------------------------------------------------------------
 // Every PCG kernel takes `batch` (default 1): a batch of independent solves

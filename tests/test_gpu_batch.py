@@ -93,8 +93,27 @@ def test_batch_validation():
     with pytest.raises(ValueError):
         K.pcg_batch(a, bs, m0, [0.1], SolverOptions())
     m64 = K.build_preconditioner(term.row_factor, term.col_factor, 1.0, K.PrecisionFormat.fp64())
-    with pytest.raises(Exception, match="fp16 reference-exact"):
+    with pytest.raises(Exception, match="fp16 preconditioner"):
         K.pcg_batch(a, bs, m64, [0.1, 0.2], SolverOptions())
+
+
+@pytest.mark.parametrize("n,count", [(128, 4), (96, 3)])
+def test_tensor_mode_batch_equals_single_solves(n, count):
+    """KP_ACCUM_TENSOR batches: tcgen05 products with the images stacked along
+    M (n % 128 == 0) or one image at a time; each image equals the single
+    tensor-mode solve bit for bit."""
+    a, term, tps = batch_problem(n, count)
+    m0 = K.build_preconditioner(term.row_factor, term.col_factor, 1.0, H, accum="tensor")
+    lams = [0.02 * (1 + i) for i in range(count)]
+    opts = SolverOptions(max_iterations=20, rel_residual_tol=1e-6)
+    res = K.pcg_batch(a, np.stack([tp.b for tp in tps]), m0, lams, opts,
+                      x_true=np.stack([tp.x_true for tp in tps]))
+    for i, tp in enumerate(tps):
+        o = SolverOptions(lambda_=lams[i], max_iterations=20, rel_residual_tol=1e-6, x_true=tp.x_true)
+        single = K.pcg(a, tp.b, K.with_lambda(m0, lams[i]), o)
+        assert res[i].history.iterations_used == single.history.iterations_used
+        assert res[i].history.residual_norm == single.history.residual_norm
+        assert np.array_equal(res[i].x, single.x)
 
 
 def test_discrepancy_batch_equals_per_image():
