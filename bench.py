@@ -429,7 +429,9 @@ def run_c4(args):
         check(L.kp_profile_read(1, C.byref(tt), C.byref(tc)))
         check(L.kp_profile_enable(0))
         nb = sum(1 for v in lams if v is not None)
-        batches = 1 + max(r.iterations for r in res_p)  # batched M-solves that ran (initial + per iteration)
+        # batched M-solves that ran: the longest image's msolve_count (a solve
+        # stopped at the iteration cap skips its last M-solve)
+        batches = max(r.msolve_count for r in res_p)
         work = 2.0 * nb * float(sh.n) ** 3  # binary16 ops per launch (all images of the batch)
         ach = work / (tt.value / (4 * batches) / 1e3) / 1e12 if tc.value else 0.0
         import paper_2311_15393_b200 as K

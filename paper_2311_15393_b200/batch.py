@@ -31,6 +31,7 @@ class ImageResult:
     rel_err: float
     abort_reason: str = ""
     no_root: bool = False
+    msolve_count: int = 0  # M-solves that ran (history.msolve_count)
 
 
 RESULT_FIELDS = ("image", "noise_level", "lam", "iterations", "converged", "rel_err", "no_root")
@@ -215,7 +216,7 @@ class C4Shard:
                 continue
             h = res[q].history
             outl.append(ImageResult(i, noise_levels[q], lams[q], h.iterations_used, h.converged,
-                                    h.relative_error[-1], h.abort_reason))
+                                    h.relative_error[-1], h.abort_reason, msolve_count=h.msolve_count))
         return outl
 
     def solve_batch(self, images, probs: dict, lams: dict | None = None) -> list:

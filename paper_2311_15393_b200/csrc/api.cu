@@ -473,8 +473,8 @@ bool msolve_f16x(const kp_precond* p) {
 int msolve_partials_ctas(const kp_precond* p) {
   if (is_generic(p->fmt)) return LP_PART_CTAS;
   if (covers_double(p->fmt)) return gemm_f64_num_ctas(p->n, p->n);
-  if (p->accum == KP_ACCUM_TENSOR) return VEC_CTAS;
-  return msolve_f16x(p) ? gemm_f16x_num_ctas(p->n, p->n) : gemm_f16ref_num_ctas(p->n, p->n);
+  if (p->accum == KP_ACCUM_TENSOR || msolve_f16x(p)) return VEC_CTAS;  // msolve_finish_f16 partials
+  return gemm_f16ref_num_ctas(p->n, p->n);  // gemm_f16ref's fused FP64 epilogue, one slot per tile
 }
 
 // zero-initialised gemm_f16x fix-up workspace for M x N products
@@ -602,10 +602,22 @@ void msolve(kp_precond* p, const double* r, double* z, const double* d0, const d
     gemm_x(g, KC_PRECOND);
     g.hash_a = sh->hash_vrt_b.p;
     g.A = {sh->vrt_b.p, ldh}, g.B = {p->t3h.p, ldh};  // z(i,j) = lp(t3 V_r^T), as (j, i)
-    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z, g.epi.cm = n, g.epi.cn = 1;
-    g.epi.vm = n, g.epi.vn = 1, g.epi.d0 = d0, g.epi.d1a = d1a, g.epi.d1b = d1b;
-    g.epi.partials = p->part.p;
-    gemm_x(g, KC_PRECOND);
+    // binary16 z into t1h (free once the second product has read it), then
+    // one HBM pass widens it (exactly) and forms the dot partials: an FP64
+    // epilogue with the dots inside the product cost 16 % more per product
+    // (its stores / loads stall the warps that drain TMEM)
+    // (gemm_f16ref, small n: the FP64 epilogue with fused dots saves that
+    // extra launch, which is what counts at n < 512)
+    if (f16x) {
+      g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->t1h.p, g.epi.cm = ldh, g.epi.cn = 1;
+      gemm_x(g, KC_PRECOND);
+      msolve_finish_f16(p->t1h.p, ldh, n, z, d0, d1a, d1b, p->part.p, status);
+    } else {
+      g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z, g.epi.cm = n, g.epi.cn = 1;
+      g.epi.vm = n, g.epi.vn = 1, g.epi.d0 = d0, g.epi.d1a = d1a, g.epi.d1b = d1b;
+      g.epi.partials = p->part.p;
+      gemm_x(g, KC_PRECOND);
+    }
     return;
   }
   // KP_ACCUM_TENSOR: tcgen05 kind::f16 products (gemm_f16tc). Its epilogue
@@ -1023,24 +1035,17 @@ void run_pcg(kp_operator* op, const double* b_in, kp_precond* m, const kp_solver
 // image's arithmetic is exactly the single solve's (same kernels, same
 // per-image reduction grids), so results equal kp_pcg image by image.
 
-// Partial slots per image of a batched M-solve.
-int msolve_batch_slots(const kp_precond* p, bool stacked) {
-  const int n = p->n;
-  if (!stacked) return msolve_partials_ctas(p);
-  return msolve_f16x(p) ? gemm_f16x_partials_per_image(n, n) : 0;
-}
 bool msolve_batch_stacked(const kp_precond* p, int B) {
   // f16x tiles are 32 wide, f16ref tiles up to 64, tcgen05 (tensor mode)
   // tiles 128 tall: images must start on a tile
   if (p->accum == KP_ACCUM_TENSOR) return p->n % 128 == 0;
   return msolve_f16x(p) ? p->n % 32 == 0 : p->n % 64 == 0;
 }
+// Partial slots per image of a batched M-solve.
 int msolve_batch_slots_all(const kp_precond* p, int B) {
-  const int n = p->n;
-  if (p->accum == KP_ACCUM_TENSOR) return VEC_CTAS;  // msolve_finish partials per image
+  if (p->accum == KP_ACCUM_TENSOR || msolve_f16x(p)) return VEC_CTAS;  // msolve_finish_f16
   if (!msolve_batch_stacked(p, B)) return msolve_partials_ctas(p);
-  return msolve_f16x(p) ? gemm_f16x_partials_per_image(n, n)
-                        : gemm_f16ref_partials_per_image(n, B * n, n);
+  return gemm_f16ref_partials_per_image(p->n, B * p->n, p->n);
 }
 
 void ensure_batch_ws(kp_precond* p, int B, const std::vector<double>& lambdas) {
@@ -1056,12 +1061,14 @@ void ensure_batch_ws(kp_precond* p, int B, const std::vector<double>& lambdas) {
     fill_u16(p->b_t1h.p, p->b_t1h.n, 0x8000);
     fill_u16(p->b_t3h.p, p->b_t3h.n, 0x8000);
     p->b_s16.alloc(size_t(B) * nn);
-    p->b_part.alloc(size_t(B) * msolve_batch_slots_all(p, B) * 4);
-    if (msolve_f16x(p)) {
-      ensure_zfix(p->b_zfix, n, B * n);
-      p->b_hash.alloc(rows);
-    }
     p->bcap = B;
+  }
+  // partial slots depend on the engine (process-wide setting): size them per call
+  if (p->b_part.n < size_t(B) * msolve_batch_slots_all(p, B) * 4)
+    p->b_part.alloc(size_t(B) * msolve_batch_slots_all(p, B) * 4);
+  if (msolve_f16x(p) && p->b_zfix.n < size_t(f16x_zfix_words(n, B * n)) + 2) {
+    ensure_zfix(p->b_zfix, n, B * n);
+    p->b_hash.alloc(size_t(B) * n);
   }
   // per-image S = round16(1 / ((s_r s_c)^2 + lambda_i^2)) (factor.cpp:62-76)
   const auto& sh = *p->sh;
@@ -1151,12 +1158,21 @@ void msolve_batch(kp_precond* p, int B, double* z, const double* d0, const doubl
     run();
     g.hash_a = sh->hash_vrt_b.p;
     g.A = {sh->vrt_b.p, ldh}, g.B = {p->b_t3h.p + ho, ldh};  // z(i,j) = lp(t3 V_r^T), as (j, i)
-    g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z + vo, g.epi.cm = n, g.epi.cn = 1;
-    g.epi.vm = n, g.epi.vn = 1;
-    g.epi.d0 = d0 ? d0 + vo : nullptr, g.epi.d1a = d1a ? d1a + vo : nullptr, g.epi.d1b = d1b ? d1b + vo : nullptr;
-    g.epi.partials = p->b_part.p + size_t(gi) * slots * 4;
-    batch_epi(g.epi, long(nn));
-    run();
+    if (f16x) {  // binary16 z, widened with the dots in one pass (as msolve)
+      g.epi = F16Epilogue{}, g.epi.mode = F16OUT_HALF, g.epi.Ch = p->b_t1h.p + ho, g.epi.cm = ldh, g.epi.cn = 1;
+      batch_epi(g.epi, long(n) * ldh);
+      run();
+      msolve_finish_f16(p->b_t1h.p + ho, ldh, n, z + vo, d0 ? d0 + vo : nullptr, d1a ? d1a + vo : nullptr,
+                        d1b ? d1b + vo : nullptr, p->b_part.p + size_t(gi) * slots * 4, status, per);
+    } else {
+      g.epi = F16Epilogue{}, g.epi.mode = F16OUT_F64, g.epi.Cd = z + vo, g.epi.cm = n, g.epi.cn = 1;
+      g.epi.vm = n, g.epi.vn = 1;
+      g.epi.d0 = d0 ? d0 + vo : nullptr, g.epi.d1a = d1a ? d1a + vo : nullptr;
+      g.epi.d1b = d1b ? d1b + vo : nullptr;
+      g.epi.partials = p->b_part.p + size_t(gi) * slots * 4;
+      batch_epi(g.epi, long(nn));
+      run();
+    }
   }
 }
 

@@ -7,7 +7,6 @@ import os
 import subprocess
 import sys
 
-import numpy as np
 import pytest
 
 from paper_2311_15393_b200 import cli
@@ -72,7 +71,6 @@ def test_exit_codes_without_gpu(tmp_path):
 
 @pytest.mark.gpu
 def test_solve_and_compare_verbs(tmp_path):
-    import paper_2311_15393_b200 as K
     out = tmp_path / "solve"
     r = run_cli("solve", "--n", "64", "--param", "gcv", "--solver", "pcg", "--tol", "1e-6", "--out", str(out))
     assert r.returncode == 0, r.stderr
@@ -100,7 +98,6 @@ def test_solve_and_compare_verbs(tmp_path):
     assert {"baseline", "precond", "flexible", "m_baseline", "m_precond"} <= set(w)
     hdr = next(csv.reader(open(cmp_out / "comparison.csv", newline="")))
     assert hdr[-3:] == ["fpcg_relative_error", "fpcg_residual_norm", "fpcg_work_units"]
-    del K
 
 
 @pytest.mark.gpu
@@ -121,4 +118,3 @@ def test_sweep_generate_decompose_verbs(tmp_path):
     j = json.load(open(d / "decompose.json"))
     assert j["schema"] == "kronprec.decompose/1" and j["terms"] >= 1
     assert 0.0 <= j["rel_error"] <= 1.0 and j["rel_error_rounded"] >= j["rel_error"] - 1e-3
-    del np
