@@ -17,6 +17,15 @@
 //
 // Packing: one f16x2 register holds outputs (m, n) and (m, n+16) of the same
 // k, so A is broadcast (PRMT) and all tree adds are vertical.
+//
+// Split K inside the CTA (KS = 2 or 4 groups of 128 threads, small
+// products): when the padded k-tile count is KS * V with V a power of two,
+// the tree over the KS * V units is KS complete subtrees of V units joined
+// by a balanced top (a0 + a1 for KS = 2, (a0 + a1) + (a2 + a3) for KS = 4),
+// so group g streams units [gV, (g+1)V) and group 0 adds the KS subtree
+// values in that order — bit-identical, with KS times the warps per tile
+// (a 256 x 256 product has only 64 tiles: latency-bound with one warp per
+// SM sub-partition).
 #include "gemm_f16ref.cuh"
 
 #include <cstdlib>
@@ -74,12 +83,15 @@ __device__ __forceinline__ uint32_t part(const uint4& v, int q) {
 // shared-memory counter stack (16: levels >= 4 in smem; 32: level 4 also in
 // registers; 64: levels 4 and 5 in registers — the whole 64-leaf k-tile is
 // reduced in registers and pushed once, the smallest stack).
-template <int STAGES, int UNIT, int BN>
-__global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs args, int levels) {
+template <int STAGES, int UNIT, int BN, int KS>
+__global__ void __launch_bounds__(THREADS * KS) gemm_f16ref_kernel(const F16GemmArgs args, int levels) {
   pdl_wait();
   constexpr int NP = BN / 32, NACC = nacc(BN), STAGE_BYTES = stage_bytes(BN);
   if (args.status && *args.status != 0) return;
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem_all[];
+  const int kgroup = KS > 1 ? int(threadIdx.x) / THREADS : 0;  // this thread's K range (split K)
+  // per group: STAGES tiles, then its counter stack
+  unsigned char* smem = smem_all + size_t(kgroup) * (STAGES * STAGE_BYTES + size_t(levels) * NACC * THREADS * 4);
   uint32_t* stack = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES);
 
   const int M = args.M, N = args.N;
@@ -92,11 +104,13 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
   const int tile_n = (pid % (GROUP_M * grid_n)) / gsize;
   const int m_base = tile_m * BM, n_base = tile_n * BN;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = int(threadIdx.x) - kgroup * THREADS, lane = tid & 31, warp = tid >> 5;
   const int tn = lane & 15, tm = warp * 2 + (lane >> 4);
 
-  // K extent actually streamed: whole 64-wide tiles (padding is neutral).
-  const int KT = (args.K + BKH - 1) / BKH;
+  // K extent actually streamed: whole 64-wide tiles (padding is neutral);
+  // with split K this group's KT of them, starting at k-tile kt0.
+  const int KT_all = (args.K + BKH - 1) / BKH;
+  const int KT = KT_all / KS, kt0 = kgroup * KT;
   const uint32_t sbase = smem_u32(smem);
 
   // Per-thread copy plan, computed once: chunk i of every k-tile is the 16-byte
@@ -125,7 +139,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
     const uint32_t sa = sbase + uint32_t(stage * STAGE_BYTES);
 #pragma unroll
     for (int i = 0; i < NCH; ++i)
-      cp_async16(sa + dst_off[i], valid[i] ? src0[i] + kt * BKH : src0[i], valid[i]);
+      cp_async16(sa + dst_off[i], valid[i] ? src0[i] + (kt0 + kt) * BKH : src0[i], valid[i]);
   };
 
 #pragma unroll
@@ -235,6 +249,29 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
 #pragma unroll
     for (int q = 0; q < NACC; ++q) acc[q] = 0x80008000u;  // K == 0 cannot occur (checked)
   }
+  if constexpr (KS > 1) {  // join the KS subtrees in tree order; group 0 finishes
+    uint32_t* xch = reinterpret_cast<uint32_t*>(smem_all);  // the stage buffers are free now
+    __syncthreads();
+    if (kgroup > 0) {
+#pragma unroll
+      for (int q = 0; q < NACC; ++q) xch[((kgroup - 1) * NACC + q) * THREADS + tid] = acc[q];
+    }
+    __syncthreads();
+    if (kgroup > 0) return;
+    uint32_t a1[NACC];
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) a1[q] = xch[q * THREADS + tid];
+    if constexpr (KS == 2) {
+#pragma unroll
+      for (int q = 0; q < NACC; ++q) acc[q] = hadd2(acc[q], a1[q]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < NACC; ++q) {
+        const uint32_t a2 = xch[(1 * NACC + q) * THREADS + tid], a3 = xch[(2 * NACC + q) * THREADS + tid];
+        acc[q] = hadd2(hadd2(acc[q], a1[q]), hadd2(a2, a3));
+      }
+    }
+  }
 
   // ---- epilogue ----
   const F16Epilogue& e = args.epi;
@@ -287,7 +324,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f16ref_kernel(const F16GemmArgs 
       s2 += __shfl_xor_sync(0xffffffffu, s2, off);
     }
     if (lane == 0) red[warp][0] = s0, red[warp][1] = s1, red[warp][2] = s2;
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;\n" ::"n"(THREADS) : "memory");  // group 0's warps only
     if (tid == 0) {
       double a0 = 0, a1 = 0, a2 = 0;
       for (int w = 0; w < THREADS / 32; ++w) a0 += red[w][0], a1 += red[w][1], a2 += red[w][2];
@@ -318,19 +355,45 @@ int f16ref_bn(int M, int N) {
   return cdiv(M, BM) * cdiv(N, 64) < 8 * ctx().num_sms ? 32 : 64;
 }
 
-template <int STAGES, int UNIT, int BN>
+template <int STAGES, int UNIT, int BN, int KS>
 void launch_f16ref_bn(const F16GemmArgs& a, int kernel_class) {
-  const int kt = (a.K + BKH - 1) / BKH;
+  const int kt = (a.K + BKH - 1) / BKH / KS;
   const int units = kt * (BKH / UNIT);
   int levels = 1;
   while ((1 << levels) <= units) ++levels;
-  const size_t smem = size_t(STAGES) * stage_bytes(BN) + size_t(levels) * nacc(BN) * THREADS * 4;
-  auto kern = gemm_f16ref_kernel<STAGES, UNIT, BN>;
+  const size_t smem = size_t(KS) * (size_t(STAGES) * stage_bytes(BN) + size_t(levels) * nacc(BN) * THREADS * 4);
+  auto kern = gemm_f16ref_kernel<STAGES, UNIT, BN, KS>;
   set_smem_limit(reinterpret_cast<const void*>(kern), smem);
   LaunchScope scope(kernel_class);
   const unsigned grid = cdiv(a.M, BM) * cdiv(a.N, BN);
-  launch_pdl(kern, dim3(grid), dim3(THREADS), smem, a, levels);
+  launch_pdl(kern, dim3(grid), dim3(THREADS * KS), smem, a, levels);
   check_launch("gemm_f16ref");
+}
+
+// Split K inside the CTA (see the header) when the tile grid cannot fill
+// the SMs (< 2 CTAs per SM) and the padded k-tile count is KS times a power
+// of two. KP_F16REF_KSPLIT=1 disables.
+int f16ref_ksplit(int tiles, int K) {
+  static const int off = [] {
+    const char* e = getenv("KP_F16REF_KSPLIT");
+    return e && atoi(e) == 1;
+  }();
+  if (off || tiles >= 2 * ctx().num_sms) return 1;
+  const int kt = (K + BKH - 1) / BKH;
+  auto pow2 = [](int v) { return v > 0 && (v & (v - 1)) == 0; };
+  if (kt % 4 == 0 && pow2(kt / 4)) return 4;
+  if (kt % 2 == 0 && pow2(kt / 2)) return 2;
+  return 1;
+}
+
+template <int STAGES, int UNIT, int BN>
+void launch_f16ref_ks(const F16GemmArgs& a, int kernel_class) {
+  const int tiles = int(cdiv(a.M, BM) * cdiv(a.N, BN));
+  switch (f16ref_ksplit(tiles, a.K)) {
+    case 4: launch_f16ref_bn<STAGES, UNIT, BN, 4>(a, kernel_class); break;
+    case 2: launch_f16ref_bn<STAGES, UNIT, BN, 2>(a, kernel_class); break;
+    default: launch_f16ref_bn<STAGES, UNIT, BN, 1>(a, kernel_class); break;
+  }
 }
 
 template <int STAGES, int UNIT>
@@ -338,9 +401,9 @@ void launch_f16ref(const F16GemmArgs& a, int kernel_class) {
   // batched products take the tile width of one image's product, so every
   // image is tiled (and its partials grouped) exactly as a single product
   if (f16ref_bn(a.M, a.epi.n_img ? a.epi.n_img : a.N) == 32)
-    launch_f16ref_bn<STAGES, UNIT, 32>(a, kernel_class);
+    launch_f16ref_ks<STAGES, UNIT, 32>(a, kernel_class);
   else
-    launch_f16ref_bn<STAGES, UNIT, 64>(a, kernel_class);
+    launch_f16ref_ks<STAGES, UNIT, 64>(a, kernel_class);
 }
 
 int f16ref_cfg() {
