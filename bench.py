@@ -378,7 +378,16 @@ def run_c4(args):
     images = 64
     mine = list(shard(images, ws, rank))
     sh = C4Shard(n=args.size, svd=args.svd, device=local)
+    t_gen = time.time()
     probs = {i: sh.problem(i) for i in mine}  # input generation is not timed
+    t_gen_host = time.time() - t_gen
+    # the same images generated on the device (kp_generate_test_problems), for the record
+    from paper_2311_15393_b200 import problems as Pm
+    check(L.kp_synchronize())
+    t_gen = time.time()
+    Pm.make_test_problems_device(sh.a, [4000 + i for i in mine], [5000 + i for i in mine],
+                                 [probs[i].noise_level for i in mine])
+    t_gen_dev = time.time() - t_gen
     batched = args.c4_mode == "batch"
     pinned = []
 
@@ -512,6 +521,10 @@ def run_c4(args):
                        "note": "value is already end to end: every solve goes through the public "
                                "API with host buffers (b, x_true in, x out inside the timed region)"},
                "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof,
+               "problem_generation_s": {"host": t_gen_host, "device": t_gen_dev,
+                                        "note": "untimed setup: this rank's images by the host "
+                                                "generator vs kp_generate_test_problems (incl. copies "
+                                                "back to the host)"},
                "cpu_baseline": cpu,
                "results": [{k: r[k] for k in ("image", "lam", "iterations", "rel_err")}
                            for r in allres[:6]],

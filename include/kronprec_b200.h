@@ -328,6 +328,23 @@ int kp_filtered_solution(const kp_precond* p, const double* b, double lambda,
  * one-point-at-a-time bisection. */
 int kp_discrepancy(const kp_spectral* sd, double noise_norm, double eta,
                    kp_param_choice* choice);
+/* make_test_problem (deblur.cpp:201-229) for `batch` images on the device:
+ * x_true = the BASELINE blob image of image_seeds[i] (`blobs` Gaussian blobs,
+ * clipped to [0, 1]), b_true = A x_true with this operator, noise =
+ * Rng(noise_seeds[i]).normal() draws scaled to noise_levels[i] *
+ * ||b_true||, b = b_true + noise. The mt19937_64 stream is the reference's
+ * bit for bit (kp_rng_raw); the normals use the device log / sin / cos, so
+ * noise and b match the host generator to the last bits. x_true, b, noise
+ * (optional): batch * n^2 doubles (host or device per device_pointers);
+ * noise_norms (optional, host): ||noise_i||. */
+int kp_generate_test_problems(const kp_operator* op, int batch,
+                              const unsigned long long* image_seeds, int blobs,
+                              const unsigned long long* noise_seeds,
+                              const double* noise_levels, double* x_true, double* b,
+                              double* noise, double* noise_norms, int device_pointers);
+/* std::mt19937_64 on the device (test hook): `count` raw outputs per seed,
+ * out[i * count + k]. */
+int kp_rng_raw(const unsigned long long* seeds, int batch, long count, unsigned long long* out);
 /* The discrepancy lambda of `batch` right-hand sides b (batch * n^2 host
  * doubles, image i at i * n^2) sharing the preconditioner factors of p:
  * make_spectral_data(p, b_i) + discrepancy(sd_i, noise_norms[i], eta) for

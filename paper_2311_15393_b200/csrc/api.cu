@@ -31,6 +31,9 @@
 #include "gemm_f16tc.cuh"
 #include "gemm_f16x.cuh"
 #include "svd_dev.h"
+#include "problem_dev.h"
+
+extern "C" void kpg_blob_params(int n, uint64_t seed, int blobs, double* out);  // problem.cpp
 #include "lp_generic.cuh"
 #include "gemm_f64.cuh"
 #include "host_la.h"
@@ -2336,6 +2339,63 @@ int kp_wgcv_objective(const kp_spectral* sd, double omega, double lambda, double
 // its own spectral data (same per-lambda sums, same host decisions).
 // status[i]: 0, or KP_ERR_NO_ROOT (no sign change in the bracket) /
 // KP_ERR_RUNTIME (non-finite objective) with lambdas[i] = NaN.
+// make_test_problem (deblur.cpp:201-229) for `batch` images on the device:
+// x_true = the BASELINE blob image (seed image_seeds[i], `blobs` blobs; blob
+// parameters drawn by the host Rng exactly as kpg_blob_image draws them),
+// b_true = A x_true (this operator), noise from Rng(noise_seeds[i]).normal()
+// scaled to noise_levels[i] * ||b_true|| (problem_dev.cu), b = b_true +
+// noise. x_true / b / noise: batch * n^2 (host or device per
+// device_pointers; noise optional); noise_norms: host, batch (optional).
+int kp_generate_test_problems(const kp_operator* opc, int batch, const unsigned long long* image_seeds,
+                              int blobs, const unsigned long long* noise_seeds, const double* noise_levels,
+                              double* x_true, double* b, double* noise, double* noise_norms,
+                              int device_pointers) {
+  KP_API({
+    auto* op = const_cast<kp_operator*>(opc);
+    if (!op || batch < 1 || blobs < 0 || !image_seeds || !noise_seeds || !noise_levels || !x_true || !b)
+      throw InvalidArgument("generate_test_problems: bad arguments");
+    for (int i = 0; i < batch; ++i)
+      if (noise_levels[i] < 0.0) throw InvalidArgument("make_test_problem: negative noise level");
+    const int n = op->n;
+    const size_t nn = size_t(n) * n, bnn = size_t(batch) * nn;
+    std::vector<double> params(size_t(batch) * std::max(blobs, 1) * 4);
+    for (int i = 0; i < batch; ++i) kpg_blob_params(n, image_seeds[i], blobs, params.data() + size_t(i) * blobs * 4);
+    DBuf<double> dparams(params.size()), dlev(batch), dnorm(batch);
+    DBuf<uint64_t> dseeds(batch);
+    dparams.upload(params.data(), params.size());
+    dlev.upload(noise_levels, batch);
+    KP_CUDA(cudaMemcpyAsync(dseeds.p, noise_seeds, batch * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx().stream));
+    const bool dev = device_pointers != 0;
+    DBuf<double> own_x, own_b, own_e, bt(bnn);
+    double* dx = dev ? x_true : (own_x.alloc(bnn), own_x.p);
+    double* db = dev ? b : (own_b.alloc(bnn), own_b.p);
+    double* de = (dev && noise) ? noise : (own_e.alloc(bnn), own_e.p);
+    blob_images_dev(n, batch, blobs, dparams.p, dx);
+    op_apply_batch(op, batch, dx, bt.p, false, nullptr, nullptr, nullptr, nullptr);  // b_true = A x_true
+    rng_normals_dev(dseeds.p, batch, long(nn), de);
+    add_noise_dev(batch, nn, dlev.p, bt.p, de, db, dnorm.p);
+    if (!dev) {
+      KP_CUDA(cudaMemcpyAsync(x_true, dx, bnn * sizeof(double), cudaMemcpyDeviceToHost, ctx().stream));
+      KP_CUDA(cudaMemcpyAsync(b, db, bnn * sizeof(double), cudaMemcpyDeviceToHost, ctx().stream));
+      if (noise) KP_CUDA(cudaMemcpyAsync(noise, de, bnn * sizeof(double), cudaMemcpyDeviceToHost, ctx().stream));
+    }
+    if (noise_norms) dnorm.download(noise_norms, batch);
+    sync();
+  })
+}
+// std::mt19937_64 on the device (test hook): count raw outputs per seed
+int kp_rng_raw(const unsigned long long* seeds, int batch, long count, unsigned long long* out) {
+  KP_API({
+    if (!seeds || !out || batch < 1 || count < 0) throw InvalidArgument("rng_raw: bad arguments");
+    DBuf<uint64_t> ds(batch), dout(size_t(batch) * count);
+    KP_CUDA(cudaMemcpyAsync(ds.p, seeds, batch * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx().stream));
+    mt19937_64_raw(ds.p, batch, count, dout.p);
+    KP_CUDA(cudaMemcpyAsync(out, dout.p, size_t(batch) * count * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                            ctx().stream));
+    sync();
+  })
+}
+
 int kp_discrepancy_batch(const kp_precond* p, int batch, const double* b, const double* noise_norms,
                          double eta, double* lambdas, int* status) {
   KP_API({

@@ -87,6 +87,17 @@ void kpg_rng_uniforms(uint64_t seed, long count, double lo, double hi,
   Rng rng(seed);
   for (long i = 0; i < count; ++i) out[i] = rng.uniform(lo, hi);
 }
+// The blob parameters kpg_blob_image draws, {ci, cj, w, amp} per blob
+// (for the on-device generator, problem_dev.cu).
+void kpg_blob_params(int n, uint64_t seed, int blobs, double* out) {
+  Rng rng(seed);
+  for (int b = 0; b < blobs; ++b) {
+    out[4 * b] = rng.uniform(0.0, double(n));
+    out[4 * b + 1] = rng.uniform(0.0, double(n));
+    out[4 * b + 2] = rng.uniform(5.0, 30.0);
+    out[4 * b + 3] = rng.uniform();
+  }
+}
 
 // make_psf (deblur.cpp:130-155). kind: 0 gaussian, 1 defocus, 2 motion
 // (45-degree diagonal), 3 shake, 4 speckle. out: np*np column-major.

@@ -165,6 +165,42 @@ def make_test_problem(image: np.ndarray, psf: Psf, noise_level: float, seed: int
     return TestProblem(a, x_true, b_true, noise, b, noise_level, seed, psf, n)
 
 
+def make_test_problems_device(a: KroneckerSum, image_seeds, noise_seeds, noise_levels, blobs: int = 20,
+                              device_out=None):
+    """make_test_problem (deblur.cpp:201-229) for a batch of blob images on
+    the device (kp_generate_test_problems): returns (x_true, b, noise,
+    noise_norms) as batch x n^2 host arrays, or writes x_true / b into the
+    caller's device buffers `device_out = (x_ptr, b_ptr)` and returns the
+    noise norms only."""
+    n = a.n
+    batch = len(image_seeds)
+    seeds = np.ascontiguousarray(np.asarray(image_seeds, dtype=np.uint64))
+    nseeds = np.ascontiguousarray(np.asarray(noise_seeds, dtype=np.uint64))
+    lev = np.ascontiguousarray(np.asarray(noise_levels, dtype=np.float64))
+    if nseeds.size != batch or lev.size != batch:
+        raise ValueError("make_test_problems_device: one noise seed and level per image")
+    norms = np.empty(batch)
+    from ._lib import check
+    L = lib()
+    if device_out is not None:
+        check(L.kp_generate_test_problems(a.handle(), batch, seeds.ctypes.data, blobs, nseeds.ctypes.data,
+                                          ptr(lev), device_out[0], device_out[1], None, ptr(norms), 1))
+        return norms
+    x, b, e = np.empty((batch, n * n)), np.empty((batch, n * n)), np.empty((batch, n * n))
+    check(L.kp_generate_test_problems(a.handle(), batch, seeds.ctypes.data, blobs, nseeds.ctypes.data,
+                                      ptr(lev), ptr(x), ptr(b), ptr(e), ptr(norms), 0))
+    return x, b, e, norms
+
+
+def rng_raw_device(seeds, count: int) -> np.ndarray:
+    """std::mt19937_64 outputs on the device (count per seed)."""
+    from ._lib import check
+    s = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+    out = np.empty((s.size, count), dtype=np.uint64)
+    check(lib().kp_rng_raw(s.ctypes.data, s.size, count, out.ctypes.data))
+    return out
+
+
 def host_svd(a: np.ndarray):
     """LAPACK dgesdd (same backend the device path uses for its setup)."""
     a = f64(a)
