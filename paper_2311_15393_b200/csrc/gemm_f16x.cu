@@ -109,6 +109,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#ifndef KP_F16X_SUSPEND
+#define KP_F16X_SUSPEND 0
+#endif
+// Epilogue waits: with a suspend-time hint the waiting warp sleeps until the
+// phase completes instead of re-polling (the polls take issue slots from the
+// warps doing the tree adds on the same sub-partition).
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+#if KP_F16X_SUSPEND
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity), "n"(KP_F16X_SUSPEND)
+      : "memory");
+#else
+  mbar_wait(bar, parity);
+#endif
+}
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
@@ -340,7 +358,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t p01[4], v64[4];
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          mbar_wait(my_tfull, tphase);
+          mbar_wait_sleep(my_tfull, tphase);
           tphase ^= 1;
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           // 16-leaf trees of outputs (2p, 2p+1): leaves kl = 0..15 sit in
