@@ -872,6 +872,18 @@ def main():
                                   "n^3 adds on the f16x2 pipe bound the 2 n^3 ops",
                    "work_per_launch": f"{half_ops:.4g} half-ops", "launches": pm_launches,
                    "ms_per_launch": pm_ms / pm_launches if pm_launches else None}
+        # the tensor-pipe view: every rounded leaf is one column of a K = 16
+        # kind::f16 MMA (16 MACs), so the MMAs issue 32 n^3 flop per launch
+        pk = peaks()
+        exp_tf = 32.0 * float(n) ** 3 / (pm_ms / pm_launches / 1e3) / 1e12 if pm_launches else 0.0
+        pm_line["tensor_pipe"] = {
+            "issued_mma_tflops": exp_tf, "frac_of_bf16_burst": exp_tf / pk["bf16_tflops"],
+            "frac_of_bf16_sustained": exp_tf / pk["bf16_tflops_sustained"],
+            "useful_frac_of_bf16_burst": pm_ach / pk["bf16_tflops"],
+            "note": "the MMAs form the n^3 rounded products (one live k per B column); the n^3 rounded "
+                    "tree adds cannot run on the tensor pipe (fp32 accumulation has no per-add "
+                    "binary16 rounding), so the f16x2 add rate is the ceiling (ncu: tensor pipe 34 % "
+                    "busy, profiles/r02_ncu_f16x.txt)"}
     else:
         pm_line = {"bound": "compute", "pipe": "f16x2 CUDA-core FMA pipe (reference-exact rounding "
                                               "needs a binary16 rounding per product and per sum)",

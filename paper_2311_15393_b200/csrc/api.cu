@@ -2435,20 +2435,10 @@ int kp_discrepancy_batch(const kp_precond* p, int batch, const double* b, const 
                     std::vector<double>& out) {
       const int B = int(act.size());
       DBuf<double> dl(size_t(B) * m), sums(size_t(B) * m * 2);
+      DBuf<int> didx(B);
       dl.upload(lam.data(), size_t(B) * m);
-      // images of `act` are contiguous in bhat only when all are active: use a
-      // compacted copy of their coefficients otherwise
-      const double* bh = bhat.p;
-      DBuf<double> comp;
-      bool all = B == batch;
-      if (!all) {
-        comp.alloc(size_t(B) * nn);
-        for (int q = 0; q < B; ++q)
-          KP_CUDA(cudaMemcpyAsync(comp.p + size_t(q) * nn, bhat.p + size_t(act[q]) * nn, nn * sizeof(double),
-                                  cudaMemcpyDeviceToDevice, ctx().stream));
-        bh = comp.p;
-      }
-      spectral_sums(SK_RESID, sh.d_s_r.p, sh.d_s_c.p, bh, nullptr, n, dl.p, m, 0.0, sums.p, B);
+      KP_CUDA(cudaMemcpyAsync(didx.p, act.data(), B * sizeof(int), cudaMemcpyHostToDevice, ctx().stream));
+      spectral_sums(SK_RESID, sh.d_s_r.p, sh.d_s_c.p, bhat.p, nullptr, n, dl.p, m, 0.0, sums.p, B, didx.p);
       std::vector<double> hsum(size_t(B) * m * 2);
       sums.download(hsum.data(), hsum.size());
       sync();

@@ -625,14 +625,15 @@ __global__ void cgls_next_kernel(DevState* st) {
 template <int LC, int KIND>
 __global__ void spectral_sums_kernel(const double* s_r, const double* s_c, const double* bhat,
                                      const double* xhat, int n, const double* lambdas, int m,
-                                     double omega, double* part) {
+                                     double omega, double* part, const int* img_index) {
   pdl_wait();
-  {  // batch image blockIdx.y: its own coefficients, lambdas and partials
-    const size_t img = blockIdx.y;
+  {  // batch row blockIdx.y: its own lambdas and partials; the coefficients of
+     // image img_index[y] (or y)
+    const size_t row = blockIdx.y, img = img_index ? size_t(img_index[row]) : row;
     bhat += img * size_t(n) * n;
     if (xhat) xhat += img * size_t(n) * n;
-    lambdas += img * m;
-    part += img * size_t(m) * gridDim.x * 2;
+    lambdas += row * m;
+    part += row * size_t(m) * gridDim.x * 2;
   }
   __shared__ double red[VEC_THREADS / 32][2 * LC];
   const size_t nn = size_t(n) * n;
@@ -870,31 +871,32 @@ void spectral_filter(const double* s_r, const double* s_c, int n, double l2, dou
 
 template <int KIND>
 void launch_sums(const double* s_r, const double* s_c, const double* bhat, const double* xhat,
-                 int n, const double* lambdas, int m, double omega, double* part, int batch) {
+                 int n, const double* lambdas, int m, double omega, double* part, int batch,
+                 const int* img_index) {
   // lambdas per pass: 1, 4 (the discrepancy look-ahead's 3) or LCHUNK; every
   // value is summed in the same element order whatever the width
   const dim3 grid(VEC_CTAS, batch);
   if (m == 1)
     KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<1, KIND>), grid, VEC_THREADS, s_r, s_c, bhat,
-              xhat, n, lambdas, m, omega, part);
+              xhat, n, lambdas, m, omega, part, img_index);
   else if (m <= 4)
     KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<4, KIND>), grid, VEC_THREADS, s_r, s_c, bhat,
-              xhat, n, lambdas, m, omega, part);
+              xhat, n, lambdas, m, omega, part, img_index);
   else
     KP_LAUNCH(KC_SPECTRAL, (spectral_sums_kernel<LCHUNK, KIND>), grid, VEC_THREADS, s_r, s_c,
-              bhat, xhat, n, lambdas, m, omega, part);
+              bhat, xhat, n, lambdas, m, omega, part, img_index);
 }
 
 void spectral_sums(int kind, const double* s_r, const double* s_c, const double* bhat,
                    const double* xhat, int n, const double* lambdas, int m, double omega,
-                   double* out, int batch) {
+                   double* out, int batch, const int* img_index) {
   DBuf<double> part(size_t(batch) * m * VEC_CTAS * 2);
   switch (kind) {
-    case SK_GCV: launch_sums<SK_GCV>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch); break;
-    case SK_RESID: launch_sums<SK_RESID>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch); break;
-    case SK_OPT: launch_sums<SK_OPT>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch); break;
-    case SK_WGCV: launch_sums<SK_WGCV>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch); break;
-    case SK_WTRACE: launch_sums<SK_WTRACE>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch); break;
+    case SK_GCV: launch_sums<SK_GCV>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch, img_index); break;
+    case SK_RESID: launch_sums<SK_RESID>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch, img_index); break;
+    case SK_OPT: launch_sums<SK_OPT>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch, img_index); break;
+    case SK_WGCV: launch_sums<SK_WGCV>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch, img_index); break;
+    case SK_WTRACE: launch_sums<SK_WTRACE>(s_r, s_c, bhat, xhat, n, lambdas, m, omega, part.p, batch, img_index); break;
     default: throw InvalidArgument("spectral_sums: bad kind");
   }
   // one finishing block per (image, lambda) row, in the same fixed order

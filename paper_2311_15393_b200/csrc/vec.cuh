@@ -127,10 +127,11 @@ enum SpectralKind {
 };
 // c(i,j) *= sigma / (sigma^2 + l2) (filtered_solution coefficients), device
 void spectral_filter(const double* s_r, const double* s_c, int n, double l2, double* c);
-// batch > 1: `batch` images (bhat / xhat at image * n^2, lambdas at image *
-// m, out rows image * m + q), each summed exactly as a single call would.
+// batch > 1: `batch` rows (lambdas at row * m, out rows row * m + q) over
+// the coefficients of image img_index[row] (device; nullptr: image = row) at
+// image * n^2, each summed exactly as a single call would.
 void spectral_sums(int kind, const double* s_r, const double* s_c, const double* bhat,
                    const double* xhat, int n, const double* lambdas, int m, double omega,
-                   double* out, int batch = 1);
+                   double* out, int batch = 1, const int* img_index = nullptr);
 
 }  // namespace kp
