@@ -1,7 +1,7 @@
 mkdir -p gpurun_out/r02v
 exec > gpurun_out/r02v/log.txt 2>&1
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC"
-for v in "-DKP_F16X_DUAL=1" "" "-DKP_F16X_DUAL=1"; do
+for v in "-DKP_F16X_TESTWAIT=1" "" "-DKP_F16X_TESTWAIT=1"; do
   $NV $v -c paper_2311_15393_b200/csrc/gemm_f16x.cu -o paper_2311_15393_b200/_build/gemm_f16x.cu.o 2>/dev/null && python -c "from paper_2311_15393_b200 import build; build.build_library()"
   VARIANT="$v" timeout 300 python tools/f16x_quick.py 2>&1 | tail -1
 done
