@@ -132,3 +132,28 @@ def test_c5_cgls_first_iterates_1e10():
     for k in range(len(g["residual_norm"])):
         assert res.history.residual_norm[k] == pytest.approx(g["residual_norm"][k], rel=1e-10)
         assert res.history.relative_error[k] == pytest.approx(g["relative_error"][k], rel=1e-10)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_lp_matmul_random_shapes_bitwise(engine, seed):
+    """Ragged shapes (M, N not multiples of the tiles, K not a multiple of
+    64, K = 1, single rows / columns) and mixed magnitudes incl. signed zeros,
+    subnormal products and a few infinities in B (A must stay finite for
+    gemm_f16x, see gemm_f16x.cu): both engines against the oracle, bit for
+    bit."""
+    rng = np.random.default_rng(1000 + seed)
+    m, k, n = (int(x) for x in rng.integers(1, 300, 3))
+    if seed == 0:
+        m, k, n = 1, 1, 1
+    elif seed == 1:
+        k = 1
+    scale_a = 2.0 ** rng.integers(-14, 6, (m, k))
+    scale_b = 2.0 ** rng.integers(-14, 6, (k, n))
+    a = f16(rng.standard_normal((m, k)) * scale_a)
+    b = f16(rng.standard_normal((k, n)) * scale_b)
+    a[rng.random((m, k)) < 0.05] = -0.0
+    b[rng.random((k, n)) < 0.05] = 0.0
+    if seed % 3 == 2:
+        b[rng.random((k, n)) < 0.01] = np.inf
+    c = K.lp_matmul(a, b, H)
+    assert same_bits(c, O.lp_matmul(a, b, H))
