@@ -758,6 +758,17 @@ void batch_status(const DevState* st, int count, DevState* out) {
   check_launch("batch_status");
 }
 
+// Threads of a single-block scalar kernel summing `parts` partial slots: one
+// slot per thread up to 1024 (a 32-slot sum needs one warp, not 32 — these
+// kernels sit on every iteration's critical path at small n). A function of
+// the slot counts only, so batched and single solves reduce identically.
+static unsigned scalar_threads(int parts, int parts2 = 0) {
+  const int p = parts > parts2 ? parts : parts2;
+  unsigned t = 32;
+  while (t < unsigned(p) && t < unsigned(SCALAR_THREADS)) t <<= 1;
+  return t;
+}
+
 void vec_copy(double* dst, const double* src, size_t n, const int* status) {
   KP_LAUNCH(KC_VECTOR, copy_kernel, vec_grid(n), VEC_THREADS, dst, src, n, status);
 }
@@ -795,13 +806,13 @@ void msolve_finish_f16(const __half* z16, long ldh, int n, double* z, const doub
 
 void pcg_init_scalar(DevState* st, DevHistory h, const double* part_r, int nr,
                      const double* part_xt, int nxt, int batch) {
-  KP_LAUNCH(KC_VECTOR, pcg_init_scalar_kernel, batch, SCALAR_THREADS, st, h, part_r, nr, part_xt, nxt);
+  KP_LAUNCH(KC_VECTOR, pcg_init_scalar_kernel, batch, scalar_threads(nr, nxt), st, h, part_r, nr, part_xt, nxt);
 }
 void pcg_init_msolve_scalar(DevState* st, const double* part_z, int nz, int batch) {
-  KP_LAUNCH(KC_VECTOR, pcg_init_msolve_scalar_kernel, batch, SCALAR_THREADS, st, part_z, nz);
+  KP_LAUNCH(KC_VECTOR, pcg_init_msolve_scalar_kernel, batch, scalar_threads(nz), st, part_z, nz);
 }
 void pcg_alpha_scalar(DevState* st, const double* part_pq, int n, int batch) {
-  KP_LAUNCH(KC_VECTOR, pcg_alpha_scalar_kernel, batch, SCALAR_THREADS, st, part_pq, n);
+  KP_LAUNCH(KC_VECTOR, pcg_alpha_scalar_kernel, batch, scalar_threads(n), st, part_pq, n);
 }
 
 int pcg_update_ctas(int n) {
@@ -823,10 +834,10 @@ void pcg_update(DevState* st, DevHistory h, double* x, double* r, double* r_prev
               q, z, xt, r16, n, ldh, partials);
 }
 void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n, int batch) {
-  KP_LAUNCH(KC_VECTOR, pcg_resid_scalar_kernel, batch, SCALAR_THREADS, st, h, part, n);
+  KP_LAUNCH(KC_VECTOR, pcg_resid_scalar_kernel, batch, scalar_threads(n), st, h, part, n);
 }
 void pcg_beta_scalar(DevState* st, const double* part_z, int n, int batch) {
-  KP_LAUNCH(KC_VECTOR, pcg_beta_scalar_kernel, batch, SCALAR_THREADS, st, part_z, n);
+  KP_LAUNCH(KC_VECTOR, pcg_beta_scalar_kernel, batch, scalar_threads(n), st, part_z, n);
 }
 void pcg_p_update(DevState* st, double* p, const double* z, size_t nn, int batch) {
   const bool vec2 = nn % 2 == 0 && al16(p) && al16(z);
@@ -835,10 +846,10 @@ void pcg_p_update(DevState* st, double* p, const double* z, size_t nn, int batch
 
 void cgls_init_scalar(DevState* st, DevHistory h, const double* part_s, int ns,
                       const double* part_xt, int nxt) {
-  KP_LAUNCH(KC_VECTOR, cgls_init_scalar_kernel, 1, SCALAR_THREADS, st, h, part_s, ns, part_xt, nxt);
+  KP_LAUNCH(KC_VECTOR, cgls_init_scalar_kernel, 1, scalar_threads(ns, nxt), st, h, part_s, ns, part_xt, nxt);
 }
 void cgls_alpha_scalar(DevState* st, const double* part_q, int nq, const double* part_p, int np) {
-  KP_LAUNCH(KC_VECTOR, cgls_alpha_scalar_kernel, 1, SCALAR_THREADS, st, part_q, nq, part_p, np);
+  KP_LAUNCH(KC_VECTOR, cgls_alpha_scalar_kernel, 1, scalar_threads(nq, np), st, part_q, nq, part_p, np);
 }
 void cgls_update(DevState* st, DevHistory h, double* x, double* rt, const double* p,
                  const double* q, const double* xt, size_t nn, double* partials) {
@@ -851,7 +862,7 @@ void cgls_update(DevState* st, DevHistory h, double* x, double* rt, const double
 }
 void cgls_resid_scalar(DevState* st, DevHistory h, const double* part_s, int ns,
                        const double* part_x, int nx) {
-  KP_LAUNCH(KC_VECTOR, cgls_resid_scalar_kernel, 1, SCALAR_THREADS, st, h, part_s, ns, part_x, nx);
+  KP_LAUNCH(KC_VECTOR, cgls_resid_scalar_kernel, 1, scalar_threads(ns, nx), st, h, part_s, ns, part_x, nx);
 }
 void cgls_p_update(DevState* st, double* p, const double* s, double* s_prev, size_t nn,
                    double* partials) {
