@@ -808,8 +808,9 @@ void gemm_f16x(const F16GemmArgs& a_in, int kernel_class) {
   const int grid = std::min(tiles, ctx().num_sms);
   {
     LaunchScope scope(kernel_class);
-    static const int xflags = [] { const char* e = getenv("KP_F16X_XFLAGS"); return e ? atoi(e) : 0; }();
-    launch_pdl(gemm_f16x_kernel, dim3(grid), dim3(NUM_THREADS), smem, ma, mb, a, levels, xflags);
+    // xflags: ablation switches of the profiling experiments (skip the TMA
+    // waits / the expansion / per-group B slices); always 0 here
+    launch_pdl(gemm_f16x_kernel, dim3(grid), dim3(NUM_THREADS), smem, ma, mb, a, levels, 0);
     check_launch("gemm_f16x");
   }
   {
