@@ -238,7 +238,10 @@ __global__ void __launch_bounds__(A_THREADS, KP_BAND_A_MINB) band_cols_kernel(co
 // double-buffered with cp.async so term k+1 streams in while term k's
 // correlation runs.
 template <int TAPS>
-__global__ void __launch_bounds__(B_THREADS) band_rows_kernel(const double* __restrict__ Y, int n,
+// 41 taps (C5): held to 64 registers (4 CTAs / SM; unconstrained, the
+// batched epilogue's pointers took it to 82 and 2 CTAs / SM: 0.28 -> 0.38 ms
+// per pass); the shorter bands measured best unconstrained.
+__global__ void __launch_bounds__(B_THREADS, TAPS == 41 ? 4 : 1) band_rows_kernel(const double* __restrict__ Y, int n,
                                                               int r, const __grid_constant__ BandTaps t,
                                                               const F64Epilogue e,
                                                               const int* status) {
