@@ -237,18 +237,20 @@ __global__ void __launch_bounds__(A_THREADS, KP_BAND_A_MINB) band_cols_kernel(co
 // Pass B. The Y_k tiles (B_TJ + taps - 1 columns of B_TA rows) are
 // double-buffered with cp.async so term k+1 streams in while term k's
 // correlation runs.
-template <int TAPS>
+template <int TAPS, bool BATCH>
 // 41 taps (C5): held to 64 registers (4 CTAs / SM; unconstrained, the
 // batched epilogue's pointers took it to 82 and 2 CTAs / SM: 0.28 -> 0.38 ms
-// per pass); the shorter bands measured best unconstrained.
-__global__ void __launch_bounds__(B_THREADS, TAPS == 41 ? 4 : 1) band_rows_kernel(const double* __restrict__ Y, int n,
+// per pass); the shorter bands measured best unconstrained (min blocks 0 =
+// no occupancy target: 64 / 64 / 55 registers at 31 / 19 / 17 taps, where
+// a target of 1 let ptxas take 85).
+__global__ void __launch_bounds__(B_THREADS, TAPS == 41 ? 4 : 0) band_rows_kernel(const double* __restrict__ Y, int n,
                                                               int r, const __grid_constant__ BandTaps t,
                                                               const F64Epilogue e,
                                                               const int* status) {
   pdl_wait();
   if (stopped(status)) return;
   extern __shared__ double sm[];
-  Y += size_t(blockIdx.z) * r * n * n;  // batched images (grid.z)
+  if (BATCH) Y += size_t(blockIdx.z) * r * n * n;  // batched images (grid.z)
   const int rows = (TAPS > 0 ? TAPS : t.taps) + B_TJ - 1;  // rows loaded
   const int buf_doubles = rows_halo<TAPS>(t.taps) * B_TA;
   const int a0 = blockIdx.y * B_TA, j0 = blockIdx.x * B_TJ;
@@ -319,27 +321,48 @@ __global__ void __launch_bounds__(B_THREADS, TAPS == 41 ? 4 : 1) band_rows_kerne
   // epilogue (same contract as the GEMM epilogue; image blockIdx.z)
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
   const int m = a0 + a;
-  const long zo = long(blockIdx.z) * e.img;
-  double* const C = e.C + zo;
-  const double* const mul = e.mul ? e.mul + zo : nullptr;
-  const double* const addv = e.addv ? e.addv + zo : nullptr;
-  const double addc = e.addc_img ? e.addc_img[blockIdx.z] : e.addc;
-  const double* const d0 = e.d0 ? e.d0 + zo : nullptr;
-  const double* const d1a = e.d1a ? e.d1a + zo : nullptr;
-  const double* const d1b = e.d1b ? e.d1b + zo : nullptr;
+  if constexpr (!BATCH) {
+    // single image: the epilogue reads e.* straight from the parameter bank
+    // (copying the pointers into locals costs registers and, at 41 taps,
+    // occupancy)
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int j = j0 + 8 * jq + q;
-    if (m >= n || j >= n) continue;
-    double v = acc[q];
-    const long vi = long(m) * e.vm + long(j) * e.vn;
-    if (mul) v *= mul[vi];
-    if (addv) v = __dadd_rn(v, __dmul_rn(addc, addv[vi]));  // + lambda^2 p, unfused as Eigen
-    C[long(m) * e.cm + long(j) * e.cn] = v;
-    if (e.partials) {
-      if (e.d0) s0 += v * (e.d0_self ? v : d0[vi]);
-      if (d1a) s1 += v * (d1b ? (d1a[vi] - d1b[vi]) : d1a[vi]);
-      if (e.count_nonfinite && !isfinite(v)) s2 += 1.0;
+    for (int q = 0; q < 8; ++q) {
+      const int j = j0 + 8 * jq + q;
+      if (m >= n || j >= n) continue;
+      double v = acc[q];
+      const long vi = long(m) * e.vm + long(j) * e.vn;
+      if (e.mul) v *= e.mul[vi];
+      if (e.addv) v = __dadd_rn(v, __dmul_rn(e.addc, e.addv[vi]));  // + lambda^2 p, unfused as Eigen
+      e.C[long(m) * e.cm + long(j) * e.cn] = v;
+      if (e.partials) {
+        if (e.d0) s0 += v * (e.d0_self ? v : e.d0[vi]);
+        if (e.d1a) s1 += v * (e.d1b ? (e.d1a[vi] - e.d1b[vi]) : e.d1a[vi]);
+        if (e.count_nonfinite && !isfinite(v)) s2 += 1.0;
+      }
+    }
+  } else {
+    const long zo = long(blockIdx.z) * e.img;
+    double* const C = e.C + zo;
+    const double* const mul = e.mul ? e.mul + zo : nullptr;
+    const double* const addv = e.addv ? e.addv + zo : nullptr;
+    const double addc = e.addc_img ? e.addc_img[blockIdx.z] : e.addc;
+    const double* const d0 = e.d0 ? e.d0 + zo : nullptr;
+    const double* const d1a = e.d1a ? e.d1a + zo : nullptr;
+    const double* const d1b = e.d1b ? e.d1b + zo : nullptr;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = j0 + 8 * jq + q;
+      if (m >= n || j >= n) continue;
+      double v = acc[q];
+      const long vi = long(m) * e.vm + long(j) * e.vn;
+      if (mul) v *= mul[vi];
+      if (addv) v = __dadd_rn(v, __dmul_rn(addc, addv[vi]));
+      C[long(m) * e.cm + long(j) * e.cn] = v;
+      if (e.partials) {
+        if (e.d0) s0 += v * (e.d0_self ? v : d0[vi]);
+        if (d1a) s1 += v * (d1b ? (d1a[vi] - d1b[vi]) : d1a[vi]);
+        if (e.count_nonfinite && !isfinite(v)) s2 += 1.0;
+      }
     }
   }
   if (e.partials) {
@@ -356,7 +379,8 @@ __global__ void __launch_bounds__(B_THREADS, TAPS == 41 ? 4 : 1) band_rows_kerne
     if (threadIdx.x == 0) {
       double x0 = 0, x1 = 0, x2 = 0;
       for (int w = 0; w < B_THREADS / 32; ++w) x0 += red[w][0], x1 += red[w][1], x2 += red[w][2];
-      double* o = e.partials + (long(blockIdx.z) * e.part_img + long(blockIdx.y) * gridDim.x + blockIdx.x) * 4;
+      double* o = e.partials + ((BATCH ? long(blockIdx.z) * e.part_img : 0L) + long(blockIdx.y) * gridDim.x +
+                                blockIdx.x) * 4;
       o[0] = x0, o[1] = x1, o[2] = x2, o[3] = 0.0;
     }
   }
@@ -529,7 +553,7 @@ struct RowsLaunch {
   static void run(const double* Y, int n, int r, const BandTaps& t, const F64Epilogue& e,
                   const int* status, int batch) {
     const size_t smem = 2 * size_t(rows_halo<TAPS>(t.taps)) * B_TA * sizeof(double);  // two buffers
-    auto k = band_rows_kernel<TAPS>;
+    auto k = batch > 1 ? band_rows_kernel<TAPS, true> : band_rows_kernel<TAPS, false>;
     set_smem_limit(reinterpret_cast<const void*>(k), smem);
     dim3 grid(cdiv(n, B_TJ), cdiv(n, B_TA), batch);
     launch_pdl(k, grid, dim3(B_THREADS), smem, Y, n, r, t, e, status);

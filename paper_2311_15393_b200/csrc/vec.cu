@@ -260,7 +260,7 @@ __global__ void pcg_alpha_scalar_kernel(DevState* st, const double* part, int n)
 // elements of a pair lie in the same column, so the binary16 copy of r is a
 // single half2 store into the padded B-operand layout (row l, ldh stride).
 template <bool VEC2>
-__global__ void pcg_update_kernel(const DevState* st, DevHistory h, double* x, double* r,
+__global__ void __launch_bounds__(VEC_THREADS, 4) pcg_update_kernel(const DevState* st, DevHistory h, double* x, double* r,
                                   double* r_prev, const double* p, const double* q,
                                   const double* z, const double* xt, __half* r16, int n,
                                   long ldh, double* part) {
