@@ -142,6 +142,11 @@ int kp_profile_enable(int on);
 int kp_profile_read(int kernel_class, double* total_ms, long long* launches);
 int kp_profile_reset(void);
 long long kp_launch_count(void);   /* kernels launched by this library (all threads) */
+/* How solves ran their iterations: as one device-side loop (a CUDA graph
+ * with a WHILE conditional node; the default) or as host-polled graph
+ * replays (profiled solves, KP_GRAPH_LOOP=0, or a loop graph that could not
+ * be built). Counts since load, all threads. */
+int kp_drive_stats(long long* loop_solves, long long* polled_solves);
 /* Process-wide engine for reference-exact binary16 products (see above);
  * kp_get_fp16_products reports whether size n would use the tensor engine. */
 int kp_set_fp16_products(int mode);

@@ -66,7 +66,7 @@ class kp_param_choice(C.Structure):
 EXPORTS = [
     "kp_last_error", "kp_init", "kp_synchronize", "kp_device_alloc", "kp_device_free",
     "kp_memcpy_h2d", "kp_memcpy_d2h", "kp_profile_enable", "kp_profile_read",
-    "kp_profile_reset", "kp_launch_count", "kp_operator_create", "kp_operator_destroy",
+    "kp_profile_reset", "kp_launch_count", "kp_drive_stats", "kp_operator_create", "kp_operator_destroy",
     "kp_operator_info", "kp_kronsum_apply", "kp_kronsum_apply_transpose", "kp_normal_matvec",
     "kp_precond_build", "kp_precond_build_from_svd", "kp_precond_with_lambda",
     "kp_precond_destroy", "kp_precond_solve", "kp_precond_export", "kp_precond_info",
@@ -101,6 +101,7 @@ def lib() -> C.CDLL:
             "kp_profile_enable": ([I], I),
             "kp_profile_read": ([I, C.POINTER(D), C.POINTER(C.c_longlong)], I),
             "kp_profile_reset": ([], I), "kp_launch_count": ([], C.c_longlong),
+            "kp_drive_stats": ([C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)], I),
             "kp_operator_create": ([I, I, P, P, C.POINTER(V)], I),
             "kp_operator_destroy": ([P], I),
             "kp_operator_info": ([P, C.POINTER(I), C.POINTER(I)], I),

@@ -10,6 +10,7 @@ from __future__ import annotations
 import concurrent.futures as cf
 import glob
 import os
+import shlex
 import shutil
 import subprocess
 import sys
@@ -77,6 +78,7 @@ def build_library(verbose: bool = False, force: bool = False) -> str:
             extra = ["-fmad=false"] if os.path.basename(src) in NO_FMAD else []
             jobs.append([NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                          "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3", *extra,
+                         *shlex.split(os.environ.get("KP_NVCC_EXTRA", "")),  # A/B variant builds
                          "-c", src, "-o", obj])
     for src in cpp:
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")

@@ -55,6 +55,7 @@ Ctx& ctx() {
 }
 
 std::atomic<long long> g_launches{0};
+std::atomic<long long> g_loop_solves{0}, g_polled_solves{0};  // drive() modes (kp_drive_stats)
 
 void ensure_init() {
   Ctx& c = ctx();
@@ -131,6 +132,22 @@ static void profile_collect() {
 }
 
 static void sync() { KP_CUDA(cudaStreamSynchronize(ctx().stream)); }
+
+// Device-side solve loop (drive()): the condition of the WHILE graph node is
+// "status still RUNNING"; `count` counts the bodies run (reset by the head
+// node) and bounds the loop at `limit` bodies whatever the status says.
+__global__ void loop_cond_kernel(cudaGraphConditionalHandle h, const int* status, int* count, int limit,
+                                 int head) {
+  pdl_wait();
+  const int c = head ? 0 : *count + 1;
+  *count = c;
+  cudaGraphSetConditional(h, (*status == ST_RUNNING && c < limit) ? 1u : 0u);
+}
+static void loop_cond(cudaGraphConditionalHandle h, const int* status, int* count, int limit, bool head) {
+  LaunchScope scope(KC_VECTOR);
+  launch_pdl(loop_cond_kernel, dim3(1), dim3(1), 0, h, status, count, limit, head ? 1 : 0);
+  check_launch("solve loop condition");
+}
 
 // ============================================================================
 // small device helpers
@@ -241,8 +258,15 @@ struct SolverWorkspace {
   int* poll = nullptr;
   cudaEvent_t poll_ev[2] = {nullptr, nullptr};
   cudaGraphExec_t exec = nullptr;  // last solve's iteration graph (drive())
+  cudaGraphExec_t exec_loop = nullptr;  // last solve's device-loop graph (drive())
+  DBuf<int> loop_count;                 // bodies run by the device loop
+  int* loop_counter() {
+    if (!loop_count.p) loop_count.alloc(1);
+    return loop_count.p;
+  }
   ~SolverWorkspace() {
     if (exec) cudaGraphExecDestroy(exec);
+    if (exec_loop) cudaGraphExecDestroy(exec_loop);
     if (host_state) cudaFreeHost(host_state);
     if (host_bstates) cudaFreeHost(host_bstates);
     if (poll) cudaFreeHost(poll);
@@ -852,8 +876,106 @@ void setup_state(Solve& s, const kp_solver_options* o, bool has_xt, bool flexibl
 // profiling the iteration is captured once into a CUDA graph and replayed;
 // the host polls the status word in growing chunks (overshoot iterations are
 // device no-ops).
+// The whole iteration loop as ONE graph launch: a head kernel sets the
+// condition from the status word, a WHILE conditional node replays the
+// captured iteration (+ a one-thread kernel that re-evaluates the condition)
+// until the status leaves RUNNING — no host polls, no overshoot iterations.
+// Returns false (nothing enqueued) when the graph cannot be built, e.g. an
+// iteration whose capture holds a node type conditional bodies do not allow;
+// drive() then falls back to host-polled replay.
+bool drive_loop(Solve& s, int maxit, const std::function<void()>& iteration) {
+  Ctx& c = ctx();
+  SolverWorkspace& ws = s.op->ws;
+  int* count = ws.loop_counter();
+  const int* status = &s.st->status;
+  const int limit = maxit + 2;  // the state machine stops at maxit; this only guards
+  cudaGraph_t g = nullptr;
+  KP_CUDA(cudaGraphCreate(&g, 0));
+  const long long before = c.launches;
+  long long body_launches = 0;
+  cudaGraphConditionalHandle h;
+  auto fail = [&]() {
+    cudaGetLastError();
+    if (g) cudaGraphDestroy(g);
+    g_launches.fetch_sub(c.launches - before, std::memory_order_relaxed);  // captured, not launched
+    c.launches = before;
+    return false;
+  };
+  if (cudaGraphConditionalHandleCreate(&h, g, 0, 0) != cudaSuccess) return fail();
+  if (cudaStreamBeginCaptureToGraph(c.stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+      cudaSuccess)
+    return fail();
+  cudaGraph_t cap = nullptr;
+  try {
+    loop_cond(h, status, count, limit, true);
+  } catch (...) {
+    cudaStreamEndCapture(c.stream, &cap);
+    throw;
+  }
+  if (cudaStreamEndCapture(c.stream, &cap) != cudaSuccess) return fail();
+  cudaGraphNode_t head;
+  size_t nnodes = 1;
+  if (cudaGraphGetNodes(g, &head, &nnodes) != cudaSuccess || nnodes != 1) return fail();
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t loop;
+  if (cudaGraphAddNode(&loop, g, &head, 1, &cp) != cudaSuccess) return fail();
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  if (cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+      cudaSuccess)
+    return fail();
+  const long long body0 = c.launches;
+  try {
+    iteration();
+    loop_cond(h, status, count, limit, false);
+  } catch (...) {
+    cudaStreamEndCapture(c.stream, &cap);
+    fail();
+    throw;
+  }
+  body_launches = c.launches - body0;
+  if (cudaStreamEndCapture(c.stream, &cap) != cudaSuccess) return fail();
+  if (ws.exec_loop) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(ws.exec_loop, g, &info) != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphExecDestroy(ws.exec_loop);
+      ws.exec_loop = nullptr;
+    }
+  }
+  if (!ws.exec_loop && cudaGraphInstantiate(&ws.exec_loop, g, 0) != cudaSuccess) {
+    ws.exec_loop = nullptr;
+    return fail();
+  }
+  cudaGraphDestroy(g);
+  g = nullptr;
+  // captured launches are counted when they run: head + body x bodies run
+  g_launches.fetch_sub(c.launches - before, std::memory_order_relaxed);
+  c.launches = before;
+  KP_CUDA(cudaGraphLaunch(ws.exec_loop, c.stream));
+  int* slot = ws.poll_slots();
+  KP_CUDA(cudaMemcpyAsync(slot, count, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  sync();
+  const long long ran = 1 + body_launches * (long long)slot[0];
+  c.launches += ran;
+  g_launches.fetch_add(ran, std::memory_order_relaxed);
+  g_loop_solves.fetch_add(1, std::memory_order_relaxed);
+  if (slot[0] >= limit) throw std::runtime_error("solver: device loop guard reached (status never left RUNNING)");
+  return true;
+}
+
+static bool loop_graphs_enabled() {  // read per solve (tests switch it)
+  const char* e = getenv("KP_GRAPH_LOOP");
+  return !(e && e[0] == '0');
+}
+
 void drive(Solve& s, int maxit, const std::function<void()>& iteration) {
   Ctx& c = ctx();
+  if (!c.profile && loop_graphs_enabled() && drive_loop(s, maxit, iteration)) return;
+  g_polled_solves.fetch_add(1, std::memory_order_relaxed);
   cudaGraphExec_t exec = nullptr;
   long long per_iter_launches = 0;
   if (!c.profile) {
@@ -1740,6 +1862,12 @@ int kp_profile_read(int cls, double* total_ms, long long* launches) {
   })
 }
 long long kp_launch_count(void) { return kp::g_launches.load(); }
+int kp_drive_stats(long long* loop_solves, long long* polled_solves) {
+  KP_API({
+    if (loop_solves) *loop_solves = kp::g_loop_solves.load();
+    if (polled_solves) *polled_solves = kp::g_polled_solves.load();
+  })
+}
 int kp_set_fp16_products(int mode) {
   KP_API({
     if (mode < KP_FP16_PRODUCTS_AUTO || mode > KP_FP16_PRODUCTS_TENSOR)

@@ -90,6 +90,8 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Ar
 // with launch_pdl(), so consecutive kernels on the stream (and in the
 // captured iteration graphs) overlap one kernel's launch with the previous
 // one's tail while keeping full stream-order visibility of its results.
+// (An explicit early griddepcontrol.launch_dependents after the wait was
+// measured: C1 12.1k vs 12.8k it/s, C2 +1 %, C5 -0.5 % — not adopted.)
 __device__ __forceinline__ void pdl_wait() {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 900)
   asm volatile("griddepcontrol.wait;\n" ::: "memory");

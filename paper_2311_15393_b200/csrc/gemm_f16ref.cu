@@ -33,12 +33,14 @@
 namespace kp {
 namespace {
 
-constexpr int BM = 32, BKH = 64, THREADS = 128;
+constexpr int BKH = 64, THREADS = 128;
 constexpr int ROW_BYTES = BKH * 2;  // 128
-// BN = 64 (4 m-rows x 2 n-pairs = 8 packed accumulators per thread) or 32
-// (4 x 1; twice the CTAs and warps for problems too small to fill the SMs).
-constexpr int stage_bytes(int bn) { return (BM + bn) * ROW_BYTES; }
-constexpr int nacc(int bn) { return 4 * (bn / 32); }
+// Tiles BM x BN: BN = 64 (4 m-rows x 2 n-pairs = 8 packed accumulators per
+// thread) or 32 (4 x 1; twice the CTAs and warps for problems too small to
+// fill the SMs); BM = 32, or 16 (2 x 1) when even the 32 x 32 grid leaves SMs
+// idle (a 256 x 256 product: 128 CTAs instead of 64).
+constexpr int stage_bytes(int bm, int bn) { return (bm + bn) * ROW_BYTES; }
+constexpr int nacc(int bm, int bn) { return (bm / 8) * (bn / 32); }
 constexpr int GROUP_M = 8;
 
 __device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
@@ -83,10 +85,10 @@ __device__ __forceinline__ uint32_t part(const uint4& v, int q) {
 // shared-memory counter stack (16: levels >= 4 in smem; 32: level 4 also in
 // registers; 64: levels 4 and 5 in registers — the whole 64-leaf k-tile is
 // reduced in registers and pushed once, the smallest stack).
-template <int STAGES, int UNIT, int BN, int KS>
+template <int STAGES, int UNIT, int BN, int KS, int BM>
 __global__ void __launch_bounds__(THREADS * KS) gemm_f16ref_kernel(const F16GemmArgs args, int levels) {
   pdl_wait();
-  constexpr int NP = BN / 32, NACC = nacc(BN), STAGE_BYTES = stage_bytes(BN);
+  constexpr int NP = BN / 32, MI = BM / 8, NACC = nacc(BM, BN), STAGE_BYTES = stage_bytes(BM, BN);
   if (args.status && *args.status != 0) return;
   extern __shared__ __align__(128) unsigned char smem_all[];
   const int kgroup = KS > 1 ? int(threadIdx.x) / THREADS : 0;  // this thread's K range (split K)
@@ -169,9 +171,9 @@ __global__ void __launch_bounds__(THREADS * KS) gemm_f16ref_kernel(const F16Gemm
 #pragma unroll
     for (int sub = 0; sub < 8; ++sub) {  // 8-leaf sub-chunk = one 16-byte smem chunk
       const uint32_t ca = uint32_t(sub << 4) ^ xa, cb = uint32_t(sub << 4) ^ xb;
-      uint4 af[4], bfr[2 * NP];
+      uint4 af[MI], bfr[2 * NP];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = lds128(sa + ca + uint32_t(i * 8 * ROW_BYTES));
+      for (int i = 0; i < MI; ++i) af[i] = lds128(sa + ca + uint32_t(i * 8 * ROW_BYTES));
 #pragma unroll
       for (int j = 0; j < 2 * NP; ++j) bfr[j] = lds128(sb + cb + uint32_t(j * 16 * ROW_BYTES));
       uint32_t v8[NACC];
@@ -184,7 +186,7 @@ __global__ void __launch_bounds__(THREADS * KS) gemm_f16ref_kernel(const F16Gemm
           bhi[kp] = highs(part(bfr[2 * p], kp), part(bfr[2 * p + 1], kp));
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < MI; ++i) {
           uint32_t s4[4];
 #pragma unroll
           for (int kp = 0; kp < 4; ++kp) {
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(THREADS * KS) gemm_f16ref_kernel(const F16Gemm
   const double* const d1a = e.d1a ? e.d1a + img * e.v_img : nullptr;
   const double* const d1b = e.d1b ? e.d1b + img * e.v_img : nullptr;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int p = 0; p < NP; ++p)
 #pragma unroll
@@ -352,17 +354,28 @@ int f16ref_bn(int M, int N) {
     return e ? atoi(e) : 0;
   }();
   if (forced == 32 || forced == 64) return forced;
-  return cdiv(M, BM) * cdiv(N, 64) < 8 * ctx().num_sms ? 32 : 64;
+  return cdiv(M, 32) * cdiv(N, 64) < 8 * ctx().num_sms ? 32 : 64;
+}
+// Tile height: 16 when the 32 x 32 grid has fewer CTAs than SMs (n < ~390),
+// else 32. KP_F16REF_BM=32 forces 32.
+int f16ref_bm(int M, int N) {
+  static const int forced = [] {
+    const char* e = getenv("KP_F16REF_BM");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 32) return 32;
+  return f16ref_bn(M, N) == 32 && cdiv(M, 32) * cdiv(N, 32) < ctx().num_sms ? 16 : 32;
 }
 
-template <int STAGES, int UNIT, int BN, int KS>
+template <int STAGES, int UNIT, int BN, int KS, int BM>
 void launch_f16ref_bn(const F16GemmArgs& a, int kernel_class) {
   const int kt = (a.K + BKH - 1) / BKH / KS;
   const int units = kt * (BKH / UNIT);
   int levels = 1;
   while ((1 << levels) <= units) ++levels;
-  const size_t smem = size_t(KS) * (size_t(STAGES) * stage_bytes(BN) + size_t(levels) * nacc(BN) * THREADS * 4);
-  auto kern = gemm_f16ref_kernel<STAGES, UNIT, BN, KS>;
+  const size_t smem =
+      size_t(KS) * (size_t(STAGES) * stage_bytes(BM, BN) + size_t(levels) * nacc(BM, BN) * THREADS * 4);
+  auto kern = gemm_f16ref_kernel<STAGES, UNIT, BN, KS, BM>;
   set_smem_limit(reinterpret_cast<const void*>(kern), smem);
   LaunchScope scope(kernel_class);
   const unsigned grid = cdiv(a.M, BM) * cdiv(a.N, BN);
@@ -386,24 +399,27 @@ int f16ref_ksplit(int tiles, int K) {
   return 1;
 }
 
-template <int STAGES, int UNIT, int BN>
+template <int STAGES, int UNIT, int BN, int BM>
 void launch_f16ref_ks(const F16GemmArgs& a, int kernel_class) {
   const int tiles = int(cdiv(a.M, BM) * cdiv(a.N, BN));
   switch (f16ref_ksplit(tiles, a.K)) {
-    case 4: launch_f16ref_bn<STAGES, UNIT, BN, 4>(a, kernel_class); break;
-    case 2: launch_f16ref_bn<STAGES, UNIT, BN, 2>(a, kernel_class); break;
-    default: launch_f16ref_bn<STAGES, UNIT, BN, 1>(a, kernel_class); break;
+    case 4: launch_f16ref_bn<STAGES, UNIT, BN, 4, BM>(a, kernel_class); break;
+    case 2: launch_f16ref_bn<STAGES, UNIT, BN, 2, BM>(a, kernel_class); break;
+    default: launch_f16ref_bn<STAGES, UNIT, BN, 1, BM>(a, kernel_class); break;
   }
 }
 
 template <int STAGES, int UNIT>
 void launch_f16ref(const F16GemmArgs& a, int kernel_class) {
-  // batched products take the tile width of one image's product, so every
+  // batched products take the tile shape of one image's product, so every
   // image is tiled (and its partials grouped) exactly as a single product
-  if (f16ref_bn(a.M, a.epi.n_img ? a.epi.n_img : a.N) == 32)
-    launch_f16ref_ks<STAGES, UNIT, 32>(a, kernel_class);
+  const int nimg = a.epi.n_img ? a.epi.n_img : a.N;
+  if (f16ref_bn(a.M, nimg) == 64)
+    launch_f16ref_ks<STAGES, UNIT, 64, 32>(a, kernel_class);
+  else if (f16ref_bm(a.M, nimg) == 32)
+    launch_f16ref_ks<STAGES, UNIT, 32, 32>(a, kernel_class);
   else
-    launch_f16ref_ks<STAGES, UNIT, 64>(a, kernel_class);
+    launch_f16ref_ks<STAGES, UNIT, 32, 16>(a, kernel_class);
 }
 
 int f16ref_cfg() {
@@ -416,9 +432,9 @@ int f16ref_cfg() {
 
 }  // namespace
 
-int gemm_f16ref_num_ctas(int M, int N) { return int(cdiv(M, BM) * cdiv(N, f16ref_bn(M, N))); }
+int gemm_f16ref_num_ctas(int M, int N) { return int(cdiv(M, f16ref_bm(M, N)) * cdiv(N, f16ref_bn(M, N))); }
 int gemm_f16ref_partials_per_image(int M, int N, int n_img) {
-  return int(cdiv(M, BM) * (n_img / f16ref_bn(M, n_img)));
+  return int(cdiv(M, f16ref_bm(M, n_img)) * (n_img / f16ref_bn(M, n_img)));
 }
 
 void gemm_f16ref(const F16GemmArgs& a, int kernel_class) {
