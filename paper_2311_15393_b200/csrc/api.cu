@@ -876,6 +876,18 @@ void setup_state(Solve& s, const kp_solver_options* o, bool has_xt, bool flexibl
 // profiling the iteration is captured once into a CUDA graph and replayed;
 // the host polls the status word in growing chunks (overshoot iterations are
 // device no-ops).
+// Which PCG scalar steps fold into the neighbouring vector kernels (their
+// slot sums fit one vector CTA: small n). KP_FOLD_SCALARS=0 keeps the
+// separate scalar kernels (identical results).
+struct PcgFold {
+  bool alpha, resid, beta;
+};
+static PcgFold pcg_fold(int n_op_slots, int n_vec_slots, int n_msolve_slots) {
+  const char* e = getenv("KP_FOLD_SCALARS");
+  if (e && e[0] == '0') return {false, false, false};
+  return {pcg_fold_ok(n_op_slots), pcg_fold_ok(n_vec_slots), pcg_fold_ok(n_msolve_slots)};
+}
+
 // The whole iteration loop as ONE graph launch: a head kernel sets the
 // condition from the status word, a WHILE conditional node replays the
 // captured iteration (+ a one-thread kernel that re-evaluates the condition)
@@ -1124,6 +1136,7 @@ void run_pcg(kp_operator* op, const double* b_in, kp_precond* m, const kp_solver
   pcg_init_msolve_scalar(s.st, m->part.p, nms);
   vec_copy(p.p, z.p, nn, status);
 
+  const PcgFold fold = pcg_fold(nop, pcg_update_ctas(n), nms);
   auto iteration = [&]() {
     // q = A^T (A p) + lambda^2 p, with p.q partials (normal_matvec)
     op_apply(op, p.p, ap.p, false, nullptr, status);
@@ -1131,13 +1144,14 @@ void run_pcg(kp_operator* op, const double* b_in, kp_precond* m, const kp_solver
     ne.addv = p.p, ne.addc = o->lambda * o->lambda;
     ne.d0 = p.p, ne.partials = part_op.p;
     op_apply(op, ap.p, q.p, true, &ne, status);
-    pcg_alpha_scalar(s.st, part_op.p, nop);
+    if (!fold.alpha) pcg_alpha_scalar(s.st, part_op.p, nop);
     pcg_update(s.st, s.dh, x, r.p, flexible ? rprev.p : nullptr, p.p, q.p, z.p, xt,
-               fp16 ? m->r16.p : nullptr, n, fp16 ? m->sh->ldh : 0, part_vec.p);
-    pcg_resid_scalar(s.st, s.dh, part_vec.p, pcg_update_ctas(n));
+               fp16 ? m->r16.p : nullptr, n, fp16 ? m->sh->ldh : 0, part_vec.p, 1,
+               fold.alpha ? part_op.p : nullptr, nop, fold.resid);
+    if (!fold.resid) pcg_resid_scalar(s.st, s.dh, part_vec.p, pcg_update_ctas(n));
     msolve(m, r.p, z.p, r.p, flexible ? r.p : nullptr, flexible ? rprev.p : nullptr, status);
-    pcg_beta_scalar(s.st, m->part.p, nms);
-    pcg_p_update(s.st, p.p, z.p, nn);
+    if (!fold.beta) pcg_beta_scalar(s.st, m->part.p, nms);
+    pcg_p_update(s.st, p.p, z.p, nn, 1, fold.beta ? m->part.p : nullptr, nms);
   };
   drive(s, o->max_iterations, iteration);
   finish(s, o, hist, 2.25);
@@ -1431,18 +1445,20 @@ void run_pcg_batch(kp_operator* op, kp_precond* m, int B, const double* b_in, co
   batch_status(states, B, s.st);
   vec_copy(p, z, bnn, status);
 
+  const PcgFold fold = pcg_fold(nop, nvec, nms);
   auto iteration = [&]() {
     op_apply_batch(op, B, p, ap, false, nullptr, nullptr, nullptr, status);
     F64Epilogue ne;
     ne.addv = p, ne.d0 = p, ne.partials = part_op;
     op_apply_batch(op, B, ap, q, true, &ne, l2_dev, &l2, status);  // A^T A p + lambda_i^2 p
-    pcg_alpha_scalar(states, part_op, nop, B);
-    pcg_update(states, s.dh, x, r, rprev, p, q, z, xt, m->b_r16.p, n, ldh, part_vec, B);
-    pcg_resid_scalar(states, s.dh, part_vec, nvec, B);
+    if (!fold.alpha) pcg_alpha_scalar(states, part_op, nop, B);
+    pcg_update(states, s.dh, x, r, rprev, p, q, z, xt, m->b_r16.p, n, ldh, part_vec, B,
+               fold.alpha ? part_op : nullptr, nop, fold.resid);
+    if (!fold.resid) pcg_resid_scalar(states, s.dh, part_vec, nvec, B);
     batch_status(states, B, s.st);
     msolve_batch(m, B, z, r, flexible ? r : nullptr, rprev, status);
-    pcg_beta_scalar(states, m->b_part.p, nms, B);
-    pcg_p_update(states, p, z, nn, B);
+    if (!fold.beta) pcg_beta_scalar(states, m->b_part.p, nms, B);
+    pcg_p_update(states, p, z, nn, B, fold.beta ? m->b_part.p : nullptr, nms);
     batch_status(states, B, s.st);
   };
   drive(s, o->max_iterations, iteration);

@@ -40,20 +40,47 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double (*red)[NV]) {
   }
 }
 
-// Sum of component q of a [n][4] partials array, fixed order, one block of
-// SCALAR_THREADS threads (wide, so the partials of an 8192-tile GEMM are read
-// with few dependent steps per thread).
+// Sum of component q of a [n][4] partials array in fixed order by the first
+// T threads of the block (T a power of two >= 32, <= blockDim.x; every
+// thread of the block must call it), returned to all threads: thread t < T
+// sums slots t, t + T, ..., warp sums by xor shuffles, then the T / 32 warp
+// sums in order from 0.0 — a function of (n, T) only, so a scalar kernel of
+// T threads and a wider vector CTA folding the same step agree bit for bit.
+// L2 loads: the slots may come from other CTAs of the running kernel.
 constexpr int SCALAR_THREADS = 1024;
-__device__ double sum_partials(const double* part, int n, int q) {
-  __shared__ double red[SCALAR_THREADS / 32][1];
-  double v[1] = {0.0};
-  for (int i = threadIdx.x; i < n; i += blockDim.x) v[0] += part[size_t(i) * 4 + q];
-  block_sum<1>(v, red);
-  __syncthreads();
+__device__ double sum_slots(const double* part, int n, int q, int T) {
+  __shared__ double red[SCALAR_THREADS / 32];
   __shared__ double out;
-  if (threadIdx.x == 0) out = v[0];
+  double v = 0.0;
+  if (int(threadIdx.x) < T)
+    for (int i = threadIdx.x; i < n; i += T) v += __ldcg(part + size_t(i) * 4 + q);
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (T >> 5); ++w) s += red[w];
+    out = s;
+  }
   __syncthreads();
   return out;
+}
+__device__ double sum_partials(const double* part, int n, int q) { return sum_slots(part, n, q, blockDim.x); }
+
+// Last-CTA election for the folded scalar tails: every CTA of the (x) grid
+// calls it once after writing its partials; true in all threads of the CTA
+// that finished last, which then sees every CTA's writes. Resets the ticket.
+__device__ bool last_cta(DevState* st) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&st->ticket, 1u) == gridDim.x - 1;
+    if (last) st->ticket = 0u;
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
 }
 
 __device__ __forceinline__ bool stopped(const DevState* st) { return st->status != ST_RUNNING; }
@@ -238,32 +265,73 @@ __global__ void pcg_init_msolve_scalar_kernel(DevState* st, const double* part_z
     st->status = ST_ABORTED, st->abort_code = AB_POSITIVITY_INIT, st->abort_iter = 0;
 }
 
+// alpha = rho / p.q with the curvature checks (krylov.cpp:100-109); all
+// threads get alpha, `writer` records it / the abort. False: aborted.
+__device__ bool pcg_alpha_body(DevState* st, const double* part, int n, int T, bool writer, double& alpha) {
+  const double pq = sum_slots(part, n, 0, T);
+  if (!isfinite(pq)) {
+    if (writer) st->status = ST_ABORTED, st->abort_code = AB_CURV_NONFINITE, st->abort_iter = st->k;
+    return false;
+  }
+  if (pq <= 0.0) {
+    if (writer) st->status = ST_ABORTED, st->abort_code = AB_CURV_BREAKDOWN, st->abort_iter = st->k;
+    return false;
+  }
+  alpha = st->rho / pq;
+  if (writer) st->alpha = alpha;
+  return true;
+}
+
 __global__ void pcg_alpha_scalar_kernel(DevState* st, const double* part, int n) {
   pdl_wait();
   st += blockIdx.x, part += size_t(blockIdx.x) * n * 4;
   if (stopped(st)) return;
-  const double pq = sum_partials(part, n, 0);
-  if (threadIdx.x) return;
-  if (!isfinite(pq)) {
-    st->status = ST_ABORTED, st->abort_code = AB_CURV_NONFINITE, st->abort_iter = st->k;
-    return;
-  }
-  if (pq <= 0.0) {
-    st->status = ST_ABORTED, st->abort_code = AB_CURV_BREAKDOWN, st->abort_iter = st->k;
-    return;
-  }
-  st->alpha = st->rho / pq;
+  double alpha;
+  pcg_alpha_body(st, part, n, blockDim.x, threadIdx.x == 0, alpha);
 }
+
+// ||r||, history row, convergence / cap (krylov.cpp:113-126) from the
+// pcg_update partials; thread 0 writes.
+__device__ void pcg_resid_body(DevState* st, DevHistory h, const double* part, int n, int T) {
+  const double rr = sum_slots(part, n, 0, T);
+  const double ee = st->has_xt ? sum_slots(part, n, 1, T) : 0.0;
+  const double rz = st->track_cos ? sum_slots(part, n, 2, T) : 0.0;
+  const double zz = st->track_cos ? sum_slots(part, n, 3, T) : 0.0;
+  if (threadIdx.x) return;
+  const int k = st->k;
+  const double rnorm = sqrt(rr);
+  if (!isfinite(rnorm)) {
+    st->status = ST_ABORTED, st->abort_code = AB_RESID_NONFINITE, st->abort_iter = k;
+    return;
+  }
+  if (st->track_cos) {  // rec.cosine(r, z) (krylov.cpp:40-46)
+    const double denom = rnorm * sqrt(zz);
+    if (h.cosines) h.cosines[st->ncos] = denom > 0.0 ? fabs(rz) / denom : 0.0;
+    st->ncos++;
+  }
+  const int row = st->rows;
+  h.resid[row] = rnorm;
+  if (st->has_xt) h.relerr[row] = sqrt(ee) / st->xnorm;
+  st->rows = row + 1;
+  st->iterations_used = k;
+  if (rnorm <= st->tol * st->r0) {
+    st->status = ST_CONVERGED;
+    return;
+  }
+  if (k == st->maxit) st->status = ST_MAXIT;
+}
+
 
 // Elements are processed in pairs (16-byte vector accesses) when n is even
 // and every pointer is 16-byte aligned (VEC2), else one at a time. Both
 // elements of a pair lie in the same column, so the binary16 copy of r is a
 // single half2 store into the padded B-operand layout (row l, ldh stride).
 template <bool VEC2>
-__global__ void __launch_bounds__(VEC_THREADS, 4) pcg_update_kernel(const DevState* st, DevHistory h, double* x, double* r,
+__global__ void __launch_bounds__(VEC_THREADS, 4) pcg_update_kernel(DevState* st, DevHistory h, double* x, double* r,
                                   double* r_prev, const double* p, const double* q,
                                   const double* z, const double* xt, __half* r16, int n,
-                                  long ldh, double* part) {
+                                  long ldh, double* part, const double* part_pq, int n_pq,
+                                  int t_pq, int t_resid) {
   pdl_wait();
   {  // image blockIdx.y of a batch
     const int img = blockIdx.y;
@@ -275,10 +343,16 @@ __global__ void __launch_bounds__(VEC_THREADS, 4) pcg_update_kernel(const DevSta
     if (xt) xt += o;
     if (r16) r16 += size_t(img) * n * ldh;
     part += size_t(img) * gridDim.x * 4;
+    if (part_pq) part_pq += size_t(img) * n_pq * 4;
   }
   if (stopped(st)) return;
   __shared__ double red[VEC_THREADS / 32][4];
-  const double alpha = st->alpha;
+  double alpha;
+  if (part_pq) {  // folded pcg_alpha_scalar: every CTA forms the same alpha
+    if (!pcg_alpha_body(st, part_pq, n_pq, t_pq, blockIdx.x == 0 && threadIdx.x == 0, alpha)) return;
+  } else {
+    alpha = st->alpha;
+  }
   const bool has_xt = st->has_xt, cos = st->track_cos;
   const unsigned un = unsigned(n);
   double* it = (st->record && h.iterates) ? h.iterates + size_t(st->rows) * n * n : nullptr;
@@ -353,69 +427,74 @@ __global__ void __launch_bounds__(VEC_THREADS, 4) pcg_update_kernel(const DevSta
     double* o = part + size_t(blockIdx.x) * 4;
     o[0] = v[0], o[1] = v[1], o[2] = v[2], o[3] = v[3];
   }
+  // folded pcg_resid_scalar: the last CTA reduces every CTA's partials
+  if (t_resid && last_cta(st)) pcg_resid_body(st, h, part, gridDim.x, t_resid);
 }
 
 __global__ void pcg_resid_scalar_kernel(DevState* st, DevHistory h, const double* part, int n) {
   pdl_wait();
   st += blockIdx.x, h = hist_of(h, blockIdx.x, 0), part += size_t(blockIdx.x) * n * 4;
   if (stopped(st)) return;
-  const double rr = sum_partials(part, n, 0);
-  const double ee = st->has_xt ? sum_partials(part, n, 1) : 0.0;
-  const double rz = st->track_cos ? sum_partials(part, n, 2) : 0.0;
-  const double zz = st->track_cos ? sum_partials(part, n, 3) : 0.0;
-  if (threadIdx.x) return;
+  pcg_resid_body(st, h, part, n, blockDim.x);
+}
+
+// beta from the M-solve partials (krylov.cpp:127-132: z.r or z.(r - r_prev)
+// over rho) with the non-finite checks; `writer` counts the M-solve and
+// records beta / rz / the abort. False: aborted.
+__device__ bool pcg_beta_body(DevState* st, const double* part, int n, int T, bool writer, double& beta,
+                              double& rz) {
+  rz = sum_slots(part, n, 0, T);
+  const double zdr = sum_slots(part, n, 1, T);
+  const double bad = sum_slots(part, n, 2, T);
   const int k = st->k;
-  const double rnorm = sqrt(rr);
-  if (!isfinite(rnorm)) {
-    st->status = ST_ABORTED, st->abort_code = AB_RESID_NONFINITE, st->abort_iter = k;
-    return;
+  if (writer) st->msolve_count++;
+  if (bad > 0.0) {
+    if (writer) st->status = ST_ABORTED, st->abort_code = AB_M_NONFINITE, st->abort_iter = k;
+    return false;
   }
-  if (st->track_cos) {  // rec.cosine(r, z) (krylov.cpp:40-46)
-    const double denom = rnorm * sqrt(zz);
-    if (h.cosines) h.cosines[st->ncos] = denom > 0.0 ? fabs(rz) / denom : 0.0;
-    st->ncos++;
+  beta = st->flexible ? zdr / st->rho : rz / st->rho;
+  if (!isfinite(beta) || !isfinite(rz)) {
+    if (writer) st->status = ST_ABORTED, st->abort_code = AB_INNER_NONFINITE, st->abort_iter = k;
+    return false;
   }
-  const int row = st->rows;
-  h.resid[row] = rnorm;
-  if (st->has_xt) h.relerr[row] = sqrt(ee) / st->xnorm;
-  st->rows = row + 1;
-  st->iterations_used = k;
-  if (rnorm <= st->tol * st->r0) {
-    st->status = ST_CONVERGED;
-    return;
-  }
-  if (k == st->maxit) st->status = ST_MAXIT;
+  if (writer) st->beta = beta, st->rz = rz;
+  return true;
 }
 
 __global__ void pcg_beta_scalar_kernel(DevState* st, const double* part, int n) {
   pdl_wait();
   st += blockIdx.x, part += size_t(blockIdx.x) * n * 4;
   if (stopped(st)) return;
-  const double rz = sum_partials(part, n, 0);
-  const double zdr = sum_partials(part, n, 1);
-  const double bad = sum_partials(part, n, 2);
-  if (threadIdx.x) return;
-  const int k = st->k;
-  st->msolve_count++;
-  if (bad > 0.0) {
-    st->status = ST_ABORTED, st->abort_code = AB_M_NONFINITE, st->abort_iter = k;
-    return;
-  }
-  const double beta = st->flexible ? zdr / st->rho : rz / st->rho;
-  if (!isfinite(beta) || !isfinite(rz)) {
-    st->status = ST_ABORTED, st->abort_code = AB_INNER_NONFINITE, st->abort_iter = k;
-    return;
-  }
-  st->beta = beta;
-  st->rz = rz;
+  double beta, rz;
+  pcg_beta_body(st, part, n, blockDim.x, threadIdx.x == 0, beta, rz);
 }
 
-// p = z + beta p, then rho = rz with the positivity check (krylov.cpp:133-138)
-__global__ void pcg_p_update_kernel(DevState* st, double* p, const double* z, size_t nn, bool vec2) {
+// rho = rz and the positivity check, then the next iteration (krylov.cpp:133-138)
+__device__ void pcg_next_iteration(DevState* st, double rz) {
+  st->rho = rz;
+  if (st->rho <= 0.0) {
+    st->status = ST_ABORTED, st->abort_code = AB_POSITIVITY, st->abort_iter = st->k;
+    return;
+  }
+  st->k++;
+}
+
+// p = z + beta p, then the rho step. part_z: beta folded in (every CTA forms
+// it from the M-solve partials; the rho step, which changes the rho those
+// CTAs read, waits for the last CTA to finish).
+__global__ void pcg_p_update_kernel(DevState* st, double* p, const double* z, size_t nn, bool vec2,
+                                    const double* part_z, int nz, int t_z) {
   pdl_wait();
   st += blockIdx.y, p += blockIdx.y * nn, z += blockIdx.y * nn;  // image blockIdx.y of a batch
   if (stopped(st)) return;
-  const double beta = st->beta;
+  double beta, rz = 0.0;
+  if (part_z) {
+    if (!pcg_beta_body(st, part_z + size_t(blockIdx.y) * nz * 4, nz, t_z, blockIdx.x == 0 && threadIdx.x == 0,
+                       beta, rz))
+      return;
+  } else {
+    beta = st->beta;
+  }
   if (vec2) {
     for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < nn / 2;
          k += size_t(gridDim.x) * blockDim.x) {
@@ -429,16 +508,15 @@ __global__ void pcg_p_update_kernel(DevState* st, double* p, const double* z, si
          i += size_t(gridDim.x) * blockDim.x)
       p[i] = z[i] + beta * p[i];
   }
-  // rho = rz and the positivity check, by one thread once its share of p is
-  // done (no other CTA reads rho or k; a CTA that starts after an abort skips
-  // its share of p, which the stopped solve never reads again)
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
-  st->rho = st->rz;
-  if (st->rho <= 0.0) {
-    st->status = ST_ABORTED, st->abort_code = AB_POSITIVITY, st->abort_iter = st->k;
+  if (part_z) {
+    if (last_cta(st) && threadIdx.x == 0) pcg_next_iteration(st, rz);
     return;
   }
-  st->k++;
+  // unfolded: by one thread once its share of p is done (no other CTA reads
+  // rho or k; a CTA that starts after an abort skips its share of p, which
+  // the stopped solve never reads again)
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  pcg_next_iteration(st, st->rz);
 }
 
 // ---------------------------------------------------------------------------
@@ -815,6 +893,8 @@ void pcg_alpha_scalar(DevState* st, const double* part_pq, int n, int batch) {
   KP_LAUNCH(KC_VECTOR, pcg_alpha_scalar_kernel, batch, scalar_threads(n), st, part_pq, n);
 }
 
+bool pcg_fold_ok(int slots) { return scalar_threads(slots) <= unsigned(VEC_THREADS); }
+
 int pcg_update_ctas(int n) {
   // one pair (or element) per thread at most; the fixed VEC_CTAS from n ~ 1560 up
   const size_t units = (n % 2 == 0) ? size_t(n) * n / 2 : size_t(n) * n;
@@ -822,16 +902,20 @@ int pcg_update_ctas(int n) {
 }
 void pcg_update(DevState* st, DevHistory h, double* x, double* r, double* r_prev, const double* p,
                 const double* q, const double* z, const double* xt, __half* r16, int n, long ldh,
-                double* partials, int batch) {
+                double* partials, int batch, const double* part_pq, int n_pq, bool fold_resid) {
   const bool vec2 = n % 2 == 0 && al16(x) && al16(r) && al16(r_prev) && al16(p) && al16(q) &&
                     al16(z) && al16(xt) && al16(h.iterates) && ldh % 2 == 0;
-  const dim3 grid(pcg_update_ctas(n), batch);
+  const int ctas = pcg_update_ctas(n);
+  const dim3 grid(ctas, batch);
+  if ((part_pq && !pcg_fold_ok(n_pq)) || (fold_resid && !pcg_fold_ok(ctas)))
+    throw std::logic_error("pcg_update: scalar step too wide to fold");
+  const int t_pq = part_pq ? int(scalar_threads(n_pq)) : 0, t_resid = fold_resid ? int(scalar_threads(ctas)) : 0;
   if (vec2)
     KP_LAUNCH(KC_VECTOR, pcg_update_kernel<true>, grid, VEC_THREADS, st, h, x, r, r_prev, p, q,
-              z, xt, r16, n, ldh, partials);
+              z, xt, r16, n, ldh, partials, part_pq, n_pq, t_pq, t_resid);
   else
     KP_LAUNCH(KC_VECTOR, pcg_update_kernel<false>, grid, VEC_THREADS, st, h, x, r, r_prev, p,
-              q, z, xt, r16, n, ldh, partials);
+              q, z, xt, r16, n, ldh, partials, part_pq, n_pq, t_pq, t_resid);
 }
 void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n, int batch) {
   KP_LAUNCH(KC_VECTOR, pcg_resid_scalar_kernel, batch, scalar_threads(n), st, h, part, n);
@@ -839,9 +923,12 @@ void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n, int
 void pcg_beta_scalar(DevState* st, const double* part_z, int n, int batch) {
   KP_LAUNCH(KC_VECTOR, pcg_beta_scalar_kernel, batch, scalar_threads(n), st, part_z, n);
 }
-void pcg_p_update(DevState* st, double* p, const double* z, size_t nn, int batch) {
+void pcg_p_update(DevState* st, double* p, const double* z, size_t nn, int batch, const double* part_z,
+                  int nz) {
   const bool vec2 = nn % 2 == 0 && al16(p) && al16(z);
-  KP_LAUNCH(KC_VECTOR, pcg_p_update_kernel, dim3(vec_grid(nn), batch), VEC_THREADS, st, p, z, nn, vec2);
+  if (part_z && !pcg_fold_ok(nz)) throw std::logic_error("pcg_p_update: scalar step too wide to fold");
+  KP_LAUNCH(KC_VECTOR, pcg_p_update_kernel, dim3(vec_grid(nn), batch), VEC_THREADS, st, p, z, nn, vec2,
+            part_z, nz, part_z ? int(scalar_threads(nz)) : 0);
 }
 
 void cgls_init_scalar(DevState* st, DevHistory h, const double* part_s, int ns,

@@ -36,7 +36,7 @@ struct DevState {
   int track_cos;
   int has_xt;
   int record;
-  int pad0;
+  unsigned ticket;  // CTAs done in the running fused kernel (last-CTA tails); 0 between kernels
   double tol, l2, work_per_iter;
   double r0, xnorm, rho, alpha, beta, gamma, pnorm2, rz, snorm_prev;
 };
@@ -90,15 +90,28 @@ void pcg_init_msolve_scalar(DevState* st, const double* part_z, int nz, int batc
 void pcg_alpha_scalar(DevState* st, const double* part_pq, int n, int batch = 1);
 // CTAs (= partials) pcg_update uses at size n (fixed for a given n)
 int pcg_update_ctas(int n);
+// Scalar steps folded into the neighbouring vector kernel (small n, where
+// each launch is a fixed ~2 us on the iteration's critical path): possible
+// when the slot sum fits one vector CTA (a function of the slot count only,
+// so batched and single solves fold identically; the sums are the same
+// fixed-order reductions, so the results are bit-identical either way).
+bool pcg_fold_ok(int slots);
 // x += a p; r -= a q; [r_prev = r]; R16 = round16(r); partials:
-// [0] ||r||^2, [1] ||x - xt||^2, [2] r.z, [3] ||z||^2
+// [0] ||r||^2, [1] ||x - xt||^2, [2] r.z, [3] ||z||^2.
+// part_pq != nullptr: alpha (pcg_alpha_scalar over part_pq / n_pq slots) is
+// formed in every CTA first; fold_resid: the last CTA to finish runs
+// pcg_resid_scalar over the kernel's own partials.
 void pcg_update(DevState* st, DevHistory h, double* x, double* r, double* r_prev,
                 const double* p, const double* q, const double* z, const double* xt, __half* r16,
-                int n, long ldh, double* partials, int batch = 1);
+                int n, long ldh, double* partials, int batch = 1, const double* part_pq = nullptr,
+                int n_pq = 0, bool fold_resid = false);
 void pcg_resid_scalar(DevState* st, DevHistory h, const double* part, int n, int batch = 1);
 void pcg_beta_scalar(DevState* st, const double* part_z, int n, int batch = 1);
-// p = z + beta p
-void pcg_p_update(DevState* st, double* p, const double* z, size_t nn, int batch = 1);
+// p = z + beta p; part_z != nullptr: beta (pcg_beta_scalar over part_z / nz
+// slots) formed in every CTA first, the rho / positivity / k step by the
+// last CTA to finish
+void pcg_p_update(DevState* st, double* p, const double* z, size_t nn, int batch = 1,
+                  const double* part_z = nullptr, int nz = 0);
 // out->status = ST_RUNNING while any of st[0..count) runs, else ST_CONVERGED
 void batch_status(const DevState* st, int count, DevState* out);
 

@@ -163,3 +163,19 @@ def test_device_svd_backend():
     finally:
         K.set_svd_backend("host")
     assert np.array_equal(K.precond_solve(gd, r), K.precond_solve(g, r))
+
+
+def test_zero_x_true_rejected_single_and_batch():
+    """krylov.cpp:21-25: an all-zero x_true is invalid_argument("solver:
+    x_true must be nonzero") — raised by the library's device-side check for
+    single and batched solves (no host pass over x_true)."""
+    a, term, tps = batch_problem(64, 3)
+    m0 = K.build_preconditioner(term.row_factor, term.col_factor, 1.0, H)
+    z = np.zeros_like(tps[0].x_true)
+    with pytest.raises(ValueError, match="x_true must be nonzero"):
+        K.pcg(a, tps[0].b, K.with_lambda(m0, 0.05),
+              SolverOptions(lambda_=0.05, max_iterations=5, rel_residual_tol=1e-6, x_true=z))
+    bs = np.stack([tp.b for tp in tps])
+    xts = np.stack([tps[0].x_true, z, tps[2].x_true])
+    with pytest.raises(ValueError, match="x_true must be nonzero"):
+        K.pcg_batch(a, bs, m0, [0.05] * 3, SolverOptions(max_iterations=5, rel_residual_tol=1e-6), x_true=xts)

@@ -19,6 +19,9 @@ from paper_2311_15393_b200._lib import check, kp_history, kp_solver_options, lib
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C1"
 nsolve = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+# CUPTI does not see kernels inside conditional (device-loop) graph bodies
+import os  # noqa: E402
+os.environ.setdefault("KP_GRAPH_LOOP", "0")
 L = lib()
 check(L.kp_init(0))
 torch.cuda.set_device(0)
