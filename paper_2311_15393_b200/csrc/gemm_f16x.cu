@@ -77,8 +77,24 @@ constexpr int BM = 128, BN = 32, BK = 64, NSTAGE = KP_F16X_NSTAGE, NGROUP = 4, N
 #ifndef KP_F16X_HALF
 #define KP_F16X_HALF 0
 #endif
+// KP_F16X_SWP: the epilogue warps read each buffer as two 64-column loads and
+// overlap every load with the tree adds of the previously loaded half (the
+// second half of a step is added while the next step's first half loads).
+// Measured slower (3.29 vs 2.90 ms at n = 4096): the adds issued between the
+// loads keep the TMEM buffer ~500 cycles instead of ~230, and the MMA round
+// trip becomes the bound (profiles/r02_f16x_timeline.txt).
+#ifndef KP_F16X_SWP
+#define KP_F16X_SWP 0
+#endif
 // KP_F16X_PAIR: one N = 256 MMA (one TMEM buffer) covers two output groups
 // (fewer MMAs / commits); 0: one N = 128 MMA per group (measured slower).
+#ifndef KP_F16X_NISS
+#define KP_F16X_NISS 1
+#endif
+// KP_F16X_NISS: MMA-issuing threads. 1: warp 1 issues every buffer, warps 2-3
+// expand B. 2: warps 1 and 2 issue the even / odd TMEM buffers (an MMA +
+// commit costs the issuing thread ~120 cycles), warp 3 expands alone.
+constexpr int NISS = KP_F16X_NISS;
 constexpr int GPB = KP_F16X_PAIR ? 2 : 1;             // output groups per TMEM buffer
 constexpr int NMMA = GPB * NCOL, NBUF = NGROUP / GPB;
 constexpr int EPI_WARPS = 16, EPI_THREADS = 32 * EPI_WARPS;
@@ -90,6 +106,20 @@ constexpr int BEXP_GROUP_BYTES = NCOL * BK * 2; // 16 KB: 128 expanded rows x 64
 constexpr int BEXP_BYTES = NGROUP * BEXP_GROUP_BYTES;
 constexpr int REG_LEVELS = KP_F16X_REGLV;       // counter levels kept in registers (2 or 3)
 
+#ifndef KP_F16X_TRACE
+#define KP_F16X_TRACE 0
+#endif
+#if KP_F16X_TRACE
+// Timeline instrumentation (profiling builds only): clock64 stamps of CTA 0's
+// second tile. [0, 4096): issuer(s), ((kt*4+kk)*NBUF+h)*4 + {before tempty
+// wait, after it, after mma+commit, -}; [4096, 4096 + 2*256*8): epilogue warps
+// 4 and 12, (kt*4+kk)*8 + {before tfull wait, after, after wait::ld, after
+// arrive, after adds}; [8192 + 256*issuer, +64*4): issuer stage waits.
+__device__ long long f16x_trace[16384];
+#define TR(cond, idx) do { if (cond) f16x_trace[idx] = clock64(); } while (0)
+#else
+#define TR(cond, idx) do { } while (0)
+#endif
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -223,8 +253,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   for (int i = tid; i < 2 * BEXP_BYTES / 16; i += NUM_THREADS)
     reinterpret_cast<uint4*>(bexp)[i] = make_uint4(0, 0, 0, 0);
   if (tid == 0) {
-    for (int s = 0; s < NSTAGE; ++s) mbar_init(smem_u32(&full_bar[s]), 1), mbar_init(smem_u32(&empty_bar[s]), 1);
-    for (int s = 0; s < 2; ++s) mbar_init(smem_u32(&bfull_bar[s]), 2), mbar_init(smem_u32(&bempty_bar[s]), 1);
+    for (int s = 0; s < NSTAGE; ++s) mbar_init(smem_u32(&full_bar[s]), 1), mbar_init(smem_u32(&empty_bar[s]), NISS);
+    for (int s = 0; s < 2; ++s)
+      mbar_init(smem_u32(&bfull_bar[s]), NISS == 1 ? 2 : 1), mbar_init(smem_u32(&bempty_bar[s]), NISS);
     for (int h = 0; h < NBUF; ++h)
       mbar_init(smem_u32(&tfull_bar[h]), 1), mbar_init(smem_u32(&tempty_bar[h]), 4 * GPB);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -269,18 +300,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ===== MMA issuer =====
+  } else if (warp == 1 || (NISS == 2 && warp == 2)) {
+    if (lane == 0) {  // ===== MMA issuer(s) =====
+      const int h0 = warp - 1;  // first buffer of this issuer (stride NISS)
       const uint32_t tfull0 = smem_u32(&tfull_bar[0]), tempty0 = smem_u32(&tempty_bar[0]);
       int stage = 0;
       uint32_t phase = 0;
       int bi = 0;  // expanded-B buffer use counter
       uint32_t tphase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        [[maybe_unused]] const bool tr = t == blockIdx.x + gridDim.x && blockIdx.x == 0 && KT == 64;
         for (int kt = 0; kt < KT; ++kt, ++bi) {
           const int b = bi & 1;
+          TR(tr, 8192 + (warp - 1) * 256 + kt * 4 + 0);
           if (!(xflags & 8)) mbar_wait(smem_u32(&full_bar[stage]), phase);                    // A landed
+          TR(tr, 8192 + (warp - 1) * 256 + kt * 4 + 1);
           if (!(xflags & 2)) mbar_wait(smem_u32(&bfull_bar[b]), uint32_t((bi >> 1) & 1));     // B expanded
+          TR(tr, 8192 + (warp - 1) * 256 + kt * 4 + 2);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           // descriptors: the start-address field advances by 2 per 32-byte k-slice
           const uint64_t da = make_desc(sbase + uint32_t(stage * STAGE_BYTES));
@@ -290,12 +326,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // one N = 128 MMA per output group g into its own TMEM buffer, so
             // each epilogue set waits only on its own leaves
 #pragma unroll
-            for (int h = 0; h < NBUF; ++h) {
+            for (int h = h0; h < NBUF; h += NISS) {
+              TR(tr, ((kt * 4 + kk) * NBUF + h) * 4 + 0);
               mbar_wait(tempty0 + 8 * h, tphase ^ 1);
+              TR(tr, ((kt * 4 + kk) * NBUF + h) * 4 + 1);
               asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
               umma_leaves(tmem + uint32_t(h * NMMA), da + uint64_t(2 * kk),
                           db + uint64_t(((xflags & 1 ? 0 : h) * GPB * BEXP_GROUP_BYTES) >> 4) + uint64_t(2 * kk));
               umma_commit(tfull0 + 8 * h);
+              TR(tr, ((kt * 4 + kk) * NBUF + h) * 4 + 2);
             }
             tphase ^= 1;
           }
@@ -305,7 +344,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp == 2 || warp == 3) {  // ===== B expanders =====
+  } else if ((NISS == 1 && warp == 2) || warp == 3) {  // ===== B expanders =====
     // lane j scatters raw row j (output column nb + j): element k goes to
     // group j/8, expanded row (k%16)*8 + j%8, column k. Warp 2 takes
     // k = 0..31, warp 3 k = 32..63. With k = 8ch + e the swizzled offset is
@@ -313,11 +352,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int bi = 0;
-    const int jl = lane & 7, ch0 = (warp - 2) * 4;
+    constexpr int NCH = NISS == 1 ? 4 : 8;  // 16-byte k chunks per expander warp
+    const int jl = lane & 7, ch0 = NISS == 1 ? (warp - 2) * 4 : 0;
     const uint32_t lane_off = uint32_t((lane >> 3) * BEXP_GROUP_BYTES + jl * 128);
-    uint32_t xo[4];
+    uint32_t xo[NCH];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) xo[c] = uint32_t(((ch0 + c) ^ jl) << 4);
+    for (int c = 0; c < NCH; ++c) xo[c] = uint32_t(((ch0 + c) ^ jl) << 4);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       for (int kt = 0; kt < KT; ++kt, ++bi) {
         const int b = bi & 1;
@@ -326,7 +366,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const unsigned char* raw = smem + stage * STAGE_BYTES + A_BYTES + lane * (BK * 2) + ch0 * 16;
         unsigned char* dst = bexp + b * BEXP_BYTES + lane_off;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < NCH; ++c) {
           const uint4 q = *reinterpret_cast<const uint4*>(raw + c * 16);
           const uint32_t w[4] = {q.x, q.y, q.z, q.w};
           unsigned char* d = dst + xo[c] + ((ch0 + c) & 1) * 8 * 1024;
@@ -354,11 +394,102 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tile_coords(t, mb, nb);
       uint32_t r0[4], r1[4], r2[4];
       int cnt = 0;
+      [[maybe_unused]] const bool tr =
+          t == blockIdx.x + gridDim.x && blockIdx.x == 0 && KT == 64 && lane == 0 && (warp == 4 || warp == 12);
+      [[maybe_unused]] const int trb = 4096 + (warp == 12 ? 2048 : 0);
+      uint32_t p01[4], v64[4];
+      // push the 64-leaf unit v64 into the per-output binary counter
+      // (the low REG_LEVELS levels in registers, higher levels in shared memory)
+      auto push_unit = [&]() {
+        if (!(cnt & 1)) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) r0[p] = v64[p];
+      } else {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) v64[p] = hadd2(r0[p], v64[p]);
+        if (!(cnt & 2)) {
+#pragma unroll
+          for (int p = 0; p < 4; ++p) r1[p] = v64[p];
+        } else {
+#pragma unroll
+          for (int p = 0; p < 4; ++p) v64[p] = hadd2(r1[p], v64[p]);
+          bool carry = true;
+          if constexpr (REG_LEVELS == 3) {
+            if (!(cnt & 4)) {
+#pragma unroll
+              for (int p = 0; p < 4; ++p) r2[p] = v64[p];
+              carry = false;
+            } else {
+#pragma unroll
+              for (int p = 0; p < 4; ++p) v64[p] = hadd2(r2[p], v64[p]);
+            }
+          }
+          if (carry) {
+          int c = cnt >> REG_LEVELS, lvl = 0;
+          while (c & 1) {
+#pragma unroll
+            for (int p = 0; p < 4; ++p) v64[p] = hadd2(stack[(lvl * 4 + p) * EPI_THREADS + et], v64[p]);
+            c >>= 1;
+            ++lvl;
+          }
+#pragma unroll
+          for (int p = 0; p < 4; ++p) stack[(lvl * 4 + p) * EPI_THREADS + et] = v64[p];
+          }
+        }
+      }
+        ++cnt;
+      };
+#if KP_F16X_SWP
+      uint32_t vb[32], h0[4];  // second half of the previous step (kl = 8..15), first-half sums
+      // finish step pk: s16 = h0 + tree8(vb), merge into the 64-leaf unit
+      auto finish = [&](int pk) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const uint32_t c = hadd2(hadd2(vb[0 * 4 + p], vb[1 * 4 + p]), hadd2(vb[2 * 4 + p], vb[3 * 4 + p]));
+          const uint32_t d = hadd2(hadd2(vb[4 * 4 + p], vb[5 * 4 + p]), hadd2(vb[6 * 4 + p], vb[7 * 4 + p]));
+          const uint32_t s16 = hadd2(h0[p], hadd2(c, d));
+          if (pk == 0 || pk == 2) v64[p] = s16;
+          else if (pk == 1) p01[p] = hadd2(v64[p], s16);
+          else v64[p] = hadd2(p01[p], hadd2(v64[p], s16));
+        }
+        if (pk == 3) push_unit();
+      };
       for (int kt = 0; kt < KT; ++kt) {
-        uint32_t p01[4], v64[4];
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
+          TR(tr, trb + (kt * 4 + kk) * 8 + 0);
           mbar_wait_sleep(my_tfull, tphase);
+          TR(tr, trb + (kt * 4 + kk) * 8 + 1);
+          tphase ^= 1;
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          uint32_t va[32];  // v[kl*4 + p], kl = 0..7
+          tmem_ld64_pack(tbuf, va);
+          if (kk > 0) finish(kk - 1);
+          else if (kt > 0) finish(3);
+          tmem_ld_wait();
+          tmem_ld64_pack(tbuf + 64, vb);
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const uint32_t a = hadd2(hadd2(va[0 * 4 + p], va[1 * 4 + p]), hadd2(va[2 * 4 + p], va[3 * 4 + p]));
+            const uint32_t b = hadd2(hadd2(va[4 * 4 + p], va[5 * 4 + p]), hadd2(va[6 * 4 + p], va[7 * 4 + p]));
+            h0[p] = hadd2(a, b);
+          }
+          tmem_ld_wait();
+          TR(tr, trb + (kt * 4 + kk) * 8 + 2);
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(my_tempty);
+          TR(tr, trb + (kt * 4 + kk) * 8 + 3);
+        }
+      }
+      finish(3);
+#else
+      for (int kt = 0; kt < KT; ++kt) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          TR(tr, trb + (kt * 4 + kk) * 8 + 0);
+          mbar_wait_sleep(my_tfull, tphase);
+          TR(tr, trb + (kt * 4 + kk) * 8 + 1);
           tphase ^= 1;
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           // 16-leaf trees of outputs (2p, 2p+1): leaves kl = 0..15 sit in
@@ -399,9 +530,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #if !KP_F16X_EARLY
             tmem_ld_wait();
 #endif
+            TR(tr, trb + (kt * 4 + kk) * 8 + 2);
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(my_tempty);
+            TR(tr, trb + (kt * 4 + kk) * 8 + 3);
 #if KP_F16X_EARLY
             tmem_ld_wait();
 #endif
@@ -422,47 +555,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             else if (kk == 1) p01[p] = hadd2(v64[p], s16[p]);
             else v64[p] = hadd2(p01[p], hadd2(v64[p], s16[p]));
           }
+#if KP_F16X_TRACE
+          if (tr) { asm volatile("" ::"r"(v64[0]), "r"(v64[1]), "r"(v64[2]), "r"(v64[3])); }
+          TR(tr, trb + (kt * 4 + kk) * 8 + 4);
+#endif
         }
-        // push the 64-leaf unit into the per-output binary counter
-        // (the low REG_LEVELS levels in registers, higher levels in shared memory)
-        if (!(cnt & 1)) {
-#pragma unroll
-          for (int p = 0; p < 4; ++p) r0[p] = v64[p];
-        } else {
-#pragma unroll
-          for (int p = 0; p < 4; ++p) v64[p] = hadd2(r0[p], v64[p]);
-          if (!(cnt & 2)) {
-#pragma unroll
-            for (int p = 0; p < 4; ++p) r1[p] = v64[p];
-          } else {
-#pragma unroll
-            for (int p = 0; p < 4; ++p) v64[p] = hadd2(r1[p], v64[p]);
-            bool carry = true;
-            if constexpr (REG_LEVELS == 3) {
-              if (!(cnt & 4)) {
-#pragma unroll
-                for (int p = 0; p < 4; ++p) r2[p] = v64[p];
-                carry = false;
-              } else {
-#pragma unroll
-                for (int p = 0; p < 4; ++p) v64[p] = hadd2(r2[p], v64[p]);
-              }
-            }
-            if (carry) {
-            int c = cnt >> REG_LEVELS, lvl = 0;
-            while (c & 1) {
-#pragma unroll
-              for (int p = 0; p < 4; ++p) v64[p] = hadd2(stack[(lvl * 4 + p) * EPI_THREADS + et], v64[p]);
-              c >>= 1;
-              ++lvl;
-            }
-#pragma unroll
-            for (int p = 0; p < 4; ++p) stack[(lvl * 4 + p) * EPI_THREADS + et] = v64[p];
-            }
-          }
-        }
-        ++cnt;
+        push_unit();
       }
+#endif
       // bottom-up merge of the leftover counter levels (bits of cnt)
       uint32_t acc[4];
       bool have = false;
@@ -773,6 +873,13 @@ void row_hash_launch(const F16Operand& X, int rows, int K, unsigned long long* o
 
 }  // namespace
 
+#if KP_F16X_TRACE
+}  // namespace kp
+extern "C" int kp_debug_f16x_trace(long long* out, int n) {
+  return int(cudaMemcpyFromSymbol(out, kp::f16x_trace, sizeof(long long) * size_t(n)));
+}
+namespace kp {
+#endif
 long f16x_zfix_words(int M, int N) { return long(M) * N; }
 int gemm_f16x_num_ctas(int M, int N) { return int(cdiv(M, BM) * cdiv(N, BN)); }
 int gemm_f16x_partials_per_image(int M, int n_img) { return int(cdiv(M, BM) * (n_img / BN)); }
