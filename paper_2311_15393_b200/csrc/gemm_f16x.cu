@@ -61,6 +61,9 @@
 namespace kp {
 namespace {
 
+#ifndef KP_F16X_TRACE
+#define KP_F16X_TRACE 0
+#endif
 #ifndef KP_F16X_NSTAGE
 #define KP_F16X_NSTAGE 2
 #endif
@@ -71,23 +74,9 @@ constexpr int BM = 128, BN = 32, BK = 64, NSTAGE = KP_F16X_NSTAGE, NGROUP = 4, N
 #ifndef KP_F16X_PAIR
 #define KP_F16X_PAIR 1
 #endif
-#ifndef KP_F16X_EARLY
-#define KP_F16X_EARLY 0
-#endif
-#ifndef KP_F16X_HALF
-#define KP_F16X_HALF 0
-#endif
-// KP_F16X_SWP: the epilogue warps read each buffer as two 64-column loads and
-// overlap every load with the tree adds of the previously loaded half (the
-// second half of a step is added while the next step's first half loads).
-// Measured slower (3.29 vs 2.90 ms at n = 4096): the adds issued between the
-// loads keep the TMEM buffer ~500 cycles instead of ~230, and the MMA round
-// trip becomes the bound (profiles/r02_f16x_timeline.txt).
-#ifndef KP_F16X_SWP
-#define KP_F16X_SWP 0
-#endif
-// KP_F16X_PAIR: one N = 256 MMA (one TMEM buffer) covers two output groups
-// (fewer MMAs / commits); 0: one N = 128 MMA per group (measured slower).
+// Measured and removed (profiles/r02_f16x_variants.txt, r02_f16x_timeline.txt):
+// releasing the buffer before tcgen05.wait::ld (wrong results), two 64-column
+// loads per step in the 16-warp kernel with or without overlapped adds.
 #ifndef KP_F16X_NISS
 #define KP_F16X_NISS 1
 #endif
@@ -97,7 +86,17 @@ constexpr int BM = 128, BN = 32, BK = 64, NSTAGE = KP_F16X_NSTAGE, NGROUP = 4, N
 constexpr int NISS = KP_F16X_NISS;
 constexpr int GPB = KP_F16X_PAIR ? 2 : 1;             // output groups per TMEM buffer
 constexpr int NMMA = GPB * NCOL, NBUF = NGROUP / GPB;
-constexpr int EPI_WARPS = 16, EPI_THREADS = 32 * EPI_WARPS;
+// KP_F16X_W8: 8 epilogue warps with two output groups each (one per TMEM
+// buffer) and software-pipelined 64-column loads (140 registers, every load
+// under the adds of the previous chunk), instead of 16 warps with one group
+// and one 128-column load per step. Bit-identical; measured slower (3.113 vs
+// 2.888 ms at n = 4096, profiles/r02_f16x_variants.txt), so off.
+#ifndef KP_F16X_W8
+#define KP_F16X_W8 0
+#endif
+static_assert(!KP_F16X_W8 || (KP_F16X_PAIR == 1 && !KP_F16X_TRACE), "W8 needs the paired buffers; the timeline build is the 16-warp kernel");
+constexpr int NSET = KP_F16X_W8 ? 2 : 1;  // output groups per epilogue thread
+constexpr int EPI_WARPS = 16 / NSET, EPI_THREADS = 32 * EPI_WARPS;
 constexpr int NUM_THREADS = 32 * 4 + EPI_THREADS;
 constexpr int A_BYTES = BM * BK * 2;            // 16 KB
 constexpr int BRAW_BYTES = BN * BK * 2;         // 4 KB
@@ -106,9 +105,6 @@ constexpr int BEXP_GROUP_BYTES = NCOL * BK * 2; // 16 KB: 128 expanded rows x 64
 constexpr int BEXP_BYTES = NGROUP * BEXP_GROUP_BYTES;
 constexpr int REG_LEVELS = KP_F16X_REGLV;       // counter levels kept in registers (2 or 3)
 
-#ifndef KP_F16X_TRACE
-#define KP_F16X_TRACE 0
-#endif
 #if KP_F16X_TRACE
 // Timeline instrumentation (profiling builds only): clock64 stamps of CTA 0's
 // second tile. [0, 4096): issuer(s), ((kt*4+kk)*NBUF+h)*4 + {before tempty
@@ -382,108 +378,127 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp >= 4) {  // ===== epilogue sets =====
-    const int et = tid - 128;              // 0..511
-    const int g = (warp - 4) >> 2;         // output group = TMEM buffer (columns g*128)
-    const uint32_t my_tfull = smem_u32(&tfull_bar[g / GPB]), my_tempty = smem_u32(&tempty_bar[g / GPB]);
+    const int et = tid - 128;              // 0..EPI_THREADS-1
     const int quad = warp & 3;             // TMEM lane quadrant
-    const uint32_t tbuf = tmem + (uint32_t(quad * 32) << 16) + uint32_t(g * NCOL);
+    // Output groups of this thread: NSET = 1: group (warp-4)/4; NSET = 2 (8
+    // epilogue warps): groups half and half + 2 - one from each TMEM buffer.
+    const int g0 = (warp - 4) >> 2;
+    const uint32_t tlane = tmem + (uint32_t(quad * 32) << 16);
     const F16Epilogue& e = args.epi;
+    const int SL = levels > REG_LEVELS ? levels - REG_LEVELS : 0;  // counter levels kept in shared memory
     uint32_t tphase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       int mb, nb;
       tile_coords(t, mb, nb);
-      uint32_t r0[4], r1[4], r2[4];
-      int cnt = 0;
-      [[maybe_unused]] const bool tr =
-          t == blockIdx.x + gridDim.x && blockIdx.x == 0 && KT == 64 && lane == 0 && (warp == 4 || warp == 12);
-      [[maybe_unused]] const int trb = 4096 + (warp == 12 ? 2048 : 0);
-      uint32_t p01[4], v64[4];
-      // push the 64-leaf unit v64 into the per-output binary counter
+      uint32_t r0[NSET][4], r1[NSET][4], r2[NSET][4], p01[NSET][4], v64[NSET][4];
+      int cnt[NSET];
+#pragma unroll
+      for (int st = 0; st < NSET; ++st) cnt[st] = 0;
+      // push the 64-leaf unit v64[st] into the per-output binary counter
       // (the low REG_LEVELS levels in registers, higher levels in shared memory)
-      auto push_unit = [&]() {
-        if (!(cnt & 1)) {
+      auto push_unit = [&](const int st) {
+        uint32_t* const stk = stack + size_t(st) * SL * 4 * EPI_THREADS;
+        const int cn = cnt[st];
+        if (!(cn & 1)) {
 #pragma unroll
-        for (int p = 0; p < 4; ++p) r0[p] = v64[p];
-      } else {
-#pragma unroll
-        for (int p = 0; p < 4; ++p) v64[p] = hadd2(r0[p], v64[p]);
-        if (!(cnt & 2)) {
-#pragma unroll
-          for (int p = 0; p < 4; ++p) r1[p] = v64[p];
+          for (int p = 0; p < 4; ++p) r0[st][p] = v64[st][p];
         } else {
 #pragma unroll
-          for (int p = 0; p < 4; ++p) v64[p] = hadd2(r1[p], v64[p]);
-          bool carry = true;
-          if constexpr (REG_LEVELS == 3) {
-            if (!(cnt & 4)) {
+          for (int p = 0; p < 4; ++p) v64[st][p] = hadd2(r0[st][p], v64[st][p]);
+          if (!(cn & 2)) {
 #pragma unroll
-              for (int p = 0; p < 4; ++p) r2[p] = v64[p];
-              carry = false;
-            } else {
+            for (int p = 0; p < 4; ++p) r1[st][p] = v64[st][p];
+          } else {
 #pragma unroll
-              for (int p = 0; p < 4; ++p) v64[p] = hadd2(r2[p], v64[p]);
+            for (int p = 0; p < 4; ++p) v64[st][p] = hadd2(r1[st][p], v64[st][p]);
+            bool carry = true;
+            if constexpr (REG_LEVELS == 3) {
+              if (!(cn & 4)) {
+#pragma unroll
+                for (int p = 0; p < 4; ++p) r2[st][p] = v64[st][p];
+                carry = false;
+              } else {
+#pragma unroll
+                for (int p = 0; p < 4; ++p) v64[st][p] = hadd2(r2[st][p], v64[st][p]);
+              }
+            }
+            if (carry) {
+              int c = cn >> REG_LEVELS, lvl = 0;
+              while (c & 1) {
+#pragma unroll
+                for (int p = 0; p < 4; ++p) v64[st][p] = hadd2(stk[(lvl * 4 + p) * EPI_THREADS + et], v64[st][p]);
+                c >>= 1;
+                ++lvl;
+              }
+#pragma unroll
+              for (int p = 0; p < 4; ++p) stk[(lvl * 4 + p) * EPI_THREADS + et] = v64[st][p];
             }
           }
-          if (carry) {
-          int c = cnt >> REG_LEVELS, lvl = 0;
-          while (c & 1) {
-#pragma unroll
-            for (int p = 0; p < 4; ++p) v64[p] = hadd2(stack[(lvl * 4 + p) * EPI_THREADS + et], v64[p]);
-            c >>= 1;
-            ++lvl;
-          }
-#pragma unroll
-          for (int p = 0; p < 4; ++p) stack[(lvl * 4 + p) * EPI_THREADS + et] = v64[p];
-          }
         }
-      }
-        ++cnt;
+        cnt[st] = cn + 1;
       };
-#if KP_F16X_SWP
-      uint32_t vb[32], h0[4];  // second half of the previous step (kl = 8..15), first-half sums
-      // finish step pk: s16 = h0 + tree8(vb), merge into the 64-leaf unit
-      auto finish = [&](int pk) {
+      // merge the 16-leaf sum s16 of k-slice kk into the 64-leaf unit of set st
+      auto merge16 = [&](const int st, const int kk, const uint32_t (&s16)[4]) {
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          const uint32_t c = hadd2(hadd2(vb[0 * 4 + p], vb[1 * 4 + p]), hadd2(vb[2 * 4 + p], vb[3 * 4 + p]));
-          const uint32_t d = hadd2(hadd2(vb[4 * 4 + p], vb[5 * 4 + p]), hadd2(vb[6 * 4 + p], vb[7 * 4 + p]));
-          const uint32_t s16 = hadd2(h0[p], hadd2(c, d));
-          if (pk == 0 || pk == 2) v64[p] = s16;
-          else if (pk == 1) p01[p] = hadd2(v64[p], s16);
-          else v64[p] = hadd2(p01[p], hadd2(v64[p], s16));
+          if (kk == 0 || kk == 2) v64[st][p] = s16[p];
+          else if (kk == 1) p01[st][p] = hadd2(v64[st][p], s16[p]);
+          else v64[st][p] = hadd2(p01[st][p], hadd2(v64[st][p], s16[p]));
         }
-        if (pk == 3) push_unit();
+        if (kk == 3) push_unit(st);
       };
+#if KP_F16X_W8
+      // 8 epilogue warps, two per sub-partition: every 64-column load runs
+      // under the tree adds of the previously loaded 64 columns, and a warp
+      // alternates between the two TMEM buffers (X / Y: the two leaf chunks).
+      uint32_t X[32], Y[32], h0[4];
+      auto tree8 = [&](const uint32_t (&v)[32], uint32_t (&o)[4]) {  // v[kl*4 + p], 8 leaves per output
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const uint32_t a = hadd2(hadd2(v[0 * 4 + p], v[1 * 4 + p]), hadd2(v[2 * 4 + p], v[3 * 4 + p]));
+          const uint32_t b = hadd2(hadd2(v[4 * 4 + p], v[5 * 4 + p]), hadd2(v[6 * 4 + p], v[7 * 4 + p]));
+          o[p] = hadd2(a, b);
+        }
+      };
+      auto finish = [&](const int st, const int kk) {  // s16 = h0 + tree8(Y)
+        uint32_t hi[4], s16[4];
+        tree8(Y, hi);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) s16[p] = hadd2(h0[p], hi[p]);
+        merge16(st, kk, s16);
+      };
+      const uint32_t tfull0 = smem_u32(&tfull_bar[0]), tempty0 = smem_u32(&tempty_bar[0]);
       for (int kt = 0; kt < KT; ++kt) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          TR(tr, trb + (kt * 4 + kk) * 8 + 0);
-          mbar_wait_sleep(my_tfull, tphase);
-          TR(tr, trb + (kt * 4 + kk) * 8 + 1);
-          tphase ^= 1;
-          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          uint32_t va[32];  // v[kl*4 + p], kl = 0..7
-          tmem_ld64_pack(tbuf, va);
-          if (kk > 0) finish(kk - 1);
-          else if (kt > 0) finish(3);
-          tmem_ld_wait();
-          tmem_ld64_pack(tbuf + 64, vb);
 #pragma unroll
-          for (int p = 0; p < 4; ++p) {
-            const uint32_t a = hadd2(hadd2(va[0 * 4 + p], va[1 * 4 + p]), hadd2(va[2 * 4 + p], va[3 * 4 + p]));
-            const uint32_t b = hadd2(hadd2(va[4 * 4 + p], va[5 * 4 + p]), hadd2(va[6 * 4 + p], va[7 * 4 + p]));
-            h0[p] = hadd2(a, b);
+          for (int st = 0; st < 2; ++st) {
+            const uint32_t tb = tlane + uint32_t(st * NMMA + g0 * NCOL);
+            mbar_wait_sleep(tfull0 + 8 * st, tphase);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            tmem_ld64_pack(tb, X);  // leaves kl = 0..7
+            // the previous chunk pair (other buffer): its second half is still in Y
+            if (st == 1) finish(0, kk);
+            else if (kk > 0) finish(1, kk - 1);
+            else if (kt > 0) finish(1, 3);
+            tmem_ld_wait();
+            tmem_ld64_pack(tb + 64, Y);  // leaves kl = 8..15
+            tree8(X, h0);
+            tmem_ld_wait();
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty0 + 8 * st);
           }
-          tmem_ld_wait();
-          TR(tr, trb + (kt * 4 + kk) * 8 + 2);
-          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(my_tempty);
-          TR(tr, trb + (kt * 4 + kk) * 8 + 3);
+          tphase ^= 1;
         }
       }
-      finish(3);
+      finish(1, 3);
 #else
+      [[maybe_unused]] const bool tr =
+          t == blockIdx.x + gridDim.x && blockIdx.x == 0 && KT == 64 && lane == 0 && (warp == 4 || warp == 12);
+      [[maybe_unused]] const int trb = 4096 + (warp == 12 ? 2048 : 0);
+      const uint32_t my_tfull = smem_u32(&tfull_bar[g0 / GPB]), my_tempty = smem_u32(&tempty_bar[g0 / GPB]);
+      const uint32_t tbuf = tlane + uint32_t(g0 * NCOL);
       for (int kt = 0; kt < KT; ++kt) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
@@ -496,48 +511,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // TMEM columns kl*8 + jl; s16 = ((l0+l1)+(l2+l3) + ...) exactly as
           // pairwise_block_reduce pairs them
           uint32_t s16[4];
-#if KP_F16X_HALF
-          {  // two 64-column loads: fewer live registers (no spills)
-            uint32_t h0[4];
-            {
-              uint32_t v[32];  // v[kl*4 + p], kl = 0..7
-              tmem_ld64_pack(tbuf, v);
-              tmem_ld_wait();
-#pragma unroll
-              for (int p = 0; p < 4; ++p) {
-                const uint32_t a = hadd2(hadd2(v[0 * 4 + p], v[1 * 4 + p]), hadd2(v[2 * 4 + p], v[3 * 4 + p]));
-                const uint32_t b = hadd2(hadd2(v[4 * 4 + p], v[5 * 4 + p]), hadd2(v[6 * 4 + p], v[7 * 4 + p]));
-                h0[p] = hadd2(a, b);
-              }
-            }
-            uint32_t v[32];  // kl = 8..15
-            tmem_ld64_pack(tbuf + 64, v);
-            tmem_ld_wait();
-            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(my_tempty);
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-              const uint32_t c = hadd2(hadd2(v[0 * 4 + p], v[1 * 4 + p]), hadd2(v[2 * 4 + p], v[3 * 4 + p]));
-              const uint32_t d = hadd2(hadd2(v[4 * 4 + p], v[5 * 4 + p]), hadd2(v[6 * 4 + p], v[7 * 4 + p]));
-              s16[p] = hadd2(h0[p], hadd2(c, d));
-            }
-          }
-#else
           {
             uint32_t v[64];  // v[kl*4 + p]
             tmem_ld128_pack(tbuf, v);
-#if !KP_F16X_EARLY
-            tmem_ld_wait();
-#endif
+            tmem_ld_wait();  // required before the release: an early arrive was measured wrong
             TR(tr, trb + (kt * 4 + kk) * 8 + 2);
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(my_tempty);
             TR(tr, trb + (kt * 4 + kk) * 8 + 3);
-#if KP_F16X_EARLY
-            tmem_ld_wait();
-#endif
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
               uint32_t s8[8];
@@ -548,44 +530,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               s16[p] = hadd2(hadd2(a, b), hadd2(c, d));
             }
           }
-#endif
-#pragma unroll
-          for (int p = 0; p < 4; ++p) {
-            if (kk == 0 || kk == 2) v64[p] = s16[p];
-            else if (kk == 1) p01[p] = hadd2(v64[p], s16[p]);
-            else v64[p] = hadd2(p01[p], hadd2(v64[p], s16[p]));
-          }
+          merge16(0, kk, s16);
 #if KP_F16X_TRACE
-          if (tr) { asm volatile("" ::"r"(v64[0]), "r"(v64[1]), "r"(v64[2]), "r"(v64[3])); }
+          if (tr) { asm volatile("" ::"r"(v64[0][0]), "r"(v64[0][1]), "r"(v64[0][2]), "r"(v64[0][3])); }
           TR(tr, trb + (kt * 4 + kk) * 8 + 4);
 #endif
         }
-        push_unit();
       }
 #endif
+      const int m = mb + quad * 32 + lane;
+      int nlb;
+      const int img = epi_image(e, nb, nlb);
+      const int NL = e.n_img ? e.n_img : N;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int st = 0; st < NSET; ++st) {
+      const int g = g0 + 2 * st;
       // bottom-up merge of the leftover counter levels (bits of cnt)
       uint32_t acc[4];
       bool have = false;
+      const uint32_t* const stk = stack + size_t(st) * SL * 4 * EPI_THREADS;
       for (int L = 0; L < levels; ++L) {
-        if (!((cnt >> L) & 1)) continue;
+        if (!((cnt[st] >> L) & 1)) continue;
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          const uint32_t s = L == 0                      ? r0[p]
-                             : L == 1                      ? r1[p]
-                             : (REG_LEVELS == 3 && L == 2) ? r2[p]
-                                                           : stack[((L - REG_LEVELS) * 4 + p) * EPI_THREADS + et];
+          const uint32_t s = L == 0                      ? r0[st][p]
+                             : L == 1                      ? r1[st][p]
+                             : (REG_LEVELS == 3 && L == 2) ? r2[st][p]
+                                                           : stk[((L - REG_LEVELS) * 4 + p) * EPI_THREADS + et];
           acc[p] = have ? hadd2(s, acc[p]) : s;
         }
         have = true;
       }
       // ---- epilogue: row m, outputs n0 .. n0+7 (image-local; see F16Epilogue) ----
-      const int m = mb + quad * 32 + lane;
-      int nlb;
-      const int img = epi_image(e, nb, nlb);
-      const int NL = e.n_img ? e.n_img : N;
       const int n0 = nlb + g * 8;
       const int ng0 = nb + g * 8;  // global column (B operand row, hash index)
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
       uint32_t zbits = 0;  // outputs whose tree value is +-0
       if (m < M) {
 #pragma unroll
@@ -676,6 +655,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (uint32_t zb = zbits; zb; zb &= zb - 1, ++q)
           list[base + q] = unsigned(long(m) * N + ng0 + (__ffs(zb) - 1));
       }
+      }  // sets
       if (e.mode == F16OUT_F64 && e.partials) {  // fixed-order per-tile partials
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
@@ -907,7 +887,7 @@ void gemm_f16x(const F16GemmArgs& a_in, int kernel_class) {
   const int levels = counter_levels(a.K);
   const int smem_levels = levels > REG_LEVELS ? levels - REG_LEVELS : 0;
   const size_t smem = 1024 + size_t(NSTAGE) * STAGE_BYTES + 2 * size_t(BEXP_BYTES) +
-                      size_t(smem_levels) * 4 * EPI_THREADS * 4;
+                      size_t(smem_levels) * 4 * EPI_THREADS * 4 * NSET;
   if (smem > 227 * 1024) throw InvalidArgument("gemm_f16x: K too large for the counter stack");
   set_smem_limit(reinterpret_cast<const void*>(gemm_f16x_kernel), smem);
   const CUtensorMap ma = make_map(a.A, a.M, BM, true), mb = make_map(a.B, a.N, BN, false);
