@@ -76,7 +76,9 @@ constexpr int BM = 128, BN = 32, BK = 64, NSTAGE = KP_F16X_NSTAGE, NGROUP = 4, N
 #endif
 // Measured and removed (profiles/r02_f16x_variants.txt, r02_f16x_timeline.txt):
 // releasing the buffer before tcgen05.wait::ld (wrong results), two 64-column
-// loads per step in the 16-warp kernel with or without overlapped adds.
+// loads per step in the 16-warp kernel with or without overlapped adds, a
+// barrier-enforced alternation of the two buffers' warps between loading and
+// adding (3.47 ms).
 #ifndef KP_F16X_NISS
 #define KP_F16X_NISS 1
 #endif
