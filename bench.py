@@ -846,7 +846,7 @@ def main():
         op_src = "measured DFMA peak, profiles/r01_microbench_peaks.txt"
     else:  # each of the two GEMMs of an apply
         op_flops_per_launch = 2.0 * r * float(n) ** 3
-        op_peak, op_kernel = DMMA_PEAK_TFLOPS, "gemm_f64_kernel (DMMA m16n8k16)"
+        op_peak, op_kernel = DMMA_PEAK_TFLOPS, "gemm_f64_tma_kernel (DMMA m16n8k16, TMA-staged 128x128 tiles)"
         op_src = "measured DMMA f64 peak, profiles/r01_microbench_peaks.txt"
     op_ach = op_flops_per_launch / (op_ms / op_launches / 1e3) / 1e12 if op_launches else 0.0
     pm_ms, _ = prof["precond_gemm_f16ref"]
@@ -913,7 +913,7 @@ def main():
         cfg.problem.a.set_mode("auto")
         d_ach = 2.0 * r * float(n) ** 3 / (t_.value / c_.value / 1e3) / 1e12
         dense = {"bound": "tensor", "achieved": d_ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                 "frac": d_ach / DMMA_PEAK_TFLOPS, "kernel": "gemm_f64_kernel (DMMA m16n8k16)",
+                 "frac": d_ach / DMMA_PEAK_TFLOPS, "kernel": "gemm_f64_tma_kernel (DMMA m16n8k16, TMA-staged 128x128 tiles)",
                  "ms_per_launch": t_.value / c_.value, "launches": c_.value}
 
     out = None

@@ -5,16 +5,24 @@
 // dimension by the caller (api.cu), so one launch covers all r terms.
 //
 // Design (sm_100a): mma.sync.aligned.m16n8k16 f64 (DMMA; measured 37.0 TF/s
-// peak on B200, profiles/r01_microbench_peaks.txt), cp.async multistage
-// pipeline into XOR-swizzled K-major tiles (16 doubles = one 128-byte row per
-// M/N index; 16-byte chunk c of row r lives at c ^ (r & 7)), so every fragment
-// load is a conflict-free LDS.128. The K index inside an MMA is permuted
+// peak on B200, profiles/r01_microbench_peaks.txt), multistage pipeline into
+// XOR-swizzled K-major tiles (16 doubles = one 128-byte row per M/N index;
+// 16-byte chunk c of row r lives at c ^ (r & 7) - the TMA SWIZZLE_128B
+// pattern), so every fragment load is a conflict-free LDS.128. The 128 x 128
+// tiles are staged by TMA (cp.async.bulk.tensor 3-D boxes of 16 doubles x 128
+// rows over (k, row, term), zero fill outside the matrix, one elected thread,
+// full mbarrier per stage; the per-iteration __syncthreads frees the stage
+// being refilled); the 64 x 64 tiles of small problems and operands TMA
+// cannot address (odd leading dimension, unaligned base) use cp.async. The K index inside an MMA is permuted
 // (logical k = t + 4j <-> physical 4t + j) so each lane fetches its four K
 // values as 32 contiguous bytes; A and B use the same permutation, which only
 // reorders the exact FP64 sum.
 #include "gemm_f64.cuh"
 
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
+#include <string>
 
 namespace kp {
 namespace {
@@ -39,6 +47,30 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 __device__ __forceinline__ void lds128(uint32_t addr, double& x, double& y) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(addr));
 }
@@ -56,9 +88,9 @@ __device__ __forceinline__ void dmma16(double (&c)[4], const double (&a)[8], con
 // of CTAs shares A and B tiles in L2.
 constexpr int GROUP_M = 16;
 
-template <int BM, int BN, int WM, int WN, int STAGES, int KSUB, bool VEC16>
-__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
-    gemm_f64_kernel(const F64GemmArgs args) {
+template <int BM, int BN, int WM, int WN, int STAGES, int KSUB, bool VEC16, bool TMA>
+__device__ __forceinline__ void gemm_f64_body(const F64GemmArgs& args, const CUtensorMap* map_a,
+                                              const CUtensorMap* map_b) {
   pdl_wait();
   constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   constexpr int THREADS = WARPS_M * WARPS_N * 32;
@@ -69,7 +101,11 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 
   if (args.status && *args.status != 0) return;
 
-  extern __shared__ __align__(128) double smem[];
+  extern __shared__ __align__(1024) double smem_dyn[];
+  // SWIZZLE_128B boxes repeat every 1024 bytes: the TMA path needs that alignment
+  double* smem = TMA ? reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023))
+                     : smem_dyn;
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
 
   const int M = args.M, N = args.N;
   const int grid_m = (M + BM - 1) / BM, grid_n = (N + BN - 1) / BN;
@@ -91,9 +127,34 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 
   const uint32_t smem_base = smem_u32(smem);
 
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&full_bar[s]), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map_a)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map_b)) : "memory");
+    }
+    __syncthreads();
+  }
+
   auto load_tile = [&](int kt, int stage) {
     const int b = kt / kt_per_batch;
     const int k0 = (kt % kt_per_batch) * KT_DEPTH;
+    if constexpr (TMA) {
+      // one thread: KSUB boxes of 16 doubles x BM (BN) rows per operand
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        const uint32_t fb = smem_u32(&full_bar[stage]);
+        mbar_expect_tx(fb, uint32_t(STAGE_DOUBLES * 8));
+#pragma unroll
+        for (int sub = 0; sub < KSUB; ++sub) {
+          const uint32_t sa = smem_base + uint32_t(stage * STAGE_DOUBLES + sub * SUB_DOUBLES) * 8u;
+          tma_load_3d(sa, map_a, fb, k0 + sub * BK, m_base, b);
+          tma_load_3d(sa + uint32_t(BM * BK) * 8u, map_b, fb, k0 + sub * BK, n_base, b);
+        }
+      }
+      return;
+    }
     constexpr int CHUNKS_A = BM * 8, CHUNKS_B = BN * 8, CHUNKS = (CHUNKS_A + CHUNKS_B) * KSUB;
 #pragma unroll
     for (int id = tid; id < CHUNKS; id += THREADS) {
@@ -133,16 +194,19 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < total_kt) load_tile(s, s);
-    cp_async_commit();
+    if constexpr (!TMA) cp_async_commit();
   }
 
   for (int kt = 0; kt < total_kt; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
+    if constexpr (TMA)
+      mbar_wait(smem_u32(&full_bar[kt % STAGES]), uint32_t((kt / STAGES) & 1));
+    else
+      cp_async_wait<STAGES - 2>();
+    __syncthreads();  // every warp is done with the stage refilled below
     {
       const int nk = kt + STAGES - 1;
       if (nk < total_kt) load_tile(nk, nk % STAGES);
-      cp_async_commit();
+      if constexpr (!TMA) cp_async_commit();
     }
     const int stage = kt % STAGES;
 #pragma unroll
@@ -172,7 +236,7 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
       }
     }
   }
-  cp_async_wait<0>();
+  if constexpr (!TMA) cp_async_wait<0>();
 
   // ---- epilogue ----
   const F64Epilogue& e = args.epi;
@@ -217,8 +281,56 @@ __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
   }
 }
 
+template <int BM, int BN, int WM, int WN, int STAGES, int KSUB, bool VEC16>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+    gemm_f64_kernel(const F64GemmArgs args) {
+  gemm_f64_body<BM, BN, WM, WN, STAGES, KSUB, VEC16, false>(args, nullptr, nullptr);
+}
+
 template <int BM, int BN, int WM, int WN, int STAGES, int KSUB>
-void launch_cfg(const F64GemmArgs& a) {
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+    gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                        const F64GemmArgs args) {
+  gemm_f64_body<BM, BN, WM, WN, STAGES, KSUB, true, true>(args, &map_a, &map_b);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    KP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// (k, row, term) view of a K-major operand: Kb x rows x nb doubles, box 16 x box_rows x 1
+CUtensorMap make_map_f64(const F64Operand& op, int rows, int Kb, int nb, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {cuuint64_t(Kb), cuuint64_t(rows), cuuint64_t(nb)};
+  const cuuint64_t bstride = op.bstride ? cuuint64_t(op.bstride) : cuuint64_t(op.ld) * rows;
+  const cuuint64_t strides[2] = {cuuint64_t(op.ld) * 8, bstride * 8};
+  const cuuint32_t box[3] = {cuuint32_t(BK), cuuint32_t(box_rows), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(op.p), dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (f64) failed: " + std::to_string(int(r)));
+  return m;
+}
+
+// KP_F64_TMA=0 keeps the cp.async staging for the big tiles (A/B measurement).
+bool f64_tma_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("KP_F64_TMA");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, int KSUB>
+void launch_cfg(const F64GemmArgs& a, bool allow_tma = false) {
   constexpr int THREADS = (BM / WM) * (BN / WN) * 32;
   constexpr size_t SMEM = size_t(STAGES) * KSUB * (BM + BN) * BK * sizeof(double);
   const unsigned grid = cdiv(a.M, BM) * cdiv(a.N, BN);
@@ -226,7 +338,12 @@ void launch_cfg(const F64GemmArgs& a) {
                      (a.A.bstride % 2 == 0) && (a.B.bstride % 2 == 0) &&
                      (reinterpret_cast<uintptr_t>(a.A.p) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(a.B.p) % 16 == 0);
-  if (vec16) {
+  if (vec16 && allow_tma && f64_tma_enabled() && SMEM + 1024 <= 227 * 1024) {
+    auto k = gemm_f64_tma_kernel<BM, BN, WM, WN, STAGES, KSUB>;
+    set_smem_limit(reinterpret_cast<const void*>(k), SMEM + 1024);
+    const CUtensorMap ma = make_map_f64(a.A, a.M, a.Kb, a.nb, BM), mb = make_map_f64(a.B, a.N, a.Kb, a.nb, BN);
+    launch_pdl(k, dim3(grid), dim3(THREADS), SMEM + 1024, ma, mb, a);
+  } else if (vec16) {
     auto k = gemm_f64_kernel<BM, BN, WM, WN, STAGES, KSUB, true>;
     set_smem_limit(reinterpret_cast<const void*>(k), SMEM);
     launch_pdl(k, dim3(grid), dim3(THREADS), SMEM, a);
@@ -259,7 +376,7 @@ void launch_big(const F64GemmArgs& a) {
     case 3: launch_cfg<128, 128, 32, 32, 3, 2>(a); break;   // 16 warps, 32-deep stages
     case 4: launch_cfg<128, 64, 32, 32, 4, 1>(a); break;    // 8 warps, 2 CTAs/SM
     case 5: launch_cfg<128, 128, 64, 32, 4, 1>(a); break;   // 8 warps, 16-deep stages
-    default: launch_cfg<128, 128, 64, 32, 3, 2>(a); break;  // 8 warps, 32-deep stages
+    default: launch_cfg<128, 128, 64, 32, 3, 2>(a, true); break;  // 8 warps, 32-deep stages, TMA
   }
 }
 
