@@ -256,6 +256,17 @@ int kp_precond_info(const kp_precond* p, int* n, double* lambda,
 /* ---- emulated low-precision BLAS: precision.hpp / lpblas.hpp ----------- */
 /* round_array (precision.cpp:82-95) for any format; host arrays. */
 int kp_round_array(const double* x, long count, kp_format fmt, double* out);
+/* round_value (precision.cpp:82-86): scalar rounding, not tallied. */
+int kp_round_value(double x, kp_format fmt, double* out);
+/* RoundCallSession / round_call_count (precision.hpp:55-66, precision.cpp:11,
+ * 90, 111-119): the calling thread's tally of vectorised rounding calls. The
+ * device path fuses the roundings into its kernels, so the tally is kept
+ * analytically: every API call adds the number of round_inplace calls the
+ * reference makes for it (round_array 1; lp_matmul 1 + ceil(log2 k) for a
+ * live format; build_preconditioner 3; with_lambda 1; precond_solve and every
+ * M-solve of pcg / fpcg 2 + 4 (1 + ceil(log2 n)) for a live format, 0 for a
+ * double-covering one). A session is the difference of two reads. */
+int kp_round_call_count(unsigned long long* count);
 /* lp_matmul (lpblas.cpp:59-70): c = tree_k round(a(:,k) b(k,:)), one
  * rounding per pairwise stage; a m x k, b k x n, c m x n, column-major host
  * arrays. Bit-identical to the reference for every format. */

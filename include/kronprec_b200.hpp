@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <memory>
+#include <cstdint>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -48,6 +49,27 @@ inline Vec round_array(const Vec& a, kp_format fmt) {
   check(kp_round_array(a.data(), long(a.size()), fmt, out.data()));
   return out;
 }
+// round_value (precision.cpp:82-86)
+inline double round_value(double x, kp_format fmt) {
+  double out = 0.0;
+  check(kp_round_value(x, fmt, &out));
+  return out;
+}
+// RoundCallSession / round_call_count (precision.hpp:55-66)
+class RoundCallSession {
+ public:
+  RoundCallSession() : start_(now()) {}
+  std::uint64_t count() const { return now() - start_; }
+
+ private:
+  static std::uint64_t now() {
+    unsigned long long n = 0;
+    check(kp_round_call_count(&n));
+    return n;
+  }
+  std::uint64_t start_;
+};
+inline std::uint64_t round_call_count(const RoundCallSession& s) { return s.count(); }
 // lp_matmul (lpblas.cpp:59-70): a m x k, b k x n, column-major
 inline Vec lp_matmul(const Vec& a, const Vec& b, int m, int k, int n, kp_format fmt) {
   if (a.size() != size_t(m) * k || b.size() != size_t(k) * n)

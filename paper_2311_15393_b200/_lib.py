@@ -78,6 +78,7 @@ EXPORTS = [
     "kp_lp_matmul_ex", "kp_set_fp16_products", "kp_get_fp16_products", "kp_psf_to_kronsum",
     "kp_nearest_kron", "kp_pcg_batch", "kp_fpcg_batch", "kp_svd", "kp_set_svd_backend",
     "kp_get_svd_backend", "kp_discrepancy_batch", "kp_generate_test_problems", "kp_rng_raw",
+    "kp_round_value", "kp_round_call_count",
 ]
 
 _lib = None
@@ -138,6 +139,8 @@ def lib() -> C.CDLL:
             "kp_wgcv": ([P, D, C.POINTER(kp_param_choice)], I),
             "kp_filtered_solution": ([P, P, D, P], I),
             "kp_round_array": ([P, C.c_long, kp_format, P], I),
+            "kp_round_value": ([D, kp_format, C.POINTER(D)], I),
+            "kp_round_call_count": ([C.POINTER(C.c_ulonglong)], I),
             "kp_lp_matmul": ([I, I, I, P, P, kp_format, P], I),
             "kp_lp_matmul_ex": ([I, I, I, P, P, kp_format, I, P], I),
             "kp_discrepancy": ([P, D, D, C.POINTER(kp_param_choice)], I),

@@ -354,6 +354,21 @@ bool is_fp16(const kp_format& f) {
 // Neither fp16 (f16x2 GEMMs) nor double-covering (DMMA GEMMs): the generic
 // emulation path (lp_generic.cu), exact for any (t, emax, subnormals).
 bool is_generic(const kp_format& f) { return !covers_double(f) && !is_fp16(f); }
+
+// RoundCallSession (precision.hpp:55-66, precision.cpp:11,90): the reference
+// tallies its vectorised rounding calls per thread. The device path fuses
+// those roundings into kernels, so the tally is kept analytically - the
+// number of round_inplace calls the reference makes for the same API call.
+thread_local unsigned long long g_round_calls = 0;
+int tree_stages(long k) {  // pairwise_block_reduce (lpblas.cpp:13-30): stages for k blocks
+  int stages = 0;
+  while (k > 1) k = k / 2 + k % 2, ++stages;
+  return stages;
+}
+// precond_solve (factor.cpp:117-132): round r, round S .* t2, four lp_matmul
+unsigned long long msolve_round_calls(const kp_format& fmt, int n) {
+  return covers_double(fmt) ? 0ull : 2ull + 4ull * (1 + tree_stages(n));
+}
 LpFormat lp_format(const kp_format& f) {
   LpFormat l;
   l.t = f.significand_bits, l.emax = f.max_exponent, l.sub = f.subnormals_enabled != 0;
@@ -2091,6 +2106,7 @@ int kp_precond_build(const double* a_r, const double* a_c, int n, double lambda,
     kpla::Svd c = factor_svd(a_c, n, be);
     *out = precond_from_svd(n, std::move(r.u), std::move(r.s), std::move(r.v), std::move(c.u),
                             std::move(c.s), std::move(c.v), lambda, fmt, accum);
+    g_round_calls += 3;  // round_array of V_r, V_c, S (factor.cpp:100-102)
   })
 }
 int kp_precond_build_from_svd(int n, const double* u_r, const double* s_r, const double* v_r,
@@ -2101,6 +2117,7 @@ int kp_precond_build_from_svd(int n, const double* u_r, const double* s_r, const
     auto vec = [&](const double* p, size_t k) { return std::vector<double>(p, p + k); };
     *out = precond_from_svd(n, vec(u_r, nn), vec(s_r, n), vec(v_r, nn), vec(u_c, nn), vec(s_c, n),
                             vec(v_c, nn), lambda, fmt, accum);
+    g_round_calls += 3;
   })
 }
 int kp_precond_with_lambda(const kp_precond* p, double lambda, kp_precond** out) {
@@ -2111,9 +2128,16 @@ int kp_precond_with_lambda(const kp_precond* p, double lambda, kp_precond** out)
     q->sh = p->sh, q->n = p->n, q->lambda = lambda, q->fmt = p->fmt, q->accum = p->accum;
     set_weights(q.get());
     *out = q.release();
+    g_round_calls += 1;  // round_array of S (factor.cpp:113)
   })
 }
 int kp_precond_destroy(kp_precond* p) { KP_API(delete p) }
+int kp_round_call_count(unsigned long long* count) {
+  KP_API({
+    if (!count) throw InvalidArgument("round_call_count: null output");
+    *count = g_round_calls;
+  })
+}
 int kp_precond_solve(const kp_precond* pc, const double* r, double* z) {
   KP_API({
     auto* p = const_cast<kp_precond*>(pc);
@@ -2124,6 +2148,7 @@ int kp_precond_solve(const kp_precond* pc, const double* r, double* z) {
     msolve(p, dr.p, dz.p, nullptr, nullptr, nullptr, nullptr);
     dz.download(z, nn);
     sync();
+    g_round_calls += msolve_round_calls(p->fmt, p->n);
   })
 }
 int kp_precond_export(const kp_precond* p, int field, double* out) {
@@ -2188,11 +2213,25 @@ int kp_round_array(const double* x, long count, kp_format fmt, double* out) {
   KP_API({
     check_format(fmt);
     if (count < 0 || (count && (!x || !out))) throw InvalidArgument("round_array: bad arguments");
+    g_round_calls += 1;  // round_inplace counts every call (precision.cpp:90)
     if (!count) return KP_OK;
     DBuf<double> d(static_cast<size_t>(count));
     d.upload(x, size_t(count));
     lp_round_array(d.p, size_t(count), lp_format(fmt), d.p, KC_PRECOND);
     d.download(out, size_t(count));
+    sync();
+  })
+}
+// round_value (precision.cpp:82-86): one scalar through the same device kernel;
+// scalar rounding is not tallied (precision.hpp:40).
+int kp_round_value(double x, kp_format fmt, double* out) {
+  KP_API({
+    check_format(fmt);
+    if (!out) throw InvalidArgument("round_value: null output");
+    DBuf<double> d(1);
+    d.upload(&x, 1);
+    lp_round_array(d.p, 1, lp_format(fmt), d.p, KC_PRECOND);
+    d.download(out, 1);
     sync();
   })
 }
@@ -2206,6 +2245,7 @@ int kp_lp_matmul_ex(int m, int k, int n, const double* a, const double* b, kp_fo
     check_format(fmt);
     if (m < 0 || n < 0 || k < 0) throw InvalidArgument("lp_matmul: negative dimension");
     if (k == 0) throw InvalidArgument("lp_matmul: empty input");
+    if (!covers_double(fmt)) g_round_calls += (round_leaves ? 1 : 0) + tree_stages(k);  // lpblas.cpp:24,68
     if (m == 0 || n == 0) return KP_OK;
     const size_t na = size_t(m) * k, nb = size_t(k) * n, nc = size_t(m) * n;
     DBuf<double> da(na), db(nb), dc(nc);
@@ -2255,21 +2295,33 @@ int kp_cgls(const kp_operator* op, const double* b, const kp_solver_options* o, 
 }
 int kp_pcg(const kp_operator* op, const double* b, const kp_precond* m, const kp_solver_options* o,
            double* x, kp_history* h) {
-  KP_API(run_pcg(const_cast<kp_operator*>(op), b, const_cast<kp_precond*>(m), o, x, h, false))
+  KP_API({
+    run_pcg(const_cast<kp_operator*>(op), b, const_cast<kp_precond*>(m), o, x, h, false);
+    if (h) g_round_calls += (unsigned long long)h->msolve_count * msolve_round_calls(m->fmt, m->n);
+  })
 }
 int kp_fpcg(const kp_operator* op, const double* b, const kp_precond* m,
             const kp_solver_options* o, double* x, kp_history* h) {
-  KP_API(run_pcg(const_cast<kp_operator*>(op), b, const_cast<kp_precond*>(m), o, x, h, true))
+  KP_API({
+    run_pcg(const_cast<kp_operator*>(op), b, const_cast<kp_precond*>(m), o, x, h, true);
+    if (h) g_round_calls += (unsigned long long)h->msolve_count * msolve_round_calls(m->fmt, m->n);
+  })
 }
 int kp_pcg_batch(const kp_operator* op, const kp_precond* m, int batch, const double* b,
                  const double* lambdas, const kp_solver_options* o, double* x, kp_history* h) {
-  KP_API(run_pcg_batch(const_cast<kp_operator*>(op), const_cast<kp_precond*>(m), batch, b, lambdas, o, x, h,
-                       false))
+  KP_API({
+    run_pcg_batch(const_cast<kp_operator*>(op), const_cast<kp_precond*>(m), batch, b, lambdas, o, x, h, false);
+    for (int i = 0; h && i < batch; ++i)
+      g_round_calls += (unsigned long long)h[i].msolve_count * msolve_round_calls(m->fmt, m->n);
+  })
 }
 int kp_fpcg_batch(const kp_operator* op, const kp_precond* m, int batch, const double* b,
                   const double* lambdas, const kp_solver_options* o, double* x, kp_history* h) {
-  KP_API(run_pcg_batch(const_cast<kp_operator*>(op), const_cast<kp_precond*>(m), batch, b, lambdas, o, x, h,
-                       true))
+  KP_API({
+    run_pcg_batch(const_cast<kp_operator*>(op), const_cast<kp_precond*>(m), batch, b, lambdas, o, x, h, true);
+    for (int i = 0; h && i < batch; ++i)
+      g_round_calls += (unsigned long long)h[i].msolve_count * msolve_round_calls(m->fmt, m->n);
+  })
 }
 
 // ---- lambda selection ------------------------------------------------------------

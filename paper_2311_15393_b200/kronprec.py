@@ -21,7 +21,7 @@ from ._lib import (KP_ACCUM_REFERENCE, KP_ACCUM_TENSOR, NoRootError, check, f64,
                    kp_history, kp_param_choice, kp_solver_options, lib, ptr)
 
 __all__ = [
-    "PrecisionFormat", "round_value", "round_array", "lp_matmul", "lp_matvec", "lp_dot",
+    "PrecisionFormat", "round_value", "round_array", "RoundCallSession", "round_call_count", "lp_matmul", "lp_matvec", "lp_dot",
     "pairwise_sum", "KronTerm", "KroneckerSum", "vec", "unvec", "kronsum_apply",
     "kronsum_apply_transpose", "normal_matvec", "KronSvdPreconditioner",
     "build_preconditioner", "build_preconditioner_from_svd", "with_lambda", "precond_solve",
@@ -94,7 +94,32 @@ class PrecisionFormat:
 # ---------------------------------------------------------------------------
 # precision.hpp:39-51, lpblas.hpp:9-33 — device emulation, any format
 def round_value(x: float, fmt: PrecisionFormat) -> float:
-    return float(round_array(np.array([x], dtype=np.float64), fmt)[0])
+    """round_value (precision.cpp:82-86); not tallied by RoundCallSession."""
+    out = C.c_double()
+    check(lib().kp_round_value(float(x), fmt.c(), C.byref(out)))
+    return out.value
+
+
+class RoundCallSession:
+    """Tally of the vectorised rounding calls made on the current thread since
+    construction (precision.hpp:55-66); sessions may nest. The device path
+    counts the round_inplace calls the reference makes for the same API call."""
+
+    def __init__(self):
+        self._start = _round_calls()
+
+    def count(self) -> int:
+        return _round_calls() - self._start
+
+
+def _round_calls() -> int:
+    n = C.c_ulonglong()
+    check(lib().kp_round_call_count(C.byref(n)))
+    return int(n.value)
+
+
+def round_call_count(session: RoundCallSession) -> int:  # precision.cpp:117-119
+    return session.count()
 
 
 def round_array(a, fmt: PrecisionFormat) -> np.ndarray:

@@ -47,6 +47,38 @@ int main() {
   SolveResult rp = pcg(A, b, mx, po);
   CHECK(rp.history.converged && rp.history.iterations_used == 1);
 
+  // rounding-call budget (test_factor.cpp:302-317, test_krylov.cpp:259-287)
+  {
+    const int n8 = 8;
+    Vec t8(size_t(n8) * n8, 0.0);
+    for (int i = 0; i < n8; ++i)
+      for (int j = 0; j < n8; ++j) t8[size_t(j) * n8 + i] = (i == j) ? 0.5 : (std::abs(i - j) == 1 ? 0.25 : 0.0);
+    KronSvdPreconditioner p16 = build_preconditioner(t8, t8, n8, 0.05, fp16());
+    RoundCallSession s;
+    (void)precond_solve(p16, Vec(64, 1.0));
+    CHECK(s.count() == 2 + 4 * (1 + 3));
+    KronSvdPreconditioner p64 = build_preconditioner(t8, t8, n8, 0.05, fp64());
+    RoundCallSession s2;
+    (void)precond_solve(p64, Vec(64, 1.0));
+    CHECK(s2.count() == 0);
+    KroneckerSum A8({KronTerm{t8, t8}}, n8);
+    Vec b8(64);
+    for (int i = 0; i < 64; ++i) b8[i] = std::sin(0.3 + i);
+    SolverOptions o8;
+    o8.lambda = 0.05, o8.max_iterations = 10, o8.rel_residual_tol = 1e-12;
+    RoundCallSession base;
+    (void)cgls(A8, b8, o8);
+    CHECK(round_call_count(base) == 0);
+    RoundCallSession prec;
+    SolveResult r8 = pcg(A8, b8, p16, o8);
+    CHECK(round_call_count(prec) == std::uint64_t(18) * std::uint64_t(r8.history.msolve_count));
+    CHECK(r8.history.msolve_count >= r8.history.iterations_used);
+    RoundCallSession dbl;
+    (void)pcg(A8, b8, p64, o8);
+    CHECK(round_call_count(dbl) == 0);
+    CHECK(round_value(0.1, fp16()) == 0.0999755859375);
+  }
+
   // emulated low-precision BLAS (test_lpblas.cpp pins)
   CHECK(round_array(Vec{1.0 + 1.0 / 4096}, fp16())[0] == 1.0);
   const Vec c = lp_matmul(Vec{1, 3, 2, 4}, Vec{5, 7, 6, 8}, 2, 2, 2, fp16());  // [[1,2],[3,4]] x [[5,6],[7,8]]

@@ -160,3 +160,57 @@ def test_generic_format_pcg_matches_oracle():
         assert abs(h.iterations_used - ho.iterations_used) <= 2
         assert h.converged == ho.converged
         assert abs(h.relative_error[-1] - ho.relative_error[-1]) <= 1e-3
+
+
+def test_round_call_session_matches_reference_budget():
+    """RoundCallSession (precision.hpp:55-66): the reference's own budgets -
+    test_factor.cpp:302-317 (2 + 4 (1 + 3) calls per fp16 M-solve at n = 8,
+    none for fp64) and test_krylov.cpp:259-287 (all rounding happens inside
+    the preconditioner solves) - and the oracle's tally for the BLAS calls."""
+    n = 8
+    t = 0.5 * np.eye(n) + 0.25 * (np.eye(n, k=1) + np.eye(n, k=-1))
+    p16 = K.build_preconditioner(t, t, 0.05, H)
+    s = K.RoundCallSession()
+    K.precond_solve(p16, np.ones(n * n))
+    assert s.count() == 2 + 4 * (1 + 3)
+    p64 = K.build_preconditioner(t, t, 0.05, D)
+    s2 = K.RoundCallSession()
+    K.precond_solve(p64, np.ones(n * n))
+    assert s2.count() == 0
+    a = K.KroneckerSum([K.KronTerm(t, t)], n)
+    b = np.sin(0.3 + np.arange(n * n))
+    opts = K.SolverOptions(lambda_=0.05, max_iterations=10, rel_residual_tol=1e-12)
+    base = K.RoundCallSession()
+    K.cgls(a, b, opts)
+    assert K.round_call_count(base) == 0
+    prec = K.RoundCallSession()
+    rp = K.pcg(a, b, p16, opts)
+    assert K.round_call_count(prec) == 18 * rp.history.msolve_count
+    assert rp.history.msolve_count >= rp.history.iterations_used
+    flex = K.RoundCallSession()
+    rf = K.fpcg(a, b, p16, opts)
+    assert flex.count() == 18 * rf.history.msolve_count
+    dbl = K.RoundCallSession()
+    K.pcg(a, b, p64, opts)
+    assert dbl.count() == 0
+    # sessions nest; scalar rounding is not tallied; BLAS calls against the oracle's tally
+    outer = K.RoundCallSession()
+    K.round_value(0.1, H)
+    assert outer.count() == 0
+    rng = np.random.default_rng(2)
+    x, y = rng.standard_normal((5, 37)), rng.standard_normal((37, 3))
+    for fmt in (H, BF, D):
+        inner = K.RoundCallSession()
+        o0 = O.round_calls()
+        K.round_array(x, fmt), O.round_array(x, fmt)
+        K.lp_matmul(x, y, fmt), O.lp_matmul(x, y, fmt)
+        K.lp_matvec(x, y[:, 0], fmt), O.lp_matvec(x, y[:, 0], fmt)
+        K.lp_dot(x[0], y[:, 0], fmt), O.lp_dot(x[0], y[:, 0], fmt)
+        K.pairwise_sum(K.round_array(x[0], fmt), fmt), O.pairwise_sum(O.round_array(x[0], fmt), fmt)
+        assert inner.count() == O.round_calls() - o0
+    assert outer.count() > 0
+    b0 = K.RoundCallSession()
+    q = K.build_preconditioner(t, t, 0.05, H)
+    assert b0.count() == 3
+    K.with_lambda(q, 0.1)
+    assert b0.count() == 4
