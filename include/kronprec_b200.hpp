@@ -78,6 +78,25 @@ inline Vec lp_matmul(const Vec& a, const Vec& b, int m, int k, int n, kp_format 
   check(kp_lp_matmul(m, k, n, a.data(), b.data(), fmt, c.data()));
   return c;
 }
+// lp_matvec (lpblas.cpp:48-57): a m x k column-major
+inline Vec lp_matvec(const Vec& a, const Vec& v, int m, int k, kp_format fmt) {
+  if (a.size() != size_t(m) * k || v.size() != size_t(k)) throw std::invalid_argument("lp_matvec: shape mismatch");
+  return lp_matmul(a, v, m, k, 1, fmt);
+}
+// lp_dot (lpblas.cpp:39-46)
+inline double lp_dot(const Vec& x, const Vec& y, kp_format fmt) {
+  if (x.size() != y.size()) throw std::invalid_argument("lp_dot: length mismatch");
+  if (x.empty()) throw std::invalid_argument("lp_dot: empty input");
+  return lp_matmul(x, y, 1, int(x.size()), 1, fmt)[0];
+}
+// pairwise_sum (lpblas.cpp:34-37): the addends are taken as already rounded
+inline double pairwise_sum(const Vec& z, kp_format fmt) {
+  if (z.empty()) throw std::invalid_argument("pairwise_sum: empty input");
+  const Vec ones(z.size(), 1.0);
+  double out = 0.0;
+  check(kp_lp_matmul_ex(1, int(z.size()), 1, z.data(), ones.data(), fmt, 0, &out));
+  return out;
+}
 
 // KronTerm / KroneckerSum (kron.hpp:12-22): factors are n*n column-major.
 struct KronTerm {
@@ -162,6 +181,20 @@ inline Vec kronsum_apply_transpose(const KroneckerSum& k, const Vec& y) {  // kr
   if (y.size() != size_t(k.n()) * k.n()) throw std::invalid_argument("kron_apply: vector length is not n^2");
   check(kp_kronsum_apply_transpose(k.handle(), y.data(), out.data()));
   return out;
+}
+// kron_apply (kron.cpp:62-71): (C (x) D) y = vec(D unvec(y) C^T)
+inline Vec kron_apply(const Vec& c, const Vec& d, int n, const Vec& y) {
+  if (n < 1 || c.size() != size_t(n) * n || d.size() != size_t(n) * n)
+    throw std::invalid_argument("kron_apply: factors must be square and equally sized");
+  if (y.size() != size_t(n) * n) throw std::invalid_argument("kron_apply: vector length is not n^2");
+  return kronsum_apply(KroneckerSum({KronTerm{c, d}}, n), y);
+}
+// svd_dense (factor.cpp:14-23): backend KP_SVD_HOST (LAPACK) or KP_SVD_DEVICE (cuSOLVER)
+inline SvdTriple svd_dense(const Vec& a, int n, int backend = 0) {
+  if (n < 1 || a.size() != size_t(n) * n) throw std::invalid_argument("svd_dense: square, non-empty matrix expected");
+  SvdTriple t{Vec(size_t(n) * n), Vec(size_t(n)), Vec(size_t(n) * n)};
+  check(kp_svd(a.data(), n, backend, t.u.data(), t.s.data(), t.v.data()));
+  return t;
 }
 inline Vec normal_matvec(const KroneckerSum& a, double lambda, const Vec& p) {  // krylov.cpp:146-152
   if (p.size() != size_t(a.n()) * a.n()) throw std::invalid_argument("normal_matvec: length mismatch");
@@ -327,6 +360,42 @@ inline SpectralData make_spectral_data(const KronSvdPreconditioner& p, const Vec
 inline SpectralData make_spectral_data(const KronSvdPreconditioner& p, const Vec& b,
                                        const Vec& x_true) {
   return SpectralData(p, b, &x_true);
+}
+// approx_spectrum / project_b / project_x (factor.hpp:76-88, factor.cpp:134-187)
+struct ApproxSpectrum {
+  Vec sigma;
+  std::vector<long> perm;
+};
+inline ApproxSpectrum approx_spectrum(const KronSvdPreconditioner& p) {
+  const int n = p.n();
+  Vec sr(static_cast<size_t>(n), 0.0), sc(static_cast<size_t>(n), 0.0);
+  check(kp_precond_export(p.handle(), 4, sr.data()));
+  check(kp_precond_export(p.handle(), 5, sc.data()));
+  const size_t nn = size_t(n) * n;
+  Vec products(nn);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) products[size_t(j) * n + i] = sr[j] * sc[i];
+  ApproxSpectrum out{Vec(nn), std::vector<long>(nn)};
+  for (size_t k = 0; k < nn; ++k) out.perm[k] = long(k);
+  std::stable_sort(out.perm.begin(), out.perm.end(), [&](long a, long b) { return products[a] > products[b]; });
+  for (size_t k = 0; k < nn; ++k) out.sigma[k] = products[size_t(out.perm[k])];
+  return out;
+}
+inline Vec project_b(const KronSvdPreconditioner& p, const Vec& b) {
+  const size_t nn = size_t(p.n()) * p.n();
+  if (b.size() != nn) throw std::invalid_argument("project: vector length is not n^2");
+  SpectralData sd(p, b);
+  Vec sigma(nn), bh(nn);
+  check(kp_spectral_export(sd.handle(), sigma.data(), bh.data()));
+  return bh;
+}
+inline Vec project_x(const KronSvdPreconditioner& p, const Vec& x) {
+  const size_t nn = size_t(p.n()) * p.n();
+  if (x.size() != nn) throw std::invalid_argument("project: vector length is not n^2");
+  SpectralData sd(p, x, &x);
+  Vec xh(nn);
+  check(kp_spectral_export_xhat(sd.handle(), xh.data()));
+  return xh;
 }
 inline double opt_objective(const SpectralData& sd, double lambda) {
   double v;

@@ -22,10 +22,10 @@ from ._lib import (KP_ACCUM_REFERENCE, KP_ACCUM_TENSOR, NoRootError, check, f64,
 
 __all__ = [
     "PrecisionFormat", "round_value", "round_array", "RoundCallSession", "round_call_count", "lp_matmul", "lp_matvec", "lp_dot",
-    "pairwise_sum", "KronTerm", "KroneckerSum", "vec", "unvec", "kronsum_apply",
+    "pairwise_sum", "KronTerm", "KroneckerSum", "vec", "unvec", "kron_apply", "kronsum_apply",
     "kronsum_apply_transpose", "normal_matvec", "KronSvdPreconditioner",
     "build_preconditioner", "build_preconditioner_from_svd", "with_lambda", "precond_solve",
-    "SolverOptions", "ConvergenceHistory", "SolveResult", "cgls", "pcg", "fpcg", "pcg_batch", "fpcg_batch", "discrepancy_batch", "svd", "set_svd_backend",
+    "SolverOptions", "ConvergenceHistory", "SolveResult", "cgls", "pcg", "fpcg", "pcg_batch", "fpcg_batch", "discrepancy_batch", "svd", "svd_dense", "set_svd_backend", "ApproxSpectrum", "approx_spectrum", "project_b", "project_x",
     "plateau_iteration", "WorkReport", "work_report", "SpectralData", "make_spectral_data",
     "ParamChoice", "gcv_objective", "opt_objective", "wgcv_objective", "discrepancy_gap", "gcv",
     "gcv_grid", "lambda_opt", "wgcv", "discrepancy", "filtered_solution", "NoRootError",
@@ -292,6 +292,19 @@ def kronsum_apply_transpose(k: KroneckerSum, y) -> np.ndarray:  # kron.cpp:81-88
     out = np.empty_like(y)
     check(lib().kp_kronsum_apply_transpose(k.handle(), ptr(y), ptr(out)))
     return out
+
+
+def kron_apply(c, d, y) -> np.ndarray:  # kron.cpp:62-71
+    """(C (x) D) y = vec(D unvec(y) C^T) on the device operator kernels."""
+    c = np.asarray(c, dtype=np.float64)
+    d = np.asarray(d, dtype=np.float64)
+    n = c.shape[0] if c.ndim == 2 else 0
+    if c.shape != (n, n) or d.shape != (n, n) or n == 0:
+        raise ValueError("kron_apply: factors must be square and equally sized")
+    y = np.asarray(y, dtype=np.float64).reshape(-1)
+    if y.size != n * n:
+        raise ValueError("kron_apply: vector length is not n^2")
+    return kronsum_apply(KroneckerSum([KronTerm(c, d)], n), y)
 
 
 def normal_matvec(a: KroneckerSum, lambda_: float, p) -> np.ndarray:  # krylov.cpp:146-152
@@ -586,6 +599,10 @@ def svd(a, backend: str = "host"):
     return u, sv, v
 
 
+def svd_dense(a, backend: str = "host") -> SvdTriple:  # factor.cpp:14-23
+    return SvdTriple(*svd(a, backend))
+
+
 def set_svd_backend(backend: str) -> None:
     """Backend of build_preconditioner's factor SVDs (process-wide)."""
     check(lib().kp_set_svd_backend(_SVD_BACKENDS[backend]))
@@ -707,6 +724,31 @@ class SpectralData:
                 self._h = None
         except Exception:
             pass
+
+
+@dataclass
+class ApproxSpectrum:  # factor.hpp:76-79
+    sigma: np.ndarray
+    perm: np.ndarray
+
+
+def approx_spectrum(p: KronSvdPreconditioner) -> ApproxSpectrum:
+    """factor.cpp:134-153: sigma(k) = s_r(j) s_c(i) sorted nonincreasing by a
+    stable sort of the column-major index j n + i (index bookkeeping on the
+    host, as the device export's ordering)."""
+    products = np.outer(np.asarray(p.svd_r.s), np.asarray(p.svd_c.s)).reshape(-1)  # [j*n + i]
+    perm = np.argsort(-products, kind="stable")
+    return ApproxSpectrum(products[perm], perm)
+
+
+def project_b(p: KronSvdPreconditioner, b) -> np.ndarray:  # factor.cpp:179-182
+    """vec(U_c^T B U_r) reordered like approx_spectrum (device DMMA projections)."""
+    return make_spectral_data(p, b).b_hat
+
+
+def project_x(p: KronSvdPreconditioner, x) -> np.ndarray:  # factor.cpp:184-187
+    """vec(V_c^T X V_r) reordered like approx_spectrum."""
+    return make_spectral_data(p, x, x).x_hat
 
 
 def make_spectral_data(p: KronSvdPreconditioner, b, x_true=None) -> SpectralData:

@@ -79,6 +79,34 @@ int main() {
     CHECK(round_value(0.1, fp16()) == 0.0999755859375);
   }
 
+  // kron_apply / svd_dense / approx_spectrum / project_b / project_x (kron.hpp:29-31, factor.hpp:19, 76-88)
+  {
+    const int n3 = 3;
+    Vec c3 = {1, 2, 3, 0, 1, 4, 5, 6, 0}, d3 = {2, 0, 1, 1, 3, 0, 0, 1, 1}, y3(9);
+    for (int i = 0; i < 9; ++i) y3[i] = 1.0 + i;
+    Vec k3 = kron_apply(c3, d3, n3, y3);
+    // (C (x) D) y entry (j n + i) = sum_{l,m} C(j,l) D(i,m) y(l n + m)
+    for (int j = 0; j < n3; ++j)
+      for (int i = 0; i < n3; ++i) {
+        double ref = 0.0;
+        for (int l = 0; l < n3; ++l)
+          for (int m2 = 0; m2 < n3; ++m2) ref += c3[l * n3 + j] * d3[m2 * n3 + i] * y3[l * n3 + m2];
+        CHECK(std::fabs(k3[j * n3 + i] - ref) <= 1e-12);
+      }
+    SvdTriple sv = svd_dense(c3, n3);
+    CHECK(sv.s[0] >= sv.s[1] && sv.s[1] >= sv.s[2] && sv.s[2] >= 0.0);
+    KronSvdPreconditioner p3 = build_preconditioner(c3, d3, n3, 0.1, fp16());
+    ApproxSpectrum as = approx_spectrum(p3);
+    for (size_t k = 1; k < as.sigma.size(); ++k) CHECK(as.sigma[k - 1] >= as.sigma[k]);
+    Vec pb = project_b(p3, y3), px = project_x(p3, y3);
+    double nb = 0, nx = 0, ny = 0;
+    for (int i = 0; i < 9; ++i) nb += pb[i] * pb[i], nx += px[i] * px[i], ny += y3[i] * y3[i];
+    CHECK(std::fabs(nb - ny) <= 1e-10 * ny && std::fabs(nx - ny) <= 1e-10 * ny);  // orthogonal bases
+    CHECK(lp_dot(Vec{2048, 1, 1, 1}, Vec{1, 1, 1, 1}, fp16()) == 2050.0);        // test_lpblas.cpp pin
+    CHECK(pairwise_sum(Vec{2048, 1, 1, 1}, fp16()) == 2050.0);
+    CHECK(lp_matvec(Vec{2048, 1, 1, 1}, Vec{1, 1, 1, 1}, 1, 4, fp16())[0] == 2050.0);
+  }
+
   // emulated low-precision BLAS (test_lpblas.cpp pins)
   CHECK(round_array(Vec{1.0 + 1.0 / 4096}, fp16())[0] == 1.0);
   const Vec c = lp_matmul(Vec{1, 3, 2, 4}, Vec{5, 7, 6, 8}, 2, 2, 2, fp16());  // [[1,2],[3,4]] x [[5,6],[7,8]]

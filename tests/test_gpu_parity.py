@@ -608,3 +608,34 @@ def test_discrepancy_lookahead_equals_sequential_bisection(noise):
     u = K.find_root(lambda v: K.discrepancy_gap(sd, eps, math.exp(v)),
                     math.log(got.bracket_lo), math.log(got.bracket_hi), 1e-12)
     assert got.lambda_ == math.exp(u)
+
+
+def test_reference_named_projection_callables():
+    """kron_apply (kron.cpp:62-71), svd_dense (factor.cpp:14-23), approx_spectrum /
+    project_b / project_x (factor.cpp:134-187) by their reference names, against
+    their definitions in numpy FP64."""
+    n = 24
+    rng = np.random.default_rng(31)
+    c, d = rng.standard_normal((n, n)), rng.standard_normal((n, n))
+    y = rng.standard_normal(n * n)
+    ref = (d @ y.reshape(n, n, order="F") @ c.T).reshape(-1, order="F")
+    assert np.linalg.norm(K.kron_apply(c, d, y) - ref) <= 1e-13 * np.linalg.norm(ref)
+    with pytest.raises(ValueError):
+        K.kron_apply(c, d, y[:-1])
+    t = K.svd_dense(c)
+    assert np.all(np.diff(t.s) <= 0)
+    assert np.linalg.norm(t.u @ np.diag(t.s) @ t.v.T - c) <= 1e-12 * np.linalg.norm(c)
+    p = K.build_preconditioner(c, d, 0.1, K.PrecisionFormat.fp16())
+    sr, sc = p.svd_r, p.svd_c
+    spec = K.approx_spectrum(p)
+    products = np.outer(sr.s, sc.s).reshape(-1)
+    assert np.array_equal(spec.sigma, np.sort(products)[::-1])
+    assert np.array_equal(products[spec.perm], spec.sigma)
+    assert sorted(spec.perm.tolist()) == list(range(n * n))
+    Y = y.reshape(n, n, order="F")
+    pb = (sc.u.T @ Y @ sr.u).reshape(-1, order="F")[spec.perm]
+    px = (sc.v.T @ Y @ sr.v).reshape(-1, order="F")[spec.perm]
+    assert np.linalg.norm(K.project_b(p, y) - pb) <= 1e-12 * np.linalg.norm(pb)
+    assert np.linalg.norm(K.project_x(p, y) - px) <= 1e-12 * np.linalg.norm(px)
+    with pytest.raises(ValueError):
+        K.project_b(p, y[:-1])
