@@ -2,7 +2,7 @@
  * kronprec_b200.h — C ABI of the B200-native PCG / FPCG / CGLS hot path.
  *
  * Drop-in boundary for the reference `kronprec` solver path (namespace
- * kronprec, /root/reference/proj/include/kronprec/*.hpp). Every entry point
+ * kronprec, the headers under /root/reference/proj/include/kronprec). Every entry point
  * names the reference interface it replaces. Plain pointers and sizes only:
  * matrices are dense column-major float64 (n-by-n, leading dimension n),
  * vectors are vec() = column stacking (kron.cpp:52-60), exactly like the
