@@ -897,6 +897,27 @@ def main():
                    "ms_per_launch": pm_ms / pm_launches if pm_launches else None}
     dominant, other = (pm_line, op_line) if pm_ms > op_ms else (op_line, pm_line)
 
+    # the HBM-bound vector kernels (north star: "achieved HBM GB/s for the vector
+    # kernels"): algorithmic bytes of the class per iteration and per solve over
+    # the class's device time in the profiled pass
+    vec_line = None
+    vec_ms, vec_launches = prof["vector"]
+    if solver_name in ("pcg", "fpcg") and vec_ms > 0:
+        flex = solver_name == "fpcg"
+        upd = (7 + (1 if flex else 0)) * 8 + 2     # pcg_update: x, r, p, q, x_true in; x, r (, r_prev), r16 out
+        fin = (2 + 8 + 8 + (8 if flex else 0)) if engine == "tensor" else 0  # msolve_finish_f16: z16, r (, r_prev) in; z out
+        pup = 24                                     # p = z + beta p
+        init = 8 + 8 + 10 + 16                       # x = 0, x_true.x_true, r -> r16, p = z
+        vbytes = float(nn) * (prof_iters * (upd + fin + pup) + args.steps * init)
+        pk = peaks()
+        v_ach = vbytes / (vec_ms / 1e3) / 1e9
+        vec_line = {"bound": "hbm", "achieved": v_ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": v_ach / pk["hbm_gbs"], "kernel": "pcg_update / pcg_p_update / msolve_finish_f16 "
+                    "(+ per-solve zero / dot / cast / copy)", "peak_source": pk["source"] + ": hbm_gbs",
+                    "bytes_per_iteration": float(nn) * (upd + fin + pup), "launches": vec_launches,
+                    "note": "algorithmic bytes (every vector read or written once per kernel); below "
+                            "n = 4096 the vectors fit the 126 MB L2 and the figure is not an HBM rate"}
+
     # the dense DMMA operator (the product the reference computes), for its roofline
     dense = None
     if op_mode.startswith("banded") and not args.no_dense:
@@ -952,6 +973,7 @@ def main():
                     "d2h_bytes_per_step": nn * 8 + 4 * cap * 8},
             "roofline": dominant,
             "roofline_other": other,
+            "roofline_vector": vec_line,
             "roofline_dense_operator_gemm": dense,
             "operator_mode": {"mode": op_mode, "col_taps": tc, "row_taps": tr},
             "kernels": {k: {"ms": v[0], "launches": v[1],

@@ -52,6 +52,8 @@ def test_device_arm_line():
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
     assert 0 < r["frac"] <= 1.2
     assert d["gpu_launches"] > 0
+    v = d["roofline_vector"]  # HBM view of the CG vector kernels
+    assert v["bound"] == "hbm" and v["unit"] == "GB/s" and v["achieved"] > 0 and v["peak"] > 1000
     c = d["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(c) and c["samples"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
