@@ -455,8 +455,69 @@ def run_c4(args):
                 "kernel": "gemm_f16x_kernel" if eng == "tensor" else "gemm_f16ref_kernel",
                 "work_per_launch": f"{work:.4g} half-ops ({nb} images x 2 n^3, batched along N)",
                 "launches": 4 * batches, "ms_per_launch": tt.value / (4 * batches)}
-    elapsed, solved = reduce_timing(elapsed, float(len(results) * args.steps), dist,
-                                    device="cuda" if args.dist_backend == "nccl" else "cpu")
+    # ---- device-resident pass (the line's `value`): the same batched solve with
+    # b / x_true / x in device memory (kp_discrepancy_batch_ex + kp_pcg_batch with
+    # device_pointers); the host-buffer loop above is the line's `e2e` ----
+    res_elapsed = None
+    if batched:
+        from paper_2311_15393_b200._lib import kp_history, kp_solver_options, ptr
+        B, nn_ = len(mine), sh.n * sh.n
+        dptr = []
+
+        def dalloc(count):
+            p = C.c_void_p()
+            check(L.kp_device_alloc(count * 8, C.byref(p)))
+            dptr.append(p)
+            return p
+
+        d_b, d_xt, d_x = dalloc(B * nn_), dalloc(B * nn_), dalloc(B * nn_)
+        check(L.kp_memcpy_h2d(d_b, ptr(bs), B * nn_ * 8))
+        check(L.kp_memcpy_h2d(d_xt, ptr(xts), B * nn_ * 8))
+        nz_arr = np.ascontiguousarray(np.asarray(nzs, dtype=np.float64))
+        lam_arr, st_arr = np.zeros(B), np.zeros(B, dtype=np.int32)
+        cap = 101
+        hbufs = [[np.zeros(cap) for _ in range(4)] for _ in range(B)]
+        hs = (kp_history * B)()
+
+        def run_resident():
+            check(L.kp_discrepancy_batch_ex(sh.m0.handle(), B, d_b, ptr(nz_arr), float(sh.eta), ptr(lam_arr),
+                                            st_arr.ctypes.data_as(C.c_void_p), 1))
+            if np.any(st_arr != 0):
+                return None
+            for i, (rel, res, work, cos) in enumerate(hbufs):
+                hs[i] = kp_history(capacity=cap, relative_error=ptr(rel), residual_norm=ptr(res),
+                                   work_units=ptr(work), residual_cosines=ptr(cos))
+            o = kp_solver_options(lambda_=0.0, max_iterations=100, rel_residual_tol=float(sh.tol), x_true=d_xt.value,
+                                  track_search_direction_orthogonality=0, record_iterates=0, device_pointers=1)
+            check(L.kp_pcg_batch(sh.a.handle(), sh.m0.handle(), B, d_b, ptr(lam_arr), C.byref(o), d_x, hs))
+            check(L.kp_synchronize())
+            return [hs[i].iterations_used for i in range(B)]
+
+        its_res = run_resident()  # warm-up
+        if its_res is not None:
+            if its_res != [r.iterations for r in results]:
+                raise RuntimeError("device-resident batch differs from the host-buffer batch")
+            if dist:
+                dist.barrier()
+            res_times = []
+            for _ in range(args.steps):
+                check(L.kp_synchronize())
+                check(L.kp_event_record(2))
+                run_resident()
+                check(L.kp_event_record(3))
+                ms = C.c_float()
+                check(L.kp_event_elapsed(2, 3, C.byref(ms)))
+                res_times.append(ms.value / 1e3)
+            res_elapsed = sum(res_times)
+        for p in dptr:
+            check(L.kp_device_free(p))
+    e2e_elapsed, solved = reduce_timing(elapsed, float(len(results) * args.steps), dist,
+                                        device="cuda" if args.dist_backend == "nccl" else "cpu")
+    if res_elapsed is None:
+        elapsed = e2e_elapsed
+    else:
+        elapsed, _ = reduce_timing(res_elapsed, float(len(results) * args.steps), dist,
+                                   device="cuda" if args.dist_backend == "nccl" else "cpu")
     allres = gather_results(results, dist,
                             device="cuda" if (dist and args.dist_backend == "nccl") else None)
 
@@ -517,11 +578,12 @@ def run_c4(args):
                           "no_root": sum(r["no_root"] for r in allres),
                           "l2": "each step solves 64 distinct images (8 MB inputs and ~0.1 GB of solver "
                                 "state per image), far more than the 126 MB L2; no flush needed"},
-               "e2e": {"value": solved / elapsed, "unit": "solves/s",
+               "e2e": {"value": solved / e2e_elapsed, "unit": "solves/s",
                        "h2d_bytes_per_step": 64 * 2 * 8 * sh.n * sh.n,
                        "d2h_bytes_per_step": 64 * 8 * sh.n * sh.n,
-                       "note": "value is already end to end: every solve goes through the public "
-                               "API with host buffers (b, x_true in, x out inside the timed region)"},
+                       "note": "the public API with pinned host buffers: b, x_true in, x out inside the timed "
+                               "region" + ("" if res_elapsed is not None else
+                                           "; value repeats it (no device-resident pass in this mode)")},
                "clocks": clk.summary(), "gpu_launches": int(launches), "roofline": roof,
                "problem_generation_s": {"host": t_gen_host, "device": t_gen_dev,
                                         "note": "untimed setup: this rank's images by the host "

@@ -371,6 +371,12 @@ int kp_rng_raw(const unsigned long long* seeds, int batch, long count, unsigned 
 int kp_discrepancy_batch(const kp_precond* p, int batch, const double* b,
                          const double* noise_norms, double eta, double* lambdas,
                          int* status);
+/* The same with b in device memory when device_pointers != 0 (a batch
+ * generated by kp_generate_test_problems or left by an earlier call stays
+ * resident: lambda selection + kp_pcg_batch without host round trips). */
+int kp_discrepancy_batch_ex(const kp_precond* p, int batch, const double* b,
+                            const double* noise_norms, double eta,
+                            double* lambdas, int* status, int device_pointers);
 
 #ifdef __cplusplus
 }

@@ -78,7 +78,7 @@ EXPORTS = [
     "kp_lp_matmul_ex", "kp_set_fp16_products", "kp_get_fp16_products", "kp_psf_to_kronsum",
     "kp_nearest_kron", "kp_pcg_batch", "kp_fpcg_batch", "kp_svd", "kp_set_svd_backend",
     "kp_get_svd_backend", "kp_discrepancy_batch", "kp_generate_test_problems", "kp_rng_raw",
-    "kp_round_value", "kp_round_call_count",
+    "kp_round_value", "kp_round_call_count", "kp_discrepancy_batch_ex",
 ]
 
 _lib = None
@@ -121,6 +121,7 @@ def lib() -> C.CDLL:
             "kp_svd": ([P, I, I, P, P, P], I), "kp_set_svd_backend": ([I], I),
             "kp_get_svd_backend": ([C.POINTER(I)], I),
             "kp_discrepancy_batch": ([P, I, P, P, D, P, P], I),
+            "kp_discrepancy_batch_ex": ([P, I, P, P, D, P, P, I], I),
             "kp_generate_test_problems": ([P, I, P, I, P, P, P, P, P, P, I], I),
             "kp_rng_raw": ([P, I, C.c_long, P], I),
             "kp_pcg_batch": ([P, P, I, P, P, C.POINTER(kp_solver_options), P, C.POINTER(kp_history)], I),

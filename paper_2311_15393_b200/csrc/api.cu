@@ -2594,6 +2594,10 @@ int kp_rng_raw(const unsigned long long* seeds, int batch, long count, unsigned 
 
 int kp_discrepancy_batch(const kp_precond* p, int batch, const double* b, const double* noise_norms,
                          double eta, double* lambdas, int* status) {
+  return kp_discrepancy_batch_ex(p, batch, b, noise_norms, eta, lambdas, status, 0);
+}
+int kp_discrepancy_batch_ex(const kp_precond* p, int batch, const double* b, const double* noise_norms,
+                            double eta, double* lambdas, int* status, int device_pointers) {
   KP_API({
     if (!p || !b || !noise_norms || !lambdas || !status || batch < 1)
       throw InvalidArgument("discrepancy_batch: bad arguments");
@@ -2606,10 +2610,15 @@ int kp_discrepancy_batch(const kp_precond* p, int batch, const double* b, const 
     // spectral data of every image (b_hat = vec(U_c^T B U_r), one image at a time)
     DBuf<double> bhat(size_t(batch) * nn);
     {
-      DBuf<double> db(nn);
+      DBuf<double> db;
+      if (!device_pointers) db.alloc(nn);
       for (int i = 0; i < batch; ++i) {
-        db.upload(b + size_t(i) * nn, nn);
-        project_dev(n, sh.d_u_c.p, sh.d_u_r.p, db.p, bhat.p + size_t(i) * nn);
+        if (device_pointers) {  // b already in device memory: project in place
+          project_dev(n, sh.d_u_c.p, sh.d_u_r.p, b + size_t(i) * nn, bhat.p + size_t(i) * nn);
+        } else {
+          db.upload(b + size_t(i) * nn, nn);
+          project_dev(n, sh.d_u_c.p, sh.d_u_r.p, db.p, bhat.p + size_t(i) * nn);
+        }
       }
     }
     {

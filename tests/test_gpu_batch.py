@@ -131,6 +131,21 @@ def test_discrepancy_batch_equals_per_image():
             continue
         assert st[i] == 0
         assert lam[i] == K.discrepancy(sd, noise[i], 1.01).lambda_  # bit-identical
+    # the same batch left in device memory (kp_discrepancy_batch_ex, device_pointers = 1)
+    import ctypes as C
+
+    from paper_2311_15393_b200._lib import check, lib, ptr
+    L = lib()
+    bs = np.ascontiguousarray(np.stack([tp.b for tp in tps]))
+    d_b = C.c_void_p()
+    check(L.kp_device_alloc(bs.nbytes, C.byref(d_b)))
+    check(L.kp_memcpy_h2d(d_b, ptr(bs), bs.nbytes))
+    nz = np.asarray(noise, dtype=np.float64)
+    lam_d, st_d = np.zeros(len(tps)), np.zeros(len(tps), dtype=np.int32)
+    check(L.kp_discrepancy_batch_ex(m0.handle(), len(tps), d_b, ptr(nz), 1.01, ptr(lam_d),
+                                    st_d.ctypes.data_as(C.c_void_p), 1))
+    check(L.kp_device_free(d_b))
+    assert np.array_equal(st_d, np.asarray(st)) and np.array_equal(lam_d, np.asarray(lam), equal_nan=True)
 
 
 def test_device_svd_backend():
