@@ -494,9 +494,12 @@ def run_c4(args):
             return [hs[i].iterations_used for i in range(B)]
 
         its_res = run_resident()  # warm-up
-        if its_res is not None:
-            if its_res != [r.iterations for r in results]:
-                raise RuntimeError("device-resident batch differs from the host-buffer batch")
+        if its_res is not None and its_res != [r.iterations for r in results]:
+            raise RuntimeError("device-resident batch differs from the host-buffer batch")
+        # every rank takes the same path (an image without a root on any rank: all fall back to e2e)
+        bad, _ = reduce_timing(0.0 if its_res is not None else 1.0, 0.0, dist,
+                               device="cuda" if args.dist_backend == "nccl" else "cpu")
+        if bad == 0.0:
             if dist:
                 dist.barrier()
             res_times = []
