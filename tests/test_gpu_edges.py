@@ -218,13 +218,14 @@ def test_device_pointer_mode_matches_host_mode():
             L.kp_device_free(p)
 
 
-def test_dense_operator_tma_tiles_ragged():
-    """The 128 x 128 DMMA tiles staged by TMA (n large enough for the big-tile
-    grid), ragged in M, N and K: rows, columns and the K tail outside the
-    matrix come from the TMA zero fill. kron.cpp:62-88 against numpy FP64."""
-    n = 1546
+@pytest.mark.parametrize("n,r", [(1546, 2), (700, 5), (905, 3)])
+def test_dense_operator_tma_tiles_ragged(n, r):
+    """The 128 x 128 DMMA tiles staged by TMA (big-tile grid: n = 1546, or the
+    M = r n product at n = 700), ragged in M, N and K: rows, columns and the K
+    tail outside the matrix come from the TMA zero fill; odd n (905: rows not
+    16-byte aligned) takes the cp.async staging. kron.cpp:62-88 against numpy."""
     rng = np.random.default_rng(17)
-    terms = [KronTerm(rng.standard_normal((n, n)), rng.standard_normal((n, n))) for _ in range(2)]
+    terms = [KronTerm(rng.standard_normal((n, n)), rng.standard_normal((n, n))) for _ in range(r)]
     op = KroneckerSum(terms, n)
     op.set_mode("dense")
     x = rng.standard_normal(n * n)
